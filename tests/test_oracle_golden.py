@@ -1,0 +1,98 @@
+"""Pin the C oracle (oracle/roaring_oracle.c) against golden vectors produced by
+the real reference (tests/golden/make_golden.py).  CPU only."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests.golden_io import load
+
+OPS = ("and", "or", "andnot", "xor")
+
+
+def test_pairs_materialized_and_counts():
+    g = load()
+    for a, b, res, card in zip(g["pair_a"], g["pair_b"], g["pair_res"], g["pair_card"]):
+        wa, wb = g.wire(a), g.wire(b)
+        for k, op in enumerate(OPS):
+            assert orc.op(op, wa, wb) == g.wire(res[k]), op
+            assert orc.op_cardinality(op, wa, wb) == card[k], op
+
+
+def test_container_pairs_all_type_combinations():
+    g = load()
+    seen = set()
+    for a, b, res, card, tags in zip(g["cont_a"], g["cont_b"], g["cont_res"], g["cont_card"],
+                                     g["cont_tags"]):
+        wa, wb = g.wire(a), g.wire(b)
+        seen.add(tuple(tags))
+        for k, op in enumerate(OPS):
+            assert orc.op(op, wa, wb) == g.wire(res[k]), (op, tags)
+            assert orc.container_pairwise_cardinality(op, wa, wb) == card[k], (op, tags)
+    assert len(seen) == 9  # every container-type pair is pinned
+
+
+def test_union_many():
+    g = load()
+    for members, res in zip(g["um_members"], g["um_res"]):
+        assert orc.union_many([g.wire(m) for m in members]) == g.wire(res)
+
+
+def test_union_many_order_dependent_types():
+    g = load()
+    rxy, xyr = g["um_res"][0], g["um_res"][1]
+    # same set, different container types
+    assert orc.to_array(g.wire(rxy)).tolist() == orc.to_array(g.wire(xyr)).tolist()
+    assert g.wire(rxy) != g.wire(xyr)
+
+
+def test_from_values_run_optimize_to_array():
+    g = load()
+    buf, off = g["fv_in_buf"], g["fv_in_off"]
+    for i, (res, opt, ch, arr) in enumerate(zip(g["fv_res"], g["fv_opt"], g["fv_changed"],
+                                                g["fv_arr"])):
+        vals = np.frombuffer(buf[int(off[i]):int(off[i + 1])].tobytes(), dtype="<u8")
+        w = orc.from_values(vals)
+        assert w == g.wire(res)
+        o, changed = orc.run_optimize(w)
+        assert o == g.wire(opt) and changed == bool(ch)
+        assert orc.to_array(w).tobytes() == g.wire(arr)
+
+
+def test_from_values_rejects_over_32_bits():
+    with pytest.raises(ValueError):
+        orc.from_values([1, 1 << 32])
+
+
+def test_decode_errors_match_reference():
+    g = load()
+    for img, off, msg in zip(g["bad"], g["bad_off"], g["bad_msg"]):
+        with pytest.raises(orc.OracleDecodeError) as e:
+            orc.check(g.wire(img))
+        assert e.value.offset == off
+        assert str(e.value) == msg
+
+
+def test_roundtrip_every_golden_image():
+    g = load()
+    bad = set(int(i) for i in g["bad"])
+    for i in range(len(g.off) - 1):
+        if i in bad:
+            continue
+        w = g.wire(i)
+        if w[:4] != b"ROAR":
+            continue  # raw value/array payloads
+        assert orc.roundtrip(w) == w
+
+
+def test_batch_entry_points_agree_with_single():
+    g = load()
+    wa = [g.wire(a) for a in g["pair_a"]]
+    wb = [g.wire(b) for b in g["pair_b"]]
+    bufA, offA = orc.concat(wa)
+    bufB, offB = orc.concat(wb)
+    idx = np.arange(len(wa))
+    for k, op in enumerate(OPS):
+        outs = orc.op_batch(op, bufA, offA, bufB, offB, idx, idx)
+        assert outs == [g.wire(r[k]) for r in g["pair_res"]]
+        cards = orc.op_cardinality_batch(op, bufA, offA, bufB, offB, idx, idx)
+        assert cards.tolist() == [int(c[k]) for c in g["pair_card"]]
