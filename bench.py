@@ -1,0 +1,367 @@
+"""Benchmark: batched Roaring set operations on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): 1,024 independent bitmap pairs over
+[0, 2^24) -- 256 chunks per bitmap, each value present with probability
+p ~ U[0.1, 0.5] per bitmap, so every chunk is an 8 KB bitset (4.3 GB of input
+for the 2,048 bitmaps).  One step = the four materialized ops (& | - ^) and the
+four op_cardinality counts for every pair: 8 x 262,144 container pairs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gpu|reference]
+
+Prints one JSON line (rank 0).  `value` is container-pair set ops/s with inputs
+resident in HBM (CUDA events, max over ranks); `e2e` is the same metric through
+the public API with pinned host wire images copied in and result wire images /
+counts copied out every step; `roofline` is the dominant kernel
+(bitset x bitset op) live-timed with CUDA events on its launch stream.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+OPS = ("and", "or", "andnot", "xor")
+NPAIRS = 1024
+NCHUNKS = 256
+METRIC = "container-pair set ops/sec (AND/OR/ANDNOT/XOR + cardinality counts)"
+UNIT = "container-pairs/s"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self._p = device, [], None
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self._p:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def dist_init(ws, local):
+    if ws <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def dist_max(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def workload(seed: int):
+    from paper_1709_07821_b200 import synth
+    return synth.config2(seed=seed, npairs=NPAIRS, nchunks=NCHUNKS)
+
+
+def cpu_baseline(buf, offs, max_seconds: float = 25.0):
+    """The oracle port (C restatement of the reference algorithm) on the host
+    cores, in-memory bitmaps, all threads: a bounded sample of the workload."""
+    from oracle import oracle as orc
+    threads = orc.num_threads()
+    S = orc.Session(buf, offs, threads)
+    units, t_total, pairs_done = 0, 0.0, 0
+    chunk = 64
+    # correctness-gated warm-up (harness.py:230-235)
+    S.run("and", "op_cardinality", S, [0], [NPAIRS], threads)
+    while t_total < max_seconds and pairs_done < NPAIRS:
+        ia = np.arange(pairs_done, min(pairs_done + chunk, NPAIRS))
+        ib = ia + NPAIRS
+        t0 = time.perf_counter()
+        for op in OPS:
+            S.run(op, "op", S, ia, ib, threads)
+            S.run(op, "op_cardinality", S, ia, ib, threads)
+        t_total += time.perf_counter() - t0
+        units += 8 * len(ia) * NCHUNKS
+        pairs_done += len(ia)
+    return {"value": units / t_total, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{pairs_done} of {NPAIRS} C2 bitmap pairs x (4 ops + 4 counts), in-memory, "
+                      f"oracle/roaring_oracle.c restatement, {threads} threads, {t_total:.1f} s"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    buf, offs = workload(seed=2)
+    threads = orc.num_threads()
+    S = orc.Session(buf, offs, threads)
+    sample = 32  # bitmap pairs per step (8,192 container pairs x 8)
+
+    def step(k):
+        lo = (k * sample) % NPAIRS
+        ia = np.arange(lo, lo + sample)
+        for op in OPS:
+            S.run(op, "op", S, ia, ia + NPAIRS, threads)
+            S.run(op, "op_cardinality", S, ia, ia + NPAIRS, threads)
+
+    for k in range(args.warmup):
+        step(k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(args.warmup + k)
+    dt = time.perf_counter() - t0
+    units = args.steps * sample * NCHUNKS * 8
+    value = units / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded, BASELINE.json configs[1] shape)",
+        "config": {"workload": f"C2 sample: {sample} of {NPAIRS} bitmap pairs x {NCHUNKS} bitset chunks per step, "
+                               "4 ops + 4 op_cardinality", "seed": 2},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} bitmap pairs per step (oracle/roaring_oracle.c restatement of "
+                                   "the reference algorithm, in-memory bitmaps)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    ws, rank, local = dist_env()
+    dist = dist_init(ws, local)
+    import paper_1709_07821_b200 as rb
+    from paper_1709_07821_b200 import _lib
+    _lib.set_device(local)
+    seed = 2 + rank
+    buf, offs = workload(seed)
+    A_img = (buf[:int(offs[NPAIRS])], offs[:NPAIRS + 1].copy())
+    B_img = (buf[int(offs[NPAIRS]):], (offs[NPAIRS:] - offs[NPAIRS]).astype(np.uint64))
+    A = rb.BitmapBatch.from_wire(A_img)
+    B = rb.BitmapBatch.from_wire(B_img)
+    import torch
+    counts = torch.empty(NPAIRS, dtype=torch.int64, device=f"cuda:{local}")
+
+    def step():
+        for op in OPS:
+            R = A.pairwise(op, B)
+            del R
+        for op in OPS:
+            A.pairwise_cardinality_device(op, B, counts.data_ptr(), NPAIRS)
+
+    # oracle-checked warm-up (harness.py:230-235): sampled pairs, bytes + counts
+    out_bytes = {}
+    for op in OPS:
+        R = A.pairwise(op, B)
+        pb, db, _ = R.stats()
+        out_bytes[op] = pb + db
+        if rank == 0 and not args.no_check:
+            from oracle import oracle as orc
+            got = R.select([0, NPAIRS - 1]).to_wire_list()
+            for k, p in enumerate((0, NPAIRS - 1)):
+                wa = A_img[0][int(A_img[1][p]):int(A_img[1][p + 1])].tobytes()
+                wb = B_img[0][int(B_img[1][p]):int(B_img[1][p + 1])].tobytes()
+                if got[k] != orc.op(op, wa, wb):
+                    raise SystemExit(f"parity failure in warm-up: op {op} pair {p}")
+        del R
+    for _ in range(args.warmup):
+        step()
+    _lib.synchronize()
+
+    units_per_step = 8 * NPAIRS * NCHUNKS
+    in_bytes = NPAIRS * NCHUNKS * 2 * (8 + 8192)
+
+    # ---- timed region: inputs resident in HBM (4.3 GB > 126 MB L2: no flush needed)
+    _lib.profile_reset()
+    _lib.profile(True)
+    dist_barrier(dist)
+    _lib.synchronize()
+    k0 = _lib.kernel_launches()
+    with Clocks(local) as clk:
+        e0 = _lib.Event()
+        for _ in range(args.steps):
+            step()
+        e1 = _lib.Event()
+        _lib.synchronize()
+    ms = e0.elapsed_ms(e1)
+    launches = _lib.kernel_launches() - k0
+    dist_barrier(dist)
+    ms_max = dist_max(dist, ms)
+    bp_ms, bp_n, _ = _lib.profile_query("bitset_pair")
+    bc_ms, bc_n, _ = _lib.profile_query("bitset_count")
+    _lib.profile(False)
+
+    hbm, peak_kind = peaks()
+    bytes_per_launch = (4 * in_bytes + sum(out_bytes.values())) / 4.0
+    achieved = bytes_per_launch / (bp_ms / bp_n * 1e-3) / 1e9 if bp_n else 0.0
+    count_bytes = NPAIRS * NCHUNKS * 2 * (8 + 8192) + 8 * NPAIRS
+    achieved_c = count_bytes / (bc_ms / bc_n * 1e-3) / 1e9 if bc_n else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bitset_pair")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: public API from pinned host wire images, results back to host
+    e2e = None
+    if not args.no_e2e:
+        pin_a = _lib.PinnedBuffer(A_img[0].nbytes)
+        pin_b = _lib.PinnedBuffer(B_img[0].nbytes)
+        pin_a.array[:] = A_img[0]
+        pin_b.array[:] = B_img[0]
+        out_cap = int(2 * (A_img[0].nbytes + B_img[0].nbytes))
+        pin_out = _lib.PinnedBuffer(out_cap)
+        host_counts = np.zeros(NPAIRS, dtype=np.uint64)
+
+        def e2e_step():
+            h2d = pin_a.nbytes + pin_b.nbytes
+            AA = rb.BitmapBatch.from_wire((pin_a.array, A_img[1]))
+            BB = rb.BitmapBatch.from_wire((pin_b.array, B_img[1]))
+            d2h = 0
+            for op in OPS:
+                R = AA.pairwise(op, BB)
+                wbuf, woffs = R.to_wire(out=pin_out.array)
+                d2h += int(woffs[-1])
+                del R
+            for op in OPS:
+                host_counts[:] = AA.pairwise_cardinality(op, BB)
+                d2h += host_counts.nbytes
+            return h2d, d2h
+
+        e2e_step()
+        n_e2e = max(1, min(args.steps, 3))
+        dist_barrier(dist)
+        _lib.synchronize()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(n_e2e):
+            h2d, d2h = e2e_step()
+        _lib.synchronize()
+        e2e_ms = dist_max(dist, (time.perf_counter() - t0) * 1e3 / n_e2e)
+        e2e = {"value": ws * units_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+               "path": "BitmapBatch.from_wire(pinned) -> 4x pairwise + to_wire(pinned) -> 4x pairwise_cardinality"}
+
+    base = None
+    if rank == 0 and not args.no_cpu:
+        base = cpu_baseline(*workload(2), max_seconds=args.cpu_seconds)
+
+    value = ws * units_per_step * args.steps / (ms_max * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded SplitMix64 Bernoulli bitsets, BASELINE.json configs[1] shape)",
+        "config": {"workload": f"C2: {NPAIRS} bitmap pairs x {NCHUNKS} bitset chunks (8 KB), 4 ops + 4 "
+                               "op_cardinality per step", "seed": 2, "per_rank_seed": "2 + rank",
+                   "l2": "inputs 4.3 GB per rank > 126 MB L2; no flush needed",
+                   "input_bytes": int(A_img[0].nbytes + B_img[0].nbytes)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm if hbm else None, "traffic": traffic,
+                     "kernel": "k_pair_dense<false> (bitset x bitset op + popcount + type choice)",
+                     "peak_kind": peak_kind, "frac_of_nominal_8TBps": achieved / NOMINAL_HBM_GBS,
+                     "launches": bp_n, "avg_launch_ms": bp_ms / bp_n if bp_n else None,
+                     "bytes_per_launch": bytes_per_launch,
+                     "share_of_step": (bp_ms / args.steps) / (ms / args.steps) if ms else None},
+        "roofline_count": {"kernel": "k_pair_count<false> (bitset x bitset |A and B|)", "achieved": achieved_c,
+                           "peak": hbm, "unit": "GB/s", "frac": achieved_c / hbm if hbm else None,
+                           "launches": bc_n, "avg_launch_ms": bc_ms / bc_n if bc_n else None},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": base,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("gpu", "reference"), default="gpu")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "gpu":
+        print("note: warm-up raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    return run_reference(args) if args.impl == "reference" else run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

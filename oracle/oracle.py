@@ -67,6 +67,10 @@ def lib():
         L.orc_container_card_batch.argtypes = [C.c_int, P, P, P, P, P, P, I64, P, C.c_int]
         L.orc_all_pairs_and.argtypes = [P, P, I64, P, P, I64, P, C.c_int]
         L.orc_num_threads.restype = C.c_int
+        L.orc_batch_load.argtypes = [P, P, I64, C.c_int]
+        L.orc_batch_load.restype = P
+        L.orc_batch_free.argtypes = [P]
+        L.orc_batch_run.argtypes = [C.c_int, C.c_int, P, P, P, P, I64, P, C.c_int]
         _lib = L
     return _lib
 
@@ -243,3 +247,32 @@ def all_pairs_and(buf, offs, pi, pj, threads: int = 0) -> np.ndarray:
     if rc:
         raise RuntimeError("oracle all_pairs_and failed")
     return out
+
+
+class Session:
+    """Bitmaps deserialized once into the oracle's in-memory form; run() times
+    only the restated reference algorithm (the harness protocol,
+    bench/harness.py:205-239)."""
+
+    KINDS = {"op": 0, "op_cardinality": 1, "container_pairwise": 2,
+             "container_pairwise_cardinality": 3}
+
+    def __init__(self, buf, offs, threads: int = 0):
+        buf = np.ascontiguousarray(buf, dtype=np.uint8)
+        offs = np.ascontiguousarray(offs, dtype=np.uint64)
+        self._h = lib().orc_batch_load(buf.ctypes.data, offs.ctypes.data, len(offs) - 1, threads)
+        if not self._h:
+            raise RuntimeError("oracle session: an image failed to decode")
+
+    def run(self, op_name: str, kind: str, other: "Session", ia, ib, threads: int = 0) -> np.ndarray:
+        ia, ib = _i64(ia), _i64(ib)
+        out = np.zeros(max(ia.size, 1), dtype=np.int64)
+        lib().orc_batch_run(_op_index(op_name), self.KINDS[kind], self._h, other._h, ia.ctypes.data,
+                            ib.ctypes.data, ia.size, out.ctypes.data, threads)
+        return out[:ia.size]
+
+    def __del__(self):
+        try:
+            lib().orc_batch_free(self._h)
+        except Exception:
+            pass

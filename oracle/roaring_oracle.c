@@ -1236,3 +1236,62 @@ int orc_all_pairs_and(const uint8_t *buf, const uint64_t *offs, int64_t n, const
     free(bm);
     return err;
 }
+
+/* ------------------------------------------------ in-memory sessions (CPU baseline)
+ * Deserialize once, then time only the reference algorithm on in-memory
+ * bitmaps, the way the reference harness times RoaringBitmap objects
+ * (bench/harness.py:205-239). */
+typedef struct { int64_t n; obm_t *bm; } obatch_t;
+
+void *orc_batch_load(const uint8_t *buf, const uint64_t *offs, int64_t n, int nthreads) {
+    obatch_t *b = xmalloc(sizeof(obatch_t));
+    b->n = n;
+    b->bm = xcalloc((size_t)(n ? n : 1), sizeof(obm_t));
+    int err = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads) reduction(|:err)
+#endif
+    for (int64_t i = 0; i < n; i++) {
+        char m[256]; int64_t eo;
+        if (deserialize(buf + offs[i], offs[i + 1] - offs[i], &b->bm[i], &eo, m, sizeof m)) err |= 1;
+    }
+    if (err) { for (int64_t i = 0; i < n; i++) if (b->bm[i].keys) bm_free(&b->bm[i]); free(b->bm); free(b); return NULL; }
+    return b;
+}
+
+void orc_batch_free(void *h) {
+    obatch_t *b = h;
+    if (!b) return;
+    for (int64_t i = 0; i < b->n; i++) bm_free(&b->bm[i]);
+    free(b->bm); free(b);
+}
+
+/* kind: 0 = RoaringBitmap.op (result built then dropped; its cardinality is
+ * returned), 1 = op_cardinality, 2 = container_pairwise (one-container
+ * bitmaps), 3 = container_pairwise_cardinality. */
+int orc_batch_run(int op, int kind, void *ha, void *hb, const int64_t *ia, const int64_t *ib, int64_t npairs,
+                  int64_t *out, int nthreads) {
+    obatch_t *A = ha, *B = hb;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#endif
+    for (int64_t p = 0; p < npairs; p++) {
+        const obm_t *a = &A->bm[ia[p]], *b = &B->bm[ib[p]];
+        if (kind == 0) {
+            obm_t R = bm_op(op, a, b);
+            out[p] = bm_len(&R);
+            bm_free(&R);
+        } else if (kind == 1) {
+            out[p] = bm_op_cardinality(op, a, b);
+        } else if (kind == 2) {
+            oc_t r = container_pairwise(op, &a->c[0], &b->c[0]);
+            out[p] = oc_len(&r);
+            oc_free(&r);
+        } else {
+            out[p] = container_pairwise_cardinality(op, &a->c[0], &b->c[0]);
+        }
+    }
+    return 0;
+}

@@ -1,0 +1,264 @@
+"""BitmapBatch: a device-resident collection of Roaring bitmaps (the batched API).
+
+One BitmapBatch owns one ``rs_batch`` of the C ABI (include/roaring_b200.h):
+a CSR container table plus a 16-byte aligned payload pool in HBM.  Every
+method is one batched call into hand-written sm_100a kernels; the reference's
+per-pair semantics (bitmap.py / containers.py under
+/root/reference/pkg/src/roaringset) hold for every pair of the batch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .containers import op_index
+
+
+def _u32_or_none(idx, n_expected=None):
+    if idx is None:
+        return None, None
+    a = np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+    if a.size and (a.min() < 0 or a.max() > 0xFFFFFFFF):
+        raise ValueError("bitmap index out of range")
+    a = a.astype(np.uint32)
+    return a, a.ctypes.data
+
+
+def _images(images):
+    """list[bytes] | (uint8 buf, uint64 offs) -> (buf, offs) numpy arrays."""
+    if isinstance(images, tuple) and len(images) == 2 and isinstance(images[0], np.ndarray):
+        buf, offs = images
+        return np.ascontiguousarray(buf, dtype=np.uint8), np.ascontiguousarray(offs, dtype=np.uint64)
+    images = list(images)
+    offs = np.zeros(len(images) + 1, dtype=np.uint64)
+    if images:
+        np.cumsum([len(x) for x in images], out=offs[1:])
+    buf = np.frombuffer(b"".join(images), dtype=np.uint8) if images else np.zeros(1, np.uint8)
+    return buf, offs
+
+
+class BitmapBatch:
+    __slots__ = ("_h", "__weakref__")
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                lib().rs_batch_free(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------ building
+    @classmethod
+    def from_wire(cls, images) -> "BitmapBatch":
+        """serde.deserialize (serde.py:87-169) of many images at once."""
+        buf, offs = _images(images)
+        h = C.c_void_p()
+        check(lib().rs_batch_from_wire(buf.ctypes.data, offs.ctypes.data, len(offs) - 1, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_values(cls, arrays) -> "BitmapBatch":
+        """RoaringBitmap.from_values (bitmap.py:40-62) for each array."""
+        parts = []
+        for a in arrays:
+            a = np.asarray(a)
+            if a.size:
+                a = np.asarray(a, dtype=np.uint64)
+                if int(a.max()) > 0xFFFFFFFF:
+                    raise ValueError("values must fit in 32 bits")
+            parts.append(a.astype(np.uint32, copy=False).ravel())
+        offs = np.zeros(len(parts) + 1, dtype=np.uint64)
+        if parts:
+            np.cumsum([p.size for p in parts], out=offs[1:])
+        vals = np.concatenate(parts) if parts else np.zeros(0, np.uint32)
+        return cls.from_values_flat(vals, offs)
+
+    @classmethod
+    def from_values_flat(cls, values: np.ndarray, offs: np.ndarray) -> "BitmapBatch":
+        v = np.ascontiguousarray(values, dtype=np.uint32)
+        o = np.ascontiguousarray(offs, dtype=np.uint64)
+        h = C.c_void_p()
+        check(lib().rs_batch_from_u32(v.ctypes.data if v.size else None, o.ctypes.data, len(o) - 1, 0, C.byref(h)))
+        return cls(h)
+
+    @staticmethod
+    def concat(batches) -> "BitmapBatch":
+        batches = list(batches)
+        arr = (C.c_void_p * max(len(batches), 1))(*[b._h for b in batches])
+        h = C.c_void_p()
+        check(lib().rs_batch_concat(arr, len(batches), C.byref(h)))
+        return BitmapBatch(h)
+
+    def select(self, idx) -> "BitmapBatch":
+        """Deep copy of bitmaps idx (RoaringBitmap.copy, bitmap.py:71-73)."""
+        a = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64))
+        h = C.c_void_p()
+        check(lib().rs_batch_select(self._h, a.ctypes.data, a.size, C.byref(h)))
+        return BitmapBatch(h)
+
+    # ------------------------------------------------------------- queries
+    def info(self):
+        nb, nc, pb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib().rs_batch_info(self._h, C.byref(nb), C.byref(nc), C.byref(pb)))
+        return int(nb.value), int(nc.value), int(pb.value)
+
+    def __len__(self) -> int:
+        return self.info()[0]
+
+    def stats(self):
+        """(payload bytes, descriptor bytes, {tag: count}) in the SURVEY 8(d) accounting."""
+        pb, db = C.c_uint64(), C.c_uint64()
+        tc = np.zeros(4, dtype=np.uint64)
+        check(lib().rs_batch_stats(self._h, C.byref(pb), C.byref(db), tc.ctypes.data))
+        return int(pb.value), int(db.value), {1: int(tc[1]), 2: int(tc[2]), 3: int(tc[3])}
+
+    def cardinalities(self) -> np.ndarray:
+        out = np.zeros(max(len(self), 1), dtype=np.uint64)
+        check(lib().rs_batch_cardinalities(self._h, out.ctypes.data))
+        return out[:len(self)]
+
+    def container_counts(self) -> np.ndarray:
+        out = np.zeros(max(len(self), 1), dtype=np.uint64)
+        check(lib().rs_batch_container_counts(self._h, out.ctypes.data))
+        return out[:len(self)]
+
+    # -------------------------------------------------------------- export
+    def wire_sizes(self) -> np.ndarray:
+        out = np.zeros(max(len(self), 1), dtype=np.uint64)
+        check(lib().rs_batch_wire_sizes(self._h, out.ctypes.data))
+        return out[:len(self)]
+
+    def to_wire(self, out: np.ndarray | None = None):
+        """serde.serialize of every bitmap -> (uint8 buffer, uint64 offsets)."""
+        n = len(self)
+        total = int(self.wire_sizes().sum())
+        buf = out if out is not None else np.empty(max(total, 1), dtype=np.uint8)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        check(lib().rs_batch_to_wire(self._h, buf.ctypes.data, buf.nbytes, offs.ctypes.data))
+        return buf[:total], offs
+
+    def to_wire_list(self) -> list[bytes]:
+        buf, offs = self.to_wire()
+        return [buf[int(offs[i]):int(offs[i + 1])].tobytes() for i in range(len(offs) - 1)]
+
+    def to_arrays_flat(self):
+        """RoaringBitmap.to_array of every bitmap -> (uint32 values, uint64 offsets)."""
+        n = len(self)
+        total = int(self.cardinalities().sum())
+        vals = np.empty(max(total, 1), dtype=np.uint32)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        check(lib().rs_batch_to_u32(self._h, vals.ctypes.data, vals.size, offs.ctypes.data))
+        return vals[:total], offs
+
+    def to_arrays(self) -> list[np.ndarray]:
+        vals, offs = self.to_arrays_flat()
+        return [vals[int(offs[i]):int(offs[i + 1])] for i in range(len(offs) - 1)]
+
+    def equal(self, other: "BitmapBatch", ia=None, ib=None) -> np.ndarray:
+        """Type-sensitive equality per pair (bitmap.py:87-91)."""
+        n = len(ia) if ia is not None else min(len(self), len(other))
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        check(lib().rs_batch_equal(self._h, other._h, pa, pb, n, out.ctypes.data))
+        return out[:n].astype(bool)
+
+    # ------------------------------------------------------------ hot path
+    def _npairs(self, other, ia, ib):
+        if ia is not None:
+            return len(ia)
+        if ib is not None:
+            return len(ib)
+        return min(len(self), len(other))
+
+    def pairwise(self, op: str, other: "BitmapBatch", ia=None, ib=None) -> "BitmapBatch":
+        """Bitmap p of the result = self[ia[p]] op other[ib[p]] (bitmap.py:169-210)."""
+        k = op_index(op)
+        n = self._npairs(other, ia, ib)
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        h = C.c_void_p()
+        check(lib().rs_pairwise(k, self._h, other._h, pa, pb, n, C.byref(h)))
+        return BitmapBatch(h)
+
+    def pairwise_cardinality(self, op: str, other: "BitmapBatch", ia=None, ib=None) -> np.ndarray:
+        """|self[ia[p]] op other[ib[p]]| (bitmap.py:212-241)."""
+        k = op_index(op)
+        n = self._npairs(other, ia, ib)
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        out = np.zeros(max(n, 1), dtype=np.uint64)
+        check(lib().rs_pairwise_cardinality(k, self._h, other._h, pa, pb, n, out.ctypes.data, 0))
+        return out[:n]
+
+    def pairwise_cardinality_device(self, op: str, other: "BitmapBatch", dev_out_ptr: int, n: int,
+                                    ia=None, ib=None) -> None:
+        """Asynchronous variant writing u64 counts to a device pointer."""
+        k = op_index(op)
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        check(lib().rs_pairwise_cardinality(k, self._h, other._h, pa, pb, n, C.c_void_p(dev_out_ptr), 1))
+
+    def container_pairwise(self, op: str, other: "BitmapBatch", ia=None, ib=None) -> "BitmapBatch":
+        """containers.py:450-529 over one-container bitmaps, batched."""
+        k = op_index(op)
+        n = self._npairs(other, ia, ib)
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        h = C.c_void_p()
+        check(lib().rs_container_pairwise(k, self._h, other._h, pa, pb, n, C.byref(h)))
+        return BitmapBatch(h)
+
+    def container_pairwise_cardinality(self, op: str, other: "BitmapBatch", ia=None, ib=None) -> np.ndarray:
+        """containers.py:554-570, batched."""
+        k = op_index(op)
+        n = self._npairs(other, ia, ib)
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        out = np.zeros(max(n, 1), dtype=np.uint64)
+        check(lib().rs_container_pairwise_cardinality(k, self._h, other._h, pa, pb, n, out.ctypes.data, 0))
+        return out[:n]
+
+    def union_many(self, idx=None) -> "BitmapBatch":
+        """RoaringBitmap.union_many (bitmap.py:257-304) over bitmaps idx (default: all, in order)."""
+        n = len(idx) if idx is not None else len(self)
+        a = np.ascontiguousarray(np.asarray(idx, dtype=np.uint64)) if idx is not None else None
+        h = C.c_void_p()
+        check(lib().rs_union_many(self._h, a.ctypes.data if a is not None else None, n, C.byref(h)))
+        return BitmapBatch(h)
+
+    def all_pairs_cardinality(self):
+        """(|B_i ∩ B_j|, |B_i ∪ B_j|) for all i<j in row-major order."""
+        n = len(self)
+        m = n * (n - 1) // 2
+        inter = np.zeros(max(m, 1), dtype=np.uint64)
+        uni = np.zeros(max(m, 1), dtype=np.uint64)
+        check(lib().rs_all_pairs_cardinality(self._h, inter.ctypes.data, uni.ctypes.data))
+        return inter[:m], uni[:m]
+
+    def run_optimize(self) -> np.ndarray:
+        """RoaringBitmap.run_optimize (bitmap.py:308-316) on every bitmap, in place."""
+        n = len(self)
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        check(lib().rs_batch_run_optimize(self._h, out.ctypes.data))
+        return out[:n].astype(bool)
+
+    def bitmap(self, i: int):
+        from .bitmap import RoaringBitmap
+        return RoaringBitmap._wrap(self.select([i]))
+
+    def __repr__(self) -> str:
+        nb, nc, pb = self.info()
+        return f"BitmapBatch(bitmaps={nb}, containers={nc}, pool_bytes={pb})"
+
+
+_ = _lib  # re-exported module for callers wanting stream/event helpers

@@ -1,0 +1,142 @@
+"""RoaringBitmap: drop-in for the reference's user-facing class
+(/root/reference/pkg/src/roaringset/bitmap.py:29-363), backed by the GPU.
+
+Each instance owns a one-bitmap BitmapBatch in HBM.  Set algebra, counts, wide
+unions, exports and run_optimize run as sm_100a kernels through the C ABI;
+inputs are never mutated (bitmap.py:8-9).  Container types follow the
+reference exactly, so wire images compare byte for byte.
+"""
+
+from __future__ import annotations
+
+from typing import Iterable, Iterator
+
+import numpy as np
+
+from .batch import BitmapBatch
+from .containers import OPS, Container, chunks_from_wire, container_positions, op_index
+from ._lib import DecodeError
+
+_EMPTY = b"ROAR\x00\x00\x00\x00"
+
+
+class RoaringBitmap:
+    """Compressed set of 32-bit unsigned integers (GPU-resident)."""
+
+    __slots__ = ("_b",)
+
+    def __init__(self) -> None:
+        self._b = BitmapBatch.from_wire([_EMPTY])
+
+    @classmethod
+    def _wrap(cls, batch: BitmapBatch) -> "RoaringBitmap":
+        rb = cls.__new__(cls)
+        rb._b = batch
+        return rb
+
+    # ------------------------------------------------------------- building
+    @classmethod
+    def from_values(cls, values) -> "RoaringBitmap":
+        """Bulk-build from any iterable or array of 32-bit values (bitmap.py:40-62)."""
+        arr = np.asarray(list(values) if not isinstance(values, np.ndarray) else values)
+        return cls._wrap(BitmapBatch.from_values([arr]))
+
+    @classmethod
+    def deserialize(cls, data: bytes) -> "RoaringBitmap":
+        return cls._wrap(BitmapBatch.from_wire([bytes(data)]))
+
+    def serialize(self) -> bytes:
+        return self._b.to_wire_list()[0]
+
+    def copy(self) -> "RoaringBitmap":
+        return RoaringBitmap._wrap(self._b.select([0]))
+
+    # ------------------------------------------------------------ basic API
+    def __len__(self) -> int:
+        return int(self._b.cardinalities()[0])
+
+    @property
+    def cardinality(self) -> int:
+        return len(self)
+
+    def __bool__(self) -> bool:
+        return int(self._b.container_counts()[0]) > 0
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, RoaringBitmap):
+            return NotImplemented
+        return bool(self._b.equal(other._b, [0], [0])[0])
+
+    def __repr__(self) -> str:
+        return f"RoaringBitmap(card={len(self)}, chunks={int(self._b.container_counts()[0])})"
+
+    def chunks(self) -> Iterator[tuple[int, Container]]:
+        keys, conts = chunks_from_wire(self.serialize())
+        return zip(keys, conts)
+
+    def __contains__(self, v: int) -> bool:
+        key, low = int(v) >> 16, int(v) & 0xFFFF
+        for k, c in self.chunks():
+            if k == key:
+                pos = container_positions(c)
+                i = int(np.searchsorted(pos, low))
+                return i < len(pos) and int(pos[i]) == low
+        return False
+
+    # ------------------------------------------------------------ iteration
+    def to_array(self) -> np.ndarray:
+        """All members, ascending, as uint32 (bitmap.py:136-144)."""
+        return self._b.to_arrays()[0].copy()
+
+    def __iter__(self) -> Iterator[int]:
+        return iter(self.to_array().tolist())
+
+    # ----------------------------------------------------------- set algebra
+    def op(self, op: str, other: "RoaringBitmap") -> "RoaringBitmap":
+        """and/or/andnot/xor between whole bitmaps; inputs untouched (bitmap.py:169-210)."""
+        op_index(op)
+        return RoaringBitmap._wrap(self._b.pairwise(op, other._b, [0], [0]))
+
+    def op_cardinality(self, op: str, other: "RoaringBitmap") -> int:
+        """Cardinality of op(self, other) without materializing it (bitmap.py:212-241)."""
+        op_index(op)
+        return int(self._b.pairwise_cardinality(op, other._b, [0], [0])[0])
+
+    def __and__(self, other):
+        return self.op("and", other)
+
+    def __or__(self, other):
+        return self.op("or", other)
+
+    def __sub__(self, other):
+        return self.op("andnot", other)
+
+    def __xor__(self, other):
+        return self.op("xor", other)
+
+    # ---------------------------------------------------------- wide unions
+    @staticmethod
+    def union_many(bitmaps: Iterable["RoaringBitmap"]) -> "RoaringBitmap":
+        """Sequential-fold semantics of bitmap.py:257-304, computed in one GPU pass."""
+        bitmaps = list(bitmaps)
+        if not bitmaps:
+            return RoaringBitmap()
+        batch = BitmapBatch.concat([b._b for b in bitmaps])
+        return RoaringBitmap._wrap(batch.union_many())
+
+    # ------------------------------------------------------- storage tuning
+    def run_optimize(self) -> bool:
+        """Re-pick each container's type with run candidacy (bitmap.py:308-316)."""
+        return bool(self._b.run_optimize()[0])
+
+    # ------------------------------------------------------------ validation
+    def validate(self) -> None:
+        """Raise AssertionError if a structural invariant is broken: the image is
+        re-ingested through the GPU decoder, which applies every serde check."""
+        try:
+            BitmapBatch.from_wire([self.serialize()])
+        except DecodeError as e:
+            raise AssertionError(str(e)) from None
+
+
+__all__ = ["RoaringBitmap", "OPS"]

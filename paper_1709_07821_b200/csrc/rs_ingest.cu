@@ -1,0 +1,607 @@
+// rs_ingest.cu -- batch construction: wire images (serde.deserialize) and
+// uint32 values (RoaringBitmap.from_values), plus concat / select copies.
+#include <cub/cub.cuh>
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include "rs_internal.cuh"
+
+using namespace rs;
+
+namespace {
+
+// ------------------------------------------------------------- wire ingest
+
+enum : uint8_t {
+  V_OK = 0,
+  V_ARRAY_ORDER = 1,
+  V_BITSET_CARD = 2,
+  V_BITSET_SMALL = 3,
+  V_RUN_ESCAPE = 4,
+  V_RUN_OVERLAP = 5,
+  V_RUN_CARD = 6,
+  V_RUN_ADMISSIBLE = 7
+};
+
+// Copy nbytes (even) from a 2-byte aligned source to a 16-byte aligned
+// destination with the widest access both allow; zero the 16-byte pad tail.
+__device__ void warp_copy_payload(uint8_t *__restrict__ dst, const uint8_t *__restrict__ src,
+                                  uint32_t nbytes, int lane) {
+  uintptr_t s = (uintptr_t)src;
+  if ((s & 15) == 0) {
+    uint32_t nv = nbytes >> 4;
+    for (uint32_t i = lane; i < nv; i += 32) ((uint4 *)dst)[i] = ((const uint4 *)src)[i];
+    for (uint32_t i = (nv << 3) + lane; i < (nbytes >> 1); i += 32)
+      ((uint16_t *)dst)[i] = ((const uint16_t *)src)[i];
+  } else if ((s & 7) == 0) {
+    uint32_t nv = nbytes >> 3;
+    for (uint32_t i = lane; i < nv; i += 32) ((uint64_t *)dst)[i] = ((const uint64_t *)src)[i];
+    for (uint32_t i = (nv << 2) + lane; i < (nbytes >> 1); i += 32)
+      ((uint16_t *)dst)[i] = ((const uint16_t *)src)[i];
+  } else if ((s & 3) == 0) {
+    uint32_t nv = nbytes >> 2;
+    for (uint32_t i = lane; i < nv; i += 32) ((uint32_t *)dst)[i] = ((const uint32_t *)src)[i];
+    for (uint32_t i = (nv << 1) + lane; i < (nbytes >> 1); i += 32)
+      ((uint16_t *)dst)[i] = ((const uint16_t *)src)[i];
+  } else {
+    for (uint32_t i = lane; i < (nbytes >> 1); i += 32) ((uint16_t *)dst)[i] = ((const uint16_t *)src)[i];
+  }
+  uint32_t padded = (uint32_t)rs_pad16(nbytes);
+  for (uint32_t i = (nbytes >> 1) + lane; i < (padded >> 1); i += 32) ((uint16_t *)dst)[i] = 0;
+}
+
+// One warp per container: copy the payload from the staged wire bytes into
+// the aligned pool and run the payload checks of serde.deserialize
+// (serde.py:122-164) in the reference's order.
+__global__ void k_wire_gather_validate(uint64_t nc, uint64_t nvalidate, const uint8_t *__restrict__ staged,
+                                       const uint64_t *__restrict__ src_off, DevBatch B,
+                                       uint8_t *__restrict__ pool, uint8_t *__restrict__ vcode,
+                                       uint32_t *__restrict__ vval, int *__restrict__ any_err) {
+  uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (c >= nc) return;
+  uint8_t t = B.type[c];
+  uint32_t n = B.n[c], card = B.card[c];
+  const uint8_t *src = staged + src_off[c];
+  warp_copy_payload(pool + B.off[c], src, rs_payload_bytes(t, n), lane);
+  if (c >= nvalidate) return;
+  const uint16_t *s16 = (const uint16_t *)src;
+  uint8_t code = V_OK;
+  uint32_t val = 0;
+  if (t == RS_TAG_ARRAY) {
+    bool bad = false;
+    for (uint32_t i = 1 + lane; i < n; i += 32) bad |= s16[i] <= s16[i - 1];
+    if (__any_sync(0xffffffffu, bad)) code = V_ARRAY_ORDER;
+  } else if (t == RS_TAG_BITSET) {
+    uint32_t pc = 0;
+    for (uint32_t i = lane; i < 2048; i += 32) pc += __popc((uint32_t)s16[2 * i] | ((uint32_t)s16[2 * i + 1] << 16));
+    for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    if (pc != card) { code = V_BITSET_CARD; val = pc; }
+    else if (card <= RS_ARRAY_MAX) code = V_BITSET_SMALL;
+  } else {
+    bool esc = false, ovl = false;
+    uint32_t sum = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+      uint32_t st = s16[2 * i], ln = s16[2 * i + 1];
+      esc |= st + ln > 0xFFFFu;
+      if (i > 0) ovl |= !(st > (uint32_t)s16[2 * i - 2] + s16[2 * i - 1] + 1);
+      sum += ln;
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (__any_sync(0xffffffffu, esc)) code = V_RUN_ESCAPE;
+    else if (__any_sync(0xffffffffu, ovl)) code = V_RUN_OVERLAP;
+    else if (sum + n != card) { code = V_RUN_CARD; val = sum + n; }
+    else if (!rs_run_admissible(card, n)) code = V_RUN_ADMISSIBLE;
+  }
+  if (lane == 0) {
+    vcode[c] = code;
+    vval[c] = val;
+    if (code) atomicOr(any_err, 1);
+  }
+}
+
+struct WireErr {
+  bool set = false;
+  uint64_t image = 0, container = 0;  // container: global index where payload checks stop
+  bool descriptor_stage = false;
+  int64_t offset = 0;
+  std::string msg;
+};
+
+static inline uint16_t g16(const uint8_t *p) { return (uint16_t)(p[0] | (p[1] << 8)); }
+static inline uint32_t g32(const uint8_t *p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+}  // namespace
+
+extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint64_t n,
+                                  rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  // ---- host walk of the descriptor sections (serde.py:87-169 structure).
+  std::vector<uint64_t> bm_start(n + 1, 0);
+  std::vector<uint16_t> key;
+  std::vector<uint8_t> type;
+  std::vector<uint32_t> card, cnt;
+  std::vector<uint64_t> src, poff;
+  uint64_t pool = 0;
+  WireErr err;
+  char msg[256];
+  for (uint64_t i = 0; i < n && !err.set; i++) {
+    const uint8_t *d = buf + offs[i];
+    uint64_t len = offs[i + 1] - offs[i], off = 0, start = 0;
+    uint64_t first_c = key.size();
+    bm_start[i] = first_c;
+    auto fail = [&](int64_t o, bool desc_stage) {
+      err.set = true;
+      err.image = i;
+      err.container = key.size();
+      err.descriptor_stage = desc_stage;
+      err.offset = o;
+      err.msg = msg;
+    };
+    auto need = [&](uint64_t nb, const char *what, bool desc_stage) -> bool {
+      if (len - off < nb) {
+        snprintf(msg, sizeof msg, "truncated %s: need %llu bytes, have %llu", what,
+                 (unsigned long long)nb, (unsigned long long)(len - off));
+        fail((int64_t)off, desc_stage);
+        return false;
+      }
+      start = off;
+      off += nb;
+      return true;
+    };
+    if (!need(4, "magic", true)) break;
+    if (memcmp(d, "ROAR", 4) != 0) { snprintf(msg, sizeof msg, "bad magic"); fail(0, true); break; }
+    if (!need(4, "container count", true)) break;
+    uint32_t count = g32(d + start);
+    std::vector<uint16_t> dk;
+    std::vector<uint8_t> dt;
+    std::vector<uint32_t> dc;
+    int64_t prev_key = -1;
+    bool ok = true;
+    for (uint32_t k = 0; k < count; k++) {
+      if (!need(8, "descriptor", true)) { ok = false; break; }
+      uint16_t kk = g16(d + start);
+      uint8_t tag = d[start + 2], pad = d[start + 3];
+      uint32_t cc = g32(d + start + 4);
+      if (pad != 0) { snprintf(msg, sizeof msg, "nonzero descriptor pad"); fail(start + 3, true); ok = false; break; }
+      if (tag < 1 || tag > 3) { snprintf(msg, sizeof msg, "unknown container type %u", tag); fail(start + 2, true); ok = false; break; }
+      if ((int64_t)kk <= prev_key) { snprintf(msg, sizeof msg, "keys not strictly increasing at %u", kk); fail(start, true); ok = false; break; }
+      prev_key = kk;
+      dk.push_back(kk); dt.push_back(tag); dc.push_back(cc);
+    }
+    if (!ok) break;
+    for (uint32_t k = 0; k < count; k++) {
+      uint32_t cc = dc[k], nn;
+      if (dt[k] == RS_TAG_ARRAY) {
+        if (!(cc >= 1 && cc <= RS_ARRAY_MAX)) {
+          snprintf(msg, sizeof msg, "array cardinality %u out of range", cc);
+          fail((int64_t)off, false); ok = false; break;
+        }
+        if (!need(2ull * cc, "array payload", false)) { ok = false; break; }
+        nn = cc;
+      } else if (dt[k] == RS_TAG_BITSET) {
+        if (!need(8192, "bitset payload", false)) { ok = false; break; }
+        nn = RS_WORDS;
+      } else {
+        if (!need(2, "run count", false)) { ok = false; break; }
+        nn = g16(d + start);
+        if (nn == 0) { snprintf(msg, sizeof msg, "empty run container"); fail((int64_t)start, false); ok = false; break; }
+        if (!need(4ull * nn, "run payload", false)) { ok = false; break; }
+      }
+      key.push_back(dk[k]); type.push_back(dt[k]); card.push_back(cc); cnt.push_back(nn);
+      src.push_back(offs[i] + start);
+      poff.push_back(pool);
+      pool += rs_pad16(rs_payload_bytes(dt[k], nn));
+    }
+    if (!ok) break;
+    if (off != len) {
+      snprintf(msg, sizeof msg, "%llu trailing bytes", (unsigned long long)(len - off));
+      fail((int64_t)off, false);
+      break;
+    }
+  }
+  uint64_t nc = key.size();
+  uint64_t nb_built = err.set ? err.image + 1 : n;
+  for (uint64_t i = nb_built; i <= n; i++) bm_start[i] = nc;
+  if (err.set) bm_start[err.image + 1] = nc;
+
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, n, nc, pool);
+  if (rc) { rs_batch_free(b); return rc; }
+  uint64_t stage_bytes = offs[n] - offs[0];
+  uint8_t *staged = (uint8_t *)dalloc(stage_bytes ? stage_bytes : 16);
+  uint64_t *d_src = (uint64_t *)dalloc((nc ? nc : 1) * 8);
+  uint8_t *d_vcode = (uint8_t *)dalloc(nc ? nc : 1);
+  uint32_t *d_vval = (uint32_t *)dalloc((nc ? nc : 1) * 4);
+  int *d_any = (int *)dalloc(sizeof(int));
+  if (!staged || !d_src || !d_vcode || !d_vval || !d_any) {
+    rs_batch_free(b);
+    dfree(staged); dfree(d_src); dfree(d_vcode); dfree(d_vval); dfree(d_any);
+    set_error("device allocation failed (wire ingest)");
+    return RS_ENOMEM;
+  }
+  for (uint64_t c = 0; c < nc; c++) src[c] -= offs[0];
+  RS_TRY(h2d(staged, buf + offs[0], stage_bytes));
+  RS_TRY(h2d(b->d_bm_start, bm_start.data(), (n + 1) * 8));
+  RS_TRY(h2d(b->d_key, key.data(), nc * 2));
+  RS_TRY(h2d(b->d_type, type.data(), nc));
+  RS_TRY(h2d(b->d_card, card.data(), nc * 4));
+  RS_TRY(h2d(b->d_n, cnt.data(), nc * 4));
+  RS_TRY(h2d(b->d_off, poff.data(), nc * 8));
+  RS_TRY(h2d(d_src, src.data(), nc * 8));
+  RS_CK(cudaMemsetAsync(d_any, 0, sizeof(int), g_stream));
+  RS_LAUNCH(k_wire_gather_validate, (unsigned)((nc * 32 + 255) / 256), 256, 0, nc, nc, staged, d_src,
+            b->dev(), b->d_pool, d_vcode, d_vval, d_any);
+  int any = 0;
+  RS_TRY(d2h(&any, d_any, sizeof(int)));
+  // The host walk must finish before the (pageable) host vectors go away:
+  // d2h above synchronized the stream.
+  int result = RS_OK;
+  if (any || err.set) {
+    // first failing image in order: payload errors before the host error win
+    std::vector<uint8_t> vcode(nc);
+    std::vector<uint32_t> vval(nc);
+    if (any) {
+      RS_TRY(d2h(vcode.data(), d_vcode, nc));
+      RS_TRY(d2h(vval.data(), d_vval, nc * 4));
+    }
+    bool found = false;
+    for (uint64_t c = 0; any && c < nc && !found; c++) {
+      if (!vcode[c]) continue;
+      uint64_t img = std::upper_bound(bm_start.begin(), bm_start.begin() + nb_built + 1, c) - bm_start.begin() - 1;
+      if (err.set && img > err.image) break;
+      uint64_t at = src[c] - (offs[img] - offs[0]);  // payload start inside the image
+      switch (vcode[c]) {
+        case V_ARRAY_ORDER: snprintf(msg, sizeof msg, "array values not strictly increasing"); break;
+        case V_BITSET_CARD: snprintf(msg, sizeof msg, "cardinality mismatch: descriptor says %u, payload holds %u", card[c], vval[c]); break;
+        case V_BITSET_SMALL: snprintf(msg, sizeof msg, "bitset container with only %u values", card[c]); break;
+        case V_RUN_ESCAPE: snprintf(msg, sizeof msg, "run escapes the 16-bit chunk"); break;
+        case V_RUN_OVERLAP: snprintf(msg, sizeof msg, "runs overlap or are adjacent"); break;
+        case V_RUN_CARD: snprintf(msg, sizeof msg, "cardinality mismatch: descriptor says %u, runs hold %u", card[c], vval[c]); break;
+        default: snprintf(msg, sizeof msg, "run form is not the smallest representation"); break;
+      }
+      std::string full = "at byte " + std::to_string(at) + ": " + msg;
+      set_error(full, (int64_t)at, (int64_t)img);
+      found = true;
+    }
+    if (!found) {
+      std::string full = "at byte " + std::to_string(err.offset) + ": " + err.msg;
+      set_error(full, err.offset, (int64_t)err.image);
+    }
+    result = RS_EDECODE;
+  }
+  dfree(staged); dfree(d_src); dfree(d_vcode); dfree(d_vval); dfree(d_any);
+  if (result != RS_OK) { rs_batch_free(b); return result; }
+  b->h_bm_start = bm_start;
+  b->h_valid = true;
+  RS_TRY(finalize_batch(b));
+  *out = b;
+  return RS_OK;
+}
+
+// --------------------------------------------------------- from_values ingest
+
+namespace {
+
+__global__ void k_mark_seg(uint64_t n, const uint64_t *__restrict__ offs, uint8_t *__restrict__ segstart) {
+  uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b < n && offs[b] < offs[b + 1]) segstart[offs[b]] = 1;
+}
+
+__global__ void k_check_sorted(uint64_t V, const uint32_t *__restrict__ v, const uint8_t *__restrict__ segstart,
+                               int *__restrict__ unsorted) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < V && i > 0 && !segstart[i] && v[i] <= v[i - 1]) atomicOr(unsorted, 1);
+}
+
+// warp per bitmap writes key = seg << 32 | value
+__global__ void k_make_keys(uint64_t n, const uint64_t *__restrict__ offs, const uint32_t *__restrict__ v,
+                            uint64_t *__restrict__ keys) {
+  uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  for (uint64_t i = offs[w] + lane; i < offs[w + 1]; i += 32) keys[i] = (w << 32) | v[i];
+}
+
+__global__ void k_unique_flags(uint64_t V, const uint64_t *__restrict__ keys, uint64_t *__restrict__ flag) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < V) flag[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_unique_scatter(uint64_t V, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ flag,
+                                 const uint64_t *__restrict__ pos, uint32_t *__restrict__ v_out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < V && flag[i]) v_out[pos[i]] = (uint32_t)keys[i];
+}
+
+// new segment offsets: offs[b] = #unique keys with segment < b
+__global__ void k_seg_offsets(uint64_t n, uint64_t V, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ flag,
+                              const uint64_t *__restrict__ pos, uint64_t U, uint64_t *__restrict__ offs) {
+  uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b > n) return;
+  // lower_bound over sorted keys for b << 32
+  uint64_t lo = 0, hi = V, target = b << 32;
+  while (lo < hi) {
+    uint64_t m = (lo + hi) >> 1;
+    if (keys[m] < target) lo = m + 1; else hi = m;
+  }
+  offs[b] = lo < V ? pos[lo] : U;
+}
+
+// chunk starts: value i starts a container if it starts its bitmap or its
+// high 16 bits differ from the previous value's
+__global__ void k_chunk_flags(uint64_t V, const uint32_t *__restrict__ v, const uint8_t *__restrict__ segstart,
+                              uint64_t *__restrict__ flag) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < V) flag[i] = (i == 0 || segstart[i] || (v[i] >> 16) != (v[i - 1] >> 16)) ? 1 : 0;
+}
+
+__global__ void k_chunk_starts(uint64_t V, const uint64_t *__restrict__ flag, const uint64_t *__restrict__ cpos,
+                               const uint32_t *__restrict__ v, uint64_t *__restrict__ cstart,
+                               uint16_t *__restrict__ key) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < V && flag[i]) {
+    cstart[cpos[i]] = i;
+    key[cpos[i]] = (uint16_t)(v[i] >> 16);
+  }
+}
+
+__global__ void k_chunk_meta(uint64_t C, uint64_t V, uint64_t *__restrict__ cstart, uint8_t *__restrict__ type,
+                             uint32_t *__restrict__ card, uint32_t *__restrict__ nn, uint64_t *__restrict__ psize) {
+  uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  uint64_t e = c + 1 < C ? cstart[c + 1] : V;
+  uint32_t k = (uint32_t)(e - cstart[c]);
+  card[c] = k;
+  // bitmap.py:55-59: array if <= ARRAY_MAX values, else bitset_from_positions
+  if (k <= RS_ARRAY_MAX) { type[c] = RS_TAG_ARRAY; nn[c] = k; psize[c] = rs_pad16(2ull * k); }
+  else { type[c] = RS_TAG_BITSET; nn[c] = RS_WORDS; psize[c] = 8192; }
+}
+
+__global__ void k_bm_start_from_values(uint64_t n, uint64_t V, uint64_t C, const uint64_t *__restrict__ offs,
+                                       const uint64_t *__restrict__ cpos, uint64_t *__restrict__ bm_start) {
+  uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (b <= n) bm_start[b] = offs[b] < V ? cpos[offs[b]] : C;
+}
+
+// one CTA per container: arrays copy low halves; bitsets build in smem
+__global__ void __launch_bounds__(256) k_fill_from_values(uint64_t C, uint64_t V, const uint32_t *__restrict__ v,
+                                                          const uint64_t *__restrict__ cstart, DevBatch B,
+                                                          uint8_t *__restrict__ pool) {
+  __shared__ uint32_t bits[2048];
+  uint64_t c = blockIdx.x;
+  if (c >= C) return;
+  uint64_t s = cstart[c];
+  uint32_t k = B.card[c];
+  uint8_t *dst = pool + B.off[c];
+  if (B.type[c] == RS_TAG_ARRAY) {
+    uint16_t *d16 = (uint16_t *)dst;
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) d16[i] = (uint16_t)(v[s + i] & 0xFFFF);
+    uint32_t padded = (uint32_t)rs_pad16(2ull * k) >> 1;
+    for (uint32_t i = k + threadIdx.x; i < padded; i += blockDim.x) d16[i] = 0;
+    return;
+  }
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+    uint32_t lo = v[s + i] & 0xFFFF;
+    atomicOr(&bits[lo >> 5], 1u << (lo & 31));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) ((uint4 *)dst)[i] = ((const uint4 *)bits)[i];
+}
+
+}  // namespace
+
+extern "C" int rs_batch_from_u32(const uint32_t *vals, const uint64_t *offs, uint64_t n, int on_device,
+                                 rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  uint64_t V;
+  std::vector<uint64_t> h_offs(n + 1);
+  if (on_device) RS_TRY(d2h(h_offs.data(), offs, (n + 1) * 8));
+  else memcpy(h_offs.data(), offs, (n + 1) * 8);
+  uint64_t base = h_offs[0];
+  for (auto &o : h_offs) o -= base;
+  V = h_offs[n];
+  uint64_t *d_offs = (uint64_t *)dalloc((n + 1) * 8);
+  uint32_t *d_v = (uint32_t *)dalloc((V ? V : 1) * 4);
+  uint8_t *segstart = (uint8_t *)dalloc(V ? V : 1);
+  int *d_flag = (int *)dalloc(sizeof(int));
+  if (!d_offs || !d_v || !segstart || !d_flag) { set_error("device allocation failed (from_values)"); return RS_ENOMEM; }
+  RS_TRY(h2d(d_offs, h_offs.data(), (n + 1) * 8));
+  if (V) {
+    if (on_device) RS_CK(cudaMemcpyAsync(d_v, vals + base, V * 4, cudaMemcpyDeviceToDevice, g_stream));
+    else RS_TRY(h2d(d_v, vals + base, V * 4));
+  }
+  RS_CK(cudaMemsetAsync(segstart, 0, V ? V : 1, g_stream));
+  RS_CK(cudaMemsetAsync(d_flag, 0, sizeof(int), g_stream));
+  unsigned gb = (unsigned)((n + 255) / 256), gv = (unsigned)((V + 255) / 256);
+  RS_LAUNCH(k_mark_seg, gb, 256, 0, n, d_offs, segstart);
+  RS_LAUNCH(k_check_sorted, gv, 256, 0, V, d_v, segstart, d_flag);
+  int unsorted = 0;
+  RS_TRY(d2h(&unsorted, d_flag, sizeof(int)));
+  if (unsorted) {
+    // np.unique per bitmap: radix sort of (bitmap << 32 | value), then dedup
+    uint64_t *keys = (uint64_t *)dalloc(V * 8), *flag = (uint64_t *)dalloc((V + 1) * 8),
+             *pos = (uint64_t *)dalloc((V + 1) * 8);
+    if (!keys || !flag || !pos) { set_error("device allocation failed (from_values sort)"); return RS_ENOMEM; }
+    RS_LAUNCH(k_make_keys, (unsigned)((n * 32 + 255) / 256), 256, 0, n, d_offs, d_v, keys);
+    int segbits = 1;
+    while ((1ull << segbits) <= n) segbits++;
+    RS_TRY(sort_u64(keys, V, 32 + segbits));
+    RS_LAUNCH(k_unique_flags, gv, 256, 0, V, keys, flag);
+    RS_TRY(scan_exclusive<uint64_t>(flag, pos, V));
+    uint64_t last[2];
+    RS_TRY(d2h(&last[0], pos + V - 1, 8));
+    RS_TRY(d2h(&last[1], flag + V - 1, 8));
+    uint64_t U = last[0] + last[1];
+    RS_LAUNCH(k_unique_scatter, gv, 256, 0, V, keys, flag, pos, d_v);
+    RS_LAUNCH(k_seg_offsets, (unsigned)((n + 1 + 255) / 256), 256, 0, n, V, keys, flag, pos, U, d_offs);
+    RS_TRY(d2h(h_offs.data(), d_offs, (n + 1) * 8));
+    V = U;
+    dfree(keys); dfree(flag); dfree(pos);
+    RS_CK(cudaMemsetAsync(segstart, 0, V ? V : 1, g_stream));
+    RS_LAUNCH(k_mark_seg, gb, 256, 0, n, d_offs, segstart);
+    gv = (unsigned)((V + 255) / 256);
+  }
+  // containers
+  uint64_t *cflag = (uint64_t *)dalloc((V + 1) * 8), *cpos = (uint64_t *)dalloc((V + 1) * 8);
+  if (!cflag || !cpos) { set_error("device allocation failed (from_values)"); return RS_ENOMEM; }
+  RS_LAUNCH(k_chunk_flags, gv, 256, 0, V, d_v, segstart, cflag);
+  RS_TRY(scan_exclusive<uint64_t>(cflag, cpos, V));
+  uint64_t C = 0;
+  if (V) {
+    uint64_t t[2];
+    RS_TRY(d2h(&t[0], cpos + V - 1, 8));
+    RS_TRY(d2h(&t[1], cflag + V - 1, 8));
+    C = t[0] + t[1];
+  }
+  rs_batch *b = new rs_batch();
+  // pool size needs the container types: allocate metadata first
+  uint64_t *cstart = (uint64_t *)dalloc((C ? C : 1) * 8), *psize = (uint64_t *)dalloc((C + 1) * 8);
+  b->nb = n; b->nc = C; b->cap_c = C;
+  b->d_bm_start = (uint64_t *)dalloc((n + 1) * 8);
+  b->d_bm_card = (uint64_t *)dalloc((n + 1) * 8);
+  b->d_key = (uint16_t *)dalloc((C ? C : 1) * 2);
+  b->d_type = (uint8_t *)dalloc(C ? C : 1);
+  b->d_card = (uint32_t *)dalloc((C ? C : 1) * 4);
+  b->d_n = (uint32_t *)dalloc((C ? C : 1) * 4);
+  b->d_off = (uint64_t *)dalloc((C + 1) * 8);
+  if (!cstart || !psize || !b->d_bm_start || !b->d_bm_card || !b->d_key || !b->d_type || !b->d_card ||
+      !b->d_n || !b->d_off) {
+    rs_batch_free(b);
+    set_error("device allocation failed (from_values)");
+    return RS_ENOMEM;
+  }
+  RS_LAUNCH(k_chunk_starts, gv, 256, 0, V, cflag, cpos, d_v, cstart, b->d_key);
+  RS_LAUNCH(k_chunk_meta, (unsigned)((C + 255) / 256), 256, 0, C, V, cstart, b->d_type, b->d_card, b->d_n, psize);
+  RS_LAUNCH(k_bm_start_from_values, (unsigned)((n + 1 + 255) / 256), 256, 0, n, V, C, d_offs, cpos, b->d_bm_start);
+  RS_TRY(scan_exclusive<uint64_t>(psize, b->d_off, C + 1));
+  uint64_t P = 0;
+  RS_TRY(d2h(&P, b->d_off + C, 8));
+  b->pool_bytes = P;
+  b->d_pool = (uint8_t *)dalloc(P ? P : 16);
+  if (!b->d_pool) { rs_batch_free(b); set_error("device allocation failed (from_values pool)"); return RS_ENOMEM; }
+  RS_LAUNCH(k_fill_from_values, (unsigned)C, 256, 0, C, V, d_v, cstart, b->dev(), b->d_pool);
+  dfree(cflag); dfree(cpos); dfree(cstart); dfree(psize); dfree(d_offs); dfree(d_v); dfree(segstart); dfree(d_flag);
+  RS_TRY(finalize_batch(b));
+  b->h_valid = false;
+  RS_TRY(fetch_host_meta(b));
+  *out = b;
+  return RS_OK;
+}
+
+// ------------------------------------------------------------ concat / select
+
+namespace {
+__global__ void k_shift_u64(uint64_t n, const uint64_t *__restrict__ in, uint64_t add, uint64_t *__restrict__ out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i] + add;
+}
+
+// new container j of the selection: copy metadata + payload (warp per container)
+__global__ void k_select_copy(uint64_t nc_new, uint64_t nb_new, const uint64_t *__restrict__ new_start,
+                              const uint64_t *__restrict__ src_start, DevBatch S, const uint64_t *__restrict__ new_off,
+                              uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn, uint64_t *off,
+                              uint8_t *__restrict__ pool) {
+  uint64_t j = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (j >= nc_new) return;
+  uint64_t lo = 0, hi = nb_new;  // bitmap k with new_start[k] <= j < new_start[k+1]
+  while (hi - lo > 1) {
+    uint64_t m = (lo + hi) >> 1;
+    if (new_start[m] <= j) lo = m; else hi = m;
+  }
+  uint64_t s = src_start[lo] + (j - new_start[lo]);
+  uint32_t bytes = (uint32_t)rs_pad16(rs_payload_bytes(S.type[s], S.n[s]));
+  const uint4 *src = (const uint4 *)(S.pool + S.off[s]);
+  uint4 *dst = (uint4 *)(pool + new_off[j]);
+  for (uint32_t i = lane; i < (bytes >> 4); i += 32) dst[i] = src[i];
+  if (lane == 0) {
+    key[j] = S.key[s]; type[j] = S.type[s]; card[j] = S.card[s]; nn[j] = S.n[s]; off[j] = new_off[j];
+  }
+}
+
+__global__ void k_select_sizes(uint64_t nc_new, uint64_t nb_new, const uint64_t *__restrict__ new_start,
+                               const uint64_t *__restrict__ src_start, DevBatch S, uint64_t *__restrict__ psize) {
+  uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (j > nc_new) return;
+  if (j == nc_new) { psize[j] = 0; return; }
+  uint64_t lo = 0, hi = nb_new;
+  while (hi - lo > 1) {
+    uint64_t m = (lo + hi) >> 1;
+    if (new_start[m] <= j) lo = m; else hi = m;
+  }
+  uint64_t s = src_start[lo] + (j - new_start[lo]);
+  psize[j] = rs_pad16(rs_payload_bytes(S.type[s], S.n[s]));
+}
+}  // namespace
+
+extern "C" int rs_batch_concat(const rs_batch *const *parts, uint64_t nparts, rs_batch **out) {
+  RS_TRY(ensure_device());
+  uint64_t nb = 0, nc = 0, pool = 0;
+  for (uint64_t k = 0; k < nparts; k++) {
+    RS_TRY(fetch_host_meta(parts[k]));
+    nb += parts[k]->nb; nc += parts[k]->nc; pool += parts[k]->pool_bytes;
+  }
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, nb, nc, pool);
+  if (rc) { rs_batch_free(b); return rc; }
+  b->h_bm_start.assign(1, 0);
+  uint64_t cb = 0, bb = 0, pb = 0;
+  for (uint64_t k = 0; k < nparts; k++) {
+    const rs_batch *p = parts[k];
+    RS_LAUNCH(k_shift_u64, (unsigned)((p->nb + 1 + 255) / 256), 256, 0, p->nb + 1, p->d_bm_start, cb, b->d_bm_start + bb);
+    RS_LAUNCH(k_shift_u64, (unsigned)((p->nc + 255) / 256), 256, 0, p->nc, p->d_off, pb, b->d_off + cb);
+    if (p->nc) {
+      RS_CK(cudaMemcpyAsync(b->d_key + cb, p->d_key, p->nc * 2, cudaMemcpyDeviceToDevice, g_stream));
+      RS_CK(cudaMemcpyAsync(b->d_type + cb, p->d_type, p->nc, cudaMemcpyDeviceToDevice, g_stream));
+      RS_CK(cudaMemcpyAsync(b->d_card + cb, p->d_card, p->nc * 4, cudaMemcpyDeviceToDevice, g_stream));
+      RS_CK(cudaMemcpyAsync(b->d_n + cb, p->d_n, p->nc * 4, cudaMemcpyDeviceToDevice, g_stream));
+    }
+    if (p->pool_bytes) RS_CK(cudaMemcpyAsync(b->d_pool + pb, p->d_pool, p->pool_bytes, cudaMemcpyDeviceToDevice, g_stream));
+    if (p->nb) RS_CK(cudaMemcpyAsync(b->d_bm_card + bb, p->d_bm_card, p->nb * 8, cudaMemcpyDeviceToDevice, g_stream));
+    for (uint64_t i = 1; i <= p->nb; i++) b->h_bm_start.push_back(p->h_bm_start[i] + cb);
+    cb += p->nc; bb += p->nb; pb += p->pool_bytes;
+  }
+  b->h_valid = true;
+  *out = b;
+  return RS_OK;
+}
+
+extern "C" int rs_batch_select(const rs_batch *S, const uint64_t *idx, uint64_t n, rs_batch **out) {
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(S));
+  std::vector<uint64_t> new_start(n + 1, 0), src_start(n + 1, 0);
+  for (uint64_t k = 0; k < n; k++) {
+    if (idx[k] >= S->nb) { set_error("bitmap index out of range"); return RS_EARG; }
+    src_start[k] = S->h_bm_start[idx[k]];
+    new_start[k + 1] = new_start[k] + (S->h_bm_start[idx[k] + 1] - S->h_bm_start[idx[k]]);
+  }
+  uint64_t nc = new_start[n];
+  uint64_t *d_ns = (uint64_t *)dalloc((n + 1) * 8), *d_ss = (uint64_t *)dalloc((n + 1) * 8);
+  uint64_t *psize = (uint64_t *)dalloc((nc + 1) * 8), *poff = (uint64_t *)dalloc((nc + 1) * 8);
+  if (!d_ns || !d_ss || !psize || !poff) { set_error("device allocation failed (select)"); return RS_ENOMEM; }
+  RS_TRY(h2d(d_ns, new_start.data(), (n + 1) * 8));
+  RS_TRY(h2d(d_ss, src_start.data(), (n + 1) * 8));
+  RS_LAUNCH(k_select_sizes, (unsigned)((nc + 1 + 255) / 256), 256, 0, nc, n, d_ns, d_ss, S->dev(), psize);
+  RS_TRY(scan_exclusive<uint64_t>(psize, poff, nc + 1));
+  uint64_t P = 0;
+  RS_TRY(d2h(&P, poff + nc, 8));
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, n, nc, P);
+  if (rc) { rs_batch_free(b); return rc; }
+  RS_CK(cudaMemcpyAsync(b->d_bm_start, d_ns, (n + 1) * 8, cudaMemcpyDeviceToDevice, g_stream));
+  RS_LAUNCH(k_select_copy, (unsigned)((nc * 32 + 255) / 256), 256, 0, nc, n, d_ns, d_ss, S->dev(), poff, b->d_key,
+            b->d_type, b->d_card, b->d_n, b->d_off, b->d_pool);
+  dfree(d_ns); dfree(d_ss); dfree(psize); dfree(poff);
+  RS_TRY(finalize_batch(b));
+  b->h_bm_start = new_start;
+  b->h_valid = true;
+  *out = b;
+  return RS_OK;
+}

@@ -1,0 +1,732 @@
+// rs_pairwise.cu -- the hot path: batched RoaringBitmap.op / op_cardinality
+// (bitmap.py:169-241) and container_pairwise[_cardinality]
+// (containers.py:450-570) over flattened device batches.
+//
+// Pipeline of one materialized batched op:
+//   k_pair_msize + scan      merged key-space size per bitmap pair
+//   k_merge                  merge-path join of the sorted u16 key arrays: one
+//                            thread per key, a binary search in the other side
+//                            gives its merged position and its match
+//   scans (keep, ub)         entry slot and upper-bound payload slot per output
+//   k_emit                   entry records + per-type-pair work lists
+//   per-class kernels        bitset x bitset (k_pair_dense<false>),
+//                            array x array (k_aa_merge),
+//                            everything else (k_pair_dense<true>: densify to
+//                            8 KB in smem, word op, popcount + run count,
+//                            exact result-type choice, encode), copies (k_copy)
+//   compaction               drop empty results, per-bitmap container ranges
+#include <cub/cub.cuh>
+#include <algorithm>
+#include "rs_internal.cuh"
+#include "rs_dense.cuh"
+
+using namespace rs;
+
+namespace {
+
+enum { CLS_COPY = 0, CLS_BB = 1, CLS_AA = 2, CLS_GEN = 3, NCLS = 4 };
+
+struct Entries {
+  uint16_t *key;
+  uint32_t *ca, *cb, *pair;
+  uint64_t *off;
+};
+
+struct OutDesc {
+  uint8_t *type;
+  uint32_t *card, *n;
+};
+
+struct Lists {
+  uint32_t *list[NCLS];
+  uint32_t *cnt;  // device counters [NCLS]
+  uint64_t cap;
+};
+
+__device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { return ia ? ia[p] : (uint32_t)p; }
+
+__device__ __forceinline__ int classify(uint8_t ta, uint8_t tb) {
+  if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
+  if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY) return CLS_AA;
+  return CLS_GEN;
+}
+
+// warp-aggregated append of `item` to list[cls]
+__device__ __forceinline__ void list_append(Lists L, int cls, bool active, uint32_t item) {
+  unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < NCLS; c++) {
+    unsigned m = __ballot_sync(0xffffffffu, active && cls == c);
+    if (!m) continue;
+    int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane == leader) base = atomicAdd(&L.cnt[c], (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (active && cls == c) L.list[c][base + __popc(m & ((1u << lane) - 1))] = item;
+  }
+}
+
+__global__ void k_pair_msize(uint64_t npairs, DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib,
+                             int count_mode, uint64_t *__restrict__ msz) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p > npairs) return;
+  if (p == npairs) { msz[p] = 0; return; }
+  uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+  uint64_t na = A.bm_start[a + 1] - A.bm_start[a];
+  uint64_t nb = B.bm_start[b + 1] - B.bm_start[b];
+  msz[p] = count_mode ? na : na + nb;
+}
+
+__device__ __forceinline__ uint64_t find_pair(const uint64_t *__restrict__ mbase, uint64_t npairs, uint64_t t) {
+  uint64_t lo = 0, hi = npairs;  // largest p with mbase[p] <= t
+  while (hi - lo > 1) {
+    uint64_t m = (lo + hi) >> 1;
+    if (mbase[m] <= t) lo = m; else hi = m;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t lower_bound16(const uint16_t *__restrict__ k, uint32_t n, uint16_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t m = (lo + hi) >> 1;
+    if (k[m] < x) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+__device__ __forceinline__ uint32_t upper_bound16(const uint16_t *__restrict__ k, uint32_t n, uint16_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t m = (lo + hi) >> 1;
+    if (k[m] <= x) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+// Merge-path join (bitmap.py:181-209 two-pointer walk, parallel form): thread
+// t owns one key of one side of one pair.  A keys land at i + #(B < key), B
+// keys at j + #(A <= key), so a matched B key sits right after its A partner
+// and is marked as a duplicate.  keep/ub are written at the merged position.
+__global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict__ mbase, DevBatch A, DevBatch B,
+                        const uint32_t *ia, const uint32_t *ib, int op, uint16_t *__restrict__ mkey,
+                        uint32_t *__restrict__ mca, uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
+                        uint32_t *__restrict__ keep, uint64_t *__restrict__ ub) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= M) return;
+  const bool keep_a = op != RS_OP_AND;                        // _KEEP_A, bitmap.py:21
+  const bool keep_b = op == RS_OP_OR || op == RS_OP_XOR;      // _KEEP_B, bitmap.py:22
+  uint64_t p = find_pair(mbase, npairs, t);
+  uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+  uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
+  uint32_t na = (uint32_t)(A.bm_start[a + 1] - a0), nb = (uint32_t)(B.bm_start[b + 1] - b0);
+  uint32_t l = (uint32_t)(t - mbase[p]);
+  if (l < na) {
+    uint16_t key = A.key[a0 + l];
+    uint32_t j = lower_bound16(B.key + b0, nb, key);
+    bool matched = j < nb && B.key[b0 + j] == key;
+    uint64_t pos = mbase[p] + l + j;
+    uint64_t ca = a0 + l;
+    mkey[pos] = key;
+    mca[pos] = (uint32_t)ca;
+    mcb[pos] = matched ? (uint32_t)(b0 + j) : RS_NONE;
+    mpair[pos] = (uint32_t)p;
+    bool k = matched || keep_a;
+    keep[pos] = k;
+    uint32_t u = 0;
+    if (matched) u = rs_result_ub(A.type[ca], A.card[ca], B.type[b0 + j], B.card[b0 + j], op);
+    else if (k) u = rs_payload_bytes(A.type[ca], A.n[ca]);
+    ub[pos] = rs_pad16(u);
+  } else {
+    uint32_t j = l - na;
+    uint16_t key = B.key[b0 + j];
+    uint32_t i = upper_bound16(A.key + a0, na, key);
+    bool matched = i > 0 && A.key[a0 + i - 1] == key;
+    uint64_t pos = mbase[p] + i + j;
+    bool k = !matched && keep_b;
+    keep[pos] = k;
+    ub[pos] = k ? rs_pad16(rs_payload_bytes(B.type[b0 + j], B.n[b0 + j])) : 0;
+    if (k) {
+      mkey[pos] = key;
+      mca[pos] = RS_NONE;
+      mcb[pos] = (uint32_t)(b0 + j);
+      mpair[pos] = (uint32_t)p;
+    }
+  }
+}
+
+__global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ epos,
+                       const uint64_t *__restrict__ uoff, const uint16_t *__restrict__ mkey,
+                       const uint32_t *__restrict__ mca, const uint32_t *__restrict__ mcb,
+                       const uint32_t *__restrict__ mpair, DevBatch A, DevBatch B, Entries E, Lists L) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool active = t < M && keep[t];
+  int cls = CLS_COPY;
+  uint32_t e = 0;
+  if (active) {
+    e = epos[t];
+    uint32_t ca = mca[t], cb = mcb[t];
+    E.key[e] = mkey[t];
+    E.ca[e] = ca;
+    E.cb[e] = cb;
+    E.pair[e] = mpair[t];
+    E.off[e] = uoff[t];
+    cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], B.type[cb]);
+  }
+  list_append(L, cls, active, e);
+}
+
+// per-pair first entry index (estart[npairs] = total entries)
+__global__ void k_estart(uint64_t npairs, const uint64_t *__restrict__ mbase, const uint32_t *__restrict__ epos,
+                         uint64_t *__restrict__ estart) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p <= npairs) estart[p] = epos[mbase[p]];
+}
+
+// ----------------------------------------------------------------- copies
+
+// Unmatched container kept by OR/XOR/ANDNOT: Container.copy() into the result
+// pool (bitmap.py:191-209).  One warp per container, 128-bit moves.
+__global__ void k_copy(const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                       Entries E, OutDesc O, uint8_t *__restrict__ opool, uint64_t *__restrict__ res_card) {
+  uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  uint32_t total = *cnt;
+  uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (; w < total; w += nw) {
+    uint32_t e = list[w];
+    uint32_t ca = E.ca[e];
+    const DevBatch &S = ca != RS_NONE ? A : B;
+    uint32_t c = ca != RS_NONE ? ca : E.cb[e];
+    uint8_t t = S.type[c];
+    uint32_t n = S.n[c], card = S.card[c];
+    uint32_t bytes = (uint32_t)rs_pad16(rs_payload_bytes(t, n));
+    const uint4 *src = (const uint4 *)(S.pool + S.off[c]);
+    uint4 *dst = (uint4 *)(opool + E.off[e]);
+    for (uint32_t i = lane; i < (bytes >> 4); i += 32) dst[i] = src[i];
+    if (lane == 0) {
+      O.type[e] = t;
+      O.card[e] = card;
+      O.n[e] = n;
+      atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+  }
+}
+
+// ------------------------------------------------- dense (8 KB) pair kernel
+
+using namespace rsd;
+
+// Materialized pair op over a work list.  GEN=false: bitset x bitset only
+// (bitset_op_with_count + _container_from_words, containers.py:463-465).
+// GEN=true: any matched pair; array/run sides are densified in smem first.
+template <bool GEN>
+__global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__restrict__ list, DevBatch A, DevBatch B,
+                                                   Entries E, OutDesc O, uint8_t *__restrict__ opool,
+                                                   uint64_t *__restrict__ res_card) {
+  __shared__ __align__(16) DenseSmem sm;
+  const int t = threadIdx.x;
+  const uint32_t e = list[blockIdx.x];
+  const uint32_t ca = E.ca[e], cb = E.cb[e];
+  uint8_t ta = RS_TAG_BITSET, tb = RS_TAG_BITSET;
+  uint64_t ra[4], rb[4];
+  if (!GEN) {
+    ld_words(A.pool, A.off[ca], t, ra);
+    ld_words(B.pool, B.off[cb], t, rb);
+  } else {
+    ta = A.type[ca];
+    tb = B.type[cb];
+    bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (da) sm.X[4 * t + k] = 0;
+      if (db) sm.Y[4 * t + k] = 0;
+    }
+    __syncthreads();
+    if (da) scatter_container(A, ca, ta, sm.X);
+    if (db) scatter_container(B, cb, tb, sm.Y);
+    __syncthreads();
+    if (da) { for (int k = 0; k < 4; k++) ra[k] = sm.X[4 * t + k]; } else ld_words(A.pool, A.off[ca], t, ra);
+    if (db) { for (int k = 0; k < 4; k++) rb[k] = sm.Y[4 * t + k]; } else ld_words(B.pool, B.off[cb], t, rb);
+  }
+  uint64_t r[4];
+  uint32_t pc = 0, nr = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    r[k] = rs_word_op(op, ra[k], rb[k]);
+    pc += __popcll(r[k]);
+  }
+  const bool consider = GEN && rs_consider_run(ta, tb, op);
+  if (consider) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) sm.X[4 * t + k] = r[k];
+    __syncthreads();
+    uint64_t prev = t ? sm.X[4 * t - 1] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      uint64_t cin = (k ? r[k - 1] : prev) >> 63;
+      nr += __popcll(r[k] & ~((r[k] << 1) | cin));  // _run_count_of_words, containers.py:173-178
+    }
+  }
+  uint32_t card = pc, nruns = nr;
+  block_sum2(card, nruns, sm.red);
+  uint8_t type;
+  if (card == 0) type = RS_TAG_ARRAY;
+  else if (consider && rs_run_admissible(card, nruns)) type = RS_TAG_RUN;  // container_normalize
+  else type = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;       // from_words / from_values
+  uint32_t n = 0;
+  if (card) {
+    __syncthreads();  // smem Y may still be read by the densify phase
+    n = encode_result(sm, r, pc, card, type, opool + E.off[e]);
+  }
+  if (t == 0) {
+    O.type[e] = type;
+    O.card[e] = card;
+    O.n[e] = n;
+    if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+  }
+}
+
+// Count-only: |a AND b| accumulated per bitmap pair (container_pairwise_cardinality
+// "and", bitmap.py:225-234).  Persistent over the device-sized work list.
+template <bool GEN>
+__global__ void __launch_bounds__(DT) k_pair_count(int op, const uint32_t *__restrict__ lca, const uint32_t *__restrict__ lcb,
+                                                   const uint32_t *__restrict__ lpair, const uint32_t *__restrict__ cnt,
+                                                   DevBatch A, DevBatch B, uint64_t *__restrict__ acc) {
+  __shared__ __align__(16) uint64_t X[RS_WORDS];
+  __shared__ __align__(16) uint64_t Y[RS_WORDS];
+  __shared__ uint32_t red[DT / 32][2];
+  const int t = threadIdx.x;
+  const uint32_t total = *cnt;
+  for (uint32_t i = blockIdx.x; i < total; i += gridDim.x) {
+    const uint32_t ca = lca[i], cb = lcb[i];
+    uint64_t ra[4], rb[4];
+    if (!GEN) {
+      ld_words(A.pool, A.off[ca], t, ra);
+      ld_words(B.pool, B.off[cb], t, rb);
+    } else {
+      uint8_t ta = A.type[ca], tb = B.type[cb];
+      bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
+      for (int k = 0; k < 4; k++) {
+        if (da) X[4 * t + k] = 0;
+        if (db) Y[4 * t + k] = 0;
+      }
+      __syncthreads();
+      if (da) scatter_container(A, ca, ta, X);
+      if (db) scatter_container(B, cb, tb, Y);
+      __syncthreads();
+      if (da) { for (int k = 0; k < 4; k++) ra[k] = X[4 * t + k]; } else ld_words(A.pool, A.off[ca], t, ra);
+      if (db) { for (int k = 0; k < 4; k++) rb[k] = Y[4 * t + k]; } else ld_words(B.pool, B.off[cb], t, rb);
+    }
+    uint32_t pc = 0, z = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) pc += __popcll(rs_word_op(op, ra[k], rb[k]));
+    block_sum2(pc, z, red);
+    if (t == 0 && pc) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)pc);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ compaction
+
+__global__ void k_keep_nonempty(uint64_t E, const uint32_t *__restrict__ card, uint32_t *__restrict__ keep) {
+  uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (e <= E) keep[e] = e < E && card[e] > 0;
+}
+
+__global__ void k_compact(uint64_t E, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ fpos, Entries En,
+                          OutDesc O, uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn, uint64_t *off) {
+  uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (e >= E || !keep[e]) return;
+  uint32_t f = fpos[e];
+  key[f] = En.key[e];
+  type[f] = O.type[e];
+  card[f] = O.card[e];
+  nn[f] = O.n[e];
+  off[f] = En.off[e];
+}
+
+__global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ estart, const uint32_t *__restrict__ fpos,
+                           uint64_t *__restrict__ bm_start) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p <= npairs) bm_start[p] = fpos[estart[p]];
+}
+
+// -------------------------------------------------- count-only join + formula
+
+__global__ void k_match(uint64_t Ma, uint64_t npairs, const uint64_t *__restrict__ mbase, DevBatch A, DevBatch B,
+                        const uint32_t *ia, const uint32_t *ib, Lists L, uint32_t *__restrict__ lcb_base,
+                        uint32_t *__restrict__ lpair_base) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool active = false;
+  int cls = CLS_GEN;
+  uint32_t ca = 0, cb = 0, p32 = 0;
+  if (t < Ma) {
+    uint64_t p = find_pair(mbase, npairs, t);
+    uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+    uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
+    uint32_t nb = (uint32_t)(B.bm_start[b + 1] - b0);
+    uint32_t l = (uint32_t)(t - mbase[p]);
+    uint16_t key = A.key[a0 + l];
+    uint32_t j = lower_bound16(B.key + b0, nb, key);
+    if (j < nb && B.key[b0 + j] == key) {
+      active = true;
+      ca = (uint32_t)(a0 + l);
+      cb = (uint32_t)(b0 + j);
+      p32 = (uint32_t)p;
+      cls = classify(A.type[ca], B.type[cb]);
+    }
+  }
+  // append (ca) to the class list; cb/pair go to parallel arrays at the same slot
+  unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 1; c < NCLS; c++) {
+    unsigned m = __ballot_sync(0xffffffffu, active && cls == c);
+    if (!m) continue;
+    int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane == leader) base = atomicAdd(&L.cnt[c], (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (active && cls == c) {
+      uint64_t slot = base + __popc(m & ((1u << lane) - 1));
+      L.list[c][slot] = ca;
+      lcb_base[c * L.cap + slot] = cb;
+      lpair_base[c * L.cap + slot] = p32;
+    }
+  }
+}
+
+// bitmap.py:235-241: every count from |A ∩ B|
+__global__ void k_formula(uint64_t npairs, int op, const uint64_t *__restrict__ cardA, const uint64_t *__restrict__ cardB,
+                          const uint32_t *ia, const uint32_t *ib, const uint64_t *__restrict__ inter,
+                          uint64_t *__restrict__ out) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p >= npairs) return;
+  uint64_t x = cardA[pair_a(ia, p)], y = cardB[pair_a(ib, p)], i = inter[p];
+  out[p] = op == RS_OP_AND ? i : op == RS_OP_OR ? x + y - i : op == RS_OP_ANDNOT ? x - i : x + y - 2 * i;
+}
+
+// container_pairwise_cardinality (containers.py:554-570) formula from ∩
+__global__ void k_formula_containers(uint64_t npairs, int op, DevBatch A, DevBatch B, const uint32_t *ia,
+                                     const uint32_t *ib, const uint64_t *__restrict__ inter, uint64_t *__restrict__ out) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (p >= npairs) return;
+  uint64_t x = A.card[A.bm_start[pair_a(ia, p)]], y = B.card[B.bm_start[pair_a(ib, p)]], i = inter[p];
+  out[p] = op == RS_OP_AND ? i : op == RS_OP_OR ? x + y - i : op == RS_OP_ANDNOT ? x - i : x + y - 2 * i;
+}
+
+// container-level entries: pair p -> the single containers of A[ia[p]], B[ib[p]]
+__global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib, int op,
+                               Entries E, uint64_t *__restrict__ ub, Lists L) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool active = p < npairs;
+  int cls = CLS_GEN;
+  if (active) {
+    uint32_t ca = (uint32_t)A.bm_start[pair_a(ia, p)], cb = (uint32_t)B.bm_start[pair_a(ib, p)];
+    E.key[p] = A.key[ca];
+    E.ca[p] = ca;
+    E.cb[p] = cb;
+    E.pair[p] = (uint32_t)p;
+    ub[p] = rs_pad16(rs_result_ub(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op));
+    cls = classify(A.type[ca], B.type[cb]);
+  } else if (p == npairs) {
+    ub[p] = 0;
+  }
+  list_append(L, cls, active, (uint32_t)p);
+}
+
+__global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib, Lists L,
+                            uint32_t *__restrict__ lcb_base, uint32_t *__restrict__ lpair_base) {
+  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool active = p < npairs;
+  int cls = CLS_GEN;
+  uint32_t ca = 0, cb = 0;
+  if (active) {
+    ca = (uint32_t)A.bm_start[pair_a(ia, p)];
+    cb = (uint32_t)B.bm_start[pair_a(ib, p)];
+    cls = classify(A.type[ca], B.type[cb]);
+  }
+  unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 1; c < NCLS; c++) {
+    unsigned m = __ballot_sync(0xffffffffu, active && cls == c);
+    if (!m) continue;
+    int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane == leader) base = atomicAdd(&L.cnt[c], (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (active && cls == c) {
+      uint64_t slot = base + __popc(m & ((1u << lane) - 1));
+      L.list[c][slot] = ca;
+      lcb_base[c * L.cap + slot] = cb;
+      lpair_base[c * L.cap + slot] = (uint32_t)p;
+    }
+  }
+}
+
+// ------------------------------------------------------------- host side
+
+struct Scratch {
+  std::vector<void *> ptrs;
+  void *get(size_t bytes) {
+    void *p = dalloc(bytes);
+    ptrs.push_back(p);
+    return p;
+  }
+  bool ok() const {
+    for (void *p : ptrs) if (!p) return false;
+    return true;
+  }
+  ~Scratch() { for (void *p : ptrs) dfree(p); }
+};
+
+unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
+
+int check_op(int op) {
+  if (op < 0 || op > 3) {
+    set_error("unknown op " + std::to_string(op));
+    return RS_EOP;
+  }
+  return RS_OK;
+}
+
+int upload_pairs(Scratch &S, const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
+                 uint64_t npairs, uint32_t **dia, uint32_t **dib) {
+  *dia = nullptr;
+  *dib = nullptr;
+  if (!ia && npairs > A->nb) { set_error("identity pairing needs npairs <= len(A)"); return RS_EARG; }
+  if (!ib && npairs > B->nb) { set_error("identity pairing needs npairs <= len(B)"); return RS_EARG; }
+  for (uint64_t p = 0; ia && p < npairs; p++)
+    if (ia[p] >= A->nb) { set_error("pair index out of range (A)"); return RS_EARG; }
+  for (uint64_t p = 0; ib && p < npairs; p++)
+    if (ib[p] >= B->nb) { set_error("pair index out of range (B)"); return RS_EARG; }
+  if (ia) {
+    *dia = (uint32_t *)S.get(npairs * 4);
+    if (!*dia) { set_error("device allocation failed"); return RS_ENOMEM; }
+    RS_TRY(h2d(*dia, ia, npairs * 4));
+  }
+  if (ib) {
+    *dib = (uint32_t *)S.get(npairs * 4);
+    if (!*dib) { set_error("device allocation failed"); return RS_ENOMEM; }
+    RS_TRY(h2d(*dib, ib, npairs * 4));
+  }
+  return RS_OK;
+}
+
+// Run the per-class kernels over prepared entries, then compact into `out`.
+int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratch &S, Entries En, Lists L,
+                            uint64_t E, uint64_t P, const uint32_t *hcnt, const uint64_t *d_estart, uint64_t npairs,
+                            rs_batch **out) {
+  OutDesc O;
+  O.type = (uint8_t *)S.get(E + 1);
+  O.card = (uint32_t *)S.get((E + 1) * 4);
+  O.n = (uint32_t *)S.get((E + 1) * 4);
+  uint32_t *keep2 = (uint32_t *)S.get((E + 1) * 4), *fpos = (uint32_t *)S.get((E + 1) * 4);
+  if (!S.ok()) { set_error("device allocation failed (op scratch)"); return RS_ENOMEM; }
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, npairs, E, P);
+  if (rc) { rs_batch_free(b); return rc; }
+  RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
+  DevBatch dA = A->dev(), dB = B->dev();
+  // copies: warps over the list (8 warps per CTA)
+  if (hcnt[CLS_COPY]) {
+    unsigned g = std::min<uint64_t>(grid_for(hcnt[CLS_COPY], 8), 148 * 16);
+    RS_LAUNCH_PROF("copy", hcnt[CLS_COPY], k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  }
+  RS_LAUNCH_PROF("bitset_pair", hcnt[CLS_BB], k_pair_dense<false>, hcnt[CLS_BB], DT, 0, op, L.list[CLS_BB], dA, dB, En, O, b->d_pool, b->d_bm_card);
+  RS_LAUNCH_PROF("array_pair", hcnt[CLS_AA], k_pair_dense<true>, hcnt[CLS_AA], DT, 0, op, L.list[CLS_AA], dA, dB, En, O, b->d_pool, b->d_bm_card);
+  RS_LAUNCH_PROF("generic_pair", hcnt[CLS_GEN], k_pair_dense<true>, hcnt[CLS_GEN], DT, 0, op, L.list[CLS_GEN], dA, dB, En, O, b->d_pool, b->d_bm_card);
+  // compaction: drop empty results (bitmap.py:185-188)
+  RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, O.card, keep2);
+  RS_TRY(scan_exclusive<uint32_t>(keep2, fpos, E + 1));
+  RS_LAUNCH(k_compact, grid_for(E, 256), 256, 0, E, keep2, fpos, En, O, b->d_key, b->d_type, b->d_card, b->d_n,
+            b->d_off);
+  RS_LAUNCH(k_bm_start, grid_for(npairs + 1, 256), 256, 0, npairs, d_estart, fpos, b->d_bm_start);
+  b->h_valid = false;
+  *out = b;
+  return RS_OK;
+}
+
+Lists make_lists(Scratch &S, uint64_t cap) {
+  Lists L;
+  L.cap = cap ? cap : 1;
+  for (int c = 0; c < NCLS; c++) L.list[c] = (uint32_t *)S.get(L.cap * 4);
+  L.cnt = (uint32_t *)S.get(NCLS * 4);
+  return L;
+}
+
+}  // namespace
+
+extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
+                           uint64_t npairs, rs_batch **out) {
+  RS_TRY(check_op(op));
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  RS_TRY(fetch_host_meta(A));
+  RS_TRY(fetch_host_meta(B));
+  Scratch S;
+  uint32_t *dia, *dib;
+  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
+  uint64_t M = 0;
+  for (uint64_t p = 0; p < npairs; p++) {
+    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+    M += (A->h_bm_start[a + 1] - A->h_bm_start[a]) + (B->h_bm_start[b + 1] - B->h_bm_start[b]);
+  }
+  uint64_t *msz = (uint64_t *)S.get((npairs + 1) * 8), *mbase = (uint64_t *)S.get((npairs + 1) * 8);
+  uint16_t *mkey = (uint16_t *)S.get((M + 1) * 2);
+  uint32_t *mca = (uint32_t *)S.get((M + 1) * 4), *mcb = (uint32_t *)S.get((M + 1) * 4),
+           *mpair = (uint32_t *)S.get((M + 1) * 4), *keep = (uint32_t *)S.get((M + 1) * 4),
+           *epos = (uint32_t *)S.get((M + 1) * 4);
+  uint64_t *ub = (uint64_t *)S.get((M + 1) * 8), *uoff = (uint64_t *)S.get((M + 1) * 8),
+           *estart = (uint64_t *)S.get((npairs + 1) * 8);
+  Entries En;
+  En.key = (uint16_t *)S.get((M + 1) * 2);
+  En.ca = (uint32_t *)S.get((M + 1) * 4);
+  En.cb = (uint32_t *)S.get((M + 1) * 4);
+  En.pair = (uint32_t *)S.get((M + 1) * 4);
+  En.off = (uint64_t *)S.get((M + 1) * 8);
+  Lists L = make_lists(S, M);
+  uint64_t *tot = (uint64_t *)S.get(4 * 8);
+  if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
+  DevBatch dA = A->dev(), dB = B->dev();
+  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
+  RS_CK(cudaMemsetAsync(keep + M, 0, 4, g_stream));
+  RS_CK(cudaMemsetAsync(ub + M, 0, 8, g_stream));
+  RS_LAUNCH(k_pair_msize, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, 0, msz);
+  RS_TRY(scan_exclusive<uint64_t>(msz, mbase, npairs + 1));
+  RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
+  RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
+  RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
+  RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L);
+  RS_LAUNCH(k_estart, grid_for(npairs + 1, 256), 256, 0, npairs, mbase, epos, estart);
+  // one host sync: totals for allocation and exact grids
+  struct { uint32_t E; uint32_t pad; uint64_t P; uint32_t cnt[NCLS]; } h;
+  RS_CK(cudaMemcpyAsync(&h.E, epos + M, 4, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaMemcpyAsync(&h.P, uoff + M, 8, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaMemcpyAsync(h.cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaStreamSynchronize(g_stream));
+  (void)tot;
+  return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, estart, npairs, out);
+}
+
+extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia,
+                                     const uint32_t *ib, uint64_t npairs, rs_batch **out) {
+  RS_TRY(check_op(op));
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  RS_TRY(fetch_host_meta(A));
+  RS_TRY(fetch_host_meta(B));
+  for (uint64_t p = 0; p < npairs; p++) {
+    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+    if (a < A->nb && b < B->nb &&
+        (A->h_bm_start[a + 1] - A->h_bm_start[a] != 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] != 1)) {
+      set_error("container_pairwise needs exactly one container per image");
+      return RS_ESHAPE;
+    }
+  }
+  Scratch S;
+  uint32_t *dia, *dib;
+  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
+  Entries En;
+  En.key = (uint16_t *)S.get((npairs + 1) * 2);
+  En.ca = (uint32_t *)S.get((npairs + 1) * 4);
+  En.cb = (uint32_t *)S.get((npairs + 1) * 4);
+  En.pair = (uint32_t *)S.get((npairs + 1) * 4);
+  En.off = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *ub = (uint64_t *)S.get((npairs + 1) * 8), *estart = (uint64_t *)S.get((npairs + 1) * 8);
+  Lists L = make_lists(S, npairs);
+  if (!S.ok()) { set_error("device allocation failed (container op)"); return RS_ENOMEM; }
+  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
+  DevBatch dA = A->dev(), dB = B->dev();
+  RS_LAUNCH(k_cont_entries, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, op, En, ub, L);
+  RS_TRY(scan_exclusive<uint64_t>(ub, En.off, npairs + 1));
+  // estart[p] = p (one entry per pair)
+  std::vector<uint64_t> hs(npairs + 1);
+  for (uint64_t p = 0; p <= npairs; p++) hs[p] = p;
+  RS_TRY(h2d(estart, hs.data(), (npairs + 1) * 8));
+  uint64_t P = 0;
+  uint32_t cnt[NCLS];
+  RS_CK(cudaMemcpyAsync(&P, En.off + npairs, 8, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaMemcpyAsync(cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaStreamSynchronize(g_stream));
+  return run_classes_and_compact(op, A, B, S, En, L, npairs, P, cnt, estart, npairs, out);
+}
+
+namespace {
+int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, uint32_t *lcb, uint32_t *lpair,
+                  uint64_t *inter) {
+  DevBatch dA = A->dev(), dB = B->dev();
+  const unsigned pg = 148 * 8;
+  RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB], lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap,
+            L.cnt + CLS_BB, dA, dB, inter);
+  RS_LAUNCH_PROF("array_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_AA], lcb + CLS_AA * L.cap, lpair + CLS_AA * L.cap,
+            L.cnt + CLS_AA, dA, dB, inter);
+  RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN], lcb + CLS_GEN * L.cap,
+            lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
+  return RS_OK;
+}
+}  // namespace
+
+extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia,
+                                       const uint32_t *ib, uint64_t npairs, uint64_t *counts, int counts_on_device) {
+  RS_TRY(check_op(op));
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(A));
+  RS_TRY(fetch_host_meta(B));
+  Scratch S;
+  uint32_t *dia, *dib;
+  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
+  uint64_t Ma = 0;
+  for (uint64_t p = 0; p < npairs; p++) {
+    uint32_t a = ia ? ia[p] : (uint32_t)p;
+    Ma += A->h_bm_start[a + 1] - A->h_bm_start[a];
+  }
+  uint64_t *msz = (uint64_t *)S.get((npairs + 1) * 8), *mbase = (uint64_t *)S.get((npairs + 1) * 8);
+  Lists L = make_lists(S, Ma);
+  uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);
+  uint64_t *inter = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *dout = counts_on_device ? counts : (uint64_t *)S.get((npairs + 1) * 8);
+  if (!S.ok()) { set_error("device allocation failed (count)"); return RS_ENOMEM; }
+  DevBatch dA = A->dev(), dB = B->dev();
+  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
+  RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
+  RS_LAUNCH(k_pair_msize, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, 1, msz);
+  RS_TRY(scan_exclusive<uint64_t>(msz, mbase, npairs + 1));
+  RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
+  RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
+  RS_LAUNCH(k_formula, grid_for(npairs, 256), 256, 0, npairs, op, A->d_bm_card, B->d_bm_card, dia, dib, inter, dout);
+  if (!counts_on_device) RS_TRY(d2h(counts, dout, npairs * 8));
+  return RS_OK;
+}
+
+extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia,
+                                                 const uint32_t *ib, uint64_t npairs, uint64_t *counts,
+                                                 int counts_on_device) {
+  RS_TRY(check_op(op));
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(A));
+  RS_TRY(fetch_host_meta(B));
+  for (uint64_t p = 0; p < npairs; p++) {
+    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+    if (a < A->nb && b < B->nb &&
+        (A->h_bm_start[a + 1] - A->h_bm_start[a] != 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] != 1)) {
+      set_error("container_pairwise_cardinality needs exactly one container per image");
+      return RS_ESHAPE;
+    }
+  }
+  Scratch S;
+  uint32_t *dia, *dib;
+  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
+  Lists L = make_lists(S, npairs);
+  uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);
+  uint64_t *inter = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *dout = counts_on_device ? counts : (uint64_t *)S.get((npairs + 1) * 8);
+  if (!S.ok()) { set_error("device allocation failed (count)"); return RS_ENOMEM; }
+  DevBatch dA = A->dev(), dB = B->dev();
+  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
+  RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
+  RS_LAUNCH(k_cont_list, grid_for(npairs, 256), 256, 0, npairs, dA, dB, dia, dib, L, lcb, lpair);
+  RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
+  RS_LAUNCH(k_formula_containers, grid_for(npairs, 256), 256, 0, npairs, op, dA, dB, dia, dib, inter, dout);
+  if (!counts_on_device) RS_TRY(d2h(counts, dout, npairs * 8));
+  return RS_OK;
+}

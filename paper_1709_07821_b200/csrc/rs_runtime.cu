@@ -1,0 +1,316 @@
+// rs_runtime.cu -- runtime plumbing: errors, stream, stream-ordered allocation,
+// scans/sorts (CUB device primitives), batch lifetime and metadata queries.
+#include <cub/cub.cuh>
+#include <mutex>
+#include <cstring>
+#include "rs_internal.cuh"
+
+namespace rs {
+cudaStream_t g_stream = nullptr;
+uint64_t g_launches = 0;
+static thread_local std::string t_err;
+static thread_local int64_t t_err_off = -1, t_err_idx = -1;
+static int g_device_ok = -1;
+static std::mutex g_init_mu;
+
+bool g_prof_on = false;
+struct ProfRec { std::string name; cudaEvent_t a, b; uint64_t items; };
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t prof_event() {
+  cudaEvent_t e;
+  if (!g_event_pool.empty()) { e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_mark(const char *name, cudaEvent_t a, cudaEvent_t b, uint64_t items) {
+  g_prof.push_back({name, a, b, items});
+}
+
+void set_error(const std::string &m, int64_t off, int64_t idx) {
+  t_err = m;
+  t_err_off = off;
+  t_err_idx = idx;
+}
+
+int cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+           cudaGetErrorString(e), what, file, line);
+  set_error(buf);
+  return e == cudaErrorMemoryAllocation ? RS_ENOMEM : RS_ECUDA;
+}
+
+int ensure_device() {
+  std::lock_guard<std::mutex> g(g_init_mu);
+  if (g_device_ok == 1) return RS_OK;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_error("no CUDA device available: roaring_b200 has no CPU fallback");
+    return RS_ECUDA;
+  }
+  cudaMemPool_t pool;
+  int dev = 0;
+  RS_CK(cudaGetDevice(&dev));
+  RS_CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
+  RS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  g_device_ok = 1;
+  return RS_OK;
+}
+
+void *dalloc(size_t bytes) {
+  void *p = nullptr;
+  if (bytes == 0) bytes = 16;
+  if (cudaMallocAsync(&p, bytes, g_stream) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dfree(void *p) {
+  if (p) cudaFreeAsync(p, g_stream);
+}
+
+int d2h(void *h, const void *d, size_t bytes) {
+  if (bytes) RS_CK(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaStreamSynchronize(g_stream));
+  return RS_OK;
+}
+
+int h2d(void *d, const void *h, size_t bytes) {
+  if (bytes) RS_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, g_stream));
+  return RS_OK;
+}
+
+template <typename T>
+int scan_exclusive(const T *in, T *out, uint64_t n) {
+  if (n == 0) return RS_OK;
+  size_t tmp = 0;
+  RS_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, g_stream));
+  void *t = dalloc(tmp);
+  if (!t) { set_error("device allocation failed (scan)"); return RS_ENOMEM; }
+  RS_CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int64_t)n, g_stream));
+  g_launches += 2;
+  dfree(t);
+  return RS_OK;
+}
+
+template <typename T>
+int scan_inclusive(const T *in, T *out, uint64_t n) {
+  if (n == 0) return RS_OK;
+  size_t tmp = 0;
+  RS_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, (int64_t)n, g_stream));
+  void *t = dalloc(tmp);
+  if (!t) { set_error("device allocation failed (scan)"); return RS_ENOMEM; }
+  RS_CK(cub::DeviceScan::InclusiveSum(t, tmp, in, out, (int64_t)n, g_stream));
+  g_launches += 2;
+  dfree(t);
+  return RS_OK;
+}
+
+template int scan_exclusive<uint32_t>(const uint32_t *, uint32_t *, uint64_t);
+template int scan_exclusive<uint64_t>(const uint64_t *, uint64_t *, uint64_t);
+template int scan_inclusive<uint32_t>(const uint32_t *, uint32_t *, uint64_t);
+template int scan_inclusive<uint64_t>(const uint64_t *, uint64_t *, uint64_t);
+
+int sort_u64(uint64_t *keys, uint64_t n, int end_bit) {
+  if (n <= 1) return RS_OK;
+  uint64_t *alt = (uint64_t *)dalloc(n * 8);
+  if (!alt) { set_error("device allocation failed (sort)"); return RS_ENOMEM; }
+  cub::DoubleBuffer<uint64_t> db(keys, alt);
+  size_t tmp = 0;
+  RS_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)n, 0, end_bit, g_stream));
+  void *t = dalloc(tmp);
+  if (!t) { dfree(alt); set_error("device allocation failed (sort)"); return RS_ENOMEM; }
+  RS_CK(cub::DeviceRadixSort::SortKeys(t, tmp, db, (int64_t)n, 0, end_bit, g_stream));
+  g_launches += (end_bit + 7) / 8 + 2;
+  if (db.Current() != keys)
+    RS_CK(cudaMemcpyAsync(keys, db.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream));
+  dfree(t);
+  dfree(alt);
+  return RS_OK;
+}
+
+int batch_alloc(rs_batch *b, uint64_t nb, uint64_t nc, uint64_t pool_bytes) {
+  b->nb = nb;
+  b->nc = nc;
+  b->cap_c = nc;
+  b->pool_bytes = pool_bytes;
+  b->d_bm_start = (uint64_t *)dalloc((nb + 1) * 8);
+  b->d_bm_card = (uint64_t *)dalloc((nb + 1) * 8);
+  uint64_t c = nc ? nc : 1;
+  b->d_key = (uint16_t *)dalloc(c * 2);
+  b->d_type = (uint8_t *)dalloc(c);
+  b->d_card = (uint32_t *)dalloc(c * 4);
+  b->d_n = (uint32_t *)dalloc(c * 4);
+  b->d_off = (uint64_t *)dalloc(c * 8);
+  b->d_pool = (uint8_t *)dalloc(pool_bytes ? pool_bytes : 16);
+  if (!b->d_bm_start || !b->d_bm_card || !b->d_key || !b->d_type || !b->d_card || !b->d_n ||
+      !b->d_off || !b->d_pool) {
+    set_error("device allocation failed (batch)");
+    return RS_ENOMEM;
+  }
+  return RS_OK;
+}
+
+void batch_release(rs_batch *b) {
+  dfree(b->d_bm_start); dfree(b->d_bm_card); dfree(b->d_key); dfree(b->d_type);
+  dfree(b->d_card); dfree(b->d_n); dfree(b->d_off); dfree(b->d_pool);
+  b->d_bm_start = nullptr; b->d_bm_card = nullptr; b->d_key = nullptr; b->d_type = nullptr;
+  b->d_card = nullptr; b->d_n = nullptr; b->d_off = nullptr; b->d_pool = nullptr;
+}
+
+int fetch_host_meta(const rs_batch *cb) {
+  rs_batch *b = const_cast<rs_batch *>(cb);
+  if (b->h_valid) return RS_OK;
+  b->h_bm_start.resize(b->nb + 1);
+  RS_TRY(d2h(b->h_bm_start.data(), b->d_bm_start, (b->nb + 1) * 8));
+  b->nc = b->h_bm_start[b->nb];
+  b->h_valid = true;
+  return RS_OK;
+}
+
+// RoaringBitmap.__len__ (bitmap.py:77-82): one warp per bitmap sums its cards.
+__global__ void k_bm_card(uint64_t nb, const uint64_t *__restrict__ bm_start,
+                          const uint32_t *__restrict__ card, uint64_t *__restrict__ out) {
+  uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (w >= nb) return;
+  uint64_t s = 0;
+  for (uint64_t c = bm_start[w] + lane; c < bm_start[w + 1]; c += 32) s += card[c];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s;
+}
+
+int finalize_batch(rs_batch *b) {
+  uint64_t threads = b->nb * 32;
+  RS_LAUNCH(k_bm_card, (unsigned)((threads + 255) / 256), 256, 0, b->nb, b->d_bm_start, b->d_card,
+            b->d_bm_card);
+  return RS_OK;
+}
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" {
+
+const char *rs_last_error(void) { return rs::t_err.c_str(); }
+int64_t rs_last_error_offset(void) { return rs::t_err_off; }
+int64_t rs_last_error_index(void) { return rs::t_err_idx; }
+const char *rs_version(void) { return "roaring_b200 0.1.0 (sm_100a)"; }
+uint64_t rs_kernel_launches(void) { return rs::g_launches; }
+
+int rs_set_device(int device) {
+  RS_CK(cudaSetDevice(device));
+  {
+    std::lock_guard<std::mutex> g(rs::g_init_mu);
+    rs::g_device_ok = -1;  // re-run the pool setup for this device
+  }
+  return ensure_device();
+}
+
+int rs_set_stream(void *stream) {
+  RS_TRY(ensure_device());
+  g_stream = (cudaStream_t)stream;
+  return RS_OK;
+}
+void *rs_get_stream(void) { return (void *)g_stream; }
+
+int rs_synchronize(void) {
+  RS_TRY(ensure_device());
+  RS_CK(cudaStreamSynchronize(g_stream));
+  return RS_OK;
+}
+
+int rs_host_alloc(void **ptr, uint64_t bytes) {
+  RS_TRY(ensure_device());
+  RS_CK(cudaMallocHost(ptr, bytes ? bytes : 16));
+  return RS_OK;
+}
+int rs_host_free(void *ptr) {
+  RS_CK(cudaFreeHost(ptr));
+  return RS_OK;
+}
+
+int rs_event_record(void **event) {
+  RS_TRY(ensure_device());
+  cudaEvent_t e;
+  RS_CK(cudaEventCreate(&e));
+  RS_CK(cudaEventRecord(e, g_stream));
+  *event = (void *)e;
+  return RS_OK;
+}
+int rs_event_elapsed(void *start, void *stop, float *ms) {
+  RS_CK(cudaEventSynchronize((cudaEvent_t)stop));
+  RS_CK(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+  return RS_OK;
+}
+int rs_event_destroy(void *event) {
+  RS_CK(cudaEventDestroy((cudaEvent_t)event));
+  return RS_OK;
+}
+
+int rs_profile_enable(int on) {
+  RS_TRY(ensure_device());
+  rs::g_prof_on = on != 0;
+  return RS_OK;
+}
+
+int rs_profile_reset(void) {
+  RS_CK(cudaStreamSynchronize(g_stream));
+  for (auto &r : rs::g_prof) { rs::g_event_pool.push_back(r.a); rs::g_event_pool.push_back(r.b); }
+  rs::g_prof.clear();
+  return RS_OK;
+}
+
+int rs_profile_query(const char *name, double *total_ms, uint64_t *launches, uint64_t *items) {
+  RS_CK(cudaStreamSynchronize(g_stream));
+  double t = 0;
+  uint64_t n = 0, it = 0;
+  for (auto &r : rs::g_prof) {
+    if (r.name != name) continue;
+    float ms = 0;
+    RS_CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    t += ms;
+    n++;
+    it += r.items;
+  }
+  *total_ms = t;
+  *launches = n;
+  if (items) *items = it;
+  return RS_OK;
+}
+
+int rs_batch_free(rs_batch *b) {
+  if (!b) return RS_OK;
+  batch_release(b);
+  delete b;
+  return RS_OK;
+}
+
+int rs_batch_info(const rs_batch *b, uint64_t *n_bitmaps, uint64_t *n_containers,
+                  uint64_t *pool_bytes) {
+  if (!b) { set_error("null batch"); return RS_EARG; }
+  RS_TRY(fetch_host_meta(b));
+  if (n_bitmaps) *n_bitmaps = b->nb;
+  if (n_containers) *n_containers = b->nc;
+  if (pool_bytes) *pool_bytes = b->pool_bytes;
+  return RS_OK;
+}
+
+int rs_batch_cardinalities(const rs_batch *b, uint64_t *out) {
+  if (!b) { set_error("null batch"); return RS_EARG; }
+  return d2h(out, b->d_bm_card, b->nb * 8);
+}
+
+int rs_batch_container_counts(const rs_batch *b, uint64_t *out) {
+  RS_TRY(fetch_host_meta(b));
+  for (uint64_t i = 0; i < b->nb; i++) out[i] = b->h_bm_start[i + 1] - b->h_bm_start[i];
+  return RS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,412 @@
+// rs_wide.cu -- operations over many bitmaps at once:
+//   rs_union_many            RoaringBitmap.union_many (bitmap.py:257-304)
+//   rs_all_pairs_cardinality |A∩B|, |A∪B| for all pairs (op_cardinality, bitmap.py:212-241)
+//   rs_batch_run_optimize    RoaringBitmap.run_optimize (bitmap.py:308-316)
+// All three group containers by chunk key with one radix sort of
+// (key << 40 | container index) so contributors stay in input order.
+#include <cub/cub.cuh>
+#include <algorithm>
+#include "rs_internal.cuh"
+#include "rs_dense.cuh"
+
+using namespace rs;
+using namespace rsd;
+
+namespace {
+
+unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
+
+// item t of the ordered selection -> container index; sort key = key << 40 | t
+__global__ void k_group_keys(uint64_t T, uint64_t nsel, const uint64_t *__restrict__ qbase,
+                             const uint64_t *__restrict__ qsrc, DevBatch S, uint64_t *__restrict__ keys,
+                             uint32_t *__restrict__ item_c) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  uint64_t lo = 0, hi = nsel;
+  while (hi - lo > 1) {
+    uint64_t m = (lo + hi) >> 1;
+    if (qbase[m] <= t) lo = m; else hi = m;
+  }
+  uint64_t c = qsrc[lo] + (t - qbase[lo]);
+  item_c[t] = (uint32_t)c;
+  keys[t] = ((uint64_t)S.key[c] << 40) | t;
+}
+
+__global__ void k_seg_flags(uint64_t T, const uint64_t *__restrict__ keys, uint32_t *__restrict__ flag) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i <= T) flag[i] = i < T && (i == 0 || (keys[i] >> 40) != (keys[i - 1] >> 40));
+}
+
+__global__ void k_seg_starts(uint64_t T, const uint32_t *__restrict__ flag, const uint32_t *__restrict__ pos,
+                             uint32_t *__restrict__ seg_start) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < T && flag[i]) seg_start[pos[i]] = (uint32_t)i;
+  if (i == T) seg_start[pos[T]] = (uint32_t)T;
+}
+
+// OR container c of S into the smem bitset X (no zeroing; bitsets OR word-wise)
+__device__ void or_into(const DevBatch &S, uint32_t c, uint64_t *X) {
+  uint8_t t = S.type[c];
+  if (t == RS_TAG_BITSET) {
+    uint64_t w[4];
+    ld_words(S.pool, S.off[c], threadIdx.x, w);
+#pragma unroll
+    for (int k = 0; k < 4; k++) X[4 * threadIdx.x + k] |= w[k];
+  } else {
+    scatter_container(S, c, t, X);
+  }
+}
+
+__device__ __forceinline__ void block_card_runs(const uint64_t *X, uint32_t &card, uint32_t &nruns,
+                                                uint32_t (*red)[2], bool want_runs) {
+  const int t = threadIdx.x;
+  uint32_t pc = 0, nr = 0;
+  uint64_t prev = t ? X[4 * t - 1] : 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    uint64_t w = X[4 * t + k];
+    pc += __popcll(w);
+    if (want_runs) {
+      uint64_t cin = (k ? X[4 * t + k - 1] : prev) >> 63;
+      nr += __popcll(w & ~((w << 1) | cin));
+    }
+  }
+  block_sum2(pc, nr, red);
+  card = pc;
+  nruns = nr;
+}
+
+// One CTA per chunk key replays the sequential fold of union_many
+// (SURVEY App. B): acc = copy(c0); per next contributor ci:
+//   acc bitset            -> acc |= ci, stays bitset          (bitmap.py:278-287)
+//   ci bitset             -> acc becomes bitset(ci | acc)      (:288-296)
+//   both array/run        -> container_pairwise("or")         (:297-298)
+//                            = array/bitset by card, or norm(run) if a run is involved
+__global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *__restrict__ seg_start,
+                                                   const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ keys,
+                                                   DevBatch S, uint16_t *okey, uint8_t *otype, uint32_t *ocard,
+                                                   uint32_t *on, uint64_t *ooff, uint8_t *__restrict__ opool) {
+  __shared__ __align__(16) DenseSmem sm;
+  const uint64_t g = blockIdx.x;
+  if (g >= G) return;
+  const int t = threadIdx.x;
+  uint32_t s = seg_start[g], e = seg_start[g + 1];
+#pragma unroll
+  for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
+  __syncthreads();
+  uint32_t c0 = item_c[s];
+  uint8_t acc = S.type[c0];
+  or_into(S, c0, sm.X);
+  __syncthreads();
+  for (uint32_t i = s + 1; i < e; i++) {
+    uint32_t ci = item_c[i];
+    uint8_t ti = S.type[ci];
+    or_into(S, ci, sm.X);
+    __syncthreads();
+    if (acc == RS_TAG_BITSET) continue;
+    if (ti == RS_TAG_BITSET) { acc = RS_TAG_BITSET; continue; }
+    bool run_rule = acc == RS_TAG_RUN || ti == RS_TAG_RUN;
+    uint32_t card, nruns;
+    block_card_runs(sm.X, card, nruns, sm.red, run_rule);
+    if (run_rule && rs_run_admissible(card, nruns)) acc = RS_TAG_RUN;
+    else acc = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;
+    __syncthreads();
+  }
+  uint64_t r[4];
+  uint32_t pc = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) { r[k] = sm.X[4 * t + k]; pc += __popcll(r[k]); }
+  uint32_t card = pc, z = 0;
+  block_sum2(card, z, sm.red);
+  __syncthreads();
+  uint32_t n = encode_result(sm, r, pc, card, acc, opool + g * 8192);
+  if (t == 0) {
+    okey[g] = (uint16_t)(keys[s] >> 40);
+    otype[g] = acc;
+    ocard[g] = card;
+    on[g] = n;
+    ooff[g] = g * 8192;
+  }
+}
+
+// ------------------------------------------------------------ all pairs
+
+// densify every grouped container into its own 8 KB slot
+__global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__restrict__ item_c, DevBatch S,
+                                                uint64_t *__restrict__ D) {
+  __shared__ __align__(16) uint64_t X[RS_WORDS];
+  uint64_t i = blockIdx.x;
+  if (i >= T) return;
+  const int t = threadIdx.x;
+  uint32_t c = item_c[i];
+  uint8_t type = S.type[c];
+  uint64_t *dst = D + i * RS_WORDS;
+  if (type == RS_TAG_BITSET) {
+    uint64_t w[4];
+    ld_words(S.pool, S.off[c], t, w);
+    st_words((uint8_t *)dst, 0, t, w);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; k++) X[4 * t + k] = 0;
+  __syncthreads();
+  scatter_container(S, c, type, X);
+  __syncthreads();
+  uint64_t w[4];
+  for (int k = 0; k < 4; k++) w[k] = X[4 * t + k];
+  st_words((uint8_t *)dst, 0, t, w);
+}
+
+constexpr int AP_TILE = 16;   // containers per tile side
+constexpr int AP_KW = 64;     // words per smem chunk
+
+// One CTA per (segment, tile i, tile j>=i): 16x16 popcount(AND) over 1024 words,
+// accumulated into the N x N intersection matrix.
+__global__ void __launch_bounds__(256) k_allpairs_tiles(const uint32_t *__restrict__ tp_seg,
+                                                        const uint16_t *__restrict__ tp_i, const uint16_t *__restrict__ tp_j,
+                                                        const uint32_t *__restrict__ seg_start,
+                                                        const uint64_t *__restrict__ D, const uint32_t *__restrict__ item_bm,
+                                                        uint64_t N, unsigned long long *__restrict__ M) {
+  __shared__ uint64_t Ai[AP_TILE][AP_KW + 1];
+  __shared__ uint64_t Bj[AP_TILE][AP_KW + 1];
+  uint32_t seg = tp_seg[blockIdx.x];
+  uint32_t s = seg_start[seg], m = seg_start[seg + 1] - s;
+  uint32_t ti = tp_i[blockIdx.x], tj = tp_j[blockIdx.x];
+  const int t = threadIdx.x;
+  const int u = t >> 4, v = t & 15;
+  uint32_t gu = ti * AP_TILE + u, gv = tj * AP_TILE + v;
+  uint32_t acc = 0;
+  for (int k0 = 0; k0 < RS_WORDS; k0 += AP_KW) {
+    for (int x = t; x < AP_TILE * AP_KW; x += 256) {
+      int row = x / AP_KW, col = x % AP_KW;
+      uint32_t ra = ti * AP_TILE + row, rb = tj * AP_TILE + row;
+      Ai[row][col] = ra < m ? D[(uint64_t)(s + ra) * RS_WORDS + k0 + col] : 0;
+      Bj[row][col] = rb < m ? D[(uint64_t)(s + rb) * RS_WORDS + k0 + col] : 0;
+    }
+    __syncthreads();
+#pragma unroll 16
+    for (int k = 0; k < AP_KW; k++) acc += __popcll(Ai[u][k] & Bj[v][k]);
+    __syncthreads();
+  }
+  bool valid = gu < m && gv < m && (ti != tj || u < v);
+  if (valid && acc) {
+    uint32_t bu = item_bm[s + gu], bv = item_bm[s + gv];
+    uint32_t lo = min(bu, bv), hi = max(bu, bv);
+    atomicAdd(&M[(uint64_t)lo * N + hi], (unsigned long long)acc);
+  }
+}
+
+__global__ void k_item_bitmap(uint64_t T, const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ bm_start,
+                              uint64_t nb, uint32_t *__restrict__ item_bm) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= T) return;
+  uint64_t c = item_c[i], lo = 0, hi = nb;
+  while (hi - lo > 1) {
+    uint64_t m = (lo + hi) >> 1;
+    if (bm_start[m] <= c) lo = m; else hi = m;
+  }
+  item_bm[i] = (uint32_t)lo;
+}
+
+__global__ void k_upper_triangle(uint64_t N, const unsigned long long *__restrict__ M, const uint64_t *__restrict__ card,
+                                 uint64_t *__restrict__ inter, uint64_t *__restrict__ uni) {
+  uint64_t i = blockIdx.y, j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= N || j >= N || j <= i) return;
+  uint64_t k = i * (2 * N - i - 1) / 2 + (j - i - 1);
+  uint64_t x = M[i * N + j];
+  inter[k] = x;
+  if (uni) uni[k] = card[i] + card[j] - x;
+}
+
+// --------------------------------------------------------- run_optimize
+
+// container_normalize(c, consider_run=True) (containers.py:208-241) in place:
+// the run form is only taken when strictly smaller, so it fits the slot.
+__global__ void __launch_bounds__(DT) k_run_optimize(uint64_t nc, DevBatch S, uint8_t *otype, uint32_t *on,
+                                                     uint8_t *__restrict__ pool, uint32_t *__restrict__ changed) {
+  __shared__ __align__(16) DenseSmem sm;
+  uint64_t c = blockIdx.x;
+  if (c >= nc) return;
+  uint8_t type = S.type[c];
+  if (type == RS_TAG_RUN) return;  // normalized runs stay runs
+  const int t = threadIdx.x;
+  uint64_t r[4];
+  if (type == RS_TAG_BITSET) {
+    ld_words(S.pool, S.off[c], t, r);
+    for (int k = 0; k < 4; k++) sm.X[4 * t + k] = r[k];
+  } else {
+    for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
+    __syncthreads();
+    scatter_container(S, (uint32_t)c, type, sm.X);
+    __syncthreads();
+    for (int k = 0; k < 4; k++) r[k] = sm.X[4 * t + k];
+  }
+  __syncthreads();
+  uint32_t pc = 0;
+  for (int k = 0; k < 4; k++) pc += __popcll(r[k]);
+  uint32_t card, nruns;
+  block_card_runs(sm.X, card, nruns, sm.red, true);
+  if (!rs_run_admissible(card, nruns)) return;
+  __syncthreads();
+  uint32_t n = encode_result(sm, r, pc, card, RS_TAG_RUN, pool + S.off[c]);
+  if (t == 0) {
+    otype[c] = RS_TAG_RUN;
+    on[c] = n;
+    uint64_t lo = 0, hi = S.nb;
+    while (hi - lo > 1) {
+      uint64_t m = (lo + hi) >> 1;
+      if (S.bm_start[m] <= c) lo = m; else hi = m;
+    }
+    changed[lo] = 1;
+  }
+}
+
+struct Grouped {
+  uint64_t T = 0, G = 0;
+  uint64_t *keys = nullptr;
+  uint32_t *item_c = nullptr, *seg_start = nullptr;
+  void release() { dfree(keys); dfree(item_c); dfree(seg_start); }
+};
+
+// Group the containers of bitmaps sel[0..n) (in that order) by chunk key.
+int group_by_key(const rs_batch *in, const std::vector<uint64_t> &sel, Grouped &g) {
+  uint64_t n = sel.size();
+  std::vector<uint64_t> qbase(n + 1, 0), qsrc(n + 1, 0);
+  for (uint64_t k = 0; k < n; k++) {
+    qsrc[k] = in->h_bm_start[sel[k]];
+    qbase[k + 1] = qbase[k] + (in->h_bm_start[sel[k] + 1] - in->h_bm_start[sel[k]]);
+  }
+  g.T = qbase[n];
+  uint64_t T = g.T;
+  uint64_t *d_qb = (uint64_t *)dalloc((n + 1) * 8), *d_qs = (uint64_t *)dalloc((n + 1) * 8);
+  g.keys = (uint64_t *)dalloc((T + 1) * 8);
+  g.item_c = (uint32_t *)dalloc((T + 1) * 4);
+  uint32_t *flag = (uint32_t *)dalloc((T + 1) * 4), *pos = (uint32_t *)dalloc((T + 1) * 4);
+  g.seg_start = (uint32_t *)dalloc((T + 2) * 4);
+  if (!d_qb || !d_qs || !g.keys || !g.item_c || !flag || !pos || !g.seg_start) {
+    set_error("device allocation failed (group)");
+    return RS_ENOMEM;
+  }
+  RS_TRY(h2d(d_qb, qbase.data(), (n + 1) * 8));
+  RS_TRY(h2d(d_qs, qsrc.data(), (n + 1) * 8));
+  RS_LAUNCH(k_group_keys, grid_for(T, 256), 256, 0, T, n, d_qb, d_qs, in->dev(), g.keys, g.item_c);
+  RS_TRY(sort_u64(g.keys, T, 56));
+  // item index after the sort comes from the low 40 bits: reorder item_c
+  RS_LAUNCH(k_seg_flags, grid_for(T + 1, 256), 256, 0, T, g.keys, flag);
+  RS_TRY(scan_exclusive<uint32_t>(flag, pos, T + 1));
+  RS_LAUNCH(k_seg_starts, grid_for(T + 1, 256), 256, 0, T, flag, pos, g.seg_start);
+  uint32_t G = 0;
+  RS_TRY(d2h(&G, pos + T, 4));
+  g.G = G;
+  dfree(d_qb); dfree(d_qs); dfree(flag); dfree(pos);
+  return RS_OK;
+}
+
+__global__ void k_reorder_items(uint64_t T, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ item_in,
+                                uint32_t *__restrict__ item_out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < T) item_out[i] = item_in[keys[i] & ((1ull << 40) - 1)];
+}
+
+int group_and_reorder(const rs_batch *in, const std::vector<uint64_t> &sel, Grouped &g) {
+  RS_TRY(group_by_key(in, sel, g));
+  uint32_t *sorted_c = (uint32_t *)dalloc((g.T + 1) * 4);
+  if (!sorted_c) { set_error("device allocation failed (group)"); return RS_ENOMEM; }
+  RS_LAUNCH(k_reorder_items, grid_for(g.T, 256), 256, 0, g.T, g.keys, g.item_c, sorted_c);
+  dfree(g.item_c);
+  g.item_c = sorted_c;
+  return RS_OK;
+}
+
+}  // namespace
+
+extern "C" int rs_union_many(const rs_batch *in, const uint64_t *idx, uint64_t n, rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  RS_TRY(fetch_host_meta(in));
+  std::vector<uint64_t> sel(n);
+  for (uint64_t k = 0; k < n; k++) {
+    sel[k] = idx ? idx[k] : k;
+    if (sel[k] >= in->nb) { set_error("bitmap index out of range"); return RS_EARG; }
+  }
+  Grouped g;
+  RS_TRY(group_and_reorder(in, sel, g));
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, 1, g.G, g.G * 8192);
+  if (rc) { g.release(); rs_batch_free(b); return rc; }
+  RS_LAUNCH_PROF("union_fold", g.G, k_union_fold, (unsigned)g.G, DT, 0, g.G, g.seg_start, g.item_c, g.keys, in->dev(), b->d_key, b->d_type,
+            b->d_card, b->d_n, b->d_off, b->d_pool);
+  uint64_t hs[2] = {0, g.G};
+  RS_TRY(h2d(b->d_bm_start, hs, 16));
+  RS_TRY(finalize_batch(b));
+  RS_CK(cudaStreamSynchronize(g_stream));
+  g.release();
+  b->h_bm_start.assign(hs, hs + 2);
+  b->h_valid = true;
+  *out = b;
+  return RS_OK;
+}
+
+extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uint64_t *uni) {
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(in));
+  uint64_t N = in->nb;
+  uint64_t npairs = N * (N - 1) / 2;
+  if (N < 2) return RS_OK;
+  std::vector<uint64_t> sel(N);
+  for (uint64_t k = 0; k < N; k++) sel[k] = k;
+  Grouped g;
+  RS_TRY(group_and_reorder(in, sel, g));
+  std::vector<uint32_t> hseg(g.G + 1);
+  RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
+  std::vector<uint32_t> tseg;
+  std::vector<uint16_t> ti, tj;
+  for (uint64_t s = 0; s < g.G; s++) {
+    uint32_t m = hseg[s + 1] - hseg[s];
+    if (m < 2) continue;
+    uint32_t nt = (m + AP_TILE - 1) / AP_TILE;
+    for (uint32_t a = 0; a < nt; a++)
+      for (uint32_t b2 = a; b2 < nt; b2++) { tseg.push_back((uint32_t)s); ti.push_back(a); tj.push_back(b2); }
+  }
+  uint64_t ntp = tseg.size();
+  uint64_t *D = (uint64_t *)dalloc((g.T ? g.T : 1) * 8192);
+  uint32_t *item_bm = (uint32_t *)dalloc((g.T + 1) * 4), *d_tseg = (uint32_t *)dalloc((ntp + 1) * 4);
+  uint16_t *d_ti = (uint16_t *)dalloc((ntp + 1) * 2), *d_tj = (uint16_t *)dalloc((ntp + 1) * 2);
+  unsigned long long *Mx = (unsigned long long *)dalloc(N * N * 8);
+  uint64_t *d_inter = (uint64_t *)dalloc(npairs * 8), *d_uni = (uint64_t *)dalloc(npairs * 8);
+  if (!D || !item_bm || !d_tseg || !d_ti || !d_tj || !Mx || !d_inter || !d_uni) {
+    set_error("device allocation failed (all pairs)");
+    return RS_ENOMEM;
+  }
+  RS_TRY(h2d(d_tseg, tseg.data(), ntp * 4));
+  RS_TRY(h2d(d_ti, ti.data(), ntp * 2));
+  RS_TRY(h2d(d_tj, tj.data(), ntp * 2));
+  RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
+  RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
+  RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
+  RS_LAUNCH_PROF("allpairs", ntp, k_allpairs_tiles, (unsigned)ntp, 256, 0, d_tseg, d_ti, d_tj, g.seg_start, D, item_bm, N, Mx);
+  dim3 grid(grid_for(N, 256), (unsigned)N);
+  k_upper_triangle<<<grid, 256, 0, g_stream>>>(N, Mx, in->d_bm_card, d_inter, uni ? d_uni : nullptr);
+  ++g_launches;
+  RS_CK(cudaGetLastError());
+  RS_TRY(d2h(inter, d_inter, npairs * 8));
+  if (uni) RS_TRY(d2h(uni, d_uni, npairs * 8));
+  dfree(D); dfree(item_bm); dfree(d_tseg); dfree(d_ti); dfree(d_tj); dfree(Mx); dfree(d_inter); dfree(d_uni);
+  g.release();
+  return RS_OK;
+}
+
+extern "C" int rs_batch_run_optimize(rs_batch *b, uint8_t *changed) {
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(b));
+  uint32_t *d_ch = (uint32_t *)dalloc((b->nb + 1) * 4);
+  if (!d_ch) { set_error("device allocation failed (run_optimize)"); return RS_ENOMEM; }
+  RS_CK(cudaMemsetAsync(d_ch, 0, (b->nb + 1) * 4, g_stream));
+  RS_LAUNCH(k_run_optimize, (unsigned)b->nc, DT, 0, b->nc, b->dev(), b->d_type, b->d_n, b->d_pool, d_ch);
+  std::vector<uint32_t> h(b->nb + 1);
+  RS_TRY(d2h(h.data(), d_ch, (b->nb + 1) * 4));
+  if (changed)
+    for (uint64_t i = 0; i < b->nb; i++) changed[i] = (uint8_t)(h[i] != 0);
+  dfree(d_ch);
+  return RS_OK;
+}

@@ -1,0 +1,237 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the C oracle, byte for byte on wire images (values + container
+types) and exactly on counts."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests.golden_io import load
+
+pytestmark = pytest.mark.gpu
+
+OPS = ("and", "or", "andnot", "xor")
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1709_07821_b200 as p
+    return p
+
+
+def _wires(buf, offs):
+    return [buf[int(offs[i]):int(offs[i + 1])].tobytes() for i in range(len(offs) - 1)]
+
+
+# ------------------------------------------------------------ golden vectors
+
+def test_golden_pairs_batched(pkg):
+    g = load()
+    A = pkg.BitmapBatch.from_wire([g.wire(a) for a in g["pair_a"]])
+    B = pkg.BitmapBatch.from_wire([g.wire(b) for b in g["pair_b"]])
+    for k, op in enumerate(OPS):
+        got = A.pairwise(op, B).to_wire_list()
+        want = [g.wire(r[k]) for r in g["pair_res"]]
+        bad = [i for i, (x, y) in enumerate(zip(got, want)) if x != y]
+        assert not bad, (op, bad[:5])
+        cards = A.pairwise_cardinality(op, B)
+        assert cards.tolist() == [int(c[k]) for c in g["pair_card"]], op
+
+
+def test_golden_container_pairs(pkg):
+    g = load()
+    A = pkg.BitmapBatch.from_wire([g.wire(a) for a in g["cont_a"]])
+    B = pkg.BitmapBatch.from_wire([g.wire(b) for b in g["cont_b"]])
+    for k, op in enumerate(OPS):
+        got = A.container_pairwise(op, B).to_wire_list()
+        want = [g.wire(r[k]) for r in g["cont_res"]]
+        bad = [(i, tuple(g["cont_tags"][i])) for i, (x, y) in enumerate(zip(got, want)) if x != y]
+        assert not bad, (op, bad[:5])
+        cards = A.container_pairwise_cardinality(op, B)
+        assert cards.tolist() == [int(c[k]) for c in g["cont_card"]], op
+
+
+def test_golden_union_many(pkg):
+    g = load()
+    for members, res in zip(g["um_members"], g["um_res"]):
+        ws = [g.wire(m) for m in members]
+        if not ws:
+            assert pkg.RoaringBitmap.union_many([]) == pkg.RoaringBitmap()
+            continue
+        got = pkg.BitmapBatch.from_wire(ws).union_many().to_wire_list()[0]
+        assert got == g.wire(res)
+
+
+def test_golden_from_values_run_optimize_to_array(pkg):
+    g = load()
+    buf, off = g["fv_in_buf"], g["fv_in_off"]
+    arrays = [np.frombuffer(buf[int(off[i]):int(off[i + 1])].tobytes(), dtype="<u8")
+              for i in range(len(off) - 1)]
+    B = pkg.BitmapBatch.from_values(arrays)
+    assert B.to_wire_list() == [g.wire(r) for r in g["fv_res"]]
+    vals = B.to_arrays()
+    for v, a in zip(vals, g["fv_arr"]):
+        assert v.astype("<u4").tobytes() == g.wire(a)
+    changed = B.run_optimize()
+    assert changed.tolist() == [bool(c) for c in g["fv_changed"]]
+    assert B.to_wire_list() == [g.wire(r) for r in g["fv_opt"]]
+
+
+def test_golden_decode_errors(pkg):
+    g = load()
+    for img, off, msg in zip(g["bad"], g["bad_off"], g["bad_msg"]):
+        with pytest.raises(pkg.DecodeError) as e:
+            pkg.BitmapBatch.from_wire([g.wire(img)])
+        assert e.value.offset == off and str(e.value) == msg
+
+
+# ------------------------------------------------ reference API known answers
+
+def test_bitmap_api_known_answers(pkg):
+    RB = pkg.RoaringBitmap
+    a = RB.from_values([1, 3, 5, 7])
+    b = RB.from_values([1, 2, 3, 4, 6, 7, 8, 9])
+    assert [a.op_cardinality(op, b) for op in OPS] == [3, 9, 1, 6]   # test_bitmap.py:78-85
+    assert a.op_cardinality("andnot", a) == 0
+    a = RB.from_values([5, 70000, 200000])
+    b = RB.from_values([5, 200000, 999999])
+    assert (a & b).to_array().tolist() == [5, 200000]                 # test_bitmap.py:88-95
+    assert (a | b).to_array().tolist() == [5, 70000, 200000, 999999]
+    assert (a - b).to_array().tolist() == [70000]
+    assert (a ^ b).to_array().tolist() == [70000, 999999]
+    assert list(a) == [5, 70000, 200000]
+    e = RB()
+    assert len(e) == 0 and not e and e.to_array().size == 0
+    x = RB.from_values([1, 2, 3])
+    assert x.op("or", RB()) == x and len(x.op("xor", x)) == 0
+    with pytest.raises(ValueError):
+        x.op("nand", x)
+    with pytest.raises(ValueError):
+        RB.from_values([1, 1 << 32])
+    before = x.copy()
+    for op in OPS:
+        x.op(op, a)
+        x.op_cardinality(op, a)
+    assert x == before                                                # inputs never mutated
+
+
+def test_container_level_conversions(pkg):
+    # test_containers.py:160-170: on-the-fly type conversion
+    lo = pkg.BitsetContainer(np.zeros(1024, np.uint64), 0)
+    lo = pkg.RoaringBitmap.from_values(range(5000))
+    hi = pkg.RoaringBitmap.from_values(range(4000, 9000))
+    (_, A), = list(lo.chunks())
+    (_, B), = list(hi.chunks())
+    inter = pkg.container_pairwise("and", A, B)
+    assert isinstance(inter, pkg.ArrayContainer) and len(inter) == 1000
+    union = pkg.container_pairwise("or", A, B)
+    assert isinstance(union, pkg.BitsetContainer) and len(union) == 9000
+    wa = pkg.ArrayContainer(np.arange(0, 8000, 2, dtype=np.uint16))
+    wb = pkg.ArrayContainer(np.arange(1, 8000, 2, dtype=np.uint16))
+    u = pkg.container_pairwise("or", wa, wb)
+    assert isinstance(u, pkg.BitsetContainer) and len(u) == 8000
+    assert pkg.container_pairwise_cardinality("xor", wa, wa) == 0
+
+
+# ------------------------------------------------ synthetic configs vs oracle
+
+def _check_pairs(pkg, wa, wb, A, B, ia, ib, ops=OPS, sample=None):
+    idx = np.arange(len(ia)) if sample is None else sample
+    for op in ops:
+        R = A.pairwise(op, B, ia, ib)
+        got = R.to_wire_list()
+        for p in idx:
+            assert got[p] == orc.op(op, wa[ia[p]], wb[ib[p]]), (op, int(p))
+        cards = A.pairwise_cardinality(op, B, ia, ib)
+        want = [orc.op_cardinality(op, wa[ia[p]], wb[ib[p]]) for p in range(len(ia))]
+        assert cards.tolist() == want, op
+        assert R.cardinalities().tolist() == want, op
+
+
+def test_config1_full(pkg):
+    from paper_1709_07821_b200 import synth
+    buf, offs = synth.config1()
+    w = _wires(buf, offs)
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    _check_pairs(pkg, w, w, Bt, Bt, [0], [1])
+
+
+def test_config2_subset(pkg):
+    from paper_1709_07821_b200 import synth
+    buf, offs = synth.config2(npairs=24)
+    w = _wires(buf, offs)
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    ia, ib = list(range(24)), list(range(24, 48))
+    _check_pairs(pkg, w, w, Bt, Bt, ia, ib)
+
+
+def test_config3_subset(pkg):
+    from paper_1709_07821_b200 import synth
+    n = 30000
+    buf, offs = synth.config3(npairs=n)
+    A = pkg.BitmapBatch.from_wire(synth.slice_images(buf, offs, 0, n))
+    B = pkg.BitmapBatch.from_wire(synth.slice_images(buf, offs, n, 2 * n))
+    bA, oA = synth.slice_images(buf, offs, 0, n)
+    bB, oB = synth.slice_images(buf, offs, n, 2 * n)
+    idx = np.arange(n)
+    for op in OPS:
+        got = A.container_pairwise(op, B).to_wire_list()
+        bufA, offA = orc.concat([bA[int(oA[i]):int(oA[i + 1])].tobytes() for i in range(n)])
+        want = orc.op_batch(op, bufA, offA, *orc.concat([bB[int(oB[i]):int(oB[i + 1])].tobytes() for i in range(n)]),
+                            idx, idx)
+        bad = [i for i in range(n) if got[i] != want[i]]
+        assert not bad, (op, bad[:5])
+        cards = A.container_pairwise_cardinality(op, B)
+        wc = orc.container_card_batch(op, bufA, offA, *orc.concat(
+            [bB[int(oB[i]):int(oB[i + 1])].tobytes() for i in range(n)]), idx, idx)
+        assert np.array_equal(cards.astype(np.int64), wc), op
+
+
+def test_config4_subset_pairs_and_union(pkg):
+    from paper_1709_07821_b200 import synth
+    nb = 10
+    buf, offs = synth.config4(nbitmaps=nb)
+    w = _wires(buf, offs)
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    ia, ib = list(range(nb - 1)), list(range(1, nb))
+    _check_pairs(pkg, w, w, Bt, Bt, ia, ib)
+    assert Bt.union_many().to_wire_list()[0] == orc.union_many(w)
+
+
+def test_config5_subset_all_pairs(pkg):
+    from paper_1709_07821_b200 import synth
+    nb = 20
+    buf, offs = synth.config5(nbitmaps=nb)
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    inter, uni = Bt.all_pairs_cardinality()
+    pi, pj = np.triu_indices(nb, 1)
+    want = orc.all_pairs_and(buf, offs, pi, pj)
+    assert np.array_equal(inter.astype(np.int64), want)
+    cards = Bt.cardinalities().astype(np.int64)
+    assert np.array_equal(uni.astype(np.int64), cards[pi] + cards[pj] - want)
+
+
+def test_run_optimize_matches_oracle(pkg):
+    from paper_1709_07821_b200 import synth
+    buf, offs = synth.config5(nbitmaps=6, seed=9)
+    # strip runs first: re-build from values, then run_optimize on the GPU
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    V = pkg.BitmapBatch.from_values(Bt.to_arrays())
+    ch = V.run_optimize()
+    for i, w in enumerate(V.to_wire_list()):
+        ref, rch = orc.run_optimize(orc.from_values(Bt.to_arrays()[i]))
+        assert w == ref and ch[i] == rch
+
+
+def test_edge_cases(pkg):
+    RB = pkg.RoaringBitmap
+    empty = RB()
+    full = RB.from_values(np.arange(0, 1 << 17, dtype=np.uint32))   # two full bitset chunks
+    full.run_optimize()
+    one = RB.from_values([65535])
+    cases = [empty, full, one, RB.from_values([0, 65535, 65536, (1 << 32) - 1])]
+    ws = [c.serialize() for c in cases]
+    for a, wa in zip(cases, ws):
+        for b, wb in zip(cases, ws):
+            for op in OPS:
+                assert a.op(op, b).serialize() == orc.op(op, wa, wb), op
+                assert a.op_cardinality(op, b) == orc.op_cardinality(op, wa, wb)
