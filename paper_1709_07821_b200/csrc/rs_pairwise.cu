@@ -19,12 +19,13 @@
 #include <algorithm>
 #include "rs_internal.cuh"
 #include "rs_dense.cuh"
+#include "rs_array.cuh"
 
 using namespace rs;
 
 namespace {
 
-enum { CLS_COPY = 0, CLS_BB = 1, CLS_AA = 2, CLS_GEN = 3, NCLS = 4 };
+enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, NCLS = 6 };
 
 struct Entries {
   uint16_t *key;
@@ -45,9 +46,9 @@ struct Lists {
 
 __device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { return ia ? ia[p] : (uint32_t)p; }
 
-__device__ __forceinline__ int classify(uint8_t ta, uint8_t tb) {
+__device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
-  if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY) return CLS_AA;
+  if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY) return na + nb <= 256 ? CLS_AAS : na + nb <= 2048 ? CLS_AAM : CLS_AAL;
   return CLS_GEN;
 }
 
@@ -170,7 +171,7 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
     E.cb[e] = cb;
     E.pair[e] = mpair[t];
     E.off[e] = uoff[t];
-    cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], B.type[cb]);
+    cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
   }
   list_append(L, cls, active, e);
 }
@@ -326,6 +327,54 @@ __global__ void __launch_bounds__(DT) k_pair_count(int op, const uint32_t *__res
   }
 }
 
+// ------------------------------------------------- array x array (merge path)
+
+// Materialized array x array pairs: one group of GT threads per pair
+// (array_intersect/union/difference/xor + _container_from_values).
+template <int GT, int VT>
+__global__ void __launch_bounds__(256) k_aa_pair(int op, const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
+                                                 DevBatch A, DevBatch B, Entries E, OutDesc O,
+                                                 uint8_t *__restrict__ opool, uint64_t *__restrict__ res_card) {
+  constexpr int G = 256 / GT;
+  __shared__ __align__(16) rsa::AASmem<GT, VT> sm[G];
+  const int gid = threadIdx.x / GT, lt = threadIdx.x % GT;
+  const uint32_t total = *cnt;
+  for (uint32_t i = blockIdx.x * G + gid; i < total; i += gridDim.x * G) {
+    const uint32_t e = list[i], ca = E.ca[e], cb = E.cb[e];
+    uint8_t type;
+    uint32_t n;
+    uint32_t card = rsa::aa_pair<GT, VT>(op, false, A.pool + A.off[ca], (int)A.card[ca], B.pool + B.off[cb],
+                                         (int)B.card[cb], sm[gid], gid, opool + E.off[e], type, n);
+    if (lt == 0) {
+      O.type[e] = type;
+      O.card[e] = card;
+      O.n[e] = n;
+      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+    rsa::group_sync<GT>(gid);
+  }
+}
+
+// |a ∩ b| of array x array pairs (array_intersect count_only).
+template <int GT, int VT>
+__global__ void __launch_bounds__(256) k_aa_count(const uint32_t *__restrict__ lca, const uint32_t *__restrict__ lcb,
+                                                  const uint32_t *__restrict__ lpair, const uint32_t *__restrict__ cnt,
+                                                  DevBatch A, DevBatch B, uint64_t *__restrict__ acc) {
+  constexpr int G = 256 / GT;
+  __shared__ __align__(16) rsa::AASmem<GT, VT> sm[G];
+  const int gid = threadIdx.x / GT, lt = threadIdx.x % GT;
+  const uint32_t total = *cnt;
+  for (uint32_t i = blockIdx.x * G + gid; i < total; i += gridDim.x * G) {
+    const uint32_t ca = lca[i], cb = lcb[i];
+    uint8_t type;
+    uint32_t n;
+    uint32_t c = rsa::aa_pair<GT, VT>(RS_OP_AND, true, A.pool + A.off[ca], (int)A.card[ca], B.pool + B.off[cb],
+                                      (int)B.card[cb], sm[gid], gid, nullptr, type, n);
+    if (lt == 0 && c) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)c);
+    rsa::group_sync<GT>(gid);
+  }
+}
+
 // ------------------------------------------------------------ compaction
 
 __global__ void k_keep_nonempty(uint64_t E, const uint32_t *__restrict__ card, uint32_t *__restrict__ keep) {
@@ -373,7 +422,7 @@ __global__ void k_match(uint64_t Ma, uint64_t npairs, const uint64_t *__restrict
       ca = (uint32_t)(a0 + l);
       cb = (uint32_t)(b0 + j);
       p32 = (uint32_t)p;
-      cls = classify(A.type[ca], B.type[cb]);
+      cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
     }
   }
   // append (ca) to the class list; cb/pair go to parallel arrays at the same slot
@@ -427,7 +476,7 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
     E.cb[p] = cb;
     E.pair[p] = (uint32_t)p;
     ub[p] = rs_pad16(rs_result_ub(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op));
-    cls = classify(A.type[ca], B.type[cb]);
+    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
   } else if (p == npairs) {
     ub[p] = 0;
   }
@@ -443,7 +492,7 @@ __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint3
   if (active) {
     ca = (uint32_t)A.bm_start[pair_a(ia, p)];
     cb = (uint32_t)B.bm_start[pair_a(ib, p)];
-    cls = classify(A.type[ca], B.type[cb]);
+    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
   }
   unsigned lane = threadIdx.x & 31;
 #pragma unroll
@@ -533,7 +582,12 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     RS_LAUNCH_PROF("copy", hcnt[CLS_COPY], k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O, b->d_pool, b->d_bm_card);
   }
   RS_LAUNCH_PROF("bitset_pair", hcnt[CLS_BB], k_pair_dense<false>, hcnt[CLS_BB], DT, 0, op, L.list[CLS_BB], dA, dB, En, O, b->d_pool, b->d_bm_card);
-  RS_LAUNCH_PROF("array_pair", hcnt[CLS_AA], k_pair_dense<true>, hcnt[CLS_AA], DT, 0, op, L.list[CLS_AA], dA, dB, En, O, b->d_pool, b->d_bm_card);
+  RS_LAUNCH_PROF("array_pair_s", hcnt[CLS_AAS], (k_aa_pair<32, 8>), grid_for(hcnt[CLS_AAS], 8), 256, 0, op,
+                 L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  RS_LAUNCH_PROF("array_pair_m", hcnt[CLS_AAM], (k_aa_pair<128, 16>), grid_for(hcnt[CLS_AAM], 2), 256, 0, op,
+                 L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  RS_LAUNCH_PROF("array_pair_l", hcnt[CLS_AAL], (k_aa_pair<256, 32>), hcnt[CLS_AAL], 256, 0, op,
+                 L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
   RS_LAUNCH_PROF("generic_pair", hcnt[CLS_GEN], k_pair_dense<true>, hcnt[CLS_GEN], DT, 0, op, L.list[CLS_GEN], dA, dB, En, O, b->d_pool, b->d_bm_card);
   // compaction: drop empty results (bitmap.py:185-188)
   RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, O.card, keep2);
@@ -658,8 +712,12 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
   const unsigned pg = 148 * 8;
   RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB], lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap,
             L.cnt + CLS_BB, dA, dB, inter);
-  RS_LAUNCH_PROF("array_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_AA], lcb + CLS_AA * L.cap, lpair + CLS_AA * L.cap,
-            L.cnt + CLS_AA, dA, dB, inter);
+  RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
+                 lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
+  RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
+                 lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
+  RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
+                 lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
   RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN], lcb + CLS_GEN * L.cap,
             lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
   return RS_OK;
