@@ -94,7 +94,7 @@ __device__ __forceinline__ void merge_walk(int op, const uint16_t *A, int na, co
 }
 
 template <int GT, int VT>
-struct AASmem {
+struct alignas(16) AASmem {
   static constexpr int CAP = GT * VT;                       // merged items per group
   static constexpr int CAPA = CAP < 4096 ? CAP : 4096;      // one side
   static constexpr bool BITSET = CAP > 4096;                // result can exceed 4096 values

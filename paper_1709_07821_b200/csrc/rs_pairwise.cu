@@ -20,6 +20,7 @@
 #include "rs_internal.cuh"
 #include "rs_dense.cuh"
 #include "rs_array.cuh"
+#include "rs_bitset.cuh"
 
 using namespace rs;
 
@@ -40,7 +41,8 @@ struct OutDesc {
 
 struct Lists {
   uint32_t *list[NCLS];
-  uint32_t *cnt;  // device counters [NCLS]
+  uint32_t *cnt;           // device counters [NCLS]
+  uint64_t *aoff, *boff;   // bitset x bitset items: operand payload offsets (one load for the TMA producer)
   uint64_t cap;
 };
 
@@ -52,9 +54,12 @@ __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uin
   return CLS_GEN;
 }
 
-// warp-aggregated append of `item` to list[cls]
-__device__ __forceinline__ void list_append(Lists L, int cls, bool active, uint32_t item) {
+// warp-aggregated append of `item` to list[cls] (returns the slot); bitset x
+// bitset items also record their operand payload offsets
+__device__ __forceinline__ uint32_t list_append(Lists L, int cls, bool active, uint32_t item, uint64_t aoff = 0,
+                                                uint64_t boff = 0) {
   unsigned lane = threadIdx.x & 31;
+  uint32_t slot = 0;
 #pragma unroll
   for (int c = 0; c < NCLS; c++) {
     unsigned m = __ballot_sync(0xffffffffu, active && cls == c);
@@ -63,8 +68,16 @@ __device__ __forceinline__ void list_append(Lists L, int cls, bool active, uint3
     uint32_t base = 0;
     if ((int)lane == leader) base = atomicAdd(&L.cnt[c], (uint32_t)__popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (active && cls == c) L.list[c][base + __popc(m & ((1u << lane) - 1))] = item;
+    if (active && cls == c) {
+      slot = base + __popc(m & ((1u << lane) - 1));
+      L.list[c][slot] = item;
+      if (c == CLS_BB) {
+        L.aoff[slot] = aoff;
+        L.boff[slot] = boff;
+      }
+    }
   }
+  return slot;
 }
 
 __global__ void k_pair_msize(uint64_t npairs, DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib,
@@ -163,6 +176,7 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
   bool active = t < M && keep[t];
   int cls = CLS_COPY;
   uint32_t e = 0;
+  uint64_t ao = 0, bo = 0;
   if (active) {
     e = epos[t];
     uint32_t ca = mca[t], cb = mcb[t];
@@ -172,8 +186,12 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
     E.pair[e] = mpair[t];
     E.off[e] = uoff[t];
     cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
+    if (cls == CLS_BB) {
+      ao = A.off[ca];
+      bo = B.off[cb];
+    }
   }
-  list_append(L, cls, active, e);
+  list_append(L, cls, active, e, ao, bo);
 }
 
 // per-pair first entry index (estart[npairs] = total entries)
@@ -327,6 +345,111 @@ __global__ void __launch_bounds__(DT) k_pair_count(int op, const uint32_t *__res
   }
 }
 
+// ------------------------------------- bitset x bitset, persistent + TMA ring
+
+template <int STAGES>
+__global__ void __launch_bounds__(rsb::BT) k_bb_op(int op, const uint32_t *__restrict__ list,
+                                                    const uint64_t *__restrict__ laoff, const uint64_t *__restrict__ lboff,
+                                                    uint32_t count, DevBatch A, DevBatch B, Entries E, OutDesc O,
+                                                    uint8_t *__restrict__ opool, uint64_t *__restrict__ res_card) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  auto &sm = *reinterpret_cast<rsb::BBSmem<STAGES> *>(smraw);
+  auto src = [&](uint32_t i, const uint8_t *&pa, const uint8_t *&pb) {
+    pa = A.pool + laoff[i];
+    pb = B.pool + lboff[i];
+  };
+  auto sink = [&](uint32_t i, const uint64_t *r, uint32_t pc, uint32_t card) {
+    const uint32_t e = list[i];
+    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pc, card, opool + E.off[e]);
+    if (threadIdx.x == 0) {
+      O.type[e] = card > RS_ARRAY_MAX ? RS_TAG_BITSET : RS_TAG_ARRAY;
+      O.card[e] = card;
+      O.n[e] = n;
+      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+  };
+  rsb::bb_loop<STAGES>(sm, count, op, src, sink);
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(rsb::BT) k_bb_count(int op, const uint64_t *__restrict__ laoff,
+                                                       const uint64_t *__restrict__ lboff, const uint32_t *__restrict__ lpair,
+                                                       const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                                                       uint64_t *__restrict__ acc) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  auto &sm = *reinterpret_cast<rsb::BBSmem<STAGES> *>(smraw);
+  auto src = [&](uint32_t i, const uint8_t *&pa, const uint8_t *&pb) {
+    pa = A.pool + laoff[i];
+    pb = B.pool + lboff[i];
+  };
+  auto sink = [&](uint32_t i, const uint64_t *, uint32_t, uint32_t card) {
+    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)card);
+  };
+  rsb::bb_loop<STAGES>(sm, *cnt, op, src, sink);
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+// RS_BB_KERNEL=dense selects the register-fed kernels (A/B testing);
+// RS_BB_STAGES picks the TMA ring depth (2, 3 or 4).
+int bb_kernel_choice() {
+  static int choice = -1;
+  if (choice < 0) {
+    const char *v = getenv("RS_BB_KERNEL");
+    choice = (v && std::string(v) == "dense") ? 0 : 1;
+  }
+  return choice;
+}
+
+int bb_stages() {
+  static int s = -1;
+  if (s < 0) {
+    s = env_int("RS_BB_STAGES", 2);
+    if (s < 2 || s > 4) s = 2;
+  }
+  return s;
+}
+
+template <typename K>
+unsigned persistent_grid(K kernel, size_t smem, uint64_t count) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, rsb::BT, smem);
+  uint64_t g = (uint64_t)sms * (per > 0 ? per : 1);
+  return (unsigned)(count < g ? count : g);
+}
+
+template <int S>
+int launch_bb_op(int op, const Lists &L, uint32_t count, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
+                 uint8_t *pool, uint64_t *res_card) {
+  const size_t smem = sizeof(rsb::BBSmem<S>);
+  static bool attr = false;
+  if (!attr) {
+    RS_CK(cudaFuncSetAttribute(k_bb_op<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  RS_LAUNCH_PROF("bitset_pair", count, k_bb_op<S>, persistent_grid(k_bb_op<S>, smem, count), rsb::BT, smem, op,
+                 L.list[CLS_BB], L.aoff, L.boff, count, dA, dB, En, O, pool, res_card);
+  return RS_OK;
+}
+
+template <int S>
+int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch dB, uint64_t *inter) {
+  const size_t smem = sizeof(rsb::BBSmem<S>);
+  static bool attr = false;
+  if (!attr) {
+    RS_CK(cudaFuncSetAttribute(k_bb_count<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  RS_LAUNCH_PROF("bitset_count", 0, k_bb_count<S>, persistent_grid(k_bb_count<S>, smem, L.cap), rsb::BT, smem, op,
+                 L.aoff, L.boff, lpair, L.cnt + CLS_BB, dA, dB, inter);
+  return RS_OK;
+}
+
 // ------------------------------------------------- array x array (merge path)
 
 // Materialized array x array pairs: one group of GT threads per pair
@@ -402,6 +525,23 @@ __global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ estart,
 
 // -------------------------------------------------- count-only join + formula
 
+// count-path append: ca into the class list, cb / pair into parallel arrays
+// at the same slot (and the operand offsets for bitset x bitset items)
+__device__ __forceinline__ void count_append(Lists L, int cls, bool active, uint32_t ca, uint32_t cb, uint32_t pair,
+                                             uint32_t *lcb_base, uint32_t *lpair_base, const DevBatch &A,
+                                             const DevBatch &B) {
+  uint64_t ao = 0, bo = 0;
+  if (active && cls == CLS_BB) {
+    ao = A.off[ca];
+    bo = B.off[cb];
+  }
+  uint32_t slot = list_append(L, cls, active, ca, ao, bo);
+  if (active) {
+    lcb_base[cls * L.cap + slot] = cb;
+    lpair_base[cls * L.cap + slot] = pair;
+  }
+}
+
 __global__ void k_match(uint64_t Ma, uint64_t npairs, const uint64_t *__restrict__ mbase, DevBatch A, DevBatch B,
                         const uint32_t *ia, const uint32_t *ib, Lists L, uint32_t *__restrict__ lcb_base,
                         uint32_t *__restrict__ lpair_base) {
@@ -425,23 +565,7 @@ __global__ void k_match(uint64_t Ma, uint64_t npairs, const uint64_t *__restrict
       cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
     }
   }
-  // append (ca) to the class list; cb/pair go to parallel arrays at the same slot
-  unsigned lane = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 1; c < NCLS; c++) {
-    unsigned m = __ballot_sync(0xffffffffu, active && cls == c);
-    if (!m) continue;
-    int leader = __ffs(m) - 1;
-    uint32_t base = 0;
-    if ((int)lane == leader) base = atomicAdd(&L.cnt[c], (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (active && cls == c) {
-      uint64_t slot = base + __popc(m & ((1u << lane) - 1));
-      L.list[c][slot] = ca;
-      lcb_base[c * L.cap + slot] = cb;
-      lpair_base[c * L.cap + slot] = p32;
-    }
-  }
+  count_append(L, cls, active, ca, cb, p32, lcb_base, lpair_base, A, B);
 }
 
 // bitmap.py:235-241: every count from |A ∩ B|
@@ -469,6 +593,7 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
   uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   bool active = p < npairs;
   int cls = CLS_GEN;
+  uint64_t ao = 0, bo = 0;
   if (active) {
     uint32_t ca = (uint32_t)A.bm_start[pair_a(ia, p)], cb = (uint32_t)B.bm_start[pair_a(ib, p)];
     E.key[p] = A.key[ca];
@@ -477,10 +602,14 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
     E.pair[p] = (uint32_t)p;
     ub[p] = rs_pad16(rs_result_ub(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op));
     cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
+    if (cls == CLS_BB) {
+      ao = A.off[ca];
+      bo = B.off[cb];
+    }
   } else if (p == npairs) {
     ub[p] = 0;
   }
-  list_append(L, cls, active, (uint32_t)p);
+  list_append(L, cls, active, (uint32_t)p, ao, bo);
 }
 
 __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib, Lists L,
@@ -494,22 +623,7 @@ __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint3
     cb = (uint32_t)B.bm_start[pair_a(ib, p)];
     cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
   }
-  unsigned lane = threadIdx.x & 31;
-#pragma unroll
-  for (int c = 1; c < NCLS; c++) {
-    unsigned m = __ballot_sync(0xffffffffu, active && cls == c);
-    if (!m) continue;
-    int leader = __ffs(m) - 1;
-    uint32_t base = 0;
-    if ((int)lane == leader) base = atomicAdd(&L.cnt[c], (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (active && cls == c) {
-      uint64_t slot = base + __popc(m & ((1u << lane) - 1));
-      L.list[c][slot] = ca;
-      lcb_base[c * L.cap + slot] = cb;
-      lpair_base[c * L.cap + slot] = (uint32_t)p;
-    }
-  }
+  count_append(L, cls, active, ca, cb, (uint32_t)p, lcb_base, lpair_base, A, B);
 }
 
 // ------------------------------------------------------------- host side
@@ -581,7 +695,17 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     unsigned g = std::min<uint64_t>(grid_for(hcnt[CLS_COPY], 8), 148 * 16);
     RS_LAUNCH_PROF("copy", hcnt[CLS_COPY], k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O, b->d_pool, b->d_bm_card);
   }
-  RS_LAUNCH_PROF("bitset_pair", hcnt[CLS_BB], k_pair_dense<false>, hcnt[CLS_BB], DT, 0, op, L.list[CLS_BB], dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (bb_kernel_choice() == 0) {
+    RS_LAUNCH_PROF("bitset_pair", hcnt[CLS_BB], k_pair_dense<false>, hcnt[CLS_BB], DT, 0, op, L.list[CLS_BB], dA, dB,
+                   En, O, b->d_pool, b->d_bm_card);
+  } else if (hcnt[CLS_BB]) {
+    const uint32_t n = hcnt[CLS_BB];
+    switch (bb_stages()) {
+      case 3: RS_TRY(launch_bb_op<3>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+      case 4: RS_TRY(launch_bb_op<4>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+      default: RS_TRY(launch_bb_op<2>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+    }
+  }
   RS_LAUNCH_PROF("array_pair_s", hcnt[CLS_AAS], (k_aa_pair<32, 8>), grid_for(hcnt[CLS_AAS], 8), 256, 0, op,
                  L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
   RS_LAUNCH_PROF("array_pair_m", hcnt[CLS_AAM], (k_aa_pair<128, 16>), grid_for(hcnt[CLS_AAM], 2), 256, 0, op,
@@ -605,6 +729,8 @@ Lists make_lists(Scratch &S, uint64_t cap) {
   L.cap = cap ? cap : 1;
   for (int c = 0; c < NCLS; c++) L.list[c] = (uint32_t *)S.get(L.cap * 4);
   L.cnt = (uint32_t *)S.get(NCLS * 4);
+  L.aoff = (uint64_t *)S.get(L.cap * 8);
+  L.boff = (uint64_t *)S.get(L.cap * 8);
   return L;
 }
 
@@ -710,8 +836,17 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
                   uint64_t *inter) {
   DevBatch dA = A->dev(), dB = B->dev();
   const unsigned pg = 148 * 8;
-  RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB], lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap,
-            L.cnt + CLS_BB, dA, dB, inter);
+  if (bb_kernel_choice() == 0) {
+    RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB],
+                   lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap, L.cnt + CLS_BB, dA, dB, inter);
+  } else {
+    uint32_t *lp = lpair + CLS_BB * L.cap;
+    switch (bb_stages()) {
+      case 3: RS_TRY(launch_bb_count<3>(op_kernel, L, lp, dA, dB, inter)); break;
+      case 4: RS_TRY(launch_bb_count<4>(op_kernel, L, lp, dA, dB, inter)); break;
+      default: RS_TRY(launch_bb_count<2>(op_kernel, L, lp, dA, dB, inter)); break;
+    }
+  }
   RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
                  lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
   RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
