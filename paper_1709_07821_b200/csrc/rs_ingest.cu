@@ -276,6 +276,9 @@ extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint
   dfree(staged); dfree(d_src); dfree(d_vcode); dfree(d_vval); dfree(d_any);
   if (result != RS_OK) { rs_batch_free(b); return result; }
   b->h_bm_start = bm_start;
+  uint8_t tm = 0;
+  for (uint8_t t : type) tm |= (uint8_t)(1u << t);
+  b->type_mask = tm;
   b->h_valid = true;
   RS_TRY(finalize_batch(b));
   *out = b;
@@ -490,6 +493,7 @@ extern "C" int rs_batch_from_u32(const uint32_t *vals, const uint64_t *offs, uin
   dfree(cflag); dfree(cpos); dfree(cstart); dfree(psize); dfree(d_offs); dfree(d_v); dfree(segstart); dfree(d_flag);
   RS_TRY(finalize_batch(b));
   b->h_valid = false;
+  b->type_mask = (1u << RS_TAG_ARRAY) | (1u << RS_TAG_BITSET);  // from_values never builds runs
   RS_TRY(fetch_host_meta(b));
   *out = b;
   return RS_OK;
@@ -552,6 +556,8 @@ extern "C" int rs_batch_concat(const rs_batch *const *parts, uint64_t nparts, rs
   int rc = batch_alloc(b, nb, nc, pool);
   if (rc) { rs_batch_free(b); return rc; }
   b->h_bm_start.assign(1, 0);
+  b->type_mask = 0;
+  for (uint64_t k = 0; k < nparts; k++) b->type_mask |= parts[k]->type_mask;
   uint64_t cb = 0, bb = 0, pb = 0;
   for (uint64_t k = 0; k < nparts; k++) {
     const rs_batch *p = parts[k];
@@ -601,6 +607,7 @@ extern "C" int rs_batch_select(const rs_batch *S, const uint64_t *idx, uint64_t 
   dfree(d_ns); dfree(d_ss); dfree(psize); dfree(poff);
   RS_TRY(finalize_batch(b));
   b->h_bm_start = new_start;
+  b->type_mask = S->type_mask;
   b->h_valid = true;
   *out = b;
   return RS_OK;

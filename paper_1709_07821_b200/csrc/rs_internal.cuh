@@ -51,6 +51,9 @@ struct rs_batch {
   // host mirror of bm_start (fetched lazily for op results)
   std::vector<uint64_t> h_bm_start;
   bool h_valid = false;
+  // container types that may be present (bit t = type t); lets the op
+  // pipeline skip type-pair classes that cannot occur
+  uint8_t type_mask = 0xFF;
   DevBatch dev() const {
     DevBatch d;
     d.nb = nb; d.nc = nc; d.bm_start = d_bm_start; d.key = d_key; d.type = d_type;
@@ -76,6 +79,8 @@ template <typename T> int scan_exclusive(const T *in, T *out, uint64_t n);
 template <typename T> int scan_inclusive(const T *in, T *out, uint64_t n);
 int sort_u64(uint64_t *keys, uint64_t n, int end_bit);
 int d2h(void *h, const void *d, size_t bytes);   // synchronous on g_stream
+// RS_TRACE=1: synchronize and print host wall time per phase (diagnostics only)
+void trace(const char *phase);
 // live per-kernel timing (bench roofline): events around tagged launches
 extern bool g_prof_on;
 void prof_mark(const char *name, cudaEvent_t a, cudaEvent_t b, uint64_t items);

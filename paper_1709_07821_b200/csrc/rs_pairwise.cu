@@ -239,12 +239,15 @@ using namespace rsd;
 // (bitset_op_with_count + _container_from_words, containers.py:463-465).
 // GEN=true: any matched pair; array/run sides are densified in smem first.
 template <bool GEN>
-__global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__restrict__ list, DevBatch A, DevBatch B,
+__global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__restrict__ list,
+                                                   const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
                                                    Entries E, OutDesc O, uint8_t *__restrict__ opool,
                                                    uint64_t *__restrict__ res_card) {
   __shared__ __align__(16) DenseSmem sm;
   const int t = threadIdx.x;
-  const uint32_t e = list[blockIdx.x];
+  const uint32_t total = *cnt;
+  for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+  const uint32_t e = list[item];
   const uint32_t ca = E.ca[e], cb = E.cb[e];
   uint8_t ta = RS_TAG_BITSET, tb = RS_TAG_BITSET;
   uint64_t ra[4], rb[4];
@@ -303,6 +306,8 @@ __global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__res
     O.n[e] = n;
     if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
   }
+  __syncthreads();  // smem reuse by the next item
+  }
 }
 
 // Count-only: |a AND b| accumulated per bitmap pair (container_pairwise_cardinality
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(DT) k_pair_count(int op, const uint32_t *__res
 template <int STAGES>
 __global__ void __launch_bounds__(rsb::BT) k_bb_op(int op, const uint32_t *__restrict__ list,
                                                     const uint64_t *__restrict__ laoff, const uint64_t *__restrict__ lboff,
-                                                    uint32_t count, DevBatch A, DevBatch B, Entries E, OutDesc O,
+                                                    const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B, Entries E, OutDesc O,
                                                     uint8_t *__restrict__ opool, uint64_t *__restrict__ res_card) {
   extern __shared__ __align__(128) uint8_t smraw[];
   auto &sm = *reinterpret_cast<rsb::BBSmem<STAGES> *>(smraw);
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_op(int op, const uint32_t *__res
       if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
     }
   };
-  rsb::bb_loop<STAGES>(sm, count, op, src, sink);
+  rsb::bb_loop<STAGES>(sm, *cnt, op, src, sink);
 }
 
 template <int STAGES>
@@ -424,7 +429,7 @@ unsigned persistent_grid(K kernel, size_t smem, uint64_t count) {
 }
 
 template <int S>
-int launch_bb_op(int op, const Lists &L, uint32_t count, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
+int launch_bb_op(int op, const Lists &L, uint64_t count, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
                  uint8_t *pool, uint64_t *res_card) {
   const size_t smem = sizeof(rsb::BBSmem<S>);
   static bool attr = false;
@@ -432,8 +437,8 @@ int launch_bb_op(int op, const Lists &L, uint32_t count, DevBatch dA, DevBatch d
     RS_CK(cudaFuncSetAttribute(k_bb_op<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  RS_LAUNCH_PROF("bitset_pair", count, k_bb_op<S>, persistent_grid(k_bb_op<S>, smem, count), rsb::BT, smem, op,
-                 L.list[CLS_BB], L.aoff, L.boff, count, dA, dB, En, O, pool, res_card);
+  RS_LAUNCH_PROF("bitset_pair", 0, k_bb_op<S>, persistent_grid(k_bb_op<S>, smem, count), rsb::BT, smem, op,
+                 L.list[CLS_BB], L.aoff, L.boff, L.cnt + CLS_BB, dA, dB, En, O, pool, res_card);
   return RS_OK;
 }
 
@@ -500,12 +505,14 @@ __global__ void __launch_bounds__(256) k_aa_count(const uint32_t *__restrict__ l
 
 // ------------------------------------------------------------ compaction
 
-__global__ void k_keep_nonempty(uint64_t E, const uint32_t *__restrict__ card, uint32_t *__restrict__ keep) {
+__global__ void k_keep_nonempty(uint64_t E, const uint64_t *__restrict__ dE, const uint32_t *__restrict__ card,
+                                uint32_t *__restrict__ keep) {
   uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (e <= E) keep[e] = e < E && card[e] > 0;
+  const uint64_t lim = dE ? *dE : E;
+  if (e <= E) keep[e] = e < lim && card[e] > 0;
 }
 
-__global__ void k_compact(uint64_t E, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ fpos, Entries En,
+__global__ void k_compact(uint64_t E, const uint64_t *__restrict__ dE, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ fpos, Entries En,
                           OutDesc O, uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn, uint64_t *off) {
   uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (e >= E || !keep[e]) return;
@@ -675,10 +682,45 @@ int upload_pairs(Scratch &S, const rs_batch *A, const rs_batch *B, const uint32_
   return RS_OK;
 }
 
+// Which work classes can occur between batches with these container-type
+// masks (bit t = type t present)?  Impossible classes are never launched.
+struct ClassMask {
+  bool bb, aa, gen;
+};
+ClassMask class_mask(uint8_t ma, uint8_t mb) {
+  const uint8_t AR = 1 << RS_TAG_ARRAY, BS = 1 << RS_TAG_BITSET, RN = 1 << RS_TAG_RUN;
+  ClassMask m;
+  m.bb = (ma & BS) && (mb & BS);
+  m.aa = (ma & AR) && (mb & AR);
+  m.gen = ((ma | mb) & RN) || ((ma & AR) && (mb & BS)) || ((ma & BS) && (mb & AR));
+  return m;
+}
+
+// container types an op result may hold (run results need a run input)
+uint8_t result_mask(uint8_t ma, uint8_t mb) {
+  const uint8_t AR = 1 << RS_TAG_ARRAY, BS = 1 << RS_TAG_BITSET, RN = 1 << RS_TAG_RUN;
+  return (uint8_t)(AR | BS | ((ma | mb) & RN));
+}
+
+unsigned sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return (unsigned)sms;
+}
+
 // Run the per-class kernels over prepared entries, then compact into `out`.
+// Exact mode: hcnt holds the class sizes (host) and E/P are exact.  Upper-
+// bound mode (hcnt == nullptr): E/P are capacities, the real entry count is
+// *dE on the device, and every class kernel is persistent over its device
+// counter -- the op then runs without any host synchronization.
 int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratch &S, Entries En, Lists L,
-                            uint64_t E, uint64_t P, const uint32_t *hcnt, const uint64_t *d_estart, uint64_t npairs,
-                            rs_batch **out) {
+                            uint64_t E, uint64_t P, const uint32_t *hcnt, const uint64_t *dE,
+                            const uint64_t *d_estart, uint64_t npairs, rs_batch **out) {
   OutDesc O;
   O.type = (uint8_t *)S.get(E + 1);
   O.card = (uint32_t *)S.get((E + 1) * 4);
@@ -688,35 +730,49 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   rs_batch *b = new rs_batch();
   int rc = batch_alloc(b, npairs, E, P);
   if (rc) { rs_batch_free(b); return rc; }
+  b->type_mask = result_mask(A->type_mask, B->type_mask);
   RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
   DevBatch dA = A->dev(), dB = B->dev();
-  // copies: warps over the list (8 warps per CTA)
-  if (hcnt[CLS_COPY]) {
-    unsigned g = std::min<uint64_t>(grid_for(hcnt[CLS_COPY], 8), 148 * 16);
-    RS_LAUNCH_PROF("copy", hcnt[CLS_COPY], k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  const ClassMask cm = class_mask(A->type_mask, B->type_mask);
+  const unsigned sms = sm_count();
+  auto want = [&](int c, bool possible) -> uint64_t {  // 0 = skip, else capacity for the grid
+    if (hcnt) return hcnt[c];
+    return possible ? L.cap : 0;
+  };
+  // copies: persistent warps over the list (8 warps per CTA)
+  if (uint64_t n = want(CLS_COPY, true)) {
+    unsigned g = std::min<uint64_t>(grid_for(n, 8), sms * 16);
+    RS_LAUNCH_PROF("copy", hcnt ? n : 0, k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O,
+                   b->d_pool, b->d_bm_card);
   }
-  if (bb_kernel_choice() == 0) {
-    RS_LAUNCH_PROF("bitset_pair", hcnt[CLS_BB], k_pair_dense<false>, hcnt[CLS_BB], DT, 0, op, L.list[CLS_BB], dA, dB,
-                   En, O, b->d_pool, b->d_bm_card);
-  } else if (hcnt[CLS_BB]) {
-    const uint32_t n = hcnt[CLS_BB];
-    switch (bb_stages()) {
-      case 3: RS_TRY(launch_bb_op<3>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
-      case 4: RS_TRY(launch_bb_op<4>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
-      default: RS_TRY(launch_bb_op<2>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+  if (uint64_t n = want(CLS_BB, cm.bb)) {
+    if (bb_kernel_choice() == 0) {
+      RS_LAUNCH_PROF("bitset_pair", hcnt ? n : 0, k_pair_dense<false>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
+                     L.list[CLS_BB], L.cnt + CLS_BB, dA, dB, En, O, b->d_pool, b->d_bm_card);
+    } else {
+      switch (bb_stages()) {
+        case 3: RS_TRY(launch_bb_op<3>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+        case 4: RS_TRY(launch_bb_op<4>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+        default: RS_TRY(launch_bb_op<2>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+      }
     }
   }
-  RS_LAUNCH_PROF("array_pair_s", hcnt[CLS_AAS], (k_aa_pair<32, 8>), grid_for(hcnt[CLS_AAS], 8), 256, 0, op,
-                 L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  RS_LAUNCH_PROF("array_pair_m", hcnt[CLS_AAM], (k_aa_pair<128, 16>), grid_for(hcnt[CLS_AAM], 2), 256, 0, op,
-                 L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  RS_LAUNCH_PROF("array_pair_l", hcnt[CLS_AAL], (k_aa_pair<256, 32>), hcnt[CLS_AAL], 256, 0, op,
-                 L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  RS_LAUNCH_PROF("generic_pair", hcnt[CLS_GEN], k_pair_dense<true>, hcnt[CLS_GEN], DT, 0, op, L.list[CLS_GEN], dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (uint64_t n = want(CLS_AAS, cm.aa))
+    RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
+                   0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (uint64_t n = want(CLS_AAM, cm.aa))
+    RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
+                   256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (uint64_t n = want(CLS_AAL, cm.aa))
+    RS_LAUNCH_PROF("array_pair_l", hcnt ? n : 0, (k_aa_pair<256, 32>), std::min<uint64_t>(n, sms * 8), 256, 0, op,
+                   L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (uint64_t n = want(CLS_GEN, cm.gen))
+    RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
+                   L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, b->d_bm_card);
   // compaction: drop empty results (bitmap.py:185-188)
-  RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, O.card, keep2);
+  RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, dE, O.card, keep2);
   RS_TRY(scan_exclusive<uint32_t>(keep2, fpos, E + 1));
-  RS_LAUNCH(k_compact, grid_for(E, 256), 256, 0, E, keep2, fpos, En, O, b->d_key, b->d_type, b->d_card, b->d_n,
+  RS_LAUNCH(k_compact, grid_for(E, 256), 256, 0, E, dE, keep2, fpos, En, O, b->d_key, b->d_type, b->d_card, b->d_n,
             b->d_off);
   RS_LAUNCH(k_bm_start, grid_for(npairs + 1, 256), 256, 0, npairs, d_estart, fpos, b->d_bm_start);
   b->h_valid = false;
@@ -746,11 +802,17 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   Scratch S;
   uint32_t *dia, *dib;
   RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
-  uint64_t M = 0;
+  uint64_t M = 0, Ecap = 0;
   for (uint64_t p = 0; p < npairs; p++) {
     uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
-    M += (A->h_bm_start[a + 1] - A->h_bm_start[a]) + (B->h_bm_start[b + 1] - B->h_bm_start[b]);
+    uint64_t na = A->h_bm_start[a + 1] - A->h_bm_start[a], nb = B->h_bm_start[b + 1] - B->h_bm_start[b];
+    M += na + nb;
+    Ecap += op == RS_OP_AND ? std::min(na, nb) : op == RS_OP_ANDNOT ? na : na + nb;
   }
+  // Upper-bound mode (no host sync) when an 8 KB slot per possible output
+  // container costs at most ~2x the inputs' pools; else size exactly.
+  const bool ub_mode = env_int("RS_EXACT_ALLOC", 0) == 0 &&
+                       8192.0 * (double)Ecap <= 2.0 * (double)(A->pool_bytes + B->pool_bytes) + 64e6;
   uint64_t *msz = (uint64_t *)S.get((npairs + 1) * 8), *mbase = (uint64_t *)S.get((npairs + 1) * 8);
   uint16_t *mkey = (uint16_t *)S.get((M + 1) * 2);
   uint32_t *mca = (uint32_t *)S.get((M + 1) * 4), *mcb = (uint32_t *)S.get((M + 1) * 4),
@@ -778,14 +840,17 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
   RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L);
   RS_LAUNCH(k_estart, grid_for(npairs + 1, 256), 256, 0, npairs, mbase, epos, estart);
-  // one host sync: totals for allocation and exact grids
+  if (ub_mode)
+    return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr,
+                                   estart + npairs, estart, npairs, out);
+  // exact mode: one host sync for the totals, then exact grids
   struct { uint32_t E; uint32_t pad; uint64_t P; uint32_t cnt[NCLS]; } h;
   RS_CK(cudaMemcpyAsync(&h.E, epos + M, 4, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaMemcpyAsync(&h.P, uoff + M, 8, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaMemcpyAsync(h.cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaStreamSynchronize(g_stream));
   (void)tot;
-  return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, estart, npairs, out);
+  return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, nullptr, estart, npairs, out);
 }
 
 extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia,
@@ -828,33 +893,39 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   RS_CK(cudaMemcpyAsync(&P, En.off + npairs, 8, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaMemcpyAsync(cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaStreamSynchronize(g_stream));
-  return run_classes_and_compact(op, A, B, S, En, L, npairs, P, cnt, estart, npairs, out);
+  return run_classes_and_compact(op, A, B, S, En, L, npairs, P, cnt, nullptr, estart, npairs, out);
 }
 
 namespace {
 int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, uint32_t *lcb, uint32_t *lpair,
                   uint64_t *inter) {
   DevBatch dA = A->dev(), dB = B->dev();
-  const unsigned pg = 148 * 8;
-  if (bb_kernel_choice() == 0) {
-    RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB],
-                   lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap, L.cnt + CLS_BB, dA, dB, inter);
-  } else {
-    uint32_t *lp = lpair + CLS_BB * L.cap;
-    switch (bb_stages()) {
-      case 3: RS_TRY(launch_bb_count<3>(op_kernel, L, lp, dA, dB, inter)); break;
-      case 4: RS_TRY(launch_bb_count<4>(op_kernel, L, lp, dA, dB, inter)); break;
-      default: RS_TRY(launch_bb_count<2>(op_kernel, L, lp, dA, dB, inter)); break;
+  const ClassMask cm = class_mask(A->type_mask, B->type_mask);
+  const unsigned pg = sm_count() * 8;
+  if (cm.bb) {
+    if (bb_kernel_choice() == 0) {
+      RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB],
+                     lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap, L.cnt + CLS_BB, dA, dB, inter);
+    } else {
+      uint32_t *lp = lpair + CLS_BB * L.cap;
+      switch (bb_stages()) {
+        case 3: RS_TRY(launch_bb_count<3>(op_kernel, L, lp, dA, dB, inter)); break;
+        case 4: RS_TRY(launch_bb_count<4>(op_kernel, L, lp, dA, dB, inter)); break;
+        default: RS_TRY(launch_bb_count<2>(op_kernel, L, lp, dA, dB, inter)); break;
+      }
     }
   }
-  RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
-                 lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
-  RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
-                 lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
-  RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
-                 lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
-  RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN], lcb + CLS_GEN * L.cap,
-            lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
+  if (cm.aa) {
+    RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
+                   lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
+    RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
+                   lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
+    RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
+                   lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
+  }
+  if (cm.gen)
+    RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN],
+                   lcb + CLS_GEN * L.cap, lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
   return RS_OK;
 }
 }  // namespace

@@ -1,7 +1,10 @@
 // rs_runtime.cu -- runtime plumbing: errors, stream, stream-ordered allocation,
 // scans/sorts (CUB device primitives), batch lifetime and metadata queries.
 #include <cub/cub.cuh>
+#include <chrono>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include "rs_internal.cuh"
 
@@ -26,6 +29,22 @@ cudaEvent_t prof_event() {
 }
 void prof_mark(const char *name, cudaEvent_t a, cudaEvent_t b, uint64_t items) {
   g_prof.push_back({name, a, b, items});
+}
+
+void trace(const char *phase) {
+  static int on = -1;
+  static std::chrono::steady_clock::time_point last;
+  if (on < 0) {
+    const char *v = getenv("RS_TRACE");
+    on = v && *v == '1';
+    last = std::chrono::steady_clock::now();
+  }
+  if (!on) return;
+  cudaStreamSynchronize(g_stream);
+  auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[rs_trace] %-28s %9.3f ms\n", phase,
+          std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 void set_error(const std::string &m, int64_t off, int64_t idx) {
@@ -61,18 +80,69 @@ int ensure_device() {
   return RS_OK;
 }
 
-void *dalloc(size_t bytes) {
-  void *p = nullptr;
-  if (bytes == 0) bytes = 16;
-  if (cudaMallocAsync(&p, bytes, g_stream) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
+// Caching allocator: freed blocks go to size-class free lists and are reused
+// in stream order on the single library stream (an op's scratch and result
+// pools are the same sizes step after step), so steady-state ops never call
+// into the driver.  Small blocks round to powers of two, large ones to 2 MB;
+// a cached block is reused when it is at most 1/8 larger than the request.
+static std::mutex g_alloc_mu;
+static std::multimap<size_t, void *> g_free_blocks;
+static std::unordered_map<void *, size_t> g_block_size;
+static cudaStream_t g_alloc_stream = nullptr;
+
+static size_t round_block(size_t b) {
+  if (b <= (1u << 20)) {
+    size_t r = 256;
+    while (r < b) r <<= 1;
+    return r;
   }
+  return (b + (2u << 20) - 1) & ~(size_t)((2u << 20) - 1);
+}
+
+static void release_cached_locked() {
+  for (auto &kv : g_free_blocks) {
+    cudaFreeAsync(kv.second, g_stream);
+    g_block_size.erase(kv.second);
+  }
+  g_free_blocks.clear();
+}
+
+void *dalloc(size_t bytes) {
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  if (g_alloc_stream != g_stream) {  // cached blocks are ordered on the old stream
+    cudaStreamSynchronize(g_alloc_stream);
+    g_alloc_stream = g_stream;
+  }
+  const size_t r = round_block(bytes ? bytes : 16);
+  auto it = g_free_blocks.lower_bound(r);
+  if (it != g_free_blocks.end() && it->first <= r + r / 8) {
+    void *p = it->second;
+    g_free_blocks.erase(it);
+    return p;
+  }
+  void *p = nullptr;
+  if (cudaMallocAsync(&p, r, g_stream) != cudaSuccess) {
+    cudaGetLastError();
+    release_cached_locked();
+    cudaStreamSynchronize(g_stream);
+    if (cudaMallocAsync(&p, r, g_stream) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  g_block_size[p] = r;
   return p;
 }
 
 void dfree(void *p) {
-  if (p) cudaFreeAsync(p, g_stream);
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  auto it = g_block_size.find(p);
+  if (it == g_block_size.end()) {
+    cudaFreeAsync(p, g_stream);
+    return;
+  }
+  g_free_blocks.emplace(it->second, p);
 }
 
 int d2h(void *h, const void *d, size_t bytes) {

@@ -342,6 +342,7 @@ extern "C" int rs_union_many(const rs_batch *in, const uint64_t *idx, uint64_t n
   RS_CK(cudaStreamSynchronize(g_stream));
   g.release();
   b->h_bm_start.assign(hs, hs + 2);
+  b->type_mask = (uint8_t)((1u << RS_TAG_ARRAY) | (1u << RS_TAG_BITSET) | (in->type_mask & (1u << RS_TAG_RUN)));
   b->h_valid = true;
   *out = b;
   return RS_OK;
@@ -408,5 +409,6 @@ extern "C" int rs_batch_run_optimize(rs_batch *b, uint8_t *changed) {
   if (changed)
     for (uint64_t i = 0; i < b->nb; i++) changed[i] = (uint8_t)(h[i] != 0);
   dfree(d_ch);
+  b->type_mask |= (uint8_t)(1u << RS_TAG_RUN);
   return RS_OK;
 }

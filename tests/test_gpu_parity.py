@@ -235,3 +235,17 @@ def test_edge_cases(pkg):
             for op in OPS:
                 assert a.op(op, b).serialize() == orc.op(op, wa, wb), op
                 assert a.op_cardinality(op, b) == orc.op_cardinality(op, wa, wb)
+
+
+def test_exact_and_upper_bound_allocation_agree(pkg, monkeypatch):
+    """Both result-pool sizing modes (host-synchronized exact sizes vs. the
+    no-sync upper bound) produce identical bitmaps."""
+    g = load()
+    A = pkg.BitmapBatch.from_wire([g.wire(a) for a in g["pair_a"]])
+    B = pkg.BitmapBatch.from_wire([g.wire(b) for b in g["pair_b"]])
+    for op in OPS:
+        monkeypatch.setenv("RS_EXACT_ALLOC", "1")
+        exact = A.pairwise(op, B).to_wire_list()
+        monkeypatch.setenv("RS_EXACT_ALLOC", "0")
+        fast = A.pairwise(op, B).to_wire_list()
+        assert exact == fast == [g.wire(r[OPS.index(op)]) for r in g["pair_res"]]
