@@ -1,0 +1,224 @@
+// rs_array_large.cuh -- large array x array pairs (na + nb > 2048) through an
+// 8 KB shared-memory bitset instead of a merge path.
+//
+// Same results as the two-pointer kernels (kernels/scalar.py:122-267) and
+// _container_from_values (containers.py:244-247):
+//   and     build X from A, keep the B values whose bit is set   (sorted: B order)
+//   andnot  build X from B, keep the A values whose bit is clear (sorted: A order)
+//   or/xor  build X from A, OR / XOR in B's bits (B values are distinct, so XOR
+//           flips each bit at most once), then popcount -> bitset if > 4096
+//           values, else extract the set bits in order.
+// Building from a sorted array is run-length: each thread ORs its chunk's bits
+// into a register word and issues one shared atomic per distinct word.  The
+// CTA is persistent; one thread streams the next pairs' arrays (variable sizes,
+// 16-byte padded) into a 2-stage smem ring with cp.async.bulk + mbarriers.
+#pragma once
+#include <cub/cub.cuh>
+#include "rs_internal.cuh"
+#include "rs_bitset.cuh"
+
+namespace rsl {
+
+constexpr int LT = 256;
+constexpr int LSTAGES = 2;
+
+struct LargeSmem {
+  uint16_t a[LSTAGES][RS_ARRAY_MAX];
+  uint16_t b[LSTAGES][RS_ARRAY_MAX];
+  uint64_t X[RS_WORDS];
+  uint16_t out[RS_ARRAY_MAX];
+  uint64_t bar[LSTAGES];
+  uint32_t meta[LSTAGES][3];  // na, nb, item
+  typename cub::BlockScan<uint32_t, LT>::TempStorage scan;
+  uint32_t red[2][LT / 32];
+};
+
+__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t *red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t s = 0;
+#pragma unroll
+  for (int w = 0; w < LT / 32; w++) s += red[w];
+  return s;
+}
+
+// OR (or XOR) the values v[lo, hi) of a sorted array into X with one native
+// 32-bit shared atomic per touched half-word (64-bit shared atomics lower to
+// CAS spin loops: ATOMS.CAST.SPIN.64)
+template <bool XOR>
+__device__ __forceinline__ void flush_word(uint32_t *X32, uint32_t w, uint32_t m) {
+  if (!m) return;
+  if (XOR) atomicXor(&X32[w], m);
+  else atomicOr(&X32[w], m);
+}
+
+template <bool XOR>
+__device__ __forceinline__ void set_bits_chunk(const uint16_t *v, uint32_t lo, uint32_t hi, uint64_t *X) {
+  if (lo >= hi) return;
+  uint32_t *X32 = (uint32_t *)X;
+  uint32_t w = v[lo] >> 5;
+  uint32_t m = 0;
+  for (uint32_t k = lo; k < hi; k++) {
+    uint32_t x = v[k];
+    if ((x >> 5) != w) {
+      flush_word<XOR>(X32, w, m);
+      w = x >> 5;
+      m = 0;
+    }
+    m |= 1u << (x & 31);
+  }
+  flush_word<XOR>(X32, w, m);
+}
+
+__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t &lo, uint32_t &hi) {
+  uint32_t c = (n + LT - 1) / LT;
+  lo = min(n, threadIdx.x * c);
+  hi = min(n, lo + c);
+}
+
+// Result of one pair, computed from the staged arrays.  Writes the container
+// at dst unless dst == nullptr (count only).  Returns card; type/n out.
+__device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_t na, const uint16_t *B,
+                               uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
+                               bool &stage_released) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
+  __syncthreads();
+  uint32_t lo, hi;
+  if (op == RS_OP_ANDNOT) {
+    chunk_of(nb, lo, hi);
+    set_bits_chunk<false>(B, lo, hi, sm.X);
+  } else {
+    chunk_of(na, lo, hi);
+    set_bits_chunk<false>(A, lo, hi, sm.X);
+  }
+  __syncthreads();
+  if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
+    const uint16_t *P = op == RS_OP_AND ? B : A;
+    const uint32_t np = op == RS_OP_AND ? nb : na;
+    const bool want = op == RS_OP_AND;
+    chunk_of(np, lo, hi);
+    uint32_t cnt = 0;
+    for (uint32_t k = lo; k < hi; k++) {
+      uint32_t x = P[k];
+      cnt += ((sm.X[x >> 6] >> (x & 63)) & 1) == want;
+    }
+    uint32_t base, total;
+    cub::BlockScan<uint32_t, LT>(sm.scan).ExclusiveSum(cnt, base, total);
+    type = RS_TAG_ARRAY;
+    nout = total;
+    if (!dst || total == 0) {
+      __syncthreads();
+      stage_released = true;
+      return total;
+    }
+    for (uint32_t k = lo; k < hi; k++) {
+      uint32_t x = P[k];
+      if (((sm.X[x >> 6] >> (x & 63)) & 1) == want) sm.out[base++] = (uint16_t)x;
+    }
+    __syncthreads();  // stage arrays fully read: the ring slot may be refilled
+    stage_released = true;
+    const uint32_t nvec = (2 * total + 15) >> 4;
+    if (t < 8 && total + t < nvec * 8) sm.out[total + t] = 0;
+    __syncthreads();
+    for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)sm.out)[v];
+    return total;
+  }
+  // or / xor
+  chunk_of(nb, lo, hi);
+  if (op == RS_OP_OR) set_bits_chunk<false>(B, lo, hi, sm.X);
+  else set_bits_chunk<true>(B, lo, hi, sm.X);
+  __syncthreads();
+  stage_released = true;
+  uint64_t r[4];
+  uint32_t pc = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    r[k] = sm.X[4 * t + k];
+    pc += __popcll(r[k]);
+  }
+  const uint32_t card = block_sum(pc, sm.red[parity]);
+  if (!dst || card == 0) {
+    type = RS_TAG_ARRAY;
+    nout = card;
+    return card;
+  }
+  if (card > RS_ARRAY_MAX) {
+    uint4 *p = (uint4 *)dst + 2 * t;
+    rsb::st_stream(p, make_uint4((uint32_t)r[0], (uint32_t)(r[0] >> 32), (uint32_t)r[1], (uint32_t)(r[1] >> 32)));
+    rsb::st_stream(p + 1, make_uint4((uint32_t)r[2], (uint32_t)(r[2] >> 32), (uint32_t)r[3], (uint32_t)(r[3] >> 32)));
+    type = RS_TAG_BITSET;
+    nout = RS_WORDS;
+    return card;
+  }
+  uint32_t base;
+  cub::BlockScan<uint32_t, LT>(sm.scan).ExclusiveSum(pc, base);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint64_t w = r[q];
+    while (w) {
+      sm.out[base++] = (uint16_t)((4 * t + q) * 64 + __ffsll((long long)w) - 1);
+      w &= w - 1;
+    }
+  }
+  __syncthreads();
+  const uint32_t nvec = (2 * card + 15) >> 4;
+  if (t < 8 && card + t < nvec * 8) sm.out[card + t] = 0;
+  __syncthreads();
+  for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)sm.out)[v];
+  type = RS_TAG_ARRAY;
+  nout = card;
+  return card;
+}
+
+// Persistent ring over items i = blockIdx.x + k*gridDim.x < count.
+// src(i, pa, na, pb, nb) gives the operand arrays of item i;
+// sink(i, card, type, n, dst_needed) -- called by all threads after the pair.
+template <typename Src, typename Dst, typename Sink>
+__device__ void large_loop(LargeSmem &sm, uint32_t count, int op, Src src, Dst dst_of, Sink sink) {
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int s = 0; s < LSTAGES; s++) rsb::mbar_init(&sm.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int s, uint32_t i) {
+    const uint8_t *pa, *pb;
+    uint32_t na, nb;
+    src(i, pa, na, pb, nb);
+    sm.meta[s][0] = na;
+    sm.meta[s][1] = nb;
+    sm.meta[s][2] = i;
+    const uint32_t ba = (uint32_t)rs_pad16(2ull * na), bb = (uint32_t)rs_pad16(2ull * nb);
+    rsb::mbar_expect_tx(&sm.bar[s], ba + bb);
+    rsb::bulk_g2s(sm.a[s], pa, ba, &sm.bar[s]);
+    rsb::bulk_g2s(sm.b[s], pb, bb, &sm.bar[s]);
+  };
+  if (t == 0)
+    for (int s = 0; s < LSTAGES; s++) {
+      uint32_t i = blockIdx.x + s * gridDim.x;
+      if (i < count) issue(s, i);
+    }
+  for (uint32_t k = 0;; k++) {
+    const uint32_t i = blockIdx.x + k * gridDim.x;
+    if (i >= count) break;
+    const int s = k % LSTAGES;
+    rsb::mbar_wait(&sm.bar[s], (k / LSTAGES) & 1);
+    const uint32_t na = sm.meta[s][0], nb = sm.meta[s][1];
+    uint8_t type;
+    uint32_t n;
+    bool released = false;
+    uint32_t card = large_pair(sm, op, sm.a[s], na, sm.b[s], nb, dst_of(i), k & 1, type, n, released);
+    // every path above passed a barrier after its last read of stage s
+    if (t == 0) {
+      uint32_t nx = i + LSTAGES * gridDim.x;
+      if (nx < count) issue(s, nx);
+    }
+    sink(i, card, type, n);
+    __syncthreads();  // X / out / meta reuse
+  }
+}
+
+}  // namespace rsl

@@ -39,11 +39,13 @@ static __device__ void scatter_container(const DevBatch &S, uint32_t c, uint8_t 
     uint32_t s = v[2 * r], e = s + v[2 * r + 1];
     uint32_t ws = s >> 6, we = e >> 6;
     uint64_t first = ~0ull << (s & 63), last = ~0ull >> (63 - (e & 63));
-    if (lane == 0) {
-      if (ws == we) atomicOr((unsigned long long *)&X[ws], (unsigned long long)(first & last));
-      else {
-        atomicOr((unsigned long long *)&X[ws], (unsigned long long)first);
-        atomicOr((unsigned long long *)&X[we], (unsigned long long)last);
+    if (lane < 2) {  // partial edge words via native 32-bit shared atomics (lane 0: low half, lane 1: high)
+      const uint64_t mf = ws == we ? (first & last) : first;
+      const uint32_t hf = (uint32_t)(mf >> (32 * lane));
+      if (hf) atomicOr(&X32[2 * ws + lane], hf);
+      if (ws != we) {
+        const uint32_t hl = (uint32_t)(last >> (32 * lane));
+        if (hl) atomicOr(&X32[2 * we + lane], hl);
       }
     }
     for (uint32_t w = ws + 1 + lane; w < we; w += 32) X[w] = ~0ull;

@@ -54,6 +54,7 @@ struct rs_batch {
   // container types that may be present (bit t = type t); lets the op
   // pipeline skip type-pair classes that cannot occur
   uint8_t type_mask = 0xFF;
+  int single = -1;  // 1 = every bitmap holds exactly one container (cached)
   DevBatch dev() const {
     DevBatch d;
     d.nb = nb; d.nc = nc; d.bm_start = d_bm_start; d.key = d_key; d.type = d_type;

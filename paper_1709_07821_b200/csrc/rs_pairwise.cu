@@ -21,6 +21,7 @@
 #include "rs_dense.cuh"
 #include "rs_array.cuh"
 #include "rs_bitset.cuh"
+#include "rs_array_large.cuh"
 
 using namespace rs;
 
@@ -42,9 +43,12 @@ struct OutDesc {
 struct Lists {
   uint32_t *list[NCLS];
   uint32_t *cnt;           // device counters [NCLS]
-  uint64_t *aoff, *boff;   // bitset x bitset items: operand payload offsets (one load for the TMA producer)
+  uint64_t *aoff, *boff;   // TMA-fed classes (bitset x bitset, large array x array): operand payload offsets
+  uint32_t *nab;           // large array x array: na | nb << 16
   uint64_t cap;
 };
+
+__device__ __forceinline__ bool tma_class(int c) { return c == 1 /*CLS_BB*/ || c == 4 /*CLS_AAL*/; }
 
 __device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { return ia ? ia[p] : (uint32_t)p; }
 
@@ -57,7 +61,7 @@ __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uin
 // warp-aggregated append of `item` to list[cls] (returns the slot); bitset x
 // bitset items also record their operand payload offsets
 __device__ __forceinline__ uint32_t list_append(Lists L, int cls, bool active, uint32_t item, uint64_t aoff = 0,
-                                                uint64_t boff = 0) {
+                                                uint64_t boff = 0, uint32_t nab = 0) {
   unsigned lane = threadIdx.x & 31;
   uint32_t slot = 0;
 #pragma unroll
@@ -74,6 +78,10 @@ __device__ __forceinline__ uint32_t list_append(Lists L, int cls, bool active, u
       if (c == CLS_BB) {
         L.aoff[slot] = aoff;
         L.boff[slot] = boff;
+      } else if (c == CLS_AAL) {
+        L.aoff[L.cap + slot] = aoff;
+        L.boff[L.cap + slot] = boff;
+        L.nab[slot] = nab;
       }
     }
   }
@@ -175,7 +183,7 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   bool active = t < M && keep[t];
   int cls = CLS_COPY;
-  uint32_t e = 0;
+  uint32_t e = 0, nab = 0;
   uint64_t ao = 0, bo = 0;
   if (active) {
     e = epos[t];
@@ -186,12 +194,13 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
     E.pair[e] = mpair[t];
     E.off[e] = uoff[t];
     cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
-    if (cls == CLS_BB) {
+    if (tma_class(cls)) {
       ao = A.off[ca];
       bo = B.off[cb];
+      nab = A.card[ca] | (B.card[cb] << 16);
     }
   }
-  list_append(L, cls, active, e, ao, bo);
+  list_append(L, cls, active, e, ao, bo, nab);
 }
 
 // per-pair first entry index (estart[npairs] = total entries)
@@ -455,6 +464,85 @@ int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBat
   return RS_OK;
 }
 
+// ------------------------------------ large array x array (smem bitset + TMA)
+
+__global__ void __launch_bounds__(rsl::LT) k_aa_large_op(int op, const uint32_t *__restrict__ list,
+                                                         const uint64_t *__restrict__ laoff,
+                                                         const uint64_t *__restrict__ lboff,
+                                                         const uint32_t *__restrict__ lnab,
+                                                         const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                                                         Entries E, OutDesc O, uint8_t *__restrict__ opool,
+                                                         uint64_t *__restrict__ res_card) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  auto &sm = *reinterpret_cast<rsl::LargeSmem *>(smraw);
+  auto src = [&](uint32_t i, const uint8_t *&pa, uint32_t &na, const uint8_t *&pb, uint32_t &nb) {
+    pa = A.pool + laoff[i];
+    pb = B.pool + lboff[i];
+    const uint32_t x = lnab[i];
+    na = x & 0xFFFF;
+    nb = x >> 16;
+  };
+  auto dst = [&](uint32_t i) -> uint8_t * { return opool + E.off[list[i]]; };
+  auto sink = [&](uint32_t i, uint32_t card, uint8_t type, uint32_t n) {
+    if (threadIdx.x == 0) {
+      const uint32_t e = list[i];
+      O.type[e] = type;
+      O.card[e] = card;
+      O.n[e] = n;
+      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+  };
+  rsl::large_loop(sm, *cnt, op, src, dst, sink);
+}
+
+__global__ void __launch_bounds__(rsl::LT) k_aa_large_count(const uint64_t *__restrict__ laoff,
+                                                            const uint64_t *__restrict__ lboff,
+                                                            const uint32_t *__restrict__ lnab,
+                                                            const uint32_t *__restrict__ lpair,
+                                                            const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                                                            uint64_t *__restrict__ acc) {
+  extern __shared__ __align__(128) uint8_t smraw[];
+  auto &sm = *reinterpret_cast<rsl::LargeSmem *>(smraw);
+  auto src = [&](uint32_t i, const uint8_t *&pa, uint32_t &na, const uint8_t *&pb, uint32_t &nb) {
+    pa = A.pool + laoff[i];
+    pb = B.pool + lboff[i];
+    const uint32_t x = lnab[i];
+    na = x & 0xFFFF;
+    nb = x >> 16;
+  };
+  auto dst = [&](uint32_t) -> uint8_t * { return nullptr; };
+  auto sink = [&](uint32_t i, uint32_t card, uint8_t, uint32_t) {
+    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)card);
+  };
+  rsl::large_loop(sm, *cnt, RS_OP_AND, src, dst, sink);
+}
+
+int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
+                       uint8_t *pool, uint64_t *res_card, bool exact) {
+  const size_t smem = sizeof(rsl::LargeSmem);
+  static bool attr = false;
+  if (!attr) {
+    RS_CK(cudaFuncSetAttribute(k_aa_large_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  RS_LAUNCH_PROF("array_pair_l", exact ? n : 0, k_aa_large_op, persistent_grid(k_aa_large_op, smem, n), rsl::LT,
+                 smem, op, L.list[CLS_AAL], L.aoff + L.cap, L.boff + L.cap, L.nab, L.cnt + CLS_AAL, dA, dB, En, O,
+                 pool, res_card);
+  return RS_OK;
+}
+
+int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch dB, uint64_t *inter) {
+  const size_t smem = sizeof(rsl::LargeSmem);
+  static bool attr = false;
+  if (!attr) {
+    RS_CK(cudaFuncSetAttribute(k_aa_large_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  RS_LAUNCH_PROF("array_count_l", 0, k_aa_large_count, persistent_grid(k_aa_large_count, smem, L.cap), rsl::LT,
+                 smem, L.aoff + L.cap, L.boff + L.cap, L.nab, lpair, L.cnt + CLS_AAL, dA, dB, inter);
+  return RS_OK;
+}
+
 // ------------------------------------------------- array x array (merge path)
 
 // Materialized array x array pairs: one group of GT threads per pair
@@ -538,11 +626,13 @@ __device__ __forceinline__ void count_append(Lists L, int cls, bool active, uint
                                              uint32_t *lcb_base, uint32_t *lpair_base, const DevBatch &A,
                                              const DevBatch &B) {
   uint64_t ao = 0, bo = 0;
-  if (active && cls == CLS_BB) {
+  uint32_t nab = 0;
+  if (active && tma_class(cls)) {
     ao = A.off[ca];
     bo = B.off[cb];
+    nab = A.card[ca] | (B.card[cb] << 16);
   }
-  uint32_t slot = list_append(L, cls, active, ca, ao, bo);
+  uint32_t slot = list_append(L, cls, active, ca, ao, bo, nab);
   if (active) {
     lcb_base[cls * L.cap + slot] = cb;
     lpair_base[cls * L.cap + slot] = pair;
@@ -601,6 +691,7 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
   bool active = p < npairs;
   int cls = CLS_GEN;
   uint64_t ao = 0, bo = 0;
+  uint32_t nab = 0;
   if (active) {
     uint32_t ca = (uint32_t)A.bm_start[pair_a(ia, p)], cb = (uint32_t)B.bm_start[pair_a(ib, p)];
     E.key[p] = A.key[ca];
@@ -609,14 +700,15 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
     E.pair[p] = (uint32_t)p;
     ub[p] = rs_pad16(rs_result_ub(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op));
     cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
-    if (cls == CLS_BB) {
+    if (tma_class(cls)) {
       ao = A.off[ca];
       bo = B.off[cb];
+      nab = A.card[ca] | (B.card[cb] << 16);
     }
   } else if (p == npairs) {
     ub[p] = 0;
   }
-  list_append(L, cls, active, (uint32_t)p, ao, bo);
+  list_append(L, cls, active, (uint32_t)p, ao, bo, nab);
 }
 
 __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib, Lists L,
@@ -763,9 +855,13 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   if (uint64_t n = want(CLS_AAM, cm.aa))
     RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
                    256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  if (uint64_t n = want(CLS_AAL, cm.aa))
-    RS_LAUNCH_PROF("array_pair_l", hcnt ? n : 0, (k_aa_pair<256, 32>), std::min<uint64_t>(n, sms * 8), 256, 0, op,
-                   L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (uint64_t n = want(CLS_AAL, cm.aa)) {
+    if (env_int("RS_AA_LARGE_MERGE", 0))
+      RS_LAUNCH_PROF("array_pair_l", hcnt ? n : 0, (k_aa_pair<256, 32>), std::min<uint64_t>(n, sms * 8), 256, 0, op,
+                     L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
+    else
+      RS_TRY(launch_aa_large_op(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card, hcnt != nullptr));
+  }
   if (uint64_t n = want(CLS_GEN, cm.gen))
     RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
                    L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, b->d_bm_card);
@@ -780,13 +876,43 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   return RS_OK;
 }
 
+__global__ void k_iota(uint64_t n, uint64_t *__restrict__ out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = i;
+}
+
+// container_pairwise needs exactly one container per image (checked once per
+// batch and cached, then per pair only when some image is not single)
+int check_single_containers(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
+                            uint64_t npairs) {
+  for (const rs_batch *X : {A, B}) {
+    rs_batch *x = const_cast<rs_batch *>(X);
+    if (x->single < 0) {
+      x->single = 1;
+      for (uint64_t i = 0; i < x->nb && x->single; i++)
+        if (x->h_bm_start[i + 1] - x->h_bm_start[i] != 1) x->single = 0;
+    }
+  }
+  if (A->single && B->single) return RS_OK;
+  for (uint64_t p = 0; p < npairs; p++) {
+    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+    if (a < A->nb && b < B->nb &&
+        (A->h_bm_start[a + 1] - A->h_bm_start[a] != 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] != 1)) {
+      set_error("container_pairwise needs exactly one container per image");
+      return RS_ESHAPE;
+    }
+  }
+  return RS_OK;
+}
+
 Lists make_lists(Scratch &S, uint64_t cap) {
   Lists L;
   L.cap = cap ? cap : 1;
   for (int c = 0; c < NCLS; c++) L.list[c] = (uint32_t *)S.get(L.cap * 4);
   L.cnt = (uint32_t *)S.get(NCLS * 4);
-  L.aoff = (uint64_t *)S.get(L.cap * 8);
-  L.boff = (uint64_t *)S.get(L.cap * 8);
+  L.aoff = (uint64_t *)S.get(2 * L.cap * 8);  // [0,cap): bitset class, [cap,2cap): large-array class
+  L.boff = (uint64_t *)S.get(2 * L.cap * 8);
+  L.nab = (uint32_t *)S.get(L.cap * 4);
   return L;
 }
 
@@ -860,14 +986,7 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   *out = nullptr;
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
-  for (uint64_t p = 0; p < npairs; p++) {
-    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
-    if (a < A->nb && b < B->nb &&
-        (A->h_bm_start[a + 1] - A->h_bm_start[a] != 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] != 1)) {
-      set_error("container_pairwise needs exactly one container per image");
-      return RS_ESHAPE;
-    }
-  }
+  RS_TRY(check_single_containers(A, B, ia, ib, npairs));
   Scratch S;
   uint32_t *dia, *dib;
   RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
@@ -884,10 +1003,15 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   DevBatch dA = A->dev(), dB = B->dev();
   RS_LAUNCH(k_cont_entries, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, op, En, ub, L);
   RS_TRY(scan_exclusive<uint64_t>(ub, En.off, npairs + 1));
-  // estart[p] = p (one entry per pair)
-  std::vector<uint64_t> hs(npairs + 1);
-  for (uint64_t p = 0; p <= npairs; p++) hs[p] = p;
-  RS_TRY(h2d(estart, hs.data(), (npairs + 1) * 8));
+  RS_LAUNCH(k_iota, grid_for(npairs + 1, 256), 256, 0, npairs + 1, estart);  // one entry per pair
+  // Array-only inputs with the identity pairing: every result slot is at most
+  // 2(na + nb) bytes (+16 pad), so the input pools bound the result pool and
+  // the op needs no host synchronization.
+  const uint8_t AR = 1 << RS_TAG_ARRAY;
+  if (!ia && !ib && A->type_mask == AR && B->type_mask == AR && env_int("RS_EXACT_ALLOC", 0) == 0) {
+    const uint64_t Pub = A->pool_bytes + B->pool_bytes + 16 * npairs;
+    return run_classes_and_compact(op, A, B, S, En, L, npairs, Pub, nullptr, estart + npairs, estart, npairs, out);
+  }
   uint64_t P = 0;
   uint32_t cnt[NCLS];
   RS_CK(cudaMemcpyAsync(&P, En.off + npairs, 8, cudaMemcpyDeviceToHost, g_stream));
@@ -920,8 +1044,11 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
                    lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
     RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
                    lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
-    RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
-                   lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
+    if (env_int("RS_AA_LARGE_MERGE", 0))
+      RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
+                     lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
+    else
+      RS_TRY(launch_aa_large_count(L, lpair + CLS_AAL * L.cap, dA, dB, inter));
   }
   if (cm.gen)
     RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN],
@@ -969,14 +1096,7 @@ extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, cons
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
-  for (uint64_t p = 0; p < npairs; p++) {
-    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
-    if (a < A->nb && b < B->nb &&
-        (A->h_bm_start[a + 1] - A->h_bm_start[a] != 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] != 1)) {
-      set_error("container_pairwise_cardinality needs exactly one container per image");
-      return RS_ESHAPE;
-    }
-  }
+  RS_TRY(check_single_containers(A, B, ia, ib, npairs));
   Scratch S;
   uint32_t *dia, *dib;
   RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
