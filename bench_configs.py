@@ -134,6 +134,8 @@ def c3(steps, npairs=1_000_000):
     ia_, ib_ = synth.slice_images(buf, offs, 0, npairs), synth.slice_images(buf, offs, npairs, 2 * npairs)
     A, B = rb.BitmapBatch.from_wire(ia_), rb.BitmapBatch.from_wire(ib_)
     SA, SB = orc.Session(*ia_), orc.Session(*ib_)
+    import torch
+    dev_out = torch.empty(npairs, dtype=torch.int64, device="cuda")
     sample = np.arange(0, npairs, max(1, npairs // 2000))
     in_bytes = A.stats()[0] + B.stats()[0] + 16 * npairs
     out = {"config": f"C3: {npairs} array x array container pairs, Zipf(1.2) sizes", "per_op": {}}
@@ -145,7 +147,7 @@ def c3(steps, npairs=1_000_000):
         assert np.array_equal(c.astype(np.int64), card.astype(np.int64))
         pb, db, _ = R.stats()
         ms = timed(lambda: A.container_pairwise(op, B), steps)
-        msc = timed(lambda: A.container_pairwise_cardinality(op, B), steps)
+        msc = timed(lambda: A.container_pairwise_cardinality_device(op, B, dev_out.data_ptr(), npairs), steps)
         out["per_op"][op] = {"ms": ms, "container_pairs_per_s": npairs / (ms * 1e-3),
                              "algorithmic_GBps": (in_bytes + pb + db) / (ms * 1e-3) / 1e9}
         out["per_op"][op + "_count"] = {"ms": msc, "container_pairs_per_s": npairs / (msc * 1e-3),
@@ -159,6 +161,32 @@ def c3(steps, npairs=1_000_000):
     return out
 
 
+def descriptors(buf, offs, i):
+    """(keys, container bytes incl. 8 B descriptor) of wire image i."""
+    b = buf[int(offs[i]):int(offs[i + 1])]
+    n = int(b[4:8].view("<u4")[0])
+    d = b[8:8 + 8 * n].reshape(n, 8)
+    keys = d[:, 0:2].copy().view("<u2").ravel().astype(np.int64)
+    tag = d[:, 2]
+    card = d[:, 4:8].copy().view("<u4").ravel().astype(np.int64)
+    size = np.where(tag == 1, 2 * card, np.where(tag == 2, 8192, 0)).astype(np.int64) + 8
+    # run payload sizes need the run counts: walk the payload section
+    if (tag == 3).any():
+        off = 8 + 8 * n
+        sizes = np.empty(n, dtype=np.int64)
+        for k in range(n):
+            if tag[k] == 1:
+                sizes[k] = 2 * card[k]
+            elif tag[k] == 2:
+                sizes[k] = 8192
+            else:
+                nr = int(b[off:off + 2].view("<u2")[0])
+                sizes[k] = 2 + 4 * nr
+            off += sizes[k]
+        size = sizes + 8
+    return keys, size
+
+
 def c4(steps, nbitmaps=200):
     import paper_1709_07821_b200 as rb
     from paper_1709_07821_b200 import synth
@@ -167,12 +195,29 @@ def c4(steps, nbitmaps=200):
     Bt = rb.BitmapBatch.from_wire((buf, offs))
     S = orc.Session(buf, offs)
     ia, ib = np.arange(nbitmaps - 1), np.arange(1, nbitmaps)
-    out = {"config": f"C4: {nbitmaps} mixed-container bitmaps, successive AND/OR + union_many", "per_op": {}}
+    desc = [descriptors(buf, offs, i) for i in range(nbitmaps)]
+    matched_in = copied = 0
+    n_matched = 0
+    for a, b in zip(ia, ib):
+        (ka, sa), (kb, sb) = desc[a], desc[b]
+        ma, mb = np.isin(ka, kb), np.isin(kb, ka)
+        matched_in += int(sa[ma].sum() + sb[mb].sum())
+        copied += int(sa[~ma].sum() + sb[~mb].sum())
+        n_matched += int(ma.sum())
+    out = {"config": f"C4: {nbitmaps} mixed-container bitmaps, successive AND/OR + union_many", "per_op": {},
+           "matched_container_pairs": n_matched}
+    hbm = peak()
     for op in ("and", "or"):
         R = Bt.pairwise(op, Bt, ia, ib)
         assert np.array_equal(R.cardinalities().astype(np.int64), S.run(op, "op", S, ia, ib))
+        pb, db, _ = R.stats()
+        # inputs read (matched both sides; OR also reads + copies the
+        # unmatched ones) + result containers written
+        byts = matched_in + (copied if op == "or" else 0) + pb + db
         ms = timed(lambda: Bt.pairwise(op, Bt, ia, ib), steps)
-        out["per_op"][op] = {"ms": ms, "bitmap_pairs_per_s": len(ia) / (ms * 1e-3)}
+        out["per_op"][op] = {"ms": ms, "bitmap_pairs_per_s": len(ia) / (ms * 1e-3),
+                             "container_pairs_per_s": n_matched / (ms * 1e-3),
+                             "algorithmic_GBps": byts / (ms * 1e-3) / 1e9, "frac_of_hbm": byts / (ms * 1e-3) / 1e9 / hbm}
     U = Bt.union_many()
     w = wires(buf, offs, range(nbitmaps)) if nbitmaps <= 200 else None
     if w is not None:

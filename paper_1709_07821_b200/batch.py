@@ -218,6 +218,14 @@ class BitmapBatch:
         check(lib().rs_container_pairwise(k, self._h, other._h, pa, pb, n, C.byref(h)))
         return BitmapBatch(h)
 
+    def container_pairwise_cardinality_device(self, op: str, other: "BitmapBatch", dev_out_ptr: int, n: int,
+                                              ia=None, ib=None) -> None:
+        """Asynchronous variant writing u64 counts to a device pointer."""
+        k = op_index(op)
+        a, pa = _u32_or_none(ia)
+        b, pb = _u32_or_none(ib)
+        check(lib().rs_container_pairwise_cardinality(k, self._h, other._h, pa, pb, n, C.c_void_p(dev_out_ptr), 1))
+
     def container_pairwise_cardinality(self, op: str, other: "BitmapBatch", ia=None, ib=None) -> np.ndarray:
         """containers.py:554-570, batched."""
         k = op_index(op)

@@ -26,7 +26,6 @@ struct LargeSmem {
   uint16_t a[LSTAGES][RS_ARRAY_MAX];
   uint16_t b[LSTAGES][RS_ARRAY_MAX];
   uint64_t X[RS_WORDS];
-  uint16_t out[RS_ARRAY_MAX];
   uint64_t bar[LSTAGES];
   uint32_t meta[LSTAGES][3];  // na, nb, item
   typename cub::BlockScan<uint32_t, LT>::TempStorage scan;
@@ -71,67 +70,102 @@ __device__ __forceinline__ void set_bits_chunk(const uint16_t *v, uint32_t lo, u
   flush_word<XOR>(X32, w, m);
 }
 
-__device__ __forceinline__ void chunk_of(uint32_t n, uint32_t &lo, uint32_t &hi) {
-  uint32_t c = (n + LT - 1) / LT;
-  lo = min(n, threadIdx.x * c);
-  hi = min(n, lo + c);
+// Thread t owns values [16t, 16t+16) of an array (n <= 4096 = 256 x 16): two
+// 128-bit shared loads put them in registers as 8 packed words, so the probes
+// below are independent loads (ILP) instead of a dependent smem walk.
+// Returns how many of the 16 are real.
+__device__ __forceinline__ uint32_t load16(const uint16_t *v, uint32_t n, uint32_t w[8]) {
+  const uint32_t base = 16 * threadIdx.x;
+  if (base >= n) return 0;
+  const uint4 *p = (const uint4 *)(v + base);
+  const uint4 q0 = p[0], q1 = p[1];
+  w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+  w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+  return min(16u, n - base);
+}
+
+__device__ __forceinline__ uint32_t val16(const uint32_t w[8], int k) { return (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF; }
+
+// OR / XOR the first c values (sorted) into X: one atomic per touched 32-bit word
+template <bool XOR>
+__device__ __forceinline__ void set_bits16(const uint32_t w8[8], uint32_t c, uint64_t *X) {
+  if (!c) return;
+  uint32_t *X32 = (uint32_t *)X;
+  uint32_t w = val16(w8, 0) >> 5, m = 0;
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const uint32_t x = val16(w8, k);
+    if ((uint32_t)k < c) {
+      if ((x >> 5) != w) {
+        flush_word<XOR>(X32, w, m);
+        w = x >> 5;
+        m = 0;
+      }
+      m |= 1u << (x & 31);
+    }
+  }
+  flush_word<XOR>(X32, w, m);
 }
 
 // Result of one pair, computed from the staged arrays.  Writes the container
-// at dst unless dst == nullptr (count only).  Returns card; type/n out.
+// at dst unless dst == nullptr (count only).  Returns card; type/n out.  On
+// return every thread has passed a barrier after its last read of the stage.
+// Copy `total` staged u16 values to dst with 128-bit stores (zero-padded to
+// 16 bytes); the caller has put them in `stage` before a barrier.
+__device__ __forceinline__ void flush_stage(uint16_t *stage, uint32_t total, uint8_t *dst) {
+  const int t = threadIdx.x;
+  const uint32_t nvec = (2 * total + 15) >> 4;
+  if (t < 8 && total + t < nvec * 8) stage[total + t] = 0;
+  __syncthreads();
+  for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)stage)[v];
+}
+
+// `stage` is the ring slot's A buffer: once every thread holds its values in
+// registers (first barrier) it is free until the producer refills it after
+// this pair, so it doubles as the output staging buffer.
 __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_t na, const uint16_t *B,
                                uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
-                               bool &stage_released) {
+                               uint16_t *stage) {
   const int t = threadIdx.x;
 #pragma unroll
   for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
+  uint32_t xa[8], xb[8];
+  const uint32_t ca = load16(A, na, xa), cb = load16(B, nb, xb);
   __syncthreads();
-  uint32_t lo, hi;
-  if (op == RS_OP_ANDNOT) {
-    chunk_of(nb, lo, hi);
-    set_bits_chunk<false>(B, lo, hi, sm.X);
-  } else {
-    chunk_of(na, lo, hi);
-    set_bits_chunk<false>(A, lo, hi, sm.X);
-  }
+  if (op == RS_OP_ANDNOT) set_bits16<false>(xb, cb, sm.X);
+  else set_bits16<false>(xa, ca, sm.X);
   __syncthreads();
+  const uint32_t *X32 = (const uint32_t *)sm.X;
   if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
-    const uint16_t *P = op == RS_OP_AND ? B : A;
-    const uint32_t np = op == RS_OP_AND ? nb : na;
-    const bool want = op == RS_OP_AND;
-    chunk_of(np, lo, hi);
-    uint32_t cnt = 0;
-    for (uint32_t k = lo; k < hi; k++) {
-      uint32_t x = P[k];
-      cnt += ((sm.X[x >> 6] >> (x & 63)) & 1) == want;
+    // and: keep B values present in X(A); andnot: keep A values absent from X(B)
+    const bool is_and = op == RS_OP_AND;
+    uint32_t P[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) P[k] = is_and ? xb[k] : xa[k];
+    const uint32_t cp = is_and ? cb : ca;
+    const uint32_t want = is_and ? 1u : 0u;
+    uint32_t keep = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const uint32_t x = val16(P, k);
+      if ((uint32_t)k < cp && ((X32[x >> 5] >> (x & 31)) & 1u) == want) keep |= 1u << k;
     }
     uint32_t base, total;
-    cub::BlockScan<uint32_t, LT>(sm.scan).ExclusiveSum(cnt, base, total);
+    cub::BlockScan<uint32_t, LT>(sm.scan).ExclusiveSum((uint32_t)__popc(keep), base, total);
     type = RS_TAG_ARRAY;
     nout = total;
-    if (!dst || total == 0) {
-      __syncthreads();
-      stage_released = true;
-      return total;
+    if (dst && total) {
+#pragma unroll
+      for (int k = 0; k < 16; k++)
+        if (keep >> k & 1) stage[base++] = (uint16_t)val16(P, k);
+      flush_stage(stage, total, dst);
     }
-    for (uint32_t k = lo; k < hi; k++) {
-      uint32_t x = P[k];
-      if (((sm.X[x >> 6] >> (x & 63)) & 1) == want) sm.out[base++] = (uint16_t)x;
-    }
-    __syncthreads();  // stage arrays fully read: the ring slot may be refilled
-    stage_released = true;
-    const uint32_t nvec = (2 * total + 15) >> 4;
-    if (t < 8 && total + t < nvec * 8) sm.out[total + t] = 0;
-    __syncthreads();
-    for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)sm.out)[v];
     return total;
   }
-  // or / xor
-  chunk_of(nb, lo, hi);
-  if (op == RS_OP_OR) set_bits_chunk<false>(B, lo, hi, sm.X);
-  else set_bits_chunk<true>(B, lo, hi, sm.X);
+  // or / xor: fold B into X(A); B values are distinct, so XOR flips each bit once
+  if (op == RS_OP_OR) set_bits16<false>(xb, cb, sm.X);
+  else set_bits16<true>(xb, cb, sm.X);
   __syncthreads();
-  stage_released = true;
   uint64_t r[4];
   uint32_t pc = 0;
 #pragma unroll
@@ -159,15 +193,11 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
   for (int q = 0; q < 4; q++) {
     uint64_t w = r[q];
     while (w) {
-      sm.out[base++] = (uint16_t)((4 * t + q) * 64 + __ffsll((long long)w) - 1);
+      stage[base++] = (uint16_t)((4 * t + q) * 64 + __ffsll((long long)w) - 1);
       w &= w - 1;
     }
   }
-  __syncthreads();
-  const uint32_t nvec = (2 * card + 15) >> 4;
-  if (t < 8 && card + t < nvec * 8) sm.out[card + t] = 0;
-  __syncthreads();
-  for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)sm.out)[v];
+  flush_stage(stage, card, dst);
   type = RS_TAG_ARRAY;
   nout = card;
   return card;
@@ -209,9 +239,9 @@ __device__ void large_loop(LargeSmem &sm, uint32_t count, int op, Src src, Dst d
     const uint32_t na = sm.meta[s][0], nb = sm.meta[s][1];
     uint8_t type;
     uint32_t n;
-    bool released = false;
-    uint32_t card = large_pair(sm, op, sm.a[s], na, sm.b[s], nb, dst_of(i), k & 1, type, n, released);
-    // every path above passed a barrier after its last read of stage s
+    // registers hold this thread's values after large_pair's first barrier,
+    // so stage s is free once that barrier has passed
+    uint32_t card = large_pair(sm, op, sm.a[s], na, sm.b[s], nb, dst_of(i), k & 1, type, n, sm.a[s]);
     if (t == 0) {
       uint32_t nx = i + LSTAGES * gridDim.x;
       if (nx < count) issue(s, nx);

@@ -130,15 +130,33 @@ __device__ __forceinline__ void bb_loop(BBSmem<STAGES> &sm, uint32_t count, int 
       nxt += gridDim.x;
       if (nxt < count) src(nxt, npa, npb);
     }
-    sink(i, r, pc, card);
+    sink(i, r, pc, card, sm.red[k & 1]);
   }
 }
 
+// Exclusive prefix of v over the CTA, reusing the per-warp totals that
+// block_sum() already left in red[] (no extra barrier): warp shuffle scan +
+// the totals of the warps before this one.
+__device__ __forceinline__ uint32_t block_excl_from_red(uint32_t v, const uint32_t *red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  uint32_t pre = 0;
+#pragma unroll
+  for (int k = 0; k < BT / 32; k++) pre += k < w ? red[k] : 0;
+  return pre + x - v;
+}
+
 // Encode a result set held as 4 words per thread into dst: bitset (> 4096
-// values) or sorted array via the smem staging buffer.  Returns n.
+// values) or sorted array via the smem staging buffer.  `red` holds the
+// per-warp popcount totals of this item (from block_sum).  Returns n.
 template <int STAGES>
 __device__ __forceinline__ uint32_t bb_encode(BBSmem<STAGES> &sm, const uint64_t r[4], uint32_t pc, uint32_t card,
-                                              uint8_t *dst) {
+                                              uint8_t *dst, const uint32_t *red) {
   const int t = threadIdx.x;
   if (card > RS_ARRAY_MAX) {
     uint4 *p = (uint4 *)dst + 2 * t;
@@ -147,8 +165,7 @@ __device__ __forceinline__ uint32_t bb_encode(BBSmem<STAGES> &sm, const uint64_t
     return RS_WORDS;
   }
   if (card == 0) return 0;
-  uint32_t base;
-  cub::BlockScan<uint32_t, BT>(sm.scan).ExclusiveSum(pc, base);
+  uint32_t base = block_excl_from_red(pc, red);
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     uint64_t w = r[q];
@@ -157,9 +174,8 @@ __device__ __forceinline__ uint32_t bb_encode(BBSmem<STAGES> &sm, const uint64_t
       w &= w - 1;
     }
   }
-  __syncthreads();
   const uint32_t nvec = (2 * card + 15) >> 4;
-  if (t < 8 && card + t < nvec * 8) sm.out[card + t] = 0;
+  if (t < 8 && card + t < nvec * 8) sm.out[card + t] = 0;  // pad slots are disjoint from [0, card)
   __syncthreads();
   for (uint32_t v = t; v < nvec; v += BT) ((uint4 *)dst)[v] = ((const uint4 *)sm.out)[v];
   return card;

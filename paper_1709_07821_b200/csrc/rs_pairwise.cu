@@ -52,9 +52,14 @@ __device__ __forceinline__ bool tma_class(int c) { return c == 1 /*CLS_BB*/ || c
 
 __device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { return ia ? ia[p] : (uint32_t)p; }
 
+// array x array size classes: <= 256 merged items -> warp merge path; <= c_aa_large_min
+// -> 128-thread merge path; above -> smem-bitset kernel (RS_AA_LARGE_MIN overrides)
+__constant__ uint32_t c_aa_large_min = 2048;
+
 __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
-  if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY) return na + nb <= 256 ? CLS_AAS : na + nb <= 2048 ? CLS_AAM : CLS_AAL;
+  if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY)
+    return na + nb <= 256 ? CLS_AAS : na + nb <= c_aa_large_min ? CLS_AAM : CLS_AAL;
   return CLS_GEN;
 }
 
@@ -372,9 +377,9 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_op(int op, const uint32_t *__res
     pa = A.pool + laoff[i];
     pb = B.pool + lboff[i];
   };
-  auto sink = [&](uint32_t i, const uint64_t *r, uint32_t pc, uint32_t card) {
+  auto sink = [&](uint32_t i, const uint64_t *r, uint32_t pc, uint32_t card, const uint32_t *red) {
     const uint32_t e = list[i];
-    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pc, card, opool + E.off[e]);
+    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pc, card, opool + E.off[e], red);
     if (threadIdx.x == 0) {
       O.type[e] = card > RS_ARRAY_MAX ? RS_TAG_BITSET : RS_TAG_ARRAY;
       O.card[e] = card;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_count(int op, const uint64_t *__
     pa = A.pool + laoff[i];
     pb = B.pool + lboff[i];
   };
-  auto sink = [&](uint32_t i, const uint64_t *, uint32_t, uint32_t card) {
+  auto sink = [&](uint32_t i, const uint64_t *, uint32_t, uint32_t card, const uint32_t *) {
     if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)card);
   };
   rsb::bb_loop<STAGES>(sm, *cnt, op, src, sink);
@@ -466,7 +471,7 @@ int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBat
 
 // ------------------------------------ large array x array (smem bitset + TMA)
 
-__global__ void __launch_bounds__(rsl::LT) k_aa_large_op(int op, const uint32_t *__restrict__ list,
+__global__ void __launch_bounds__(rsl::LT, 4) k_aa_large_op(int op, const uint32_t *__restrict__ list,
                                                          const uint64_t *__restrict__ laoff,
                                                          const uint64_t *__restrict__ lboff,
                                                          const uint32_t *__restrict__ lnab,
@@ -495,7 +500,7 @@ __global__ void __launch_bounds__(rsl::LT) k_aa_large_op(int op, const uint32_t 
   rsl::large_loop(sm, *cnt, op, src, dst, sink);
 }
 
-__global__ void __launch_bounds__(rsl::LT) k_aa_large_count(const uint64_t *__restrict__ laoff,
+__global__ void __launch_bounds__(rsl::LT, 4) k_aa_large_count(const uint64_t *__restrict__ laoff,
                                                             const uint64_t *__restrict__ lboff,
                                                             const uint32_t *__restrict__ lnab,
                                                             const uint32_t *__restrict__ lpair,
@@ -747,6 +752,13 @@ int check_op(int op) {
   if (op < 0 || op > 3) {
     set_error("unknown op " + std::to_string(op));
     return RS_EOP;
+  }
+  static int tuned = 0;  // one-time device tuning constants
+  if (!tuned) {
+    RS_TRY(ensure_device());
+    uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 2048);
+    RS_CK(cudaMemcpyToSymbol(c_aa_large_min, &v, sizeof v));
+    tuned = 1;
   }
   return RS_OK;
 }

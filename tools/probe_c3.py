@@ -9,11 +9,13 @@ n = int(os.environ.get("C3_PAIRS", "1000000"))
 buf, offs = synth.config3(npairs=n)
 A = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, 0, n))
 B = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, n, 2 * n))
+import torch
+dev_out = torch.empty(n, dtype=torch.int64, device="cuda")
 names = ["array_pair_s", "array_pair_m", "array_pair_l", "generic_pair", "copy",
          "array_count_s", "array_count_m", "array_count_l"]
-for op in ("and", "or"):
+for op in ("and", "or", "andnot", "xor"):
     for kind in ("op", "count"):
-        f = (lambda: A.container_pairwise(op, B)) if kind == "op" else (lambda: A.container_pairwise_cardinality(op, B))
+        f = (lambda: A.container_pairwise(op, B)) if kind == "op" else (lambda: A.container_pairwise_cardinality_device(op, B, dev_out.data_ptr(), n))
         f(); _lib.synchronize()
         _lib.profile_reset(); _lib.profile(True)
         e0 = _lib.Event(); f(); e1 = _lib.Event(); _lib.synchronize()
