@@ -53,8 +53,9 @@ __device__ __forceinline__ bool tma_class(int c) { return c == 1 /*CLS_BB*/ || c
 __device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { return ia ? ia[p] : (uint32_t)p; }
 
 // array x array size classes: <= 256 merged items -> warp merge path; <= c_aa_large_min
-// -> 128-thread merge path; above -> smem-bitset kernel (RS_AA_LARGE_MIN overrides)
-__constant__ uint32_t c_aa_large_min = 2048;
+// -> 128-thread merge path; above -> smem-bitset kernel.  Measured on C3 the
+// bitset kernel wins for everything above 256 (RS_AA_LARGE_MIN overrides).
+__constant__ uint32_t c_aa_large_min = 256;
 
 __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
@@ -756,7 +757,7 @@ int check_op(int op) {
   static int tuned = 0;  // one-time device tuning constants
   if (!tuned) {
     RS_TRY(ensure_device());
-    uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 2048);
+    uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 256);
     RS_CK(cudaMemcpyToSymbol(c_aa_large_min, &v, sizeof v));
     tuned = 1;
   }

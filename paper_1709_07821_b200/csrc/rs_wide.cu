@@ -98,12 +98,14 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
   uint8_t acc = S.type[c0];
   or_into(S, c0, sm.X);
   __syncthreads();
-  for (uint32_t i = s + 1; i < e; i++) {
+  uint32_t i = s + 1;
+  // Sequential replay while the accumulator's type can still change: only
+  // array/run steps re-decide it from the running union's card / run count.
+  for (; i < e && acc != RS_TAG_BITSET; i++) {
     uint32_t ci = item_c[i];
     uint8_t ti = S.type[ci];
     or_into(S, ci, sm.X);
     __syncthreads();
-    if (acc == RS_TAG_BITSET) continue;
     if (ti == RS_TAG_BITSET) { acc = RS_TAG_BITSET; continue; }
     bool run_rule = acc == RS_TAG_RUN || ti == RS_TAG_RUN;
     uint32_t card, nruns;
@@ -112,6 +114,29 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
     else acc = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;
     __syncthreads();
   }
+  // Once a bitset, always a bitset (bitmap.py:278-287): the rest is an
+  // order-independent OR, so all remaining contributors go in without
+  // barriers between them (their loads overlap).  Bitset contributors
+  // accumulate in registers (a plain read-modify-write of X would race with
+  // other threads' atomics); array/run contributors scatter with atomics and
+  // all-ones stores, which commute.
+  uint64_t racc[4] = {0, 0, 0, 0};
+  for (; i < e; i++) {
+    const uint32_t ci = item_c[i];
+    const uint8_t ti = S.type[ci];
+    if (ti == RS_TAG_BITSET) {
+      uint64_t w[4];
+      ld_words(S.pool, S.off[ci], t, w);
+#pragma unroll
+      for (int k = 0; k < 4; k++) racc[k] |= w[k];
+    } else {
+      scatter_container(S, ci, ti, sm.X);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; k++) sm.X[4 * t + k] |= racc[k];
+  __syncthreads();
   uint64_t r[4];
   uint32_t pc = 0;
 #pragma unroll
