@@ -85,9 +85,11 @@ __device__ __forceinline__ void issue(BBSmem<STAGES> &sm, int s, const uint8_t *
 // barrier of item k proves every thread has read it, with the pointers of the
 // item STAGES ahead fetched one iteration early (their loads are off the
 // critical path).
-template <int STAGES, typename Src, typename Sink>
-__device__ __forceinline__ void bb_loop(BBSmem<STAGES> &sm, uint32_t count, int op, Src src, Sink sink) {
+template <int STAGES, typename Src, typename Pre, typename Sink>
+__device__ __forceinline__ void bb_loop(BBSmem<STAGES> &sm, uint32_t count, int op, Src src, Pre pre, Sink sink) {
   const int t = threadIdx.x;
+  // per-item sink metadata (output slot, pair, ...) is loaded one item ahead
+  auto meta = pre(blockIdx.x < count ? blockIdx.x : 0);
   if (t == 0) {
     for (int s = 0; s < STAGES; s++) mbar_init(&sm.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -124,13 +126,15 @@ __device__ __forceinline__ void bb_loop(BBSmem<STAGES> &sm, uint32_t count, int 
       r[q] = rs_word_op(op, ra[q], rb[q]);
       pc += __popcll(r[q]);
     }
+    const auto cur = meta;
+    if (i + gridDim.x < count) meta = pre(i + gridDim.x);
     const uint32_t card = block_sum(pc, sm.red[k & 1]);  // barrier: stage s is now free
     if (t == 0 && nxt < count) {
       issue<STAGES>(sm, s, npa, npb);
       nxt += gridDim.x;
       if (nxt < count) src(nxt, npa, npb);
     }
-    sink(i, r, pc, card, sm.red[k & 1]);
+    sink(cur, r, pc, card, sm.red[k & 1]);
   }
 }
 

@@ -34,21 +34,23 @@ static __device__ void scatter_container(const DevBatch &S, uint32_t c, uint8_t 
     for (uint32_t i = threadIdx.x; i < n; i += DT) atomicOr(&X32[v[i] >> 5], 1u << (v[i] & 31));
     return;
   }
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t r = warp; r < n; r += DT / 32) {
-    uint32_t s = v[2 * r], e = s + v[2 * r + 1];
-    uint32_t ws = s >> 6, we = e >> 6;
-    uint64_t first = ~0ull << (s & 63), last = ~0ull >> (63 - (e & 63));
-    if (lane < 2) {  // partial edge words via native 32-bit shared atomics (lane 0: low half, lane 1: high)
-      const uint64_t mf = ws == we ? (first & last) : first;
-      const uint32_t hf = (uint32_t)(mf >> (32 * lane));
-      if (hf) atomicOr(&X32[2 * ws + lane], hf);
-      if (ws != we) {
-        const uint32_t hl = (uint32_t)(last >> (32 * lane));
-        if (hl) atomicOr(&X32[2 * we + lane], hl);
-      }
+  // one thread per run: the (start, length) loads of all runs are independent
+  // (a warp walking runs would chain one global load per run); edge words take
+  // native 32-bit shared atomics (other runs may share them), interior words
+  // belong to this run alone and are plain all-ones stores
+  const uint32_t *r32 = (const uint32_t *)v;
+  for (uint32_t r = threadIdx.x; r < n; r += DT) {
+    const uint32_t sl = r32[r];
+    const uint32_t s = sl & 0xFFFF, e = s + (sl >> 16);
+    const uint32_t ws = s >> 5, we = e >> 5;  // 32-bit word indices
+    const uint32_t first = ~0u << (s & 31), last = ~0u >> (31 - (e & 31));
+    if (ws == we) {
+      atomicOr(&X32[ws], first & last);
+    } else {
+      atomicOr(&X32[ws], first);
+      atomicOr(&X32[we], last);
+      for (uint32_t w = ws + 1; w < we; w++) X32[w] = ~0u;
     }
-    for (uint32_t w = ws + 1 + lane; w < we; w += 32) X[w] = ~0ull;
   }
 }
 

@@ -378,17 +378,27 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_op(int op, const uint32_t *__res
     pa = A.pool + laoff[i];
     pb = B.pool + lboff[i];
   };
-  auto sink = [&](uint32_t i, const uint64_t *r, uint32_t pc, uint32_t card, const uint32_t *red) {
-    const uint32_t e = list[i];
-    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pc, card, opool + E.off[e], red);
+  struct Meta {
+    uint32_t e, pair;
+    uint64_t off;
+  };
+  auto pre = [&](uint32_t i) {
+    Meta m;
+    m.e = list[i];
+    m.off = E.off[m.e];
+    m.pair = E.pair[m.e];
+    return m;
+  };
+  auto sink = [&](const Meta &m, const uint64_t *r, uint32_t pc, uint32_t card, const uint32_t *red) {
+    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pc, card, opool + m.off, red);
     if (threadIdx.x == 0) {
-      O.type[e] = card > RS_ARRAY_MAX ? RS_TAG_BITSET : RS_TAG_ARRAY;
-      O.card[e] = card;
-      O.n[e] = n;
-      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+      O.type[m.e] = card > RS_ARRAY_MAX ? RS_TAG_BITSET : RS_TAG_ARRAY;
+      O.card[m.e] = card;
+      O.n[m.e] = n;
+      if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
     }
   };
-  rsb::bb_loop<STAGES>(sm, *cnt, op, src, sink);
+  rsb::bb_loop<STAGES>(sm, *cnt, op, src, pre, sink);
 }
 
 template <int STAGES>
@@ -402,10 +412,11 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_count(int op, const uint64_t *__
     pa = A.pool + laoff[i];
     pb = B.pool + lboff[i];
   };
-  auto sink = [&](uint32_t i, const uint64_t *, uint32_t, uint32_t card, const uint32_t *) {
-    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)card);
+  auto pre = [&](uint32_t i) { return lpair[i]; };
+  auto sink = [&](uint32_t pair, const uint64_t *, uint32_t, uint32_t card, const uint32_t *) {
+    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[pair], (unsigned long long)card);
   };
-  rsb::bb_loop<STAGES>(sm, *cnt, op, src, sink);
+  rsb::bb_loop<STAGES>(sm, *cnt, op, src, pre, sink);
 }
 
 int env_int(const char *name, int dflt) {

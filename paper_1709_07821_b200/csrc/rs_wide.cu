@@ -45,8 +45,7 @@ __global__ void k_seg_starts(uint64_t T, const uint32_t *__restrict__ flag, cons
 }
 
 // OR container c of S into the smem bitset X (no zeroing; bitsets OR word-wise)
-__device__ void or_into(const DevBatch &S, uint32_t c, uint64_t *X) {
-  uint8_t t = S.type[c];
+__device__ void or_into(const DevBatch &S, uint32_t c, uint8_t t, uint64_t *X) {
   if (t == RS_TAG_BITSET) {
     uint64_t w[4];
     ld_words(S.pool, S.off[c], threadIdx.x, w);
@@ -87,24 +86,34 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
                                                    DevBatch S, uint16_t *okey, uint8_t *otype, uint32_t *ocard,
                                                    uint32_t *on, uint64_t *ooff, uint8_t *__restrict__ opool) {
   __shared__ __align__(16) DenseSmem sm;
+  __shared__ uint32_t mc[DT];   // contributor container index
+  __shared__ uint8_t mt[DT];    // contributor type
   const uint64_t g = blockIdx.x;
   if (g >= G) return;
   const int t = threadIdx.x;
   uint32_t s = seg_start[g], e = seg_start[g + 1];
+  // metadata of the first DT contributors in one parallel round of loads
+  if (s + t < e) {
+    const uint32_t c = item_c[s + t];
+    mc[t] = c;
+    mt[t] = S.type[c];
+  }
 #pragma unroll
   for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
   __syncthreads();
-  uint32_t c0 = item_c[s];
-  uint8_t acc = S.type[c0];
-  or_into(S, c0, sm.X);
+  auto cont = [&](uint32_t i) { return i - s < DT ? mc[i - s] : item_c[i]; };
+  auto ctype = [&](uint32_t i, uint32_t c) { return i - s < DT ? mt[i - s] : S.type[c]; };
+  uint32_t c0 = cont(s);
+  uint8_t acc = ctype(s, c0);
+  or_into(S, c0, acc, sm.X);
   __syncthreads();
   uint32_t i = s + 1;
   // Sequential replay while the accumulator's type can still change: only
   // array/run steps re-decide it from the running union's card / run count.
   for (; i < e && acc != RS_TAG_BITSET; i++) {
-    uint32_t ci = item_c[i];
-    uint8_t ti = S.type[ci];
-    or_into(S, ci, sm.X);
+    uint32_t ci = cont(i);
+    uint8_t ti = ctype(i, ci);
+    or_into(S, ci, ti, sm.X);
     __syncthreads();
     if (ti == RS_TAG_BITSET) { acc = RS_TAG_BITSET; continue; }
     bool run_rule = acc == RS_TAG_RUN || ti == RS_TAG_RUN;
@@ -122,8 +131,8 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
   // all-ones stores, which commute.
   uint64_t racc[4] = {0, 0, 0, 0};
   for (; i < e; i++) {
-    const uint32_t ci = item_c[i];
-    const uint8_t ti = S.type[ci];
+    const uint32_t ci = cont(i);
+    const uint8_t ti = ctype(i, ci);
     if (ti == RS_TAG_BITSET) {
       uint64_t w[4];
       ld_words(S.pool, S.off[ci], t, w);
