@@ -249,3 +249,21 @@ def test_exact_and_upper_bound_allocation_agree(pkg, monkeypatch):
         monkeypatch.setenv("RS_EXACT_ALLOC", "0")
         fast = A.pairwise(op, B).to_wire_list()
         assert exact == fast == [g.wire(r[OPS.index(op)]) for r in g["pair_res"]]
+
+
+def test_harness_rows_gate_and_format(pkg):
+    import io
+    from paper_1709_07821_b200 import harness, synth
+    buf, offs = synth.config4(seed=31, nbitmaps=5, nkeys=50)
+    B = pkg.BitmapBatch.from_wire((buf, offs))
+    S = orc.Session(buf, offs)
+    ia, ib = np.arange(4), np.arange(1, 5)
+    rows = harness.bench_pairwise("c4mini", B, "or", S.run("or", "op", S, ia, ib))
+    rows += harness.bench_pairwise("c4mini", B, "and", S.run("and", "op_cardinality", S, ia, ib), count_only=True)
+    rep = harness.BenchReport(rows)
+    out = io.StringIO()
+    rep.to_csv(out)
+    assert out.getvalue().splitlines()[0] == ",".join(harness.CSV_COLUMNS)
+    assert [r.metric for r in rows] == ["or", "and_count"] and all(r.value > 0 for r in rows)
+    with pytest.raises(harness.CorrectnessError):
+        harness.bench_pairwise("c4mini", B, "xor", np.zeros(4, dtype=np.int64))
