@@ -900,6 +900,29 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   return RS_OK;
 }
 
+// mbase[p] = exclusive prefix of the per-pair merged key counts (na + nb, or
+// na for the count path).  Small pair lists are summed on the host (which
+// already holds bm_start) and uploaded; large ones use a size kernel + scan.
+int pair_bases(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib, uint64_t npairs,
+               DevBatch dA, DevBatch dB, const uint32_t *dia, const uint32_t *dib, int count_mode, uint64_t *msz,
+               uint64_t *mbase) {
+  if (npairs <= 16384) {
+    std::vector<uint64_t> h(npairs + 1);
+    uint64_t acc = 0;
+    for (uint64_t p = 0; p < npairs; p++) {
+      h[p] = acc;
+      uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+      acc += (A->h_bm_start[a + 1] - A->h_bm_start[a]) +
+             (count_mode ? 0 : (B->h_bm_start[b + 1] - B->h_bm_start[b]));
+    }
+    h[npairs] = acc;
+    RS_CK(cudaMemcpyAsync(mbase, h.data(), (npairs + 1) * 8, cudaMemcpyHostToDevice, g_stream));
+    return RS_OK;
+  }
+  RS_LAUNCH(k_pair_msize, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, count_mode, msz);
+  return scan_exclusive<uint64_t>(msz, mbase, npairs + 1);
+}
+
 __global__ void k_iota(uint64_t n, uint64_t *__restrict__ out) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (i < n) out[i] = i;
@@ -983,8 +1006,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
   RS_CK(cudaMemsetAsync(keep + M, 0, 4, g_stream));
   RS_CK(cudaMemsetAsync(ub + M, 0, 8, g_stream));
-  RS_LAUNCH(k_pair_msize, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, 0, msz);
-  RS_TRY(scan_exclusive<uint64_t>(msz, mbase, npairs + 1));
+  RS_TRY(pair_bases(A, B, ia, ib, npairs, dA, dB, dia, dib, 0, msz, mbase));
   RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
@@ -1104,8 +1126,7 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   DevBatch dA = A->dev(), dB = B->dev();
   RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
   RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
-  RS_LAUNCH(k_pair_msize, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, 1, msz);
-  RS_TRY(scan_exclusive<uint64_t>(msz, mbase, npairs + 1));
+  RS_TRY(pair_bases(A, B, ia, ib, npairs, dA, dB, dia, dib, 1, msz, mbase));
   RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
   RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
   RS_LAUNCH(k_formula, grid_for(npairs, 256), 256, 0, npairs, op, A->d_bm_card, B->d_bm_card, dia, dib, inter, dout);

@@ -230,6 +230,57 @@ __global__ void __launch_bounds__(256) k_allpairs_tiles(const uint32_t *__restri
   }
 }
 
+// Register-tiled variant: 32 x 32 containers per CTA, thread (u0, v0) owns the
+// 2 x 2 block {u0, u0+16} x {v0, v0+16}, so every 4 shared loads feed 4
+// AND-popcounts.  Row stride 33 words keeps the 16 distinct v rows of a warp
+// on distinct banks; the 2 u rows of a warp are broadcasts.
+constexpr int AP2_TILE = 32;
+constexpr int AP2_KW = 32;
+
+__global__ void __launch_bounds__(256) k_allpairs_tiles2(const uint32_t *__restrict__ tp_seg,
+                                                         const uint16_t *__restrict__ tp_i, const uint16_t *__restrict__ tp_j,
+                                                         const uint32_t *__restrict__ seg_start,
+                                                         const uint64_t *__restrict__ D, const uint32_t *__restrict__ item_bm,
+                                                         uint64_t N, unsigned long long *__restrict__ M) {
+  __shared__ uint64_t Ai[AP2_TILE][AP2_KW + 1];
+  __shared__ uint64_t Bj[AP2_TILE][AP2_KW + 1];
+  const uint32_t seg = tp_seg[blockIdx.x];
+  const uint32_t s = seg_start[seg], m = seg_start[seg + 1] - s;
+  const uint32_t ti = tp_i[blockIdx.x], tj = tp_j[blockIdx.x];
+  const int t = threadIdx.x, u0 = t >> 4, v0 = t & 15;
+  uint32_t acc[4] = {0, 0, 0, 0};
+  for (int k0 = 0; k0 < RS_WORDS; k0 += AP2_KW) {
+#pragma unroll
+    for (int q = 0; q < (AP2_TILE * AP2_KW) / 256; q++) {
+      const int x = t + 256 * q, row = x / AP2_KW, col = x % AP2_KW;
+      const uint32_t ra = ti * AP2_TILE + row, rb = tj * AP2_TILE + row;
+      Ai[row][col] = ra < m ? D[(uint64_t)(s + ra) * RS_WORDS + k0 + col] : 0;
+      Bj[row][col] = rb < m ? D[(uint64_t)(s + rb) * RS_WORDS + k0 + col] : 0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < AP2_KW; k++) {
+      const uint64_t a0 = Ai[u0][k], a1 = Ai[u0 + 16][k], b0 = Bj[v0][k], b1 = Bj[v0 + 16][k];
+      acc[0] += __popcll(a0 & b0);
+      acc[1] += __popcll(a0 & b1);
+      acc[2] += __popcll(a1 & b0);
+      acc[3] += __popcll(a1 & b1);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const uint32_t u = u0 + 16 * (q >> 1), v = v0 + 16 * (q & 1);
+    const uint32_t gu = ti * AP2_TILE + u, gv = tj * AP2_TILE + v;
+    const bool valid = gu < m && gv < m && (ti != tj || u < v);
+    if (valid && acc[q]) {
+      const uint32_t bu = item_bm[s + gu], bv = item_bm[s + gv];
+      const uint32_t lo = min(bu, bv), hi = max(bu, bv);
+      atomicAdd(&M[(uint64_t)lo * N + hi], (unsigned long long)acc[q]);
+    }
+  }
+}
+
 __global__ void k_item_bitmap(uint64_t T, const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ bm_start,
                               uint64_t nb, uint32_t *__restrict__ item_bm) {
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -392,6 +443,11 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   for (uint64_t k = 0; k < N; k++) sel[k] = k;
   Grouped g;
   RS_TRY(group_and_reorder(in, sel, g));
+  // The 16x16 one-pair-per-thread tile kernel is the default: it is bound by
+  // the POPC issue rate (16/clk/SM), and the 32x32 register-tiled variant
+  // (RS_ALLPAIRS_TILES=2) measured slower (5.5 vs 4.6 ms on C5).
+  const char *tv = getenv("RS_ALLPAIRS_TILES");
+  const bool tiles2 = tv && *tv == '2';
   std::vector<uint32_t> hseg(g.G + 1);
   RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
   std::vector<uint32_t> tseg;
@@ -399,7 +455,8 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   for (uint64_t s = 0; s < g.G; s++) {
     uint32_t m = hseg[s + 1] - hseg[s];
     if (m < 2) continue;
-    uint32_t nt = (m + AP_TILE - 1) / AP_TILE;
+    const uint32_t tile = tiles2 ? AP2_TILE : AP_TILE;
+    uint32_t nt = (m + tile - 1) / tile;
     for (uint32_t a = 0; a < nt; a++)
       for (uint32_t b2 = a; b2 < nt; b2++) { tseg.push_back((uint32_t)s); ti.push_back(a); tj.push_back(b2); }
   }
@@ -419,7 +476,12 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
   RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
   RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
-  RS_LAUNCH_PROF("allpairs", ntp, k_allpairs_tiles, (unsigned)ntp, 256, 0, d_tseg, d_ti, d_tj, g.seg_start, D, item_bm, N, Mx);
+  if (tiles2)
+    RS_LAUNCH_PROF("allpairs", ntp, k_allpairs_tiles2, (unsigned)ntp, 256, 0, d_tseg, d_ti, d_tj, g.seg_start, D,
+                   item_bm, N, Mx);
+  else
+    RS_LAUNCH_PROF("allpairs", ntp, k_allpairs_tiles, (unsigned)ntp, 256, 0, d_tseg, d_ti, d_tj, g.seg_start, D,
+                   item_bm, N, Mx);
   dim3 grid(grid_for(N, 256), (unsigned)N);
   k_upper_triangle<<<grid, 256, 0, g_stream>>>(N, Mx, in->d_bm_card, d_inter, uni ? d_uni : nullptr);
   ++g_launches;
