@@ -195,6 +195,10 @@ def run_reference(args):
 
 def run_gpu(args):
     ws, rank, local = dist_env()
+    if ws > 1 and "OMP_NUM_THREADS" not in os.environ:
+        # one process per GPU: split the host cores between the ranks' generators
+        local_ws = int(os.environ.get("LOCAL_WORLD_SIZE", ws))
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // local_ws))
     dist = dist_init(ws, local)
     import paper_1709_07821_b200 as rb
     from paper_1709_07821_b200 import _lib

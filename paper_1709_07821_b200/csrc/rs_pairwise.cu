@@ -483,55 +483,73 @@ int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBat
 
 // ------------------------------------ large array x array (smem bitset + TMA)
 
-__global__ void __launch_bounds__(rsl::LT, 4) k_aa_large_op(int op, const uint32_t *__restrict__ list,
-                                                         const uint64_t *__restrict__ laoff,
-                                                         const uint64_t *__restrict__ lboff,
-                                                         const uint32_t *__restrict__ lnab,
-                                                         const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
-                                                         Entries E, OutDesc O, uint8_t *__restrict__ opool,
-                                                         uint64_t *__restrict__ res_card) {
+__global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(int op, const uint32_t *__restrict__ list,
+                                                               const uint64_t *__restrict__ laoff,
+                                                               const uint64_t *__restrict__ lboff,
+                                                               const uint32_t *__restrict__ lnab,
+                                                               const uint32_t *__restrict__ cnt, DevBatch A,
+                                                               DevBatch B, Entries E, OutDesc O,
+                                                               uint8_t *__restrict__ opool,
+                                                               uint64_t *__restrict__ res_card) {
   extern __shared__ __align__(128) uint8_t smraw[];
   auto &sm = *reinterpret_cast<rsl::LargeSmem *>(smraw);
-  auto src = [&](uint32_t i, const uint8_t *&pa, uint32_t &na, const uint8_t *&pb, uint32_t &nb) {
-    pa = A.pool + laoff[i];
-    pb = B.pool + lboff[i];
+  auto meta_of = [&](uint32_t i, uint64_t &ao, uint64_t &bo) {
+    rsl::LargeMeta m;
+    ao = laoff[i];
+    bo = lboff[i];
     const uint32_t x = lnab[i];
-    na = x & 0xFFFF;
-    nb = x >> 16;
+    m.na = x & 0xFFFF;
+    m.nb = x >> 16;
+    m.e = list[i];
+    m.dst = E.off[m.e];
+    m.pair = E.pair[m.e];
+    return m;
   };
-  auto dst = [&](uint32_t i) -> uint8_t * { return opool + E.off[list[i]]; };
-  auto sink = [&](uint32_t i, uint32_t card, uint8_t type, uint32_t n) {
+  auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t type, uint32_t n) {
     if (threadIdx.x == 0) {
-      const uint32_t e = list[i];
-      O.type[e] = type;
-      O.card[e] = card;
-      O.n[e] = n;
-      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+      O.type[m.e] = type;
+      O.card[m.e] = card;
+      O.n[m.e] = n;
+      if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
     }
   };
-  rsl::large_loop(sm, *cnt, op, src, dst, sink);
+  rsl::large_loop(sm, *cnt, op, A.pool, B.pool, opool, meta_of, sink);
 }
 
-__global__ void __launch_bounds__(rsl::LT, 4) k_aa_large_count(const uint64_t *__restrict__ laoff,
-                                                            const uint64_t *__restrict__ lboff,
-                                                            const uint32_t *__restrict__ lnab,
-                                                            const uint32_t *__restrict__ lpair,
-                                                            const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
-                                                            uint64_t *__restrict__ acc) {
+__global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint64_t *__restrict__ laoff,
+                                                                  const uint64_t *__restrict__ lboff,
+                                                                  const uint32_t *__restrict__ lnab,
+                                                                  const uint32_t *__restrict__ lpair,
+                                                                  const uint32_t *__restrict__ cnt, DevBatch A,
+                                                                  DevBatch B, uint64_t *__restrict__ acc) {
   extern __shared__ __align__(128) uint8_t smraw[];
   auto &sm = *reinterpret_cast<rsl::LargeSmem *>(smraw);
-  auto src = [&](uint32_t i, const uint8_t *&pa, uint32_t &na, const uint8_t *&pb, uint32_t &nb) {
-    pa = A.pool + laoff[i];
-    pb = B.pool + lboff[i];
+  auto meta_of = [&](uint32_t i, uint64_t &ao, uint64_t &bo) {
+    rsl::LargeMeta m;
+    ao = laoff[i];
+    bo = lboff[i];
     const uint32_t x = lnab[i];
-    na = x & 0xFFFF;
-    nb = x >> 16;
+    m.na = x & 0xFFFF;
+    m.nb = x >> 16;
+    m.e = i;
+    m.dst = 0;
+    m.pair = lpair[i];
+    return m;
   };
-  auto dst = [&](uint32_t) -> uint8_t * { return nullptr; };
-  auto sink = [&](uint32_t i, uint32_t card, uint8_t, uint32_t) {
-    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)card);
+  auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t, uint32_t) {
+    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);
   };
-  rsl::large_loop(sm, *cnt, RS_OP_AND, src, dst, sink);
+  rsl::large_loop(sm, *cnt, RS_OP_AND, A.pool, B.pool, nullptr, meta_of, sink);
+}
+
+template <typename K>
+unsigned persistent_grid_t(K kernel, int threads, size_t smem, uint64_t count) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  uint64_t g = (uint64_t)sms * (per > 0 ? per : 1);
+  return (unsigned)(count < g ? count : g);
 }
 
 int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
@@ -542,9 +560,9 @@ int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch
     RS_CK(cudaFuncSetAttribute(k_aa_large_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  RS_LAUNCH_PROF("array_pair_l", exact ? n : 0, k_aa_large_op, persistent_grid(k_aa_large_op, smem, n), rsl::LT,
-                 smem, op, L.list[CLS_AAL], L.aoff + L.cap, L.boff + L.cap, L.nab, L.cnt + CLS_AAL, dA, dB, En, O,
-                 pool, res_card);
+  RS_LAUNCH_PROF("array_pair_l", exact ? n : 0, k_aa_large_op,
+                 persistent_grid_t(k_aa_large_op, rsl::LTHREADS, smem, n), rsl::LTHREADS, smem, op, L.list[CLS_AAL],
+                 L.aoff + L.cap, L.boff + L.cap, L.nab, L.cnt + CLS_AAL, dA, dB, En, O, pool, res_card);
   return RS_OK;
 }
 
@@ -555,8 +573,9 @@ int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch
     RS_CK(cudaFuncSetAttribute(k_aa_large_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  RS_LAUNCH_PROF("array_count_l", 0, k_aa_large_count, persistent_grid(k_aa_large_count, smem, L.cap), rsl::LT,
-                 smem, L.aoff + L.cap, L.boff + L.cap, L.nab, lpair, L.cnt + CLS_AAL, dA, dB, inter);
+  RS_LAUNCH_PROF("array_count_l", 0, k_aa_large_count,
+                 persistent_grid_t(k_aa_large_count, rsl::LTHREADS, smem, L.cap), rsl::LTHREADS, smem,
+                 L.aoff + L.cap, L.boff + L.cap, L.nab, lpair, L.cnt + CLS_AAL, dA, dB, inter);
   return RS_OK;
 }
 
