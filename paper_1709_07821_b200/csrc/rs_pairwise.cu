@@ -209,12 +209,7 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
   list_append(L, cls, active, e, ao, bo, nab);
 }
 
-// per-pair first entry index (estart[npairs] = total entries)
-__global__ void k_estart(uint64_t npairs, const uint64_t *__restrict__ mbase, const uint32_t *__restrict__ epos,
-                         uint64_t *__restrict__ estart) {
-  uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (p <= npairs) estart[p] = epos[mbase[p]];
-}
+
 
 // ----------------------------------------------------------------- copies
 
@@ -629,14 +624,14 @@ __global__ void __launch_bounds__(256) k_aa_count(const uint32_t *__restrict__ l
 
 // ------------------------------------------------------------ compaction
 
-__global__ void k_keep_nonempty(uint64_t E, const uint64_t *__restrict__ dE, const uint32_t *__restrict__ card,
+__global__ void k_keep_nonempty(uint64_t E, const uint32_t *__restrict__ dE, const uint32_t *__restrict__ card,
                                 uint32_t *__restrict__ keep) {
   uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t lim = dE ? *dE : E;
   if (e <= E) keep[e] = e < lim && card[e] > 0;
 }
 
-__global__ void k_compact(uint64_t E, const uint64_t *__restrict__ dE, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ fpos, Entries En,
+__global__ void k_compact(uint64_t E, const uint32_t *__restrict__ dE, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ fpos, Entries En,
                           OutDesc O, uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn, uint64_t *off) {
   uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (e >= E || !keep[e]) return;
@@ -648,10 +643,12 @@ __global__ void k_compact(uint64_t E, const uint64_t *__restrict__ dE, const uin
   off[f] = En.off[e];
 }
 
-__global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ estart, const uint32_t *__restrict__ fpos,
-                           uint64_t *__restrict__ bm_start) {
+// result bitmap p starts at the compacted position of its first entry:
+// entry epos[mbase[p]] for a key join, entry p for container-level ops
+__global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ mbase, const uint32_t *__restrict__ epos,
+                           const uint32_t *__restrict__ fpos, uint64_t *__restrict__ bm_start) {
   uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (p <= npairs) bm_start[p] = fpos[estart[p]];
+  if (p <= npairs) bm_start[p] = fpos[mbase ? epos[mbase[p]] : p];
 }
 
 // -------------------------------------------------- count-only join + formula
@@ -779,6 +776,9 @@ struct Scratch {
 
 unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
 
+uint32_t g_aa_large_min = 256;
+bool aa_medium_possible() { return g_aa_large_min > 256; }
+
 int check_op(int op) {
   if (op < 0 || op > 3) {
     set_error("unknown op " + std::to_string(op));
@@ -788,6 +788,7 @@ int check_op(int op) {
   if (!tuned) {
     RS_TRY(ensure_device());
     uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 256);
+    g_aa_large_min = v;
     RS_CK(cudaMemcpyToSymbol(c_aa_large_min, &v, sizeof v));
     tuned = 1;
   }
@@ -854,8 +855,8 @@ unsigned sm_count() {
 // *dE on the device, and every class kernel is persistent over its device
 // counter -- the op then runs without any host synchronization.
 int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratch &S, Entries En, Lists L,
-                            uint64_t E, uint64_t P, const uint32_t *hcnt, const uint64_t *dE,
-                            const uint64_t *d_estart, uint64_t npairs, rs_batch **out) {
+                            uint64_t E, uint64_t P, const uint32_t *hcnt, const uint32_t *dE,
+                            const uint64_t *mbase, const uint32_t *epos, uint64_t npairs, rs_batch **out) {
   OutDesc O;
   O.type = (uint8_t *)S.get(E + 1);
   O.card = (uint32_t *)S.get((E + 1) * 4);
@@ -875,7 +876,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     return possible ? L.cap : 0;
   };
   // copies: persistent warps over the list (8 warps per CTA)
-  if (uint64_t n = want(CLS_COPY, true)) {
+  if (uint64_t n = want(CLS_COPY, op != RS_OP_AND)) {
     unsigned g = std::min<uint64_t>(grid_for(n, 8), sms * 16);
     RS_LAUNCH_PROF("copy", hcnt ? n : 0, k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O,
                    b->d_pool, b->d_bm_card);
@@ -895,7 +896,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   if (uint64_t n = want(CLS_AAS, cm.aa))
     RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
                    0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  if (uint64_t n = want(CLS_AAM, cm.aa))
+  if (uint64_t n = want(CLS_AAM, cm.aa && aa_medium_possible()))
     RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
                    256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
   if (uint64_t n = want(CLS_AAL, cm.aa)) {
@@ -913,7 +914,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   RS_TRY(scan_exclusive<uint32_t>(keep2, fpos, E + 1));
   RS_LAUNCH(k_compact, grid_for(E, 256), 256, 0, E, dE, keep2, fpos, En, O, b->d_key, b->d_type, b->d_card, b->d_n,
             b->d_off);
-  RS_LAUNCH(k_bm_start, grid_for(npairs + 1, 256), 256, 0, npairs, d_estart, fpos, b->d_bm_start);
+  RS_LAUNCH(k_bm_start, grid_for(npairs + 1, 256), 256, 0, npairs, mbase, epos, fpos, b->d_bm_start);
   b->h_valid = false;
   *out = b;
   return RS_OK;
@@ -942,10 +943,7 @@ int pair_bases(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const u
   return scan_exclusive<uint64_t>(msz, mbase, npairs + 1);
 }
 
-__global__ void k_iota(uint64_t n, uint64_t *__restrict__ out) {
-  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = i;
-}
+
 
 // container_pairwise needs exactly one container per image (checked once per
 // batch and cached, then per pair only when some image is not single)
@@ -1010,8 +1008,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   uint32_t *mca = (uint32_t *)S.get((M + 1) * 4), *mcb = (uint32_t *)S.get((M + 1) * 4),
            *mpair = (uint32_t *)S.get((M + 1) * 4), *keep = (uint32_t *)S.get((M + 1) * 4),
            *epos = (uint32_t *)S.get((M + 1) * 4);
-  uint64_t *ub = (uint64_t *)S.get((M + 1) * 8), *uoff = (uint64_t *)S.get((M + 1) * 8),
-           *estart = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *ub = (uint64_t *)S.get((M + 1) * 8), *uoff = (uint64_t *)S.get((M + 1) * 8);
   Entries En;
   En.key = (uint16_t *)S.get((M + 1) * 2);
   En.ca = (uint32_t *)S.get((M + 1) * 4);
@@ -1030,10 +1027,9 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
   RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L);
-  RS_LAUNCH(k_estart, grid_for(npairs + 1, 256), 256, 0, npairs, mbase, epos, estart);
   if (ub_mode)
-    return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr,
-                                   estart + npairs, estart, npairs, out);
+    return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr, epos + M,
+                                   mbase, epos, npairs, out);
   // exact mode: one host sync for the totals, then exact grids
   struct { uint32_t E; uint32_t pad; uint64_t P; uint32_t cnt[NCLS]; } h;
   RS_CK(cudaMemcpyAsync(&h.E, epos + M, 4, cudaMemcpyDeviceToHost, g_stream));
@@ -1041,7 +1037,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_CK(cudaMemcpyAsync(h.cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaStreamSynchronize(g_stream));
   (void)tot;
-  return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, nullptr, estart, npairs, out);
+  return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, nullptr, mbase, epos, npairs, out);
 }
 
 extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia,
@@ -1061,28 +1057,28 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   En.cb = (uint32_t *)S.get((npairs + 1) * 4);
   En.pair = (uint32_t *)S.get((npairs + 1) * 4);
   En.off = (uint64_t *)S.get((npairs + 1) * 8);
-  uint64_t *ub = (uint64_t *)S.get((npairs + 1) * 8), *estart = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *ub = (uint64_t *)S.get((npairs + 1) * 8);
   Lists L = make_lists(S, npairs);
   if (!S.ok()) { set_error("device allocation failed (container op)"); return RS_ENOMEM; }
   RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
   DevBatch dA = A->dev(), dB = B->dev();
   RS_LAUNCH(k_cont_entries, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, op, En, ub, L);
   RS_TRY(scan_exclusive<uint64_t>(ub, En.off, npairs + 1));
-  RS_LAUNCH(k_iota, grid_for(npairs + 1, 256), 256, 0, npairs + 1, estart);  // one entry per pair
   // Array-only inputs with the identity pairing: every result slot is at most
   // 2(na + nb) bytes (+16 pad), so the input pools bound the result pool and
   // the op needs no host synchronization.
   const uint8_t AR = 1 << RS_TAG_ARRAY;
   if (!ia && !ib && A->type_mask == AR && B->type_mask == AR && env_int("RS_EXACT_ALLOC", 0) == 0) {
     const uint64_t Pub = A->pool_bytes + B->pool_bytes + 16 * npairs;
-    return run_classes_and_compact(op, A, B, S, En, L, npairs, Pub, nullptr, estart + npairs, estart, npairs, out);
+    return run_classes_and_compact(op, A, B, S, En, L, npairs, Pub, nullptr, nullptr, nullptr, nullptr, npairs,
+                                   out);
   }
   uint64_t P = 0;
   uint32_t cnt[NCLS];
   RS_CK(cudaMemcpyAsync(&P, En.off + npairs, 8, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaMemcpyAsync(cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaStreamSynchronize(g_stream));
-  return run_classes_and_compact(op, A, B, S, En, L, npairs, P, cnt, nullptr, estart, npairs, out);
+  return run_classes_and_compact(op, A, B, S, En, L, npairs, P, cnt, nullptr, nullptr, nullptr, npairs, out);
 }
 
 namespace {
@@ -1107,8 +1103,9 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
   if (cm.aa) {
     RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
                    lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
-    RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
-                   lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
+    if (aa_medium_possible())
+      RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
+                     lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
     if (env_int("RS_AA_LARGE_MERGE", 0))
       RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
                      lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);

@@ -156,31 +156,57 @@ int h2d(void *d, const void *h, size_t bytes) {
   return RS_OK;
 }
 
-template <typename T>
-int scan_exclusive(const T *in, T *out, uint64_t n) {
+// Short scans (the per-op entry/keep/ub arrays of small batches) run in one
+// CTA: one launch instead of CUB's two plus its temp allocation.
+constexpr int SCAN_T = 256, SCAN_V = 8;
+constexpr uint64_t SCAN_SMALL_MAX = 8 * SCAN_T * SCAN_V;
+
+template <typename T, bool INCL>
+__global__ void __launch_bounds__(SCAN_T) k_scan_small(const T *in, T *out, uint32_t n) {
+  using BS = cub::BlockScan<T, SCAN_T>;
+  __shared__ typename BS::TempStorage ts;
+  T carry = 0;
+  for (uint32_t base = 0; base < n; base += SCAN_T * SCAN_V) {
+    T v[SCAN_V], r[SCAN_V];
+    const uint32_t i0 = base + threadIdx.x * SCAN_V;
+#pragma unroll
+    for (int k = 0; k < SCAN_V; k++) v[k] = i0 + k < n ? in[i0 + k] : T(0);
+    T tot;
+    if (INCL) BS(ts).InclusiveSum(v, r, tot);
+    else BS(ts).ExclusiveSum(v, r, tot);
+#pragma unroll
+    for (int k = 0; k < SCAN_V; k++)
+      if (i0 + k < n) out[i0 + k] = r[k] + carry;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+template <typename T, bool INCL>
+static int scan_impl(const T *in, T *out, uint64_t n) {
   if (n == 0) return RS_OK;
+  if (n <= SCAN_SMALL_MAX) {
+    k_scan_small<T, INCL><<<1, SCAN_T, 0, g_stream>>>(in, out, (uint32_t)n);
+    RS_CK(cudaGetLastError());
+    g_launches += 1;
+    return RS_OK;
+  }
   size_t tmp = 0;
-  RS_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, g_stream));
+  if (INCL) RS_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, (int64_t)n, g_stream));
+  else RS_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, g_stream));
   void *t = dalloc(tmp);
   if (!t) { set_error("device allocation failed (scan)"); return RS_ENOMEM; }
-  RS_CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int64_t)n, g_stream));
+  if (INCL) RS_CK(cub::DeviceScan::InclusiveSum(t, tmp, in, out, (int64_t)n, g_stream));
+  else RS_CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int64_t)n, g_stream));
   g_launches += 2;
   dfree(t);
   return RS_OK;
 }
 
 template <typename T>
-int scan_inclusive(const T *in, T *out, uint64_t n) {
-  if (n == 0) return RS_OK;
-  size_t tmp = 0;
-  RS_CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out, (int64_t)n, g_stream));
-  void *t = dalloc(tmp);
-  if (!t) { set_error("device allocation failed (scan)"); return RS_ENOMEM; }
-  RS_CK(cub::DeviceScan::InclusiveSum(t, tmp, in, out, (int64_t)n, g_stream));
-  g_launches += 2;
-  dfree(t);
-  return RS_OK;
-}
+int scan_exclusive(const T *in, T *out, uint64_t n) { return scan_impl<T, false>(in, out, n); }
+template <typename T>
+int scan_inclusive(const T *in, T *out, uint64_t n) { return scan_impl<T, true>(in, out, n); }
 
 template int scan_exclusive<uint32_t>(const uint32_t *, uint32_t *, uint64_t);
 template int scan_exclusive<uint64_t>(const uint64_t *, uint64_t *, uint64_t);
