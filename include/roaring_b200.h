@@ -119,6 +119,12 @@ int rs_batch_to_u32(const rs_batch *b, uint32_t *out, uint64_t cap, uint64_t *of
 /* Bitmap-level equality (bitmap.py:87-91): eq[p] = A[ia[p]] == B[ib[p]], host u8 out. */
 int rs_batch_equal(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
                    uint64_t npairs, uint8_t *eq);
+/* Membership (RoaringBitmap.__contains__, bitmap.py:99-104 ->
+ * container_contains, containers.py:258-268), batched: hit[q] = values[q] in
+ * bitmap ibm[q] (ibm NULL = bitmap 0 for every query).  Host arrays in/out;
+ * one thread per query on the device. */
+int rs_batch_contains(const rs_batch *b, const uint32_t *ibm, const uint32_t *values, uint64_t n,
+                      uint8_t *hit);
 
 /* ---- the hot path ------------------------------------------------------- */
 /* RoaringBitmap.op (bitmap.py:169-210) for npairs pairs: out bitmap p =

@@ -63,6 +63,7 @@ def _declare(L):
         "rs_batch_to_wire": ([P, P, U64, P], I32),
         "rs_batch_to_u32": ([P, P, U64, P], I32),
         "rs_batch_equal": ([P, P, P, P, U64, P], I32),
+        "rs_batch_contains": ([P, P, P, U64, P], I32),
         "rs_pairwise": ([I32, P, P, P, P, U64, pp], I32),
         "rs_pairwise_cardinality": ([I32, P, P, P, P, U64, P, I32], I32),
         "rs_container_pairwise": ([I32, P, P, P, P, U64, pp], I32),

@@ -172,6 +172,21 @@ class BitmapBatch:
         check(lib().rs_batch_equal(self._h, other._h, pa, pb, n, out.ctypes.data))
         return out[:n].astype(bool)
 
+    def contains(self, values, bitmaps=None) -> np.ndarray:
+        """hit[q] = values[q] in bitmap bitmaps[q] (all bitmap 0 when None);
+        RoaringBitmap.__contains__ (bitmap.py:99-104), one GPU thread per query."""
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.int64).reshape(-1))
+        if v.size and (v.min() < 0 or v.max() > 0xFFFFFFFF):
+            raise ValueError("values must fit in 32 bits")
+        v = v.astype(np.uint32)
+        n = len(v)
+        b, pb = _u32_or_none(bitmaps)
+        if b is not None and len(b) != n:
+            raise ValueError("bitmaps and values differ in length")
+        out = np.zeros(max(n, 1), dtype=np.uint8)
+        check(lib().rs_batch_contains(self._h, pb, v.ctypes.data, n, out.ctypes.data))
+        return out[:n].astype(bool)
+
     # ------------------------------------------------------------ hot path
     def _npairs(self, other, ia, ib):
         if ia is not None:

@@ -9,12 +9,12 @@ reference exactly, so wire images compare byte for byte.
 
 from __future__ import annotations
 
-from typing import Iterable, Iterator
+from typing import Callable, Iterable, Iterator
 
 import numpy as np
 
 from .batch import BitmapBatch
-from .containers import OPS, Container, chunks_from_wire, container_positions, op_index
+from .containers import OPS, Container, chunks_from_wire, op_index
 from ._lib import DecodeError
 
 _EMPTY = b"ROAR\x00\x00\x00\x00"
@@ -75,13 +75,39 @@ class RoaringBitmap:
         return zip(keys, conts)
 
     def __contains__(self, v: int) -> bool:
-        key, low = int(v) >> 16, int(v) & 0xFFFF
-        for k, c in self.chunks():
-            if k == key:
-                pos = container_positions(c)
-                i = int(np.searchsorted(pos, low))
-                return i < len(pos) and int(pos[i]) == low
-        return False
+        """Key lookup + container probe (bitmap.py:99-104) as one GPU query."""
+        v = int(v)
+        if not 0 <= v <= 0xFFFFFFFF:  # no such key in the reference either
+            return False
+        return bool(self._b.contains([v])[0])
+
+    def contains_many(self, values) -> np.ndarray:
+        """Batched membership: one GPU thread per query value."""
+        return self._b.contains(values)
+
+    # ------------------------------------------------------------- mutation
+    def add(self, v: int) -> bool:
+        """Insert v; True when the bitmap changed (bitmap.py:106-118).  The
+        container re-typing of container_add (containers.py:271-319) is the
+        OR result-type rule with a one-value array, so the update runs as a
+        GPU pairwise OR against {v}."""
+        v = int(v)
+        if not 0 <= v <= 0xFFFFFFFF:
+            raise ValueError("value out of 32-bit range")
+        if v in self:
+            return False
+        self._b = self._b.pairwise("or", BitmapBatch.from_values([np.array([v], dtype=np.uint32)]), [0], [0])
+        return True
+
+    def remove(self, v: int) -> bool:
+        """Delete v; True when the bitmap changed (bitmap.py:120-134).  Runs as
+        a GPU ANDNOT with {v}: container_remove's demotions (containers.py:322-
+        367) and the dropping of an emptied chunk are that op's result rules."""
+        v = int(v)
+        if not 0 <= v <= 0xFFFFFFFF or v not in self:
+            return False
+        self._b = self._b.pairwise("andnot", BitmapBatch.from_values([np.array([v], dtype=np.uint32)]), [0], [0])
+        return True
 
     # ------------------------------------------------------------ iteration
     def to_array(self) -> np.ndarray:
@@ -90,6 +116,17 @@ class RoaringBitmap:
 
     def __iter__(self) -> Iterator[int]:
         return iter(self.to_array().tolist())
+
+    def for_each(self, visitor: Callable[[int], bool]) -> int:
+        """Call visitor on members in ascending order while it returns True;
+        returns the number visited (bitmap.py:152-166).  The values are
+        extracted on the GPU; the visitor itself is host code."""
+        count = 0
+        for v in self.to_array().tolist():
+            count += 1
+            if not visitor(v):
+                return count
+        return count
 
     # ----------------------------------------------------------- set algebra
     def op(self, op: str, other: "RoaringBitmap") -> "RoaringBitmap":
@@ -128,6 +165,21 @@ class RoaringBitmap:
     def run_optimize(self) -> bool:
         """Re-pick each container's type with run candidacy (bitmap.py:308-316)."""
         return bool(self._b.run_optimize()[0])
+
+    def shrink_to_fit(self) -> int:
+        """Bytes reclaimed by trimming container capacity (bitmap.py:318-328).
+        Device pools are packed at exactly each container's length, so there
+        is never slack to reclaim."""
+        return 0
+
+    def memory_bytes(self) -> tuple[int, int]:
+        """(in-memory bytes, serialized bytes) under the reference's accounting
+        (bitmap.py:330-353) with capacity == length (packed device pools)."""
+        payload, _, types = self._b.stats()
+        nc = sum(types.values())
+        ser = 8 + 8 * nc + payload
+        in_mem = 16 + 7 * nc + payload - 2 * types[3]  # run payload has no u16 count in memory
+        return in_mem, ser
 
     # ------------------------------------------------------------ validation
     def validate(self) -> None:

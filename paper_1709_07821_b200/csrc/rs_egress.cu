@@ -317,3 +317,71 @@ extern "C" int rs_batch_equal(const rs_batch *A, const rs_batch *B, const uint32
   dfree(d_tb); dfree(d_a0); dfree(d_b0); dfree(d_eq);
   return RS_OK;
 }
+
+// ---------------------------------------------------------------- membership
+// container_contains (containers.py:258-268) after the key lookup of
+// RoaringBitmap.__contains__ (bitmap.py:99-104): binary search of the
+// bitmap's key list, then array search / bit test / run search.
+namespace {
+__global__ void k_contains(uint64_t n, DevBatch B, const uint32_t *__restrict__ ibm,
+                           const uint32_t *__restrict__ values, uint8_t *__restrict__ hit) {
+  uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const uint32_t v = values[q], bi = ibm ? ibm[q] : 0;
+  const uint16_t key = (uint16_t)(v >> 16), low = (uint16_t)v;
+  uint64_t lo = B.bm_start[bi], hi = B.bm_start[bi + 1];
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if (B.key[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  uint8_t r = 0;
+  if (lo < B.bm_start[bi + 1] && B.key[lo] == key) {
+    const uint8_t *src = B.pool + B.off[lo];
+    const uint32_t cn = B.n[lo];
+    const uint8_t t = B.type[lo];
+    if (t == RS_TAG_BITSET) {
+      r = (uint8_t)((((const uint64_t *)src)[low >> 6] >> (low & 63)) & 1);
+    } else if (t == RS_TAG_ARRAY) {
+      const uint16_t *a = (const uint16_t *)src;
+      uint32_t l = 0, h = cn;
+      while (l < h) {
+        uint32_t m = (l + h) >> 1;
+        if (a[m] < low) l = m + 1;
+        else h = m;
+      }
+      r = l < cn && a[l] == low;
+    } else {  // last run whose start <= low, then low <= start + length
+      const uint16_t *rv = (const uint16_t *)src;
+      uint32_t l = 0, h = cn;
+      while (l < h) {
+        uint32_t m = (l + h) >> 1;
+        if (rv[2 * m] <= low) l = m + 1;
+        else h = m;
+      }
+      r = l > 0 && (uint32_t)low <= (uint32_t)rv[2 * (l - 1)] + rv[2 * (l - 1) + 1];
+    }
+  }
+  hit[q] = r;
+}
+}  // namespace
+
+extern "C" int rs_batch_contains(const rs_batch *b, const uint32_t *ibm, const uint32_t *values, uint64_t n,
+                                 uint8_t *hit) {
+  RS_TRY(ensure_device());
+  if (n == 0) return RS_OK;
+  if (!values || !hit) { set_error("contains: null values/hit"); return RS_EARG; }
+  if (b->nb == 0) { set_error("contains: empty batch"); return RS_EARG; }
+  if (ibm)
+    for (uint64_t q = 0; q < n; q++)
+      if (ibm[q] >= b->nb) { set_error("contains: bitmap index out of range"); return RS_EARG; }
+  uint32_t *d_v = (uint32_t *)dalloc(n * 4), *d_i = ibm ? (uint32_t *)dalloc(n * 4) : nullptr;
+  uint8_t *d_h = (uint8_t *)dalloc(n);
+  if (!d_v || !d_h || (ibm && !d_i)) { set_error("device allocation failed (contains)"); return RS_ENOMEM; }
+  RS_TRY(h2d(d_v, values, n * 4));
+  if (ibm) RS_TRY(h2d(d_i, ibm, n * 4));
+  RS_LAUNCH(k_contains, grid_for(n, 256), 256, 0, n, b->dev(), d_i, d_v, d_h);
+  RS_TRY(d2h(hit, d_h, n));
+  dfree(d_v); dfree(d_i); dfree(d_h);
+  return RS_OK;
+}

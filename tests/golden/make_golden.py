@@ -19,6 +19,8 @@ the oracle, the CUDA path.  Cases:
 * ``fv_*``     -- from_values on unsorted inputs with duplicates, then
                   run_optimize (+ changed flag) and to_array.
 * ``bad_*``    -- corrupted wire images with the DecodeError offset/message.
+* ``mem_*``    -- membership queries (members, neighbours, misses) per bitmap.
+* ``mut_*``    -- add/remove sequences: changed flags and the image after each.
 """
 
 from __future__ import annotations
@@ -290,6 +292,60 @@ def main():
     add_bad(img)  # run cardinality mismatch
     out["bad"], out["bad_off"] = np.array(bad), np.array(bad_off)
     out["bad_msg"] = json.dumps(bad_msg)
+
+    # -------------------------------------- membership and point mutation
+    # __contains__ (bitmap.py:99-104) on members, neighbours and misses;
+    # add/remove sequences (bitmap.py:106-134) with the changed flags and the
+    # wire image after every step.
+    mem_bm, mem_q, mem_hit = [], [], []
+    mut_start, mut_ops, mut_changed, mut_img = [], [], [], []
+    starts = []
+    runs = RoaringBitmap._from_chunks([1], [ct.RunContainer(np.array([[0, 99], [101, 99], [300, 99]],
+                                                                      dtype=np.uint16))])
+    starts.append((runs, [("add", CHUNK + 100), ("add", CHUNK + 200), ("add", CHUNK + 201),
+                          ("remove", CHUNK + 150), ("remove", CHUNK + 0), ("remove", CHUNK + 399),
+                          ("add", CHUNK + 299), ("remove", CHUNK + 5), ("add", 7), ("remove", 7),
+                          ("remove", CHUNK + 7), ("add", (1 << 32) - 1)]))
+    full = RoaringBitmap.from_values(range(4096))
+    starts.append((full, [("add", 5000), ("remove", 5000), ("remove", 0), ("add", 0), ("add", 70000)]))
+    dense = RoaringBitmap.from_values(range(0, 8194, 2))
+    starts.append((dense, [("remove", 0), ("remove", 2), ("add", 1), ("remove", 1), ("add", 3)]))
+    for _ in range(14):
+        keyspace = int(rng.integers(2, 6))
+        b = random_bitmap(rng, keyspace)
+        vals = b.to_array()
+        seq = []
+        for _k in range(24):
+            r = rng.random()
+            if r < 0.35 and len(vals):
+                seq.append(("remove", int(rng.choice(vals))))
+            elif r < 0.6 and len(vals):
+                seq.append(("add", int(rng.choice(vals)) + int(rng.choice([-1, 1]))))
+            elif r < 0.8:
+                seq.append(("add", int(rng.integers(0, keyspace * CHUNK))))
+            else:
+                seq.append(("remove", int(rng.integers(0, keyspace * CHUNK))))
+        starts.append((b, seq))
+    for b, seq in starts:
+        vals = b.to_array().astype(np.int64)
+        q = np.concatenate([vals[:200], vals[:200] + 1, vals[:200] - 1,
+                            rng.integers(0, 8 * CHUNK, size=100)]) if len(vals) else rng.integers(0, CHUNK, 50)
+        q = np.clip(q, 0, (1 << 32) - 1).astype(np.uint32)
+        mem_bm.append(wires.add(serialize(b)))
+        mem_q.append(wires.add(q.astype("<u4").tobytes()))
+        mem_hit.append(wires.add(np.array([int(v) in b for v in q.tolist()], dtype=np.uint8).tobytes()))
+        cur = b.copy()
+        mut_start.append(wires.add(serialize(cur)))
+        ch, imgs = [], []
+        for kind, v in seq:
+            ch.append(int(cur.add(v) if kind == "add" else cur.remove(v)))
+            imgs.append(wires.add(serialize(cur)))
+        mut_ops.append([[kind, v] for kind, v in seq])
+        mut_changed.append(ch)
+        mut_img.append(imgs)
+    out["mem_bm"], out["mem_q"], out["mem_hit"] = np.array(mem_bm), np.array(mem_q), np.array(mem_hit)
+    out["mut_start"] = np.array(mut_start)
+    out["mut"] = json.dumps({"ops": mut_ops, "changed": mut_changed, "img": mut_img})
 
     out["wire_buf"], out["wire_off"] = wires.arrays()
     np.savez_compressed(OUT, **out)

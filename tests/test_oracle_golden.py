@@ -96,3 +96,29 @@ def test_batch_entry_points_agree_with_single():
         assert outs == [g.wire(r[k]) for r in g["pair_res"]]
         cards = orc.op_cardinality_batch(op, bufA, offA, bufB, offB, idx, idx)
         assert cards.tolist() == [int(c[k]) for c in g["pair_card"]]
+
+
+def test_membership_fixture_matches_oracle_export():
+    g = load()
+    for bm, q, hit in zip(g["mem_bm"], g["mem_q"], g["mem_hit"]):
+        vals = orc.to_array(g.wire(bm))
+        qs = np.frombuffer(g.wire(q), dtype="<u4")
+        want = np.frombuffer(g.wire(hit), dtype=np.uint8).astype(bool)
+        assert np.array_equal(np.isin(qs, vals), want)
+
+
+def test_point_mutation_is_op_with_singleton():
+    """add(v) / remove(v) (bitmap.py:106-134) re-type containers exactly like
+    OR / ANDNOT with the one-value bitmap {v}: the identity the GPU mirror's
+    add/remove rely on, pinned on the reference's own mutation sequences."""
+    g = load()
+    m = g["mut"]
+    for start, ops, changed, imgs in zip(g["mut_start"], m["ops"], m["changed"], m["img"]):
+        cur = g.wire(start)
+        for (kind, v), ch, img in zip(ops, changed, imgs):
+            present = v in set(orc.to_array(cur).tolist())
+            assert ch == int(present != (kind == "add")), (kind, v)
+            if ch:
+                one = orc.from_values(np.array([v], dtype=np.uint64))
+                cur = orc.op("or" if kind == "add" else "andnot", cur, one)
+            assert cur == g.wire(img), (kind, v)
