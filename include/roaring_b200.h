@@ -82,6 +82,18 @@ int rs_profile_query(const char *name, double *total_ms, uint64_t *launches, uin
  * device kernel.  The first failing image raises RS_EDECODE with the
  * reference's offset and message. */
 int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint64_t n, rs_batch **out);
+/* Same result, asynchronous: the host walk runs now (structural errors are
+ * raised here, through the synchronous path), the payload bytes are copied on
+ * the library's copy stream and checked by a kernel queued on the library
+ * stream, and the call returns without waiting.  buf must stay untouched
+ * until rs_batch_wait (pinned memory makes the copy truly asynchronous).
+ * Payload errors are reported by rs_batch_wait -- or by the first call that
+ * returns values to the host -- with the same offset and message as the
+ * synchronous path; results computed from a batch that then fails are
+ * meaningless (but stay in bounds). */
+int rs_batch_from_wire_async(const uint8_t *buf, const uint64_t *offs, uint64_t n, rs_batch **out);
+/* Read back the deferred payload checks: RS_OK or RS_EDECODE (repeatable). */
+int rs_batch_wait(const rs_batch *b);
 
 /* RoaringBitmap.from_values (bitmap.py:40-62) for n bitmaps whose uint32
  * values are concatenated in vals with offsets offs[0..n] (any order,
@@ -101,6 +113,8 @@ int rs_batch_info(const rs_batch *b, uint64_t *n_bitmaps, uint64_t *n_containers
                   uint64_t *pool_bytes);
 /* Per-bitmap cardinality (RoaringBitmap.__len__, bitmap.py:77-82) -> host u64[n]. */
 int rs_batch_cardinalities(const rs_batch *b, uint64_t *out);
+/* Same into DEVICE memory dout (u64[n]), stream-ordered, no synchronization. */
+int rs_batch_cardinalities_device(const rs_batch *b, uint64_t *dout);
 /* Per-bitmap container counts -> host u64[n]. */
 int rs_batch_container_counts(const rs_batch *b, uint64_t *out);
 /* Concatenate batches (bitmaps in order) into a new batch. */

@@ -52,10 +52,13 @@ def _declare(L):
         "rs_event_destroy": ([P], I32),
         "rs_kernel_launches": ([], U64),
         "rs_batch_from_wire": ([P, P, U64, pp], I32),
+        "rs_batch_from_wire_async": ([P, P, U64, pp], I32),
+        "rs_batch_wait": ([P], I32),
         "rs_batch_from_u32": ([P, P, U64, I32, pp], I32),
         "rs_batch_free": ([P], I32),
         "rs_batch_info": ([P, P, P, P], I32),
         "rs_batch_cardinalities": ([P, P], I32),
+        "rs_batch_cardinalities_device": ([P, P], I32),
         "rs_batch_container_counts": ([P, P], I32),
         "rs_batch_concat": ([P, U64, pp], I32),
         "rs_batch_select": ([P, P, U64, pp], I32),

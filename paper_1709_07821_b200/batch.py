@@ -42,10 +42,11 @@ def _images(images):
 
 
 class BitmapBatch:
-    __slots__ = ("_h", "__weakref__")
+    __slots__ = ("_h", "_keep", "__weakref__")
 
     def __init__(self, handle: C.c_void_p):
         self._h = handle
+        self._keep = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -58,12 +59,28 @@ class BitmapBatch:
 
     # ------------------------------------------------------------ building
     @classmethod
-    def from_wire(cls, images) -> "BitmapBatch":
-        """serde.deserialize (serde.py:87-169) of many images at once."""
+    def from_wire(cls, images, *, deferred: bool = False) -> "BitmapBatch":
+        """serde.deserialize (serde.py:87-169) of many images at once.
+
+        deferred=True returns as soon as the transfer is queued: the payload
+        bytes move on the library's copy stream (overlapping kernels already
+        queued) and their checks are read back by wait() -- or by the first
+        call that returns values to the host.  The image buffer must stay
+        alive and untouched until then; pinned memory (PinnedBuffer) makes the
+        copy asynchronous."""
         buf, offs = _images(images)
         h = C.c_void_p()
-        check(lib().rs_batch_from_wire(buf.ctypes.data, offs.ctypes.data, len(offs) - 1, C.byref(h)))
-        return cls(h)
+        fn = lib().rs_batch_from_wire_async if deferred else lib().rs_batch_from_wire
+        check(fn(buf.ctypes.data, offs.ctypes.data, len(offs) - 1, C.byref(h)))
+        b = cls(h)
+        if deferred:
+            b._keep = buf  # the copy engine reads it after we return
+        return b
+
+    def wait(self) -> "BitmapBatch":
+        """Raise DecodeError if the deferred payload checks failed."""
+        check(lib().rs_batch_wait(self._h))
+        return self
 
     @classmethod
     def from_values(cls, arrays) -> "BitmapBatch":
@@ -125,6 +142,11 @@ class BitmapBatch:
         out = np.zeros(max(len(self), 1), dtype=np.uint64)
         check(lib().rs_batch_cardinalities(self._h, out.ctypes.data))
         return out[:len(self)]
+
+    def cardinalities_device(self, dst_ptr: int) -> None:
+        """Per-bitmap cardinalities into device memory at dst_ptr (u64[n]),
+        stream-ordered, without synchronizing."""
+        check(lib().rs_batch_cardinalities_device(self._h, dst_ptr))
 
     def container_counts(self) -> np.ndarray:
         out = np.zeros(max(len(self), 1), dtype=np.uint64)

@@ -203,6 +203,7 @@ extern "C" int rs_batch_stats(const rs_batch *b, uint64_t *payload_bytes, uint64
                               uint64_t *type_counts) {
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(b));
+  RS_TRY(resolve_pending(b));
   unsigned long long *acc = (unsigned long long *)dalloc(4 * 8);
   if (!acc) { set_error("device allocation failed (stats)"); return RS_ENOMEM; }
   RS_CK(cudaMemsetAsync(acc, 0, 32, g_stream));
@@ -231,6 +232,7 @@ static int wire_offsets(const rs_batch *b, uint64_t *&ps, uint64_t *&imgoff) {
 extern "C" int rs_batch_wire_sizes(const rs_batch *b, uint64_t *sizes) {
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(b));
+  RS_TRY(resolve_pending(b));
   uint64_t *ps, *imgoff;
   RS_TRY(wire_offsets(b, ps, imgoff));
   std::vector<uint64_t> h(b->nb + 1);
@@ -244,6 +246,7 @@ extern "C" int rs_batch_wire_sizes(const rs_batch *b, uint64_t *sizes) {
 extern "C" int rs_batch_to_wire(const rs_batch *b, uint8_t *buf, uint64_t cap, uint64_t *offs) {
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(b));
+  RS_TRY(resolve_pending(b));
   uint64_t *ps, *imgoff;
   RS_TRY(wire_offsets(b, ps, imgoff));
   RS_TRY(d2h(offs, imgoff, (b->nb + 1) * 8));
@@ -265,6 +268,7 @@ extern "C" int rs_batch_to_wire(const rs_batch *b, uint8_t *buf, uint64_t cap, u
 extern "C" int rs_batch_to_u32(const rs_batch *b, uint32_t *out, uint64_t cap, uint64_t *offs) {
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(b));
+  RS_TRY(resolve_pending(b));
   uint64_t *cards = (uint64_t *)dalloc((b->nc + 1) * 8), *vpos = (uint64_t *)dalloc((b->nc + 1) * 8),
            *boffs = (uint64_t *)dalloc((b->nb + 1) * 8);
   if (!cards || !vpos || !boffs) { set_error("device allocation failed (to_u32)"); return RS_ENOMEM; }
@@ -291,6 +295,8 @@ extern "C" int rs_batch_equal(const rs_batch *A, const rs_batch *B, const uint32
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
+  RS_TRY(resolve_pending(A));
+  RS_TRY(resolve_pending(B));
   std::vector<uint64_t> tbase(npairs + 1, 0), a0s(npairs + 1, 0), b0s(npairs + 1, 0);
   std::vector<uint32_t> init(npairs + 1, 1);
   for (uint64_t p = 0; p < npairs; p++) {
@@ -369,6 +375,7 @@ __global__ void k_contains(uint64_t n, DevBatch B, const uint32_t *__restrict__ 
 extern "C" int rs_batch_contains(const rs_batch *b, const uint32_t *ibm, const uint32_t *values, uint64_t n,
                                  uint8_t *hit) {
   RS_TRY(ensure_device());
+  RS_TRY(resolve_pending(b));
   if (n == 0) return RS_OK;
   if (!values || !hit) { set_error("contains: null values/hit"); return RS_EARG; }
   if (b->nb == 0) { set_error("contains: empty batch"); return RS_EARG; }

@@ -3,6 +3,8 @@
 #include <cub/cub.cuh>
 #include <algorithm>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <string>
 #include "rs_internal.cuh"
 
@@ -52,11 +54,16 @@ __device__ void warp_copy_payload(uint8_t *__restrict__ dst, const uint8_t *__re
 
 // One warp per container: copy the payload from the staged wire bytes into
 // the aligned pool and run the payload checks of serde.deserialize
-// (serde.py:122-164) in the reference's order.
+// (serde.py:122-164) in the reference's order.  With `card_fix` (deferred
+// validation) a failing container is also made self-consistent -- escaping
+// runs clamped to the chunk, the descriptor cardinality replaced by what the
+// payload holds -- so ops issued before the checks are read back stay in
+// bounds; the batch is rejected at rs_batch_wait either way.
 __global__ void k_wire_gather_validate(uint64_t nc, uint64_t nvalidate, const uint8_t *__restrict__ staged,
                                        const uint64_t *__restrict__ src_off, DevBatch B,
                                        uint8_t *__restrict__ pool, uint8_t *__restrict__ vcode,
-                                       uint32_t *__restrict__ vval, int *__restrict__ any_err) {
+                                       uint32_t *__restrict__ vval, int *__restrict__ any_err,
+                                       uint32_t *__restrict__ card_fix) {
   uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (c >= nc) return;
@@ -67,7 +74,7 @@ __global__ void k_wire_gather_validate(uint64_t nc, uint64_t nvalidate, const ui
   if (c >= nvalidate) return;
   const uint16_t *s16 = (const uint16_t *)src;
   uint8_t code = V_OK;
-  uint32_t val = 0;
+  uint32_t val = 0, fixed = card;
   if (t == RS_TAG_ARRAY) {
     bool bad = false;
     for (uint32_t i = 1 + lane; i < n; i += 32) bad |= s16[i] <= s16[i - 1];
@@ -78,25 +85,41 @@ __global__ void k_wire_gather_validate(uint64_t nc, uint64_t nvalidate, const ui
     for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
     if (pc != card) { code = V_BITSET_CARD; val = pc; }
     else if (card <= RS_ARRAY_MAX) code = V_BITSET_SMALL;
+    fixed = pc;
   } else {
     bool esc = false, ovl = false;
-    uint32_t sum = 0;
+    uint32_t sum = 0, clamped = 0;
     for (uint32_t i = lane; i < n; i += 32) {
       uint32_t st = s16[2 * i], ln = s16[2 * i + 1];
       esc |= st + ln > 0xFFFFu;
       if (i > 0) ovl |= !(st > (uint32_t)s16[2 * i - 2] + s16[2 * i - 1] + 1);
       sum += ln;
+      clamped += min(ln, 0xFFFFu - st) + 1;
     }
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int o = 16; o; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      clamped += __shfl_xor_sync(0xffffffffu, clamped, o);
+    }
     if (__any_sync(0xffffffffu, esc)) code = V_RUN_ESCAPE;
     else if (__any_sync(0xffffffffu, ovl)) code = V_RUN_OVERLAP;
     else if (sum + n != card) { code = V_RUN_CARD; val = sum + n; }
     else if (!rs_run_admissible(card, n)) code = V_RUN_ADMISSIBLE;
+    fixed = clamped;
+    if (card_fix && code == V_RUN_ESCAPE) {
+      uint16_t *d16 = (uint16_t *)(pool + B.off[c]);
+      for (uint32_t i = lane; i < n; i += 32) {
+        uint32_t st = s16[2 * i], ln = s16[2 * i + 1];
+        d16[2 * i + 1] = (uint16_t)min(ln, 0xFFFFu - st);
+      }
+    }
   }
   if (lane == 0) {
     vcode[c] = code;
     vval[c] = val;
-    if (code) atomicOr(any_err, 1);
+    if (code) {
+      atomicOr(any_err, 1);
+      if (card_fix) card_fix[c] = fixed;
+    }
   }
 }
 
@@ -113,30 +136,30 @@ static inline uint32_t g32(const uint8_t *p) {
   return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 
-}  // namespace
-
-extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint64_t n,
-                                  rs_batch **out) {
-  RS_TRY(ensure_device());
-  *out = nullptr;
-  // ---- host walk of the descriptor sections (serde.py:87-169 structure).
-  std::vector<uint64_t> bm_start(n + 1, 0);
+// Host walk of the descriptor sections (serde.py:87-169 structure): container
+// table, payload sources and pool offsets, and the first structural error.
+struct WireWalk {
+  std::vector<uint64_t> bm_start;
   std::vector<uint16_t> key;
   std::vector<uint8_t> type;
   std::vector<uint32_t> card, cnt;
-  std::vector<uint64_t> src, poff;
-  uint64_t pool = 0;
+  std::vector<uint64_t> src, poff;  // src: absolute offset in buf
+  uint64_t pool = 0, nb_built = 0, max_runs = 0;
   WireErr err;
+};
+
+void walk_wire(const uint8_t *buf, const uint64_t *offs, uint64_t n, WireWalk &W) {
+  W.bm_start.assign(n + 1, 0);
+  WireErr &err = W.err;
   char msg[256];
   for (uint64_t i = 0; i < n && !err.set; i++) {
     const uint8_t *d = buf + offs[i];
     uint64_t len = offs[i + 1] - offs[i], off = 0, start = 0;
-    uint64_t first_c = key.size();
-    bm_start[i] = first_c;
+    W.bm_start[i] = W.key.size();
     auto fail = [&](int64_t o, bool desc_stage) {
       err.set = true;
       err.image = i;
-      err.container = key.size();
+      err.container = W.key.size();
       err.descriptor_stage = desc_stage;
       err.offset = o;
       err.msg = msg;
@@ -156,33 +179,32 @@ extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint
     if (memcmp(d, "ROAR", 4) != 0) { snprintf(msg, sizeof msg, "bad magic"); fail(0, true); break; }
     if (!need(4, "container count", true)) break;
     uint32_t count = g32(d + start);
-    std::vector<uint16_t> dk;
-    std::vector<uint8_t> dt;
-    std::vector<uint32_t> dc;
+    const uint64_t desc0 = off;
     int64_t prev_key = -1;
     bool ok = true;
     for (uint32_t k = 0; k < count; k++) {
       if (!need(8, "descriptor", true)) { ok = false; break; }
       uint16_t kk = g16(d + start);
       uint8_t tag = d[start + 2], pad = d[start + 3];
-      uint32_t cc = g32(d + start + 4);
       if (pad != 0) { snprintf(msg, sizeof msg, "nonzero descriptor pad"); fail(start + 3, true); ok = false; break; }
       if (tag < 1 || tag > 3) { snprintf(msg, sizeof msg, "unknown container type %u", tag); fail(start + 2, true); ok = false; break; }
       if ((int64_t)kk <= prev_key) { snprintf(msg, sizeof msg, "keys not strictly increasing at %u", kk); fail(start, true); ok = false; break; }
       prev_key = kk;
-      dk.push_back(kk); dt.push_back(tag); dc.push_back(cc);
     }
     if (!ok) break;
     for (uint32_t k = 0; k < count; k++) {
-      uint32_t cc = dc[k], nn;
-      if (dt[k] == RS_TAG_ARRAY) {
+      const uint8_t *dd = d + desc0 + 8ull * k;
+      uint16_t kk = g16(dd);
+      uint8_t tag = dd[2];
+      uint32_t cc = g32(dd + 4), nn;
+      if (tag == RS_TAG_ARRAY) {
         if (!(cc >= 1 && cc <= RS_ARRAY_MAX)) {
           snprintf(msg, sizeof msg, "array cardinality %u out of range", cc);
           fail((int64_t)off, false); ok = false; break;
         }
         if (!need(2ull * cc, "array payload", false)) { ok = false; break; }
         nn = cc;
-      } else if (dt[k] == RS_TAG_BITSET) {
+      } else if (tag == RS_TAG_BITSET) {
         if (!need(8192, "bitset payload", false)) { ok = false; break; }
         nn = RS_WORDS;
       } else {
@@ -190,11 +212,12 @@ extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint
         nn = g16(d + start);
         if (nn == 0) { snprintf(msg, sizeof msg, "empty run container"); fail((int64_t)start, false); ok = false; break; }
         if (!need(4ull * nn, "run payload", false)) { ok = false; break; }
+        if (nn > W.max_runs) W.max_runs = nn;
       }
-      key.push_back(dk[k]); type.push_back(dt[k]); card.push_back(cc); cnt.push_back(nn);
-      src.push_back(offs[i] + start);
-      poff.push_back(pool);
-      pool += rs_pad16(rs_payload_bytes(dt[k], nn));
+      W.key.push_back(kk); W.type.push_back(tag); W.card.push_back(cc); W.cnt.push_back(nn);
+      W.src.push_back(offs[i] + start);
+      W.poff.push_back(W.pool);
+      W.pool += rs_pad16(rs_payload_bytes(tag, nn));
     }
     if (!ok) break;
     if (off != len) {
@@ -203,13 +226,66 @@ extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint
       break;
     }
   }
-  uint64_t nc = key.size();
-  uint64_t nb_built = err.set ? err.image + 1 : n;
-  for (uint64_t i = nb_built; i <= n; i++) bm_start[i] = nc;
-  if (err.set) bm_start[err.image + 1] = nc;
+  uint64_t nc = W.key.size();
+  W.nb_built = err.set ? err.image + 1 : n;
+  for (uint64_t i = W.nb_built; i <= n; i++) W.bm_start[i] = nc;
+  if (err.set) W.bm_start[err.image + 1] = nc;
+}
+
+// The reference raises the first error in image order; within an image the
+// payload checks of earlier containers precede a later structural error.
+// vcode/vval: device check results (null when none failed); src is relative
+// to offs[0].  Sets the thread-local error; returns RS_EDECODE.
+int format_wire_error(const WireErr &err, uint64_t nc, const uint8_t *vcode, const uint32_t *vval,
+                      const std::vector<uint64_t> &bm_start, uint64_t nb_built, const std::vector<uint32_t> &card,
+                      const std::vector<uint64_t> &src, const uint64_t *offs, std::string *out_msg,
+                      int64_t *out_off, int64_t *out_idx) {
+  char msg[256];
+  for (uint64_t c = 0; vcode && c < nc; c++) {
+    if (!vcode[c]) continue;
+    uint64_t img = std::upper_bound(bm_start.begin(), bm_start.begin() + nb_built + 1, c) - bm_start.begin() - 1;
+    if (err.set && img > err.image) break;
+    uint64_t at = src[c] - (offs[img] - offs[0]);  // payload start inside the image
+    switch (vcode[c]) {
+      case V_ARRAY_ORDER: snprintf(msg, sizeof msg, "array values not strictly increasing"); break;
+      case V_BITSET_CARD: snprintf(msg, sizeof msg, "cardinality mismatch: descriptor says %u, payload holds %u", card[c], vval[c]); break;
+      case V_BITSET_SMALL: snprintf(msg, sizeof msg, "bitset container with only %u values", card[c]); break;
+      case V_RUN_ESCAPE: snprintf(msg, sizeof msg, "run escapes the 16-bit chunk"); break;
+      case V_RUN_OVERLAP: snprintf(msg, sizeof msg, "runs overlap or are adjacent"); break;
+      case V_RUN_CARD: snprintf(msg, sizeof msg, "cardinality mismatch: descriptor says %u, runs hold %u", card[c], vval[c]); break;
+      default: snprintf(msg, sizeof msg, "run form is not the smallest representation"); break;
+    }
+    *out_msg = "at byte " + std::to_string(at) + ": " + msg;
+    *out_off = (int64_t)at;
+    *out_idx = (int64_t)img;
+    set_error(*out_msg, *out_off, *out_idx);
+    return RS_EDECODE;
+  }
+  *out_msg = "at byte " + std::to_string(err.offset) + ": " + err.msg;
+  *out_off = err.offset;
+  *out_idx = (int64_t)err.image;
+  set_error(*out_msg, *out_off, *out_idx);
+  return RS_EDECODE;
+}
+
+uint8_t type_mask_of(const std::vector<uint8_t> &type) {
+  uint8_t tm = 0;
+  for (uint8_t t : type) tm |= (uint8_t)(1u << t);
+  return tm;
+}
+
+}  // namespace
+
+extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint64_t n,
+                                  rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  WireWalk W;
+  walk_wire(buf, offs, n, W);
+  const uint64_t nc = W.key.size();
 
   rs_batch *b = new rs_batch();
-  int rc = batch_alloc(b, n, nc, pool);
+  int rc = batch_alloc(b, n, nc, W.pool);
   if (rc) { rs_batch_free(b); return rc; }
   uint64_t stage_bytes = offs[n] - offs[0];
   uint8_t *staged = (uint8_t *)dalloc(stage_bytes ? stage_bytes : 16);
@@ -223,66 +299,271 @@ extern "C" int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint
     set_error("device allocation failed (wire ingest)");
     return RS_ENOMEM;
   }
-  for (uint64_t c = 0; c < nc; c++) src[c] -= offs[0];
+  for (uint64_t c = 0; c < nc; c++) W.src[c] -= offs[0];
   RS_TRY(h2d(staged, buf + offs[0], stage_bytes));
-  RS_TRY(h2d(b->d_bm_start, bm_start.data(), (n + 1) * 8));
-  RS_TRY(h2d(b->d_key, key.data(), nc * 2));
-  RS_TRY(h2d(b->d_type, type.data(), nc));
-  RS_TRY(h2d(b->d_card, card.data(), nc * 4));
-  RS_TRY(h2d(b->d_n, cnt.data(), nc * 4));
-  RS_TRY(h2d(b->d_off, poff.data(), nc * 8));
-  RS_TRY(h2d(d_src, src.data(), nc * 8));
+  RS_TRY(h2d(b->d_bm_start, W.bm_start.data(), (n + 1) * 8));
+  RS_TRY(h2d(b->d_key, W.key.data(), nc * 2));
+  RS_TRY(h2d(b->d_type, W.type.data(), nc));
+  RS_TRY(h2d(b->d_card, W.card.data(), nc * 4));
+  RS_TRY(h2d(b->d_n, W.cnt.data(), nc * 4));
+  RS_TRY(h2d(b->d_off, W.poff.data(), nc * 8));
+  RS_TRY(h2d(d_src, W.src.data(), nc * 8));
   RS_CK(cudaMemsetAsync(d_any, 0, sizeof(int), g_stream));
   RS_LAUNCH(k_wire_gather_validate, (unsigned)((nc * 32 + 255) / 256), 256, 0, nc, nc, staged, d_src,
-            b->dev(), b->d_pool, d_vcode, d_vval, d_any);
+            b->dev(), b->d_pool, d_vcode, d_vval, d_any, (uint32_t *)nullptr);
   int any = 0;
   RS_TRY(d2h(&any, d_any, sizeof(int)));
   // The host walk must finish before the (pageable) host vectors go away:
   // d2h above synchronized the stream.
   int result = RS_OK;
-  if (any || err.set) {
-    // first failing image in order: payload errors before the host error win
+  if (any || W.err.set) {
     std::vector<uint8_t> vcode(nc);
     std::vector<uint32_t> vval(nc);
     if (any) {
       RS_TRY(d2h(vcode.data(), d_vcode, nc));
       RS_TRY(d2h(vval.data(), d_vval, nc * 4));
     }
-    bool found = false;
-    for (uint64_t c = 0; any && c < nc && !found; c++) {
-      if (!vcode[c]) continue;
-      uint64_t img = std::upper_bound(bm_start.begin(), bm_start.begin() + nb_built + 1, c) - bm_start.begin() - 1;
-      if (err.set && img > err.image) break;
-      uint64_t at = src[c] - (offs[img] - offs[0]);  // payload start inside the image
-      switch (vcode[c]) {
-        case V_ARRAY_ORDER: snprintf(msg, sizeof msg, "array values not strictly increasing"); break;
-        case V_BITSET_CARD: snprintf(msg, sizeof msg, "cardinality mismatch: descriptor says %u, payload holds %u", card[c], vval[c]); break;
-        case V_BITSET_SMALL: snprintf(msg, sizeof msg, "bitset container with only %u values", card[c]); break;
-        case V_RUN_ESCAPE: snprintf(msg, sizeof msg, "run escapes the 16-bit chunk"); break;
-        case V_RUN_OVERLAP: snprintf(msg, sizeof msg, "runs overlap or are adjacent"); break;
-        case V_RUN_CARD: snprintf(msg, sizeof msg, "cardinality mismatch: descriptor says %u, runs hold %u", card[c], vval[c]); break;
-        default: snprintf(msg, sizeof msg, "run form is not the smallest representation"); break;
-      }
-      std::string full = "at byte " + std::to_string(at) + ": " + msg;
-      set_error(full, (int64_t)at, (int64_t)img);
-      found = true;
-    }
-    if (!found) {
-      std::string full = "at byte " + std::to_string(err.offset) + ": " + err.msg;
-      set_error(full, err.offset, (int64_t)err.image);
-    }
-    result = RS_EDECODE;
+    std::string m;
+    int64_t o, ix;
+    result = format_wire_error(W.err, nc, any ? vcode.data() : nullptr, vval.data(), W.bm_start, W.nb_built,
+                               W.card, W.src, offs, &m, &o, &ix);
   }
   dfree(staged); dfree(d_src); dfree(d_vcode); dfree(d_vval); dfree(d_any);
   if (result != RS_OK) { rs_batch_free(b); return result; }
-  b->h_bm_start = bm_start;
-  uint8_t tm = 0;
-  for (uint8_t t : type) tm |= (uint8_t)(1u << t);
-  b->type_mask = tm;
+  b->h_bm_start = std::move(W.bm_start);
+  b->type_mask = type_mask_of(W.type);
   b->h_valid = true;
   RS_TRY(finalize_batch(b));
   *out = b;
   return RS_OK;
+}
+
+// ------------------------------------------------ asynchronous wire ingest
+// The payload bytes go HBM-ward on a dedicated copy stream through a ring of
+// device staging slots, so the transfer of batch k+1 overlaps the kernels of
+// batch k on the library stream; payload checks are read back at
+// rs_batch_wait (or implicitly by any call that returns data to the host).
+namespace {
+
+struct PinnedBlock { uint8_t *p; size_t bytes; cudaEvent_t done; };
+struct StageSlot { uint8_t *d; size_t bytes; cudaEvent_t copied, consumed; bool in_use; };
+std::mutex g_async_mu;
+std::deque<PinnedBlock> g_pinned;  // deque: element addresses stay valid as it grows
+std::deque<StageSlot> g_slots;
+cudaStream_t g_copy = nullptr;
+int g_copy_dev = -1;
+
+int copy_stream(cudaStream_t *s) {
+  int dev = 0;
+  RS_CK(cudaGetDevice(&dev));
+  if (!g_copy || g_copy_dev != dev) {
+    RS_CK(cudaStreamCreateWithFlags(&g_copy, cudaStreamNonBlocking));
+    g_copy_dev = dev;
+  }
+  *s = g_copy;
+  return RS_OK;
+}
+
+int get_pinned(size_t bytes, PinnedBlock **out) {
+  for (auto &b : g_pinned)
+    if (b.bytes >= bytes && cudaEventQuery(b.done) == cudaSuccess) { *out = &b; return RS_OK; }
+  PinnedBlock b;
+  b.bytes = std::max<size_t>(bytes, 1 << 20);
+  RS_CK(cudaHostAlloc((void **)&b.p, b.bytes, cudaHostAllocDefault));
+  RS_CK(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
+  g_pinned.push_back(b);
+  *out = &g_pinned.back();
+  return RS_OK;
+}
+
+int get_slot(size_t bytes, StageSlot **out) {
+  for (auto &s : g_slots)
+    if (!s.in_use && s.bytes >= bytes && cudaEventQuery(s.consumed) == cudaSuccess) {
+      s.in_use = true;
+      *out = &s;
+      return RS_OK;
+    }
+  StageSlot s;
+  s.bytes = bytes;
+  s.in_use = true;
+  if (cudaMalloc((void **)&s.d, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    // out of memory: wait for the slots in flight and retry once in them
+    for (auto &t : g_slots) {
+      if (t.in_use || t.bytes < bytes) continue;
+      RS_CK(cudaEventSynchronize(t.consumed));
+      t.in_use = true;
+      *out = &t;
+      return RS_OK;
+    }
+    set_error("device allocation failed (wire staging)");
+    return RS_ENOMEM;
+  }
+  RS_CK(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
+  RS_CK(cudaEventCreateWithFlags(&s.consumed, cudaEventDisableTiming));
+  g_slots.push_back(s);
+  *out = &g_slots.back();
+  return RS_OK;
+}
+
+// staged metadata section -> the batch's container table
+__global__ void k_unpack_meta(uint64_t nb, uint64_t nc, const uint8_t *__restrict__ meta, uint64_t *bm_start,
+                              uint64_t *off, uint64_t *src, uint32_t *card, uint32_t *n, uint16_t *key,
+                              uint8_t *type) {
+  const uint64_t *m_bm = (const uint64_t *)meta;
+  const uint64_t *m_off = m_bm + rs_pad16((nb + 1) * 8) / 8;
+  const uint64_t *m_src = m_off + nc;
+  const uint32_t *m_card = (const uint32_t *)(m_src + nc);
+  const uint32_t *m_n = m_card + nc;
+  const uint16_t *m_key = (const uint16_t *)(m_n + nc);
+  const uint8_t *m_type = (const uint8_t *)(m_key + rs_pad16(nc * 2) / 2);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nc || i <= nb;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i <= nb) bm_start[i] = m_bm[i];
+    if (i < nc) {
+      off[i] = m_off[i]; src[i] = m_src[i]; card[i] = m_card[i]; n[i] = m_n[i];
+      key[i] = m_key[i]; type[i] = m_type[i];
+    }
+  }
+}
+
+}  // namespace
+
+namespace rs {
+// First use of an asynchronously ingested batch: queue its unpack + payload
+// gather/check on the library stream behind the copy.  Deferring this to the
+// consumer keeps kernels queued meanwhile (earlier batches' ops, exports)
+// from waiting on the transfer.
+int materialize(const rs_batch *cb) {
+  rs_batch *b = const_cast<rs_batch *>(cb);
+  rs_pending *P = b->pending;
+  if (!P || !P->slot) return RS_OK;
+  std::lock_guard<std::mutex> g(g_async_mu);
+  StageSlot *slot = (StageSlot *)P->slot;
+  const uint64_t nc = b->nc, n = b->nb;
+  uint64_t *d_src = (uint64_t *)dalloc((nc ? nc : 1) * 8);
+  if (!d_src) { set_error("device allocation failed (async wire ingest)"); return RS_ENOMEM; }
+  RS_CK(cudaStreamWaitEvent(g_stream, slot->copied, 0));
+  const uint64_t items = std::max<uint64_t>(nc, n + 1);
+  RS_LAUNCH(k_unpack_meta, (unsigned)std::min<uint64_t>((items + 255) / 256, 148 * 16), 256, 0, n, nc, slot->d,
+            b->d_bm_start, b->d_off, d_src, b->d_card, b->d_n, b->d_key, b->d_type);
+  RS_CK(cudaMemsetAsync(P->d_any, 0, sizeof(int), g_stream));
+  if (nc)
+    RS_LAUNCH(k_wire_gather_validate, (unsigned)((nc * 32 + 255) / 256), 256, 0, nc, nc, slot->d + P->meta_bytes,
+              d_src, b->dev(), b->d_pool, P->d_vcode, P->d_vval, P->d_any, b->d_card);
+  RS_CK(cudaEventRecord(slot->consumed, g_stream));
+  slot->in_use = false;
+  P->slot = nullptr;
+  dfree(d_src);
+  return finalize_batch(b);
+}
+
+// A batch freed before first use hands its staging slot back once the copy
+// into it has landed.
+void drop_staged(rs_batch *b) {
+  rs_pending *P = b->pending;
+  if (!P || !P->slot) return;
+  std::lock_guard<std::mutex> g(g_async_mu);
+  StageSlot *slot = (StageSlot *)P->slot;
+  cudaStreamWaitEvent(g_stream, slot->copied, 0);
+  cudaEventRecord(slot->consumed, g_stream);
+  slot->in_use = false;
+  P->slot = nullptr;
+}
+
+int resolve_pending(const rs_batch *cb) {
+  rs_batch *b = const_cast<rs_batch *>(cb);
+  rs_pending *P = b->pending;
+  if (!P) return RS_OK;
+  RS_TRY(materialize(b));
+  if (P->failed) { set_error(P->msg, P->offset, P->index); return RS_EDECODE; }
+  int any = 0;
+  RS_TRY(d2h(&any, P->d_any, sizeof(int)));
+  if (!any) {
+    dfree(P->d_any); dfree(P->d_vcode); dfree(P->d_vval);
+    delete P;
+    b->pending = nullptr;
+    return RS_OK;
+  }
+  const uint64_t nc = b->nc;
+  std::vector<uint8_t> vcode(nc);
+  std::vector<uint32_t> vval(nc);
+  RS_TRY(d2h(vcode.data(), P->d_vcode, nc));
+  RS_TRY(d2h(vval.data(), P->d_vval, nc * 4));
+  WireErr none;
+  P->failed = true;
+  return format_wire_error(none, nc, vcode.data(), vval.data(), b->h_bm_start, b->nb, P->card, P->src,
+                           P->offs.data(), &P->msg, &P->offset, &P->index);
+}
+}  // namespace rs
+
+extern "C" int rs_batch_from_wire_async(const uint8_t *buf, const uint64_t *offs, uint64_t n,
+                                        rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  WireWalk W;
+  walk_wire(buf, offs, n, W);
+  // A structural error, or a run container that can never be admissible
+  // (more runs than any valid chunk holds), goes through the synchronous path,
+  // which reports the reference's exact first error.
+  if (W.err.set || W.max_runs > RS_RUN_MAX_RUNS) return rs_batch_from_wire(buf, offs, n, out);
+  const uint64_t nc = W.key.size();
+  for (uint64_t c = 0; c < nc; c++) W.src[c] -= offs[0];
+  // metadata image: bm_start | off | src | card | n | key | type (16-B sections)
+  const size_t s_bm = rs_pad16((n + 1) * 8), s_off = nc * 8, s_card = nc * 4, s_key = rs_pad16(nc * 2);
+  const size_t meta = rs_pad16(s_bm + 2 * s_off + 2 * s_card + s_key + nc);
+  const uint64_t wire_bytes = offs[n] - offs[0];
+  PinnedBlock *pb;
+  StageSlot *slot;
+  std::unique_lock<std::mutex> lk(g_async_mu);
+  cudaStream_t cs;
+  RS_TRY(copy_stream(&cs));
+  RS_TRY(get_pinned(meta, &pb));
+  RS_TRY(get_slot(meta + rs_pad16(wire_bytes ? wire_bytes : 16), &slot));
+  {
+    uint8_t *h = pb->p;
+    memcpy(h, W.bm_start.data(), (n + 1) * 8); h += s_bm;
+    memcpy(h, W.poff.data(), s_off); h += s_off;
+    memcpy(h, W.src.data(), s_off); h += s_off;
+    memcpy(h, W.card.data(), s_card); h += s_card;
+    memcpy(h, W.cnt.data(), s_card); h += s_card;
+    memcpy(h, W.key.data(), nc * 2); h += s_key;
+    memcpy(h, W.type.data(), nc);
+  }
+  RS_CK(cudaStreamWaitEvent(cs, slot->consumed, 0));
+  RS_CK(cudaMemcpyAsync(slot->d, pb->p, meta, cudaMemcpyHostToDevice, cs));
+  if (wire_bytes) RS_CK(cudaMemcpyAsync(slot->d + meta, buf + offs[0], wire_bytes, cudaMemcpyHostToDevice, cs));
+  RS_CK(cudaEventRecord(pb->done, cs));
+  RS_CK(cudaEventRecord(slot->copied, cs));
+  lk.unlock();
+
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, n, nc, W.pool);
+  rs_pending *P = new rs_pending();
+  b->pending = P;
+  P->slot = slot;
+  P->meta_bytes = meta;
+  P->d_any = (int *)dalloc(sizeof(int));
+  P->d_vcode = (uint8_t *)dalloc(nc ? nc : 1);
+  P->d_vval = (uint32_t *)dalloc((nc ? nc : 1) * 4);
+  if (rc || !P->d_any || !P->d_vcode || !P->d_vval) {
+    rs_batch_free(b);  // hands the slot back behind the queued copy
+    set_error("device allocation failed (async wire ingest)");
+    return RS_ENOMEM;
+  }
+  P->card = std::move(W.card);
+  P->src = std::move(W.src);
+  P->offs.assign(offs, offs + n + 1);
+  b->h_bm_start = std::move(W.bm_start);
+  b->type_mask = type_mask_of(W.type);
+  b->h_valid = true;
+  *out = b;
+  return RS_OK;
+}
+
+extern "C" int rs_batch_wait(const rs_batch *b) {
+  if (!b) { set_error("null batch"); return RS_EARG; }
+  return resolve_pending(b);
 }
 
 // --------------------------------------------------------- from_values ingest

@@ -38,6 +38,22 @@ struct DevBatch {
   const uint64_t *bm_card;
 };
 
+// Deferred payload validation of an asynchronously ingested batch
+// (rs_batch_from_wire_async): the device flags plus what the host needs to
+// format the reference's DecodeError once they are read back.
+struct rs_pending {
+  int *d_any = nullptr;
+  uint8_t *d_vcode = nullptr;
+  uint32_t *d_vval = nullptr;
+  std::vector<uint32_t> card;
+  std::vector<uint64_t> src, offs;  // payload start in the staged bytes; image offsets
+  void *slot = nullptr;              // staging slot until first use (materialize)
+  uint64_t meta_bytes = 0;           // metadata section at the head of the slot
+  bool failed = false;
+  std::string msg;
+  int64_t offset = -1, index = -1;
+};
+
 struct rs_batch {
   uint64_t nb = 0, nc = 0, cap_c = 0, pool_bytes = 0;
   uint64_t *d_bm_start = nullptr;
@@ -55,6 +71,7 @@ struct rs_batch {
   // pipeline skip type-pair classes that cannot occur
   uint8_t type_mask = 0xFF;
   int single = -1;  // 1 = every bitmap holds exactly one container (cached)
+  rs_pending *pending = nullptr;  // payload checks not yet read back
   DevBatch dev() const {
     DevBatch d;
     d.nb = nb; d.nc = nc; d.bm_start = d_bm_start; d.key = d_key; d.type = d_type;
@@ -76,6 +93,9 @@ int batch_alloc(rs_batch *b, uint64_t nb, uint64_t nc, uint64_t pool_bytes);
 void batch_release(rs_batch *b);
 int fetch_host_meta(const rs_batch *b);   // fills h_bm_start (synchronizes)
 int finalize_batch(rs_batch *b);          // computes d_bm_card from containers
+int resolve_pending(const rs_batch *b);    // reads deferred checks; RS_EDECODE on failure
+int materialize(const rs_batch *b);        // queue a deferred batch's unpack/gather (first use)
+void drop_staged(rs_batch *b);             // release an unused deferred batch's staging slot
 template <typename T> int scan_exclusive(const T *in, T *out, uint64_t n);
 template <typename T> int scan_inclusive(const T *in, T *out, uint64_t n);
 int sort_u64(uint64_t *keys, uint64_t n, int end_bit);

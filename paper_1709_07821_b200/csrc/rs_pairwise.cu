@@ -1125,6 +1125,10 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
+  if (!counts_on_device) {  // host readback: surface deferred decode errors
+    RS_TRY(resolve_pending(A));
+    RS_TRY(resolve_pending(B));
+  }
   Scratch S;
   uint32_t *dia, *dib;
   RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
@@ -1157,6 +1161,10 @@ extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, cons
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
+  if (!counts_on_device) {  // host readback: surface deferred decode errors
+    RS_TRY(resolve_pending(A));
+    RS_TRY(resolve_pending(B));
+  }
   RS_TRY(check_single_containers(A, B, ia, ib, npairs));
   Scratch S;
   uint32_t *dia, *dib;

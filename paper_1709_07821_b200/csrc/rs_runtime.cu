@@ -254,6 +254,12 @@ int batch_alloc(rs_batch *b, uint64_t nb, uint64_t nc, uint64_t pool_bytes) {
 }
 
 void batch_release(rs_batch *b) {
+  if (b->pending) {
+    drop_staged(b);
+    dfree(b->pending->d_any); dfree(b->pending->d_vcode); dfree(b->pending->d_vval);
+    delete b->pending;
+    b->pending = nullptr;
+  }
   dfree(b->d_bm_start); dfree(b->d_bm_card); dfree(b->d_key); dfree(b->d_type);
   dfree(b->d_card); dfree(b->d_n); dfree(b->d_off); dfree(b->d_pool);
   b->d_bm_start = nullptr; b->d_bm_card = nullptr; b->d_key = nullptr; b->d_type = nullptr;
@@ -261,6 +267,7 @@ void batch_release(rs_batch *b) {
 }
 
 int fetch_host_meta(const rs_batch *cb) {
+  RS_TRY(materialize(cb));
   rs_batch *b = const_cast<rs_batch *>(cb);
   if (b->h_valid) return RS_OK;
   b->h_bm_start.resize(b->nb + 1);
@@ -400,7 +407,15 @@ int rs_batch_info(const rs_batch *b, uint64_t *n_bitmaps, uint64_t *n_containers
 
 int rs_batch_cardinalities(const rs_batch *b, uint64_t *out) {
   if (!b) { set_error("null batch"); return RS_EARG; }
+  RS_TRY(resolve_pending(b));
   return d2h(out, b->d_bm_card, b->nb * 8);
+}
+
+int rs_batch_cardinalities_device(const rs_batch *b, uint64_t *dout) {
+  if (!b || !dout) { set_error("null batch/out"); return RS_EARG; }
+  RS_TRY(materialize(b));
+  if (b->nb) RS_CK(cudaMemcpyAsync(dout, b->d_bm_card, b->nb * 8, cudaMemcpyDeviceToDevice, g_stream));
+  return RS_OK;
 }
 
 int rs_batch_container_counts(const rs_batch *b, uint64_t *out) {

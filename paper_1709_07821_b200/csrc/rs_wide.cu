@@ -434,6 +434,7 @@ extern "C" int rs_union_many(const rs_batch *in, const uint64_t *idx, uint64_t n
 }
 
 extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uint64_t *uni) {
+  RS_TRY(resolve_pending(in));
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(in));
   uint64_t N = in->nb;
@@ -494,6 +495,7 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
 }
 
 extern "C" int rs_batch_run_optimize(rs_batch *b, uint8_t *changed) {
+  RS_TRY(resolve_pending(b));
   RS_TRY(ensure_device());
   RS_TRY(fetch_host_meta(b));
   uint32_t *d_ch = (uint32_t *)dalloc((b->nb + 1) * 4);

@@ -267,3 +267,70 @@ def test_harness_rows_gate_and_format(pkg):
     assert [r.metric for r in rows] == ["or", "and_count"] and all(r.value > 0 for r in rows)
     with pytest.raises(harness.CorrectnessError):
         harness.bench_pairwise("c4mini", B, "xor", np.zeros(4, dtype=np.int64))
+
+
+# ---------------------------------------------- deferred (asynchronous) ingest
+
+def test_deferred_ingest_golden_pairs(pkg):
+    g = load()
+    A = pkg.BitmapBatch.from_wire([g.wire(a) for a in g["pair_a"]], deferred=True)
+    B = pkg.BitmapBatch.from_wire([g.wire(b) for b in g["pair_b"]], deferred=True)
+    for k, op in enumerate(OPS):  # ops queued before the checks are read back
+        got = A.pairwise(op, B).to_wire_list()
+        assert got == [g.wire(r[k]) for r in g["pair_res"]], op
+    A.wait()
+    B.wait()
+
+
+def test_deferred_ingest_decode_errors(pkg):
+    """Every golden DecodeError surfaces with the reference's offset and
+    message: structural ones at from_wire, payload ones at wait() or at the
+    first host readback; ops queued on a failing batch stay in bounds."""
+    g = load()
+    good = pkg.BitmapBatch.from_wire([g.wire(g["pair_a"][0])])
+    for img, off, msg in zip(g["bad"], g["bad_off"], g["bad_msg"]):
+        try:
+            b = pkg.BitmapBatch.from_wire([g.wire(img)], deferred=True)
+        except pkg.DecodeError as e:
+            assert e.offset == off and str(e) == msg
+            continue
+        for op in OPS:  # queued before the checks are known
+            b.pairwise(op, good)
+        with pytest.raises(pkg.DecodeError):  # host readback resolves the checks
+            b.pairwise_cardinality("and", good)
+        with pytest.raises(pkg.DecodeError) as e:
+            b.wait()
+        assert e.value.offset == off and str(e.value) == msg
+        with pytest.raises(pkg.DecodeError):
+            b.to_wire_list()
+        with pytest.raises(pkg.DecodeError):
+            b.wait()
+
+
+def test_deferred_ingest_pipeline_matches_sync(pkg):
+    """Chunked ingest on the copy stream overlapping ops on the library
+    stream (the e2e pattern of bench.py) gives the synchronous results."""
+    from paper_1709_07821_b200 import _lib, synth
+    buf, offs = synth.config2(npairs=32)
+    n = 32
+    pin = _lib.PinnedBuffer(int(offs[-1]))
+    pin.array[:] = buf[:int(offs[-1])]
+    A_sync = pkg.BitmapBatch.from_wire((buf[:int(offs[n])], offs[:n + 1].copy()))
+    B_sync = pkg.BitmapBatch.from_wire((buf[int(offs[n]):], offs[n:] - offs[n]))
+    want = {op: A_sync.pairwise(op, B_sync).to_wire_list() for op in OPS}
+    got = {op: [] for op in OPS}
+    batches = []
+    step = 8
+    for p0 in range(0, n, step):
+        def part(base, p0=p0):
+            o = offs[base + p0:base + p0 + step + 1]
+            return (pin.array[int(o[0]):int(o[-1])], (o - o[0]).astype(np.uint64))
+        A = pkg.BitmapBatch.from_wire(part(0), deferred=True)
+        B = pkg.BitmapBatch.from_wire(part(n), deferred=True)
+        batches += [A, B]
+        for op in OPS:
+            got[op].append(A.pairwise(op, B))
+    for b in batches:
+        b.wait()
+    for op in OPS:
+        assert [w for R in got[op] for w in R.to_wire_list()] == want[op], op
