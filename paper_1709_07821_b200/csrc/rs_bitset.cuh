@@ -13,7 +13,9 @@
 
 namespace rsb {
 
-constexpr int BT = 256;  // threads; thread t owns words [4t, 4t+4)
+constexpr int BT = 256;  // threads; thread t owns words t, t+256, t+512, t+768
+// (strided: a warp's 64-bit shared loads and global stores touch 256
+// consecutive bytes -- conflict-free, fully coalesced)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -56,18 +58,30 @@ struct BBSmem {
   uint64_t b[STAGES][RS_WORDS];
   uint16_t out[RS_ARRAY_MAX];
   uint64_t bar[STAGES];
-  typename cub::BlockScan<uint32_t, BT>::TempStorage scan;
-  uint32_t red[2][BT / 32];  // double-buffered: no trailing barrier per item
+  // per-warp totals, double-buffered (no trailing barrier per item): [0] the
+  // popcounts of words t and t+256 packed in 16-bit fields, [1] of t+512/t+768
+  uint32_t red[2][2][BT / 32];
 };
 
-__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t *red) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+// Block totals of two packed vectors (four 16-bit row counts, each <= 16384):
+// per-warp totals land in red[0..1][warp]; returns the sum of all four rows.
+__device__ __forceinline__ uint32_t block_sum_packed(uint32_t v0, uint32_t v1, uint32_t (*red)[BT / 32]) {
+  for (int o = 16; o; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = v0;
+    red[1][threadIdx.x >> 5] = v1;
+  }
   __syncthreads();
-  uint32_t s = 0;
+  uint32_t s0 = 0, s1 = 0;
 #pragma unroll
-  for (int w = 0; w < BT / 32; w++) s += red[w];
-  return s;
+  for (int w = 0; w < BT / 32; w++) {
+    s0 += red[0][w];
+    s1 += red[1][w];
+  }
+  return (s0 & 0xFFFFu) + (s0 >> 16) + (s1 & 0xFFFFu) + (s1 >> 16);
 }
 
 // Issue the two operand copies of one work item into stage `s`.
@@ -79,8 +93,9 @@ __device__ __forceinline__ void issue(BBSmem<STAGES> &sm, int s, const uint8_t *
 }
 
 // Persistent loop.  src(i, pa, pb) gives the operand pointers of item i;
-// sink(i, r[4], pc, card) consumes the result words of this thread (after a
-// block-wide reduction made `card` uniform).  Items i = blockIdx.x + k*gridDim.x.
+// sink(meta, r[4], pk0, pk1, card, red) consumes the result words of this
+// thread (words t + 256q; pk0/pk1 their packed popcounts) after a block-wide
+// reduction made `card` uniform.  Items i = blockIdx.x + k*gridDim.x.
 // Thread 0 is the producer: it refills stage s right after the reduction
 // barrier of item k proves every thread has read it, with the pointers of the
 // item STAGES ahead fetched one iteration early (their loads are off the
@@ -113,69 +128,75 @@ __device__ __forceinline__ void bb_loop(BBSmem<STAGES> &sm, uint32_t count, int 
     if (i >= count) break;
     const int s = k % STAGES;
     mbar_wait(&sm.bar[s], (k / STAGES) & 1);
-    const uint4 *xa = (const uint4 *)sm.a[s] + 2 * t, *xb = (const uint4 *)sm.b[s] + 2 * t;
-    uint4 a0 = xa[0], a1 = xa[1], b0 = xb[0], b1 = xb[1];
-    uint64_t ra[4] = {((uint64_t)a0.y << 32) | a0.x, ((uint64_t)a0.w << 32) | a0.z, ((uint64_t)a1.y << 32) | a1.x,
-                      ((uint64_t)a1.w << 32) | a1.z};
-    uint64_t rb[4] = {((uint64_t)b0.y << 32) | b0.x, ((uint64_t)b0.w << 32) | b0.z, ((uint64_t)b1.y << 32) | b1.x,
-                      ((uint64_t)b1.w << 32) | b1.z};
+    const uint64_t *xa = sm.a[s] + t, *xb = sm.b[s] + t;
     uint64_t r[4];
-    uint32_t pc = 0;
+    uint32_t pq[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      r[q] = rs_word_op(op, ra[q], rb[q]);
-      pc += __popcll(r[q]);
+      r[q] = rs_word_op(op, xa[BT * q], xb[BT * q]);
+      pq[q] = __popcll(r[q]);
     }
+    const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
     const auto cur = meta;
     if (i + gridDim.x < count) meta = pre(i + gridDim.x);
-    const uint32_t card = block_sum(pc, sm.red[k & 1]);  // barrier: stage s is now free
+    const uint32_t card = block_sum_packed(pk0, pk1, sm.red[k & 1]);  // barrier: stage s is now free
     if (t == 0 && nxt < count) {
       issue<STAGES>(sm, s, npa, npb);
       nxt += gridDim.x;
       if (nxt < count) src(nxt, npa, npb);
     }
-    sink(cur, r, pc, card, sm.red[k & 1]);
+    sink(cur, r, pk0, pk1, card, sm.red[k & 1]);
   }
 }
 
-// Exclusive prefix of v over the CTA, reusing the per-warp totals that
-// block_sum() already left in red[] (no extra barrier): warp shuffle scan +
-// the totals of the warps before this one.
-__device__ __forceinline__ uint32_t block_excl_from_red(uint32_t v, const uint32_t *red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  uint32_t pre = 0;
-#pragma unroll
-  for (int k = 0; k < BT / 32; k++) pre += k < w ? red[k] : 0;
-  return pre + x - v;
-}
-
-// Encode a result set held as 4 words per thread into dst: bitset (> 4096
-// values) or sorted array via the smem staging buffer.  `red` holds the
-// per-warp popcount totals of this item (from block_sum).  Returns n.
+// Encode a result set held as words t + 256q (q < 4) per thread into dst:
+// bitset (> 4096 values) or sorted array via the smem staging buffer.  The
+// array positions come from a scan of the packed row counts that reuses the
+// per-warp totals block_sum_packed() left in red (no extra barrier); each
+// word is then peeled from its top bit down (FLO) into its slot range.
+// Returns n.
 template <int STAGES>
-__device__ __forceinline__ uint32_t bb_encode(BBSmem<STAGES> &sm, const uint64_t r[4], uint32_t pc, uint32_t card,
-                                              uint8_t *dst, const uint32_t *red) {
+__device__ __forceinline__ uint32_t bb_encode(BBSmem<STAGES> &sm, const uint64_t r[4], uint32_t pk0, uint32_t pk1,
+                                              uint32_t card, uint8_t *dst, const uint32_t (*red)[BT / 32]) {
   const int t = threadIdx.x;
   if (card > RS_ARRAY_MAX) {
-    uint4 *p = (uint4 *)dst + 2 * t;
-    st_stream(p, make_uint4((uint32_t)r[0], (uint32_t)(r[0] >> 32), (uint32_t)r[1], (uint32_t)(r[1] >> 32)));
-    st_stream(p + 1, make_uint4((uint32_t)r[2], (uint32_t)(r[2] >> 32), (uint32_t)r[3], (uint32_t)(r[3] >> 32)));
+    uint64_t *p = (uint64_t *)dst + t;
+#pragma unroll
+    for (int q = 0; q < 4; q++) asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p + BT * q), "l"(r[q]) : "memory");
     return RS_WORDS;
   }
   if (card == 0) return 0;
-  uint32_t base = block_excl_from_red(pc, red);
+  const int lane = t & 31, w = t >> 5;
+  uint32_t x0 = pk0, x1 = pk1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+    if (lane >= o) { x0 += y0; x1 += y1; }
+  }
+  uint32_t e0 = x0 - pk0, e1 = x1 - pk1, T0 = 0, T1 = 0;  // exclusive prefix / block totals
+#pragma unroll
+  for (int k = 0; k < BT / 32; k++) {
+    const uint32_t a = red[0][k], b = red[1][k];
+    T0 += a; T1 += b;
+    if (k < w) { e0 += a; e1 += b; }
+  }
+  // word t + 256q starts after rows 0..q-1 and this row's words before t
+  const uint32_t r0 = T0 & 0xFFFFu, r1 = T0 >> 16, r2 = T1 & 0xFFFFu;
+  uint32_t end[4] = {(e0 & 0xFFFFu) + (pk0 & 0xFFFFu), r0 + (e0 >> 16) + (pk0 >> 16),
+                     r0 + r1 + (e1 & 0xFFFFu) + (pk1 & 0xFFFFu), r0 + r1 + r2 + (e1 >> 16) + (pk1 >> 16)};
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    uint64_t w = r[q];
-    while (w) {
-      sm.out[base++] = (uint16_t)((4 * t + q) * 64 + __ffsll((long long)w) - 1);
-      w &= w - 1;
+    const uint32_t pos = (uint32_t)(t + BT * q) * 64;
+    uint32_t b = end[q], hi = (uint32_t)(r[q] >> 32), lo = (uint32_t)r[q];
+    while (hi) {
+      const uint32_t p = 31 - __clz(hi);
+      sm.out[--b] = (uint16_t)(pos + 32 + p);
+      hi ^= 1u << p;
+    }
+    while (lo) {
+      const uint32_t p = 31 - __clz(lo);
+      sm.out[--b] = (uint16_t)(pos + p);
+      lo ^= 1u << p;
     }
   }
   const uint32_t nvec = (2 * card + 15) >> 4;

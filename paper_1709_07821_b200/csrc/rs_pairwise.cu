@@ -384,8 +384,9 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_op(int op, const uint32_t *__res
     m.pair = E.pair[m.e];
     return m;
   };
-  auto sink = [&](const Meta &m, const uint64_t *r, uint32_t pc, uint32_t card, const uint32_t *red) {
-    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pc, card, opool + m.off, red);
+  auto sink = [&](const Meta &m, const uint64_t *r, uint32_t pk0, uint32_t pk1, uint32_t card,
+                  const uint32_t (*red)[rsb::BT / 32]) {
+    const uint32_t n = rsb::bb_encode<STAGES>(sm, r, pk0, pk1, card, opool + m.off, red);
     if (threadIdx.x == 0) {
       O.type[m.e] = card > RS_ARRAY_MAX ? RS_TAG_BITSET : RS_TAG_ARRAY;
       O.card[m.e] = card;
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(rsb::BT) k_bb_count(int op, const uint64_t *__
     pb = B.pool + lboff[i];
   };
   auto pre = [&](uint32_t i) { return lpair[i]; };
-  auto sink = [&](uint32_t pair, const uint64_t *, uint32_t, uint32_t card, const uint32_t *) {
+  auto sink = [&](uint32_t pair, const uint64_t *, uint32_t, uint32_t, uint32_t card, const uint32_t (*)[rsb::BT / 32]) {
     if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[pair], (unsigned long long)card);
   };
   rsb::bb_loop<STAGES>(sm, *cnt, op, src, pre, sink);
