@@ -40,7 +40,7 @@ struct LargeSmem {
   uint64_t full[LSTAGES];
   uint64_t empty[LSTAGES];
   LargeMeta meta[LSTAGES];
-  uint32_t red[2][LT / 32];
+  uint32_t red[2][2][LT / 32];
 };
 
 __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(LT) : "memory"); }
@@ -51,7 +51,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 
 // consumer-only exclusive scan with total (one named barrier); the scratch is
 // double-buffered by item parity so no trailing barrier is needed
-__device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t *red, uint32_t &total) {
+__device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t (*red2)[LT / 32], uint32_t &total) {
+  uint32_t *red = red2[0];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -70,6 +71,27 @@ __device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t *red, uint32_t &t
   }
   total = tot;
   return pre + x - v;
+}
+
+// cscan over two packed vectors (16-bit fields): exclusive prefix and totals
+__device__ __forceinline__ void cscan2(uint32_t v0, uint32_t v1, uint32_t (*red)[LT / 32], uint32_t &e0,
+                                       uint32_t &e1, uint32_t &T0, uint32_t &T1) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x0 = v0, x1 = v1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+    if (lane >= o) { x0 += y0; x1 += y1; }
+  }
+  if (lane == 31) { red[0][w] = x0; red[1][w] = x1; }
+  cbar();
+  e0 = x0 - v0; e1 = x1 - v1; T0 = 0; T1 = 0;
+#pragma unroll
+  for (int k = 0; k < LT / 32; k++) {
+    const uint32_t a = red[0][k], b = red[1][k];
+    T0 += a; T1 += b;
+    if (k < w) { e0 += a; e1 += b; }
+  }
 }
 
 // OR / XOR into X with one native 32-bit shared atomic per touched word
@@ -125,31 +147,73 @@ __device__ __forceinline__ void flush_stage(uint16_t *stage, uint32_t total, uin
   for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)stage)[v];
 }
 
+// Sorted-array membership: is x in v[0, n)?  (n <= 4096: 12 probes)
+__device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, len = n;
+  while (len > 1) {
+    const uint32_t half = len >> 1;
+    if (v[lo + half] <= x) lo += half;
+    len -= half;
+  }
+  return n && v[lo] == x;
+}
+
 // One pair (consumers only).  `stage` (the ring slot's A buffer) is free once
 // the values are in registers and doubles as the output staging buffer; the
 // slot goes back to the producer only after the next pair's first barrier.
+//
+// AND (and ANDNOT with a small A) on very unequal sizes -- the smaller side
+// at most 1/16 of the larger, so at most 256 values -- skips the bitset: one
+// thread per small-side value binary-searches the larger array in shared
+// memory (array_intersect_galloping's case, kernels/scalar.py:149-176).
+// Otherwise AND builds X from the smaller side and probes the larger one (the
+// probed side's order is the output order).
 __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_t na, const uint16_t *B,
                                uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
                                uint16_t *stage, uint64_t *release) {
   const int t = threadIdx.x;
+  if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
+    const bool is_and = op == RS_OP_AND;
+    const bool a_small = is_and ? na <= nb : true;
+    const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
+    if (16 * ns <= nl) {
+      const uint16_t *S = a_small ? A : B, *L = a_small ? B : A;
+      uint32_t v = 0, keep = 0;
+      if ((uint32_t)t < ns) {
+        v = S[t];
+        keep = bsearch16(L, nl, v) == is_and;
+      }
+      uint32_t total;
+      const uint32_t base = cscan(keep, sm.red[parity], total);
+      if (t == 0 && release) mbar_arrive(release);
+      type = RS_TAG_ARRAY;
+      nout = total;
+      if (dst && total) {
+        if (keep) stage[base] = (uint16_t)v;
+        flush_stage(stage, total, dst);
+      }
+      return total;
+    }
+  }
 #pragma unroll
-  for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
+  for (int k = 0; k < 4; k++) sm.X[t + LT * k] = 0;
   uint32_t xa[8], xb[8];
   const uint32_t ca = load16(A, na, xa), cb = load16(B, nb, xb);
   cbar();
   // every consumer has finished the previous pair: its ring slot may refill
   if (t == 0 && release) mbar_arrive(release);
-  if (op == RS_OP_ANDNOT) set_bits16<false>(xb, cb, sm.X);
+  const bool build_b = op == RS_OP_ANDNOT || (op == RS_OP_AND && nb < na);
+  if (build_b) set_bits16<false>(xb, cb, sm.X);
   else set_bits16<false>(xa, ca, sm.X);
   cbar();
   const uint32_t *X32 = (const uint32_t *)sm.X;
   if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
-    const bool is_and = op == RS_OP_AND;
+    const bool probe_b = !build_b;
     uint32_t P[8];
 #pragma unroll
-    for (int k = 0; k < 8; k++) P[k] = is_and ? xb[k] : xa[k];
-    const uint32_t cp = is_and ? cb : ca;
-    const uint32_t want = is_and ? 1u : 0u;
+    for (int k = 0; k < 8; k++) P[k] = probe_b ? xb[k] : xa[k];
+    const uint32_t cp = probe_b ? cb : ca;
+    const uint32_t want = op == RS_OP_AND ? 1u : 0u;
     uint32_t keep = 0;
 #pragma unroll
     for (int k = 0; k < 16; k++) {
@@ -171,34 +235,47 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
   if (op == RS_OP_OR) set_bits16<false>(xb, cb, sm.X);
   else set_bits16<true>(xb, cb, sm.X);
   cbar();
+  // result words t + 256q (conflict-free), positions by a packed row scan
   uint64_t r[4];
-  uint32_t pc = 0;
+  uint32_t pq[4];
 #pragma unroll
-  for (int k = 0; k < 4; k++) {
-    r[k] = sm.X[4 * t + k];
-    pc += __popcll(r[k]);
+  for (int q = 0; q < 4; q++) {
+    r[q] = sm.X[t + LT * q];
+    pq[q] = __popcll(r[q]);
   }
-  uint32_t card;
-  uint32_t base = cscan(pc, sm.red[parity], card);
+  const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
+  uint32_t e0, e1, T0, T1;
+  cscan2(pk0, pk1, sm.red[parity], e0, e1, T0, T1);
+  const uint32_t r0 = T0 & 0xFFFFu, r1 = T0 >> 16, r2 = T1 & 0xFFFFu;
+  const uint32_t card = r0 + r1 + r2 + (T1 >> 16);
   if (!dst || card == 0) {
     type = RS_TAG_ARRAY;
     nout = card;
     return card;
   }
   if (card > RS_ARRAY_MAX) {
-    uint4 *p = (uint4 *)dst + 2 * t;
-    rsb::st_stream(p, make_uint4((uint32_t)r[0], (uint32_t)(r[0] >> 32), (uint32_t)r[1], (uint32_t)(r[1] >> 32)));
-    rsb::st_stream(p + 1, make_uint4((uint32_t)r[2], (uint32_t)(r[2] >> 32), (uint32_t)r[3], (uint32_t)(r[3] >> 32)));
+    uint64_t *p = (uint64_t *)dst + t;
+#pragma unroll
+    for (int q = 0; q < 4; q++) asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p + LT * q), "l"(r[q]) : "memory");
     type = RS_TAG_BITSET;
     nout = RS_WORDS;
     return card;
   }
+  const uint32_t end[4] = {(e0 & 0xFFFFu) + pq[0], r0 + (e0 >> 16) + pq[1], r0 + r1 + (e1 & 0xFFFFu) + pq[2],
+                           r0 + r1 + r2 + (e1 >> 16) + pq[3]};
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    uint64_t w = r[q];
-    while (w) {
-      stage[base++] = (uint16_t)((4 * t + q) * 64 + __ffsll((long long)w) - 1);
-      w &= w - 1;
+    const uint32_t pos = (uint32_t)(t + LT * q) * 64;
+    uint32_t b = end[q], hi = (uint32_t)(r[q] >> 32), lo = (uint32_t)r[q];
+    while (hi) {
+      const uint32_t p = 31 - __clz(hi);
+      stage[--b] = (uint16_t)(pos + 32 + p);
+      hi ^= 1u << p;
+    }
+    while (lo) {
+      const uint32_t p = 31 - __clz(lo);
+      stage[--b] = (uint16_t)(pos + p);
+      lo ^= 1u << p;
     }
   }
   flush_stage(stage, card, dst);
