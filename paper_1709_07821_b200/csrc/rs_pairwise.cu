@@ -213,25 +213,49 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
 
 // ----------------------------------------------------------------- copies
 
-// Unmatched container kept by OR/XOR/ANDNOT: Container.copy() into the result
-// pool (bitmap.py:191-209).  One warp per container, 128-bit moves.
+// Unmatched containers kept by OR / XOR / ANDNOT are deep-copied
+// (Container.copy, bitmap.py:191-209).  One warp per container, persistent
+// over the list; the next item's metadata chain (list -> entry -> container)
+// is loaded while the current payload streams, and each lane keeps four
+// 16-byte loads in flight.
 __global__ void k_copy(const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
                        Entries E, OutDesc O, uint8_t *__restrict__ opool, uint64_t *__restrict__ res_card) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t total = *cnt, nw = (gridDim.x * blockDim.x) >> 5;
+  struct Item {
+    uint32_t e, c;
+    bool from_a;
+  };
+  auto fetch = [&](uint32_t w) {
+    Item it;
+    it.e = list[w];
+    const uint32_t ca = E.ca[it.e];
+    it.from_a = ca != RS_NONE;
+    it.c = it.from_a ? ca : E.cb[it.e];
+    return it;
+  };
   uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  uint32_t total = *cnt;
-  uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  if (w >= total) return;
+  Item cur = fetch(w);
   for (; w < total; w += nw) {
-    uint32_t e = list[w];
-    uint32_t ca = E.ca[e];
-    const DevBatch &S = ca != RS_NONE ? A : B;
-    uint32_t c = ca != RS_NONE ? ca : E.cb[e];
-    uint8_t t = S.type[c];
-    uint32_t n = S.n[c], card = S.card[c];
-    uint32_t bytes = (uint32_t)rs_pad16(rs_payload_bytes(t, n));
-    const uint4 *src = (const uint4 *)(S.pool + S.off[c]);
-    uint4 *dst = (uint4 *)(opool + E.off[e]);
-    for (uint32_t i = lane; i < (bytes >> 4); i += 32) dst[i] = src[i];
+    const DevBatch &S = cur.from_a ? A : B;
+    const uint8_t t = S.type[cur.c];
+    const uint32_t n = S.n[cur.c], card = S.card[cur.c];
+    const uint4 *src = (const uint4 *)(S.pool + S.off[cur.c]);
+    uint4 *dst = (uint4 *)(opool + E.off[cur.e]);
+    const uint32_t e = cur.e;
+    if (w + nw < total) cur = fetch(w + nw);
+    const uint32_t nv = (uint32_t)(rs_pad16(rs_payload_bytes(t, n)) >> 4);
+    uint32_t i = lane;
+    for (; i + 96 < nv; i += 128) {
+      const uint4 x0 = __ldcs(src + i), x1 = __ldcs(src + i + 32), x2 = __ldcs(src + i + 64),
+                  x3 = __ldcs(src + i + 96);
+      __stcs(dst + i, x0);
+      __stcs(dst + i + 32, x1);
+      __stcs(dst + i + 64, x2);
+      __stcs(dst + i + 96, x3);
+    }
+    for (; i < nv; i += 32) __stcs(dst + i, __ldcs(src + i));
     if (lane == 0) {
       O.type[e] = t;
       O.card[e] = card;
