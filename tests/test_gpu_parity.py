@@ -210,6 +210,48 @@ def test_config5_subset_all_pairs(pkg):
     assert np.array_equal(uni.astype(np.int64), cards[pi] + cards[pj] - want)
 
 
+def _all_pairs_check(pkg, buf, offs):
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    nb = len(offs) - 1
+    inter, uni = Bt.all_pairs_cardinality()
+    pi, pj = np.triu_indices(nb, 1)
+    want = orc.all_pairs_and(buf, offs, pi, pj)
+    assert np.array_equal(inter.astype(np.int64), want)
+    cards = Bt.cardinalities().astype(np.int64)
+    assert np.array_equal(uni.astype(np.int64), cards[pi] + cards[pj] - want)
+
+
+def test_all_pairs_tensor_core_tiles(pkg, monkeypatch):
+    """The tcgen05 Gram tiles (k_allpairs_umma) on every key, including a key
+    with 300 containers (3 x 3 tile blocks, off-diagonal tiles), against the
+    oracle's pairwise intersections; and the CUDA-core tiles for the same
+    input."""
+    from paper_1709_07821_b200 import synth
+    rng = np.random.default_rng(77)
+    imgs = []
+    for i in range(300):  # one container at key 0 per bitmap: m = 300 for that key
+        kind = i % 3
+        if kind == 0:
+            v = rng.choice(65536, int(rng.integers(1, 4000)), replace=False)
+        elif kind == 1:
+            v = np.nonzero(rng.random(65536) < rng.uniform(0.1, 0.9))[0]
+        else:
+            s = int(rng.integers(0, 60000))
+            v = np.arange(s, s + int(rng.integers(1, 5000)))
+        extra = rng.choice(np.arange(1, 8), 2, replace=False) * 65536 + rng.integers(0, 65536, 2)
+        w = orc.from_values(np.concatenate([v, extra]).astype(np.uint64))
+        imgs.append(orc.run_optimize(w)[0] if i % 5 == 0 else w)
+    offs = np.zeros(len(imgs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(x) for x in imgs])
+    buf = np.frombuffer(b"".join(imgs), dtype=np.uint8)
+    monkeypatch.setenv("RS_ALLPAIRS_UMMA_MIN", "2")
+    _all_pairs_check(pkg, buf, offs)
+    b5, o5 = synth.config5(nbitmaps=160)
+    _all_pairs_check(pkg, b5, o5)
+    monkeypatch.setenv("RS_ALLPAIRS_UMMA", "0")
+    _all_pairs_check(pkg, buf, offs)
+
+
 def test_run_optimize_matches_oracle(pkg):
     from paper_1709_07821_b200 import synth
     buf, offs = synth.config5(nbitmaps=6, seed=9)

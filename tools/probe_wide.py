@@ -9,7 +9,7 @@ B4 = rb.BitmapBatch.from_wire((buf, offs))
 buf, offs = synth.config5()
 B5 = rb.BitmapBatch.from_wire((buf, offs))
 for name, f, parts in (("union_many C4", lambda: B4.union_many(), ["union_fold"]),
-                       ("all_pairs C5", lambda: B5.all_pairs_cardinality(), ["densify", "allpairs"])):
+                       ("all_pairs C5", lambda: B5.all_pairs_cardinality(), ["densify", "allpairs", "allpairs_umma"])):
     f(); _lib.synchronize()
     for rep in range(2):
         _lib.profile_reset(); _lib.profile(True)
