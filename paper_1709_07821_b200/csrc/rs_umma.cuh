@@ -6,33 +6,39 @@
 // Grouped by chunk key, the containers of one key form m bit-rows of 65,536
 // bits (densified to 8 KB), and all their pairwise intersection counts are the
 // Gram matrix G = X X^T over {0,1}: a GEMM.  On CUDA cores this is bound by
-// the POPC issue rate (16/clk/SM); the tensor cores multiply 0/1 bytes at
-// 64 clk per 128x128x32 tile-step.  Each CTA owns one 128 x 128 output tile
-// (row block ti, column block tj >= ti) of one key:
-//   * warps 0-7 (producers) stream 256-bit K chunks of the 128 (+128) rows
-//     from HBM (4 chunks prefetched in registers), expand bits to bytes
-//     {0,1} in shared memory in the canonical K-major SWIZZLE_128B layout, and
-//     arrive on the stage's `full` mbarrier;
-//   * warp 8 lane 0 issues 8 x tcgen05.mma (M=N=128, K=32) per chunk into a
-//     128-column s32 accumulator in TMEM and frees the stage with
-//     tcgen05.commit -> `empty`;
-//   * after the last chunk, warps 0-3 read the accumulator rows back with
-//     tcgen05.ld (warp w owns TMEM lanes 32w..32w+31) and add every
-//     upper-triangle count into the N x N matrix.
+// the POPC issue rate (16/clk/SM); the tensor cores multiply 0/1 bytes.  Each
+// CTA owns one tile: A = 128 rows starting at r0, B = NB <= 256 rows starting
+// at c0, both of one key.  When r0 == c0 the A rows are the first 128 rows of
+// the B operand -- one expansion feeds both descriptors -- so a key with
+// m <= 256 containers is one tile (pairs u < v with u < 128) plus, past 128,
+// a small corner left to the CUDA-core tiles.
+//   * warps 0-7 (producers) stream 256-bit K chunks of the rows from HBM (4
+//     chunks prefetched in registers), expand bits to bytes {0,1} in shared
+//     memory in the canonical K-major SWIZZLE_128B layout, and arrive on the
+//     stage's `full` mbarrier;
+//   * warp 8 lane 0 issues 8 x tcgen05.mma (M=128, N=NB, K=32) per chunk into
+//     an s32 accumulator in TMEM and frees the stage with tcgen05.commit ->
+//     `empty`;
+//   * after the last chunk every warp reads a quarter of the accumulator rows
+//     (TMEM lanes 32(w%4)..) and half of the columns back with tcgen05.ld and
+//     adds the upper-triangle counts into the N x N matrix.
 // Counts are exact: at most 65,536 per pair, accumulated in s32.
 #pragma once
 #include "rs_internal.cuh"
 
 namespace rsu {
 
-constexpr int UM = 128;                 // tile rows = tile columns
+constexpr int UM = 128;                 // tile rows (A operand, TMEM lanes)
+constexpr int UNMAX = 256;              // tile columns (B operand rows), at most
 constexpr int UKC = 256;                // K bits per smem chunk
-constexpr int UCH = UM * UKC;           // expanded bytes per operand per chunk (32 KB)
-constexpr int UNS = 3;                  // smem stages
+constexpr int UBCH = UNMAX * UKC;       // expanded B bytes per chunk (64 KB)
+constexpr int UACH = UM * UKC;          // expanded separate-A bytes per chunk (32 KB)
+constexpr int USTAGE = UBCH + UACH;
+constexpr int UNS = 2;                  // smem stages
 constexpr int UPF = 4;                  // raw chunks prefetched in registers
 constexpr int UPROD = 256;              // producer threads
 constexpr int UTHREADS = UPROD + 32;    // + the MMA-issuer warp
-constexpr size_t USMEM = (size_t)UNS * 2 * UCH + 256;
+constexpr size_t USMEM = (size_t)UNS * USTAGE + 256;
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -52,10 +58,11 @@ __host__ __device__ constexpr uint32_t idesc_u8(int m, int n) {
   return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-// Byte offset of (row, k) in one operand chunk: [k/128 atom][row/8][row%8][128 B],
-// the 16-byte units of each 128-byte row XOR-swizzled by row%8.
-__device__ __forceinline__ uint32_t sw_off(int row, int k) {
-  return (k >> 7) * (UM * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((((k & 127) >> 4) ^ (row & 7)) << 4);
+// Byte offset of (row, k) in one operand chunk of `rows` rows:
+// [k/128 atom][row/8][row%8][128 B], the 16-byte units of each 128-byte row
+// XOR-swizzled by row%8.
+__device__ __forceinline__ uint32_t sw_off(int row, int k, int rows) {
+  return (k >> 7) * (rows * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((((k & 127) >> 4) ^ (row & 7)) << 4);
 }
 
 // 4 bits -> 4 bytes {0,1} (the four shifted copies never overlap)
@@ -79,14 +86,15 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                : "memory");
 }
 
-// Expand this thread's half of one row's 256-bit chunk (two words) into `dst`.
-__device__ __forceinline__ void expand_half(uint8_t *dst, int row, int k0, const uint64_t x[2]) {
+// Expand NW consecutive words (bits k0 ..) of one row into `dst`.
+template <int NW>
+__device__ __forceinline__ void expand_words(uint8_t *dst, int row, int rows, int k0, const uint64_t *x) {
 #pragma unroll
-  for (int w = 0; w < 2; w++) {
+  for (int w = 0; w < NW; w++) {
 #pragma unroll
     for (int h = 0; h < 4; h++) {
       const uint32_t s = (uint32_t)(x[w] >> (16 * h));
-      *(uint4 *)(dst + sw_off(row, k0 + w * 64 + h * 16)) =
+      *(uint4 *)(dst + sw_off(row, k0 + w * 64 + h * 16, rows)) =
           make_uint4(spread4(s), spread4(s >> 4), spread4(s >> 8), spread4(s >> 12));
     }
   }

@@ -192,23 +192,25 @@ __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__re
   st_words((uint8_t *)dst, 0, t, w);
 }
 
-// One CTA per (key segment, 128-row block ti, 128-column block tj >= ti) on
-// the tensor cores; see rs_umma.cuh.  Counts go into the same N x N matrix
-// as the CUDA-core tiles (segments too small to fill a 128-row tile use those).
+// One CTA per tensor-core tile (see rs_umma.cuh): A = rows [r0, r0+128),
+// B = rows [c0, c0+nb) of one key segment; counts of pairs u < v go into the
+// same N x N matrix as the CUDA-core tiles.
 __global__ void __launch_bounds__(rsu::UTHREADS, 1)
-    k_allpairs_umma(const uint32_t *__restrict__ tp_seg, const uint16_t *__restrict__ tp_i,
-                    const uint16_t *__restrict__ tp_j, const uint32_t *__restrict__ seg_start,
-                    const uint64_t *__restrict__ D, const uint32_t *__restrict__ item_bm, uint64_t N,
-                    unsigned long long *__restrict__ Mx) {
+    k_allpairs_umma(const uint32_t *__restrict__ tp_seg, const uint16_t *__restrict__ tp_r0,
+                    const uint16_t *__restrict__ tp_c0, const uint16_t *__restrict__ tp_nb,
+                    const uint32_t *__restrict__ seg_start, const uint64_t *__restrict__ D,
+                    const uint32_t *__restrict__ item_bm, uint64_t N, unsigned long long *__restrict__ Mx) {
   using namespace rsu;
   extern __shared__ __align__(1024) uint8_t usm[];
-  uint64_t *full = (uint64_t *)(usm + UNS * 2 * UCH), *empty = full + UNS, *done = empty + UNS;
+  uint64_t *full = (uint64_t *)(usm + UNS * USTAGE), *empty = full + UNS, *done = empty + UNS;
   uint32_t *tslot = (uint32_t *)(done + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const uint32_t seg = tp_seg[blockIdx.x];
   const uint32_t s0 = seg_start[seg], m = seg_start[seg + 1] - s0;
-  const uint32_t ti = tp_i[blockIdx.x], tj = tp_j[blockIdx.x];
-  const bool diag = ti == tj;
+  const uint32_t r0 = tp_r0[blockIdx.x], c0 = tp_c0[blockIdx.x], nb = tp_nb[blockIdx.x];
+  const bool shared_a = r0 == c0;  // A = the first 128 rows of the B operand
+  // rows never written below (past m, past nb) must read as zero
+  for (uint32_t i = t; i < UNS * USTAGE / 16; i += UTHREADS) ((uint4 *)usm)[i] = make_uint4(0, 0, 0, 0);
   if (t == 0) {
     for (int i = 0; i < UNS; i++) {
       ubar_init(&full[i], UPROD / 32);
@@ -218,10 +220,12 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(UM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "r"(UNMAX)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -229,16 +233,17 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   constexpr int NCH = RS_WORDS * 64 / UKC;
   if (warp == UPROD / 32) {  // ------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = idesc_u8(UM, UM);
+      const uint32_t idesc = idesc_u8(UM, (int)nb);
       for (int c = 0; c < NCH; c++) {
         const int b = c % UNS;
         ubar_wait(&full[b], (c / UNS) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t ba = su32(usm + b * 2 * UCH), bb = diag ? ba : ba + UCH;
+        const uint32_t bb = su32(usm + b * USTAGE), ba = shared_a ? bb : bb + UBCH;
+        const uint32_t astride = shared_a ? UNMAX * 128 : UM * 128;
 #pragma unroll
         for (int k = 0; k < UKC / 32; k++) {
-          const uint32_t ko = (k >> 2) * (UM * 128) + (k & 3) * 32;
-          const uint64_t da = sw128_desc(ba + ko), db = sw128_desc(bb + ko);
+          const uint64_t da = sw128_desc(ba + (k >> 2) * astride + (k & 3) * 32);
+          const uint64_t db = sw128_desc(bb + (k >> 2) * (UNMAX * 128) + (k & 3) * 32);
           const uint32_t acc = (c | k) ? 1u : 0u;
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -251,32 +256,32 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
       umma_commit(done);
     }
   } else {  // ------------------------------------------- producers
-    const int row = t & (UM - 1), half = t >> 7, k0 = half * (UKC / 2);
-    const uint32_t ra = ti * UM + row, rb = tj * UM + row;
-    const uint64_t *pa = ra < m ? D + (uint64_t)(s0 + ra) * RS_WORDS + half * 2 : nullptr;
-    const uint64_t *pb = !diag && rb < m ? D + (uint64_t)(s0 + rb) * RS_WORDS + half * 2 : nullptr;
-    uint64_t xa[UPF][2], xb[UPF][2];
+    // B: thread t expands row c0 + t (all 4 words of a chunk); a separate A:
+    // thread t expands half of row r0 + (t & 127)
+    const int arow = t & (UM - 1), ahalf = t >> 7;
+    const uint64_t *pb = (uint32_t)t < nb && c0 + t < m ? D + (uint64_t)(s0 + c0 + t) * RS_WORDS : nullptr;
+    const uint64_t *pa = !shared_a && r0 + arow < m ? D + (uint64_t)(s0 + r0 + arow) * RS_WORDS + ahalf * 2 : nullptr;
+    uint64_t xb[UPF][4], xa[UPF][2];
 #pragma unroll
-    for (int q = 0; q < UPF; q++)
+    for (int q = 0; q < UPF; q++) {
 #pragma unroll
-      for (int w = 0; w < 2; w++) {
-        xa[q][w] = pa ? pa[q * (UKC / 64) + w] : 0;
-        xb[q][w] = pb ? pb[q * (UKC / 64) + w] : 0;
-      }
-    for (int c0 = 0; c0 < NCH; c0 += UPF) {
+      for (int w = 0; w < 4; w++) xb[q][w] = pb ? pb[q * (UKC / 64) + w] : 0;
+#pragma unroll
+      for (int w = 0; w < 2; w++) xa[q][w] = pa ? pa[q * (UKC / 64) + w] : 0;
+    }
+    for (int cc = 0; cc < NCH; cc += UPF) {
 #pragma unroll
       for (int q = 0; q < UPF; q++) {
-        const int c = c0 + q, b = c % UNS;
+        const int c = cc + q, b = c % UNS;
         if (c >= UNS) ubar_wait(&empty[b], ((c - UNS) / UNS) & 1);
-        uint8_t *sa = usm + b * 2 * UCH;
-        expand_half(sa, row, k0, xa[q]);
-        if (!diag) expand_half(sa + UCH, row, k0, xb[q]);
+        uint8_t *sb = usm + b * USTAGE;
+        if (pb) expand_words<4>(sb, t, UNMAX, 0, xb[q]);
+        if (pa) expand_words<2>(sb + UBCH, arow, UM, ahalf * (UKC / 2), xa[q]);
         const bool more = c + UPF < NCH;
 #pragma unroll
-        for (int w = 0; w < 2; w++) {
-          xa[q][w] = pa && more ? pa[(c + UPF) * (UKC / 64) + w] : 0;
-          xb[q][w] = pb && more ? pb[(c + UPF) * (UKC / 64) + w] : 0;
-        }
+        for (int w = 0; w < 4; w++) xb[q][w] = pb && more ? pb[(c + UPF) * (UKC / 64) + w] : 0;
+#pragma unroll
+        for (int w = 0; w < 2; w++) xa[q][w] = pa && more ? pa[(c + UPF) * (UKC / 64) + w] : 0;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) ubar_arrive(&full[b]);
@@ -285,29 +290,33 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   }
   ubar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp < 4) {  // -------------------------------------------- epilogue
-    const uint32_t u = ti * UM + 32 * warp + lane;
-    const uint32_t bu = u < m ? item_bm[s0 + u] : 0;
-    for (int c0 = 0; c0 < UM; c0 += 32) {
-      uint32_t v[32];
-      const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-          : "r"(ta));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (u < m) {
+  {  // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3, colh = warp >> 2;  // warps 0-7; the issuer warp idles
+    if (warp < 8) {
+      const uint32_t u = r0 + 32 * quarter + lane;
+      const uint32_t bu = u < m ? item_bm[s0 + u] : 0;
+      for (uint32_t cb = 128 * colh; cb < 128 * colh + 128 && cb < nb; cb += 32) {
+        uint32_t v[32];
+        const uint32_t ta = tmem + ((uint32_t)(32 * quarter) << 16) + cb;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (u < m) {
 #pragma unroll
-        for (int j = 0; j < 32; j++) {
-          const uint32_t vc = tj * UM + c0 + j;
-          if (v[j] && vc < m && (!diag || u < vc)) {
-            const uint32_t bv = item_bm[s0 + vc];
-            const uint32_t lo = min(bu, bv), hi = max(bu, bv);
-            atomicAdd(&Mx[(uint64_t)lo * N + hi], (unsigned long long)v[j]);
+          for (int j = 0; j < 32; j++) {
+            const uint32_t vc = c0 + cb + j;
+            if (v[j] && vc < m && u < vc) {
+              const uint32_t bv = item_bm[s0 + vc];
+              const uint32_t lo = min(bu, bv), hi = max(bu, bv);
+              atomicAdd(&Mx[(uint64_t)lo * N + hi], (unsigned long long)v[j]);
+            }
           }
         }
       }
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(UM) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(UNMAX) : "memory");
 }
 
 constexpr int AP_TILE = 16;   // containers per tile side
@@ -586,30 +595,42 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   std::vector<uint32_t> hseg(g.G + 1);
   RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
   std::vector<uint32_t> tseg, useg;
-  std::vector<uint16_t> ti, tj, uti, utj;
+  std::vector<uint16_t> ti, tj, ur0, uc0, unb;
+  const uint32_t tile = tiles2 ? AP2_TILE : AP_TILE;
+  auto popc_tiles = [&](uint64_t s, uint32_t first, uint32_t m) {  // tiles over rows [first*tile, m)
+    const uint32_t nt = (m + tile - 1) / tile;
+    for (uint32_t a = first; a < nt; a++)
+      for (uint32_t b2 = a; b2 < nt; b2++) { tseg.push_back((uint32_t)s); ti.push_back(a); tj.push_back(b2); }
+  };
+  auto umma_tile = [&](uint64_t s, uint32_t r0, uint32_t c0, uint32_t nb) {
+    useg.push_back((uint32_t)s); ur0.push_back(r0); uc0.push_back(c0); unb.push_back((nb + 15) & ~15u);
+  };
   for (uint64_t s = 0; s < g.G; s++) {
-    uint32_t m = hseg[s + 1] - hseg[s];
+    const uint32_t m = hseg[s + 1] - hseg[s];
     if (m < 2) continue;
-    if (use_umma && m >= umma_min) {
+    if (!use_umma || m < umma_min) {
+      popc_tiles(s, 0, m);
+    } else if (m <= (uint32_t)rsu::UNMAX) {
+      // one tile: rows 0..127 against all m rows; the corner past row 128 on CUDA cores
+      umma_tile(s, 0, 0, m);
+      if (m > (uint32_t)rsu::UM) popc_tiles(s, rsu::UM / tile, m);
+    } else {
       const uint32_t nt = (m + rsu::UM - 1) / rsu::UM;
       for (uint32_t a = 0; a < nt; a++)
-        for (uint32_t b2 = a; b2 < nt; b2++) { useg.push_back((uint32_t)s); uti.push_back(a); utj.push_back(b2); }
-      continue;
+        for (uint32_t b2 = a; b2 < nt; b2++)
+          umma_tile(s, a * rsu::UM, b2 * rsu::UM, std::min<uint32_t>(rsu::UM, m - b2 * rsu::UM));
     }
-    const uint32_t tile = tiles2 ? AP2_TILE : AP_TILE;
-    uint32_t nt = (m + tile - 1) / tile;
-    for (uint32_t a = 0; a < nt; a++)
-      for (uint32_t b2 = a; b2 < nt; b2++) { tseg.push_back((uint32_t)s); ti.push_back(a); tj.push_back(b2); }
   }
   uint64_t ntp = tseg.size(), nup = useg.size();
   uint64_t *D = (uint64_t *)dalloc((g.T ? g.T : 1) * 8192);
   uint32_t *item_bm = (uint32_t *)dalloc((g.T + 1) * 4), *d_tseg = (uint32_t *)dalloc((ntp + 1) * 4);
   uint16_t *d_ti = (uint16_t *)dalloc((ntp + 1) * 2), *d_tj = (uint16_t *)dalloc((ntp + 1) * 2);
   uint32_t *d_useg = (uint32_t *)dalloc((nup + 1) * 4);
-  uint16_t *d_uti = (uint16_t *)dalloc((nup + 1) * 2), *d_utj = (uint16_t *)dalloc((nup + 1) * 2);
+  uint16_t *d_ur0 = (uint16_t *)dalloc((nup + 1) * 2), *d_uc0 = (uint16_t *)dalloc((nup + 1) * 2),
+           *d_unb = (uint16_t *)dalloc((nup + 1) * 2);
   unsigned long long *Mx = (unsigned long long *)dalloc(N * N * 8);
   uint64_t *d_inter = (uint64_t *)dalloc(npairs * 8), *d_uni = (uint64_t *)dalloc(npairs * 8);
-  if (!D || !item_bm || !d_tseg || !d_ti || !d_tj || !d_useg || !d_uti || !d_utj || !Mx || !d_inter || !d_uni) {
+  if (!D || !item_bm || !d_tseg || !d_ti || !d_tj || !d_useg || !d_ur0 || !d_uc0 || !d_unb || !Mx || !d_inter || !d_uni) {
     set_error("device allocation failed (all pairs)");
     return RS_ENOMEM;
   }
@@ -617,8 +638,9 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_TRY(h2d(d_ti, ti.data(), ntp * 2));
   RS_TRY(h2d(d_tj, tj.data(), ntp * 2));
   RS_TRY(h2d(d_useg, useg.data(), nup * 4));
-  RS_TRY(h2d(d_uti, uti.data(), nup * 2));
-  RS_TRY(h2d(d_utj, utj.data(), nup * 2));
+  RS_TRY(h2d(d_ur0, ur0.data(), nup * 2));
+  RS_TRY(h2d(d_uc0, uc0.data(), nup * 2));
+  RS_TRY(h2d(d_unb, unb.data(), nup * 2));
   RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
   RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
   RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
@@ -628,8 +650,8 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
       RS_CK(cudaFuncSetAttribute(k_allpairs_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsu::USMEM));
       attr = true;
     }
-    RS_LAUNCH_PROF("allpairs_umma", nup, k_allpairs_umma, (unsigned)nup, rsu::UTHREADS, rsu::USMEM, d_useg, d_uti,
-                   d_utj, g.seg_start, D, item_bm, N, Mx);
+    RS_LAUNCH_PROF("allpairs_umma", nup, k_allpairs_umma, (unsigned)nup, rsu::UTHREADS, rsu::USMEM, d_useg, d_ur0,
+                   d_uc0, d_unb, g.seg_start, D, item_bm, N, Mx);
   }
   if (!ntp) {
   } else if (tiles2)
@@ -645,7 +667,7 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_TRY(d2h(inter, d_inter, npairs * 8));
   if (uni) RS_TRY(d2h(uni, d_uni, npairs * 8));
   dfree(D); dfree(item_bm); dfree(d_tseg); dfree(d_ti); dfree(d_tj); dfree(Mx); dfree(d_inter); dfree(d_uni);
-  dfree(d_useg); dfree(d_uti); dfree(d_utj);
+  dfree(d_useg); dfree(d_ur0); dfree(d_uc0); dfree(d_unb);
   g.release();
   return RS_OK;
 }

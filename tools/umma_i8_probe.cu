@@ -69,6 +69,19 @@ __device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t phase) {
       "@!p bra S_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
 
+__device__ __forceinline__ void mbar_sleep(uint64_t *bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+    if (ok) break;
+    __nanosleep(64);
+  }
+}
+
 // expand 4 bits n -> 4 bytes {0,1}
 __device__ __forceinline__ uint32_t spread4(uint32_t n) { return ((n & 0xF) * 0x00204081u) & 0x01010101u; }
 
@@ -107,7 +120,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
         const int b = c % NS;
         if (mode & 16) mbar_spin(&full[b], (c / NS) & 1);
         else if (!(mode & 32)) mbar_wait(&full[b], (c / NS) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (!(mode & 64)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = smem_u32(sm + b * CHUNK_BYTES);
 #pragma unroll
         for (int s = 0; s < ((mode & 2) ? 1 : KC / 32); s++) {
@@ -146,6 +159,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
         uint8_t *bufb = sm + b * CHUNK_BYTES;
         if (c >= NS) {
           if (mode & 32) {}
+          else if (mode & 128) mbar_sleep(&empty[b], ((c - NS) / NS) & 1);
           else if (mode & 16) mbar_spin(&empty[b], ((c - NS) / NS) & 1);
           else if (mode & 4) { if (lane == 0) mbar_wait(&empty[b], ((c - NS) / NS) & 1); __syncwarp(); }
           else mbar_wait(&empty[b], ((c - NS) / NS) & 1);
@@ -170,7 +184,8 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
       }
     }
   }
-  mbar_wait(done, 0);
+  if (mode & 128) mbar_sleep(done, 0);
+  else mbar_wait(done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp < 4)
     for (int c0 = 0; c0 < M; c0 += 32) {
@@ -228,7 +243,7 @@ int main(int argc, char **argv) {
   printf("correctness: %s (%d mismatches of %d)\n", bad ? "FAIL" : "ok", bad, M * M);
   // timing: 148 CTAs x full 65536-bit rows
   if (kwords >= 64) {
-    const int modes[] = {0, 3 | 32, 1 | 32};
+    const int modes[] = {0, 128, 3, 3 | 128, 1, 1 | 128, 3 | 32 | 128, 1 | 32 | 128};
     for (int mode : modes) {
       cudaEvent_t a, b;
       cudaEventCreate(&a); cudaEventCreate(&b);
