@@ -31,14 +31,13 @@ namespace rsu {
 constexpr int UM = 128;                 // tile rows (A operand, TMEM lanes)
 constexpr int UNMAX = 256;              // tile columns (B operand rows), at most
 constexpr int UKC = 256;                // K bits per smem chunk
-constexpr int UBCH = UNMAX * UKC;       // expanded B bytes per chunk (64 KB)
 constexpr int UACH = UM * UKC;          // expanded separate-A bytes per chunk (32 KB)
-constexpr int USTAGE = UBCH + UACH;
-constexpr int UNS = 2;                  // smem stages
+constexpr int URING = 192 * 1024;       // stage ring: as many stages as fit (<= UMAXST)
+constexpr int UMAXST = 6;
 constexpr int UPF = 4;                  // raw chunks prefetched in registers
 constexpr int UPROD = 256;              // producer threads
 constexpr int UTHREADS = UPROD + 32;    // + the MMA-issuer warp
-constexpr size_t USMEM = (size_t)UNS * USTAGE + 256;
+constexpr size_t USMEM = (size_t)URING + 256;
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 

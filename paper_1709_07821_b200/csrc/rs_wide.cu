@@ -199,20 +199,26 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
     k_allpairs_umma(const uint32_t *__restrict__ tp_seg, const uint16_t *__restrict__ tp_r0,
                     const uint16_t *__restrict__ tp_c0, const uint16_t *__restrict__ tp_nb,
                     const uint32_t *__restrict__ seg_start, const uint64_t *__restrict__ D,
-                    const uint32_t *__restrict__ item_bm, uint64_t N, unsigned long long *__restrict__ Mx) {
+                    const uint32_t *__restrict__ item_bm, uint64_t N, unsigned long long *__restrict__ Mx,
+                    int maxst) {
   using namespace rsu;
   extern __shared__ __align__(1024) uint8_t usm[];
-  uint64_t *full = (uint64_t *)(usm + UNS * USTAGE), *empty = full + UNS, *done = empty + UNS;
+  uint64_t *full = (uint64_t *)(usm + URING), *empty = full + UMAXST, *done = empty + UMAXST;
   uint32_t *tslot = (uint32_t *)(done + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const uint32_t seg = tp_seg[blockIdx.x];
   const uint32_t s0 = seg_start[seg], m = seg_start[seg + 1] - s0;
   const uint32_t r0 = tp_r0[blockIdx.x], c0 = tp_c0[blockIdx.x], nb = tp_nb[blockIdx.x];
   const bool shared_a = r0 == c0;  // A = the first 128 rows of the B operand
+  // stage layout: B operand (rows_b rows, >= the 128 rows A reads when shared),
+  // then a separate A operand; as many stages as fit in the ring
+  const uint32_t rows_b = max(nb, (uint32_t)UM);
+  const uint32_t bbytes = rows_b * (UKC / 8) * 8, sbytes = bbytes + (shared_a ? 0 : UACH);
+  const int nst = min(maxst, (int)(URING / sbytes));
   // rows never written below (past m, past nb) must read as zero
-  for (uint32_t i = t; i < UNS * USTAGE / 16; i += UTHREADS) ((uint4 *)usm)[i] = make_uint4(0, 0, 0, 0);
+  for (uint32_t i = t; i < URING / 16; i += UTHREADS) ((uint4 *)usm)[i] = make_uint4(0, 0, 0, 0);
   if (t == 0) {
-    for (int i = 0; i < UNS; i++) {
+    for (int i = 0; i < nst; i++) {
       ubar_init(&full[i], UPROD / 32);
       ubar_init(&empty[i], 1);
     }
@@ -232,18 +238,20 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   const uint32_t tmem = *tslot;
   constexpr int NCH = RS_WORDS * 64 / UKC;
   if (warp == UPROD / 32) {  // ------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = idesc_u8(UM, (int)nb);
-      for (int c = 0; c < NCH; c++) {
-        const int b = c % UNS;
-        ubar_wait(&full[b], (c / UNS) & 1);
+    // the whole warp walks the stages (no lane diverges into a spin-wait
+    // while lane 0 issues); lane 0 issues the MMAs and the commits
+    const uint32_t idesc = idesc_u8(UM, (int)nb);
+    for (int c = 0; c < NCH; c++) {
+      const int b = c % nst;
+      ubar_wait(&full[b], (c / nst) & 1);
+      if (lane == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t bb = su32(usm + b * USTAGE), ba = shared_a ? bb : bb + UBCH;
-        const uint32_t astride = shared_a ? UNMAX * 128 : UM * 128;
+        const uint32_t bb = su32(usm + b * sbytes), ba = shared_a ? bb : bb + bbytes;
+        const uint32_t astride = shared_a ? rows_b * 128 : UM * 128;
 #pragma unroll
         for (int k = 0; k < UKC / 32; k++) {
           const uint64_t da = sw128_desc(ba + (k >> 2) * astride + (k & 3) * 32);
-          const uint64_t db = sw128_desc(bb + (k >> 2) * (UNMAX * 128) + (k & 3) * 32);
+          const uint64_t db = sw128_desc(bb + (k >> 2) * (rows_b * 128) + (k & 3) * 32);
           const uint32_t acc = (c | k) ? 1u : 0u;
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -252,8 +260,9 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
               : "memory");
         }
         umma_commit(&empty[b]);
+        if (c == NCH - 1) umma_commit(done);
       }
-      umma_commit(done);
+      __syncwarp();
     }
   } else {  // ------------------------------------------- producers
     // B: thread t expands row c0 + t (all 4 words of a chunk); a separate A:
@@ -272,11 +281,11 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
     for (int cc = 0; cc < NCH; cc += UPF) {
 #pragma unroll
       for (int q = 0; q < UPF; q++) {
-        const int c = cc + q, b = c % UNS;
-        if (c >= UNS) ubar_wait(&empty[b], ((c - UNS) / UNS) & 1);
-        uint8_t *sb = usm + b * USTAGE;
-        if (pb) expand_words<4>(sb, t, UNMAX, 0, xb[q]);
-        if (pa) expand_words<2>(sb + UBCH, arow, UM, ahalf * (UKC / 2), xa[q]);
+        const int c = cc + q, b = c % nst;
+        if (c >= nst) ubar_wait(&empty[b], ((c - nst) / nst) & 1);
+        uint8_t *sb = usm + b * sbytes;
+        if (pb) expand_words<4>(sb, t, rows_b, 0, xb[q]);
+        if (pa) expand_words<2>(sb + bbytes, arow, UM, ahalf * (UKC / 2), xa[q]);
         const bool more = c + UPF < NCH;
 #pragma unroll
         for (int w = 0; w < 4; w++) xb[q][w] = pb && more ? pb[(c + UPF) * (UKC / 64) + w] : 0;
@@ -592,6 +601,8 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   const bool use_umma = !(uv && *uv == '0');
   const char *mv = getenv("RS_ALLPAIRS_UMMA_MIN");
   const uint32_t umma_min = mv && *mv ? (uint32_t)atoi(mv) : 48;
+  const char *sv = getenv("RS_UMMA_STAGES");
+  const int umma_stages = sv && *sv ? std::max(2, std::min(rsu::UMAXST, atoi(sv))) : 2;
   std::vector<uint32_t> hseg(g.G + 1);
   RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
   std::vector<uint32_t> tseg, useg;
@@ -651,7 +662,7 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
       attr = true;
     }
     RS_LAUNCH_PROF("allpairs_umma", nup, k_allpairs_umma, (unsigned)nup, rsu::UTHREADS, rsu::USMEM, d_useg, d_ur0,
-                   d_uc0, d_unb, g.seg_start, D, item_bm, N, Mx);
+                   d_uc0, d_unb, g.seg_start, D, item_bm, N, Mx, umma_stages);
   }
   if (!ntp) {
   } else if (tiles2)
