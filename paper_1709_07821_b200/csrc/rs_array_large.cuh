@@ -36,7 +36,7 @@ struct LargeMeta {
 struct LargeSmem {
   uint16_t a[LSTAGES][RS_ARRAY_MAX];
   uint16_t b[LSTAGES][RS_ARRAY_MAX];
-  uint64_t X[RS_WORDS];
+  uint64_t X[2][RS_WORDS];  // by pair parity: each pair clears its words after its last read
   uint64_t full[LSTAGES];
   uint64_t empty[LSTAGES];
   LargeMeta meta[LSTAGES];
@@ -47,6 +47,20 @@ __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(LT
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rsb::smem_u32(bar)) : "memory");
+}
+
+// The producer lane waits for a free slot suspended in the barrier (time hint
+// 1 ms; the hardware resumes it when the phase completes), so its wait does
+// not take issue slots from the consumer warps -- a polling loop with
+// __nanosleep measured 200 M spin iterations (a quarter of all instructions).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "WB_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WB_%=;\n}\n" ::"r"(rsb::smem_u32(bar)),
+      "r"(phase), "r"(1000000)
+      : "memory");
 }
 
 // consumer-only exclusive scan with total (one named barrier); the scratch is
@@ -103,17 +117,28 @@ __device__ __forceinline__ void flush_word(uint32_t *X32, uint32_t w, uint32_t m
   else atomicOr(&X32[w], m);
 }
 
-// Thread t owns values [16t, 16t+16) of an array (n <= 4096 = 256 x 16): two
-// 128-bit shared loads put them in registers as 8 packed words, so the probes
-// below are independent loads (ILP) instead of a dependent smem walk.
+// Thread t owns the contiguous values [c*t, c*t + c) of an array, c =
+// ceil(n / 256) <= 16, so every consumer gets an equal share whatever the
+// array's size (the busiest thread sets each pair's critical path).  The
+// values land in registers as 8 packed words: two 128-bit shared loads for a
+// full 16-value share, single loads otherwise.
 __device__ __forceinline__ uint32_t load16(const uint16_t *v, uint32_t n, uint32_t w[8]) {
-  const uint32_t base = 16 * threadIdx.x;
+  const uint32_t c = (n + LT - 1) / LT, base = c * threadIdx.x;
   if (base >= n) return 0;
-  const uint4 *p = (const uint4 *)(v + base);
-  const uint4 q0 = p[0], q1 = p[1];
-  w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-  w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-  return min(16u, n - base);
+  const uint32_t cnt = min(c, n - base);
+  if (c == 16) {
+    const uint4 *p = (const uint4 *)(v + base);
+    const uint4 q0 = p[0], q1 = p[1];
+    w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+    w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+    return cnt;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const uint32_t lo = 2 * k < (int)cnt ? v[base + 2 * k] : 0, hi = 2 * k + 1 < (int)cnt ? v[base + 2 * k + 1] : 0;
+    w[k] = lo | (hi << 16);
+  }
+  return cnt;
 }
 
 __device__ __forceinline__ uint32_t val16(const uint32_t w[8], int k) { return (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF; }
@@ -195,19 +220,20 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
       return total;
     }
   }
-#pragma unroll
-  for (int k = 0; k < 4; k++) sm.X[t + LT * k] = 0;
+  // X (this pair's parity) is all zero on entry: zeroed at kernel start, and
+  // every pair clears the words it owns after its last read of them; the
+  // other parity's buffer separates that clear from the next pair's scatter.
+  uint64_t *X = sm.X[parity];
+  uint32_t *X32 = (uint32_t *)X;
   uint32_t xa[8], xb[8];
   const uint32_t ca = load16(A, na, xa), cb = load16(B, nb, xb);
-  cbar();
-  // every consumer has finished the previous pair: its ring slot may refill
-  if (t == 0 && release) mbar_arrive(release);
-  const bool build_b = op == RS_OP_ANDNOT || (op == RS_OP_AND && nb < na);
-  if (build_b) set_bits16<false>(xb, cb, sm.X);
-  else set_bits16<false>(xa, ca, sm.X);
-  cbar();
-  const uint32_t *X32 = (const uint32_t *)sm.X;
   if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
+    const bool build_b = op == RS_OP_ANDNOT || (op == RS_OP_AND && nb < na);
+    if (build_b) set_bits16<false>(xb, cb, X);
+    else set_bits16<false>(xa, ca, X);
+    cbar();
+    // every consumer has finished the previous pair: its ring slot may refill
+    if (t == 0 && release) mbar_arrive(release);
     const bool probe_b = !build_b;
     uint32_t P[8];
 #pragma unroll
@@ -222,6 +248,8 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
     }
     uint32_t total;
     uint32_t base = cscan((uint32_t)__popc(keep), sm.red[parity], total);
+#pragma unroll
+    for (int q = 0; q < 4; q++) X[t + LT * q] = 0;  // every probe of this pair is done
     type = RS_TAG_ARRAY;
     nout = total;
     if (dst && total) {
@@ -232,15 +260,24 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
     }
     return total;
   }
-  if (op == RS_OP_OR) set_bits16<false>(xb, cb, sm.X);
-  else set_bits16<true>(xb, cb, sm.X);
+  // OR / XOR: both arrays in one scatter phase (the updates commute; each
+  // side's values are distinct, so XOR flips a bit once per side)
+  if (op == RS_OP_OR) {
+    set_bits16<false>(xa, ca, X);
+    set_bits16<false>(xb, cb, X);
+  } else {
+    set_bits16<true>(xa, ca, X);
+    set_bits16<true>(xb, cb, X);
+  }
   cbar();
+  if (t == 0 && release) mbar_arrive(release);
   // result words t + 256q (conflict-free), positions by a packed row scan
   uint64_t r[4];
   uint32_t pq[4];
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    r[q] = sm.X[t + LT * q];
+    r[q] = X[t + LT * q];
+    X[t + LT * q] = 0;
     pq[q] = __popcll(r[q]);
   }
   const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
@@ -298,6 +335,7 @@ __device__ void large_loop(LargeSmem &sm, uint32_t count, int op, const uint8_t 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int w = t; w < 2 * RS_WORDS; w += LTHREADS) (&sm.X[0][0])[w] = 0;
   __syncthreads();
   if (t >= LT) {  // ---------------- producer warp (one elected lane)
     if (t == LT) {
@@ -312,7 +350,7 @@ __device__ void large_loop(LargeSmem &sm, uint32_t count, int op, const uint8_t 
         uint64_t nao = 0, nbo = 0;
         LargeMeta nm = m;
         if (i + gridDim.x < count) nm = meta_of(i + gridDim.x, nao, nbo);
-        if (j >= LSTAGES) rsb::mbar_wait(&sm.empty[s], ((j / LSTAGES) - 1) & 1);
+        if (j >= LSTAGES) mbar_wait_backoff(&sm.empty[s], ((j / LSTAGES) - 1) & 1);
         sm.meta[s] = m;
         const uint32_t ba = (uint32_t)rs_pad16(2ull * m.na), bb = (uint32_t)rs_pad16(2ull * m.nb);
         rsb::mbar_expect_tx(&sm.full[s], ba + bb);
