@@ -285,7 +285,8 @@ def run_gpu(args):
         pin_b = _lib.PinnedBuffer(B_img[0].nbytes)
         pin_a.array[:] = A_img[0]
         pin_b.array[:] = B_img[0]
-        out_cap = int(2 * (A_img[0].nbytes + B_img[0].nbytes))
+        # one chunk's result images at a time (an OR of two 8 KB bitsets is at most 8 KB)
+        out_cap = int(2 * (A_img[0].nbytes + B_img[0].nbytes) // E2E_CHUNKS)
         pin_out = _lib.PinnedBuffer(out_cap)
         host_counts = np.zeros(NPAIRS, dtype=np.uint64)
 
@@ -362,7 +363,7 @@ def run_gpu(args):
 
     base = None
     if rank == 0 and not args.no_cpu:
-        base = cpu_baseline(*workload(2), max_seconds=args.cpu_seconds)
+        base = cpu_baseline(buf, offs, max_seconds=args.cpu_seconds)  # rank 0: seed 2 = this workload
 
     value = ws * units_per_step * args.steps / (ms_max * 1e-3)
     line = {
