@@ -376,3 +376,41 @@ def test_deferred_ingest_pipeline_matches_sync(pkg):
         b.wait()
     for op in OPS:
         assert [w for R in got[op] for w in R.to_wire_list()] == want[op], op
+
+
+def test_deferred_ingest_lifecycle(pkg):
+    """Deferred batches freed before first use hand their staging slot back;
+    many in flight at once; pageable input; a run container that can never be
+    admissible (> 2047 runs) takes the synchronous path and raises at once."""
+    g = load()
+    imgs = [g.wire(a) for a in g["pair_a"]]
+    want = pkg.BitmapBatch.from_wire(imgs).to_wire_list()
+    for _ in range(3):  # created and dropped unused: slots must come back
+        pkg.BitmapBatch.from_wire(imgs, deferred=True)
+    live = [pkg.BitmapBatch.from_wire(imgs, deferred=True) for _ in range(12)]
+    for b in live:
+        assert b.to_wire_list() == want
+        b.wait()
+    # > 2047 runs in one container: structurally valid, never admissible
+    runs = np.arange(0, 2 * 2100, 2, dtype=np.uint16)
+    img = (b"ROAR" + (1).to_bytes(4, "little") + (0).to_bytes(2, "little") + bytes([3, 0]) +
+           len(runs).to_bytes(4, "little") + len(runs).to_bytes(2, "little") +
+           np.stack([runs, np.zeros_like(runs)], 1).astype("<u2").tobytes())
+    with pytest.raises(pkg.DecodeError) as e:
+        pkg.BitmapBatch.from_wire([img], deferred=True)
+    with pytest.raises(pkg.DecodeError) as e2:
+        pkg.BitmapBatch.from_wire([img])
+    assert str(e.value) == str(e2.value) and e.value.offset == e2.value.offset
+
+
+def test_contains_edge_cases(pkg):
+    B = pkg.BitmapBatch.from_values([np.array([0, 65535, 65536, 1 << 31, 0xFFFFFFFF], dtype=np.uint64),
+                                     np.array([], dtype=np.uint64)])
+    q = [0, 1, 65535, 65536, 65537, 1 << 31, 0xFFFFFFFF, 0xFFFFFFFE]
+    assert B.contains(q).tolist() == [True, False, True, True, False, True, True, False]
+    assert B.contains(q, [1] * len(q)).tolist() == [False] * len(q)
+    assert B.contains([]).size == 0
+    with pytest.raises(Exception):
+        B.contains([1], [2])          # bitmap index out of range
+    with pytest.raises(ValueError):
+        B.contains([1 << 32])
