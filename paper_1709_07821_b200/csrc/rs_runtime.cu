@@ -277,7 +277,9 @@ int fetch_host_meta(const rs_batch *cb) {
   return RS_OK;
 }
 
-// RoaringBitmap.__len__ (bitmap.py:77-82): one warp per bitmap sums its cards.
+// RoaringBitmap.__len__ (bitmap.py:77-82): one warp per bitmap sums its cards
+// (one thread per bitmap when bitmaps hold few containers, e.g. config 3's
+// single-container bitmaps, where a warp would leave 31 lanes idle).
 __global__ void k_bm_card(uint64_t nb, const uint64_t *__restrict__ bm_start,
                           const uint32_t *__restrict__ card, uint64_t *__restrict__ out) {
   uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -289,7 +291,21 @@ __global__ void k_bm_card(uint64_t nb, const uint64_t *__restrict__ bm_start,
   if (lane == 0) out[w] = s;
 }
 
+__global__ void k_bm_card_thread(uint64_t nb, const uint64_t *__restrict__ bm_start,
+                                 const uint32_t *__restrict__ card, uint64_t *__restrict__ out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  uint64_t s = 0;
+  for (uint64_t c = bm_start[i]; c < bm_start[i + 1]; c++) s += card[c];
+  out[i] = s;
+}
+
 int finalize_batch(rs_batch *b) {
+  if (b->nb && b->nc <= 4 * b->nb) {
+    RS_LAUNCH(k_bm_card_thread, (unsigned)((b->nb + 255) / 256), 256, 0, b->nb, b->d_bm_start, b->d_card,
+              b->d_bm_card);
+    return RS_OK;
+  }
   uint64_t threads = b->nb * 32;
   RS_LAUNCH(k_bm_card, (unsigned)((threads + 255) / 256), 256, 0, b->nb, b->d_bm_start, b->d_card,
             b->d_bm_card);
