@@ -280,17 +280,33 @@ __global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__res
   __shared__ __align__(16) DenseSmem sm;
   const int t = threadIdx.x;
   const uint32_t total = *cnt;
+  // the next item's metadata chain (list -> entry -> containers) is loaded
+  // while the current item is processed: it is off the critical path
+  struct Item {
+    uint32_t e, ca, cb;
+    uint8_t ta, tb;
+  };
+  auto fetch = [&](uint32_t item) {
+    Item m;
+    m.e = list[item];
+    m.ca = E.ca[m.e];
+    m.cb = E.cb[m.e];
+    m.ta = GEN ? A.type[m.ca] : (uint8_t)RS_TAG_BITSET;
+    m.tb = GEN ? B.type[m.cb] : (uint8_t)RS_TAG_BITSET;
+    return m;
+  };
+  Item nxt;
+  if (blockIdx.x < total) nxt = fetch(blockIdx.x);
   for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-  const uint32_t e = list[item];
-  const uint32_t ca = E.ca[e], cb = E.cb[e];
-  uint8_t ta = RS_TAG_BITSET, tb = RS_TAG_BITSET;
+  const Item cur = nxt;
+  if (item + gridDim.x < total) nxt = fetch(item + gridDim.x);
+  const uint32_t e = cur.e, ca = cur.ca, cb = cur.cb;
+  uint8_t ta = cur.ta, tb = cur.tb;
   uint64_t ra[4], rb[4];
   if (!GEN) {
     ld_words(A.pool, A.off[ca], t, ra);
     ld_words(B.pool, B.off[cb], t, rb);
   } else {
-    ta = A.type[ca];
-    tb = B.type[cb];
     bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
@@ -932,7 +948,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
       RS_TRY(launch_aa_large_op(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card, hcnt != nullptr));
   }
   if (uint64_t n = want(CLS_GEN, cm.gen))
-    RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
+    RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 8), DT, 0, op,
                    L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, b->d_bm_card);
   // compaction: drop empty results (bitmap.py:185-188)
   RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, dE, O.card, keep2);
