@@ -218,6 +218,13 @@ def c4(steps, nbitmaps=200):
         out["per_op"][op] = {"ms": ms, "bitmap_pairs_per_s": len(ia) / (ms * 1e-3),
                              "container_pairs_per_s": n_matched / (ms * 1e-3),
                              "algorithmic_GBps": byts / (ms * 1e-3) / 1e9, "frac_of_hbm": byts / (ms * 1e-3) / 1e9 / hbm}
+    # the north_star's "mixed-container batched AND/OR pipeline": both ops'
+    # algorithmic bytes over both ops' device time
+    po = out["per_op"]
+    pipe_bytes = sum(po[o]["algorithmic_GBps"] * 1e9 * po[o]["ms"] * 1e-3 for o in ("and", "or"))
+    pipe_ms = po["and"]["ms"] + po["or"]["ms"]
+    out["and_or_pipeline"] = {"ms": pipe_ms, "algorithmic_GBps": pipe_bytes / (pipe_ms * 1e-3) / 1e9,
+                              "frac_of_hbm": pipe_bytes / (pipe_ms * 1e-3) / 1e9 / hbm}
     U = Bt.union_many()
     w = wires(buf, offs, range(nbitmaps)) if nbitmaps <= 200 else None
     if w is not None:
