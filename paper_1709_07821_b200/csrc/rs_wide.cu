@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
 
 // ------------------------------------------------------------ all pairs
 
-// densify every grouped container into its own 8 KB slot
+// densify every grouped container into its own 8 KB slot.  Thread t owns
+// words t + 256q (conflict-free smem, coalesced 64-bit stores); the slots are
+// written with streaming stores (read back once by the all-pairs tiles).
 __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__restrict__ item_c, DevBatch S,
                                                 uint64_t *__restrict__ D) {
   __shared__ __align__(16) uint64_t X[RS_WORDS];
@@ -177,19 +179,18 @@ __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__re
   uint8_t type = S.type[c];
   uint64_t *dst = D + i * RS_WORDS;
   if (type == RS_TAG_BITSET) {
-    uint64_t w[4];
-    ld_words(S.pool, S.off[c], t, w);
-    st_words((uint8_t *)dst, 0, t, w);
+    const uint64_t *src = (const uint64_t *)(S.pool + S.off[c]);
+#pragma unroll
+    for (int q = 0; q < 4; q++) __stcs(dst + t + DT * q, __ldcs(src + t + DT * q));
     return;
   }
 #pragma unroll
-  for (int k = 0; k < 4; k++) X[4 * t + k] = 0;
+  for (int q = 0; q < 4; q++) X[t + DT * q] = 0;
   __syncthreads();
   scatter_container(S, c, type, X);
   __syncthreads();
-  uint64_t w[4];
-  for (int k = 0; k < 4; k++) w[k] = X[4 * t + k];
-  st_words((uint8_t *)dst, 0, t, w);
+#pragma unroll
+  for (int q = 0; q < 4; q++) __stcs(dst + t + DT * q, X[t + DT * q]);
 }
 
 // One CTA per tensor-core tile (see rs_umma.cuh): A = rows [r0, r0+128),
@@ -589,7 +590,9 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   std::vector<uint64_t> sel(N);
   for (uint64_t k = 0; k < N; k++) sel[k] = k;
   Grouped g;
+  trace("allpairs: start");
   RS_TRY(group_and_reorder(in, sel, g));
+  trace("allpairs: group by key");
   // Keys with enough containers to fill 128-row tiles go to the tensor cores
   // (k_allpairs_umma); the rest use the CUDA-core 16x16 POPC tiles, whose cost
   // shrinks with m^2 (RS_ALLPAIRS_UMMA=0 sends everything to POPC tiles,
@@ -645,6 +648,7 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
     set_error("device allocation failed (all pairs)");
     return RS_ENOMEM;
   }
+  trace("allpairs: tile lists + allocs");
   RS_TRY(h2d(d_tseg, tseg.data(), ntp * 4));
   RS_TRY(h2d(d_ti, ti.data(), ntp * 2));
   RS_TRY(h2d(d_tj, tj.data(), ntp * 2));
@@ -654,7 +658,9 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_TRY(h2d(d_unb, unb.data(), nup * 2));
   RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
   RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
+  trace("allpairs: uploads + memset + item_bm");
   RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
+  trace("allpairs: densify");
   if (nup) {
     static bool attr = false;
     if (!attr) {
@@ -671,12 +677,15 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   else
     RS_LAUNCH_PROF("allpairs", ntp, k_allpairs_tiles, (unsigned)ntp, 256, 0, d_tseg, d_ti, d_tj, g.seg_start, D,
                    item_bm, N, Mx);
+  trace("allpairs: tiles");
   dim3 grid(grid_for(N, 256), (unsigned)N);
   k_upper_triangle<<<grid, 256, 0, g_stream>>>(N, Mx, in->d_bm_card, d_inter, uni ? d_uni : nullptr);
   ++g_launches;
   RS_CK(cudaGetLastError());
+  trace("allpairs: upper triangle");
   RS_TRY(d2h(inter, d_inter, npairs * 8));
   if (uni) RS_TRY(d2h(uni, d_uni, npairs * 8));
+  trace("allpairs: readback");
   dfree(D); dfree(item_bm); dfree(d_tseg); dfree(d_ti); dfree(d_tj); dfree(Mx); dfree(d_inter); dfree(d_uni);
   dfree(d_useg); dfree(d_ur0); dfree(d_uc0); dfree(d_unb);
   g.release();
