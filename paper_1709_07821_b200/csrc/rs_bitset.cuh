@@ -103,8 +103,9 @@ __device__ __forceinline__ void issue(BBSmem<STAGES> &sm, int s, const uint8_t *
 template <int STAGES, typename Src, typename Pre, typename Sink>
 __device__ __forceinline__ void bb_loop(BBSmem<STAGES> &sm, uint32_t count, int op, Src src, Pre pre, Sink sink) {
   const int t = threadIdx.x;
+  if (blockIdx.x >= count) return;  // no item for this CTA (the list may be empty)
   // per-item sink metadata (output slot, pair, ...) is loaded one item ahead
-  auto meta = pre(blockIdx.x < count ? blockIdx.x : 0);
+  auto meta = pre(blockIdx.x);
   if (t == 0) {
     for (int s = 0; s < STAGES; s++) mbar_init(&sm.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -140,6 +140,10 @@ __global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict_
                         uint32_t *__restrict__ mca, uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
                         uint32_t *__restrict__ keep, uint64_t *__restrict__ ub) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t == 0) {  // scan sentinels (the exclusive scans run over M + 1)
+    keep[M] = 0;
+    ub[M] = 0;
+  }
   if (t >= M) return;
   const bool keep_a = op != RS_OP_AND;                        // _KEEP_A, bitmap.py:21
   const bool keep_b = op == RS_OP_OR || op == RS_OP_XOR;      // _KEEP_B, bitmap.py:22
@@ -801,19 +805,55 @@ __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint3
 
 // ------------------------------------------------------------- host side
 
+// Per-op scratch: a bump allocator over one cached device block, so an op's
+// ~25 scratch arrays cost a pointer bump each instead of a trip through the
+// caching allocator (host time is what a small op like config 1 spends).  The
+// block is reused by the next op in stream order; scopes nest LIFO; an op
+// that outgrows it spills to dalloc and the block grows before a later op.
 struct Scratch {
-  std::vector<void *> ptrs;
+  static uint8_t *arena;
+  static size_t cap, top, want;
+  static cudaStream_t stream;
+  size_t base, need;
+  bool failed = false;
+  std::vector<void *> spill;
+  Scratch() {
+    if (top == 0) {
+      if (stream != g_stream) {  // reused blocks are ordered on the old stream
+        if (arena) cudaStreamSynchronize(stream);
+        stream = g_stream;
+      }
+      if (want > cap) {
+        dfree(arena);
+        arena = (uint8_t *)dalloc(want);
+        cap = arena ? want : 0;
+      }
+    }
+    base = need = top;
+  }
   void *get(size_t bytes) {
+    const size_t b = (bytes + 255) & ~(size_t)255;
+    need += b;
+    if (arena && top + b <= cap) {
+      void *p = arena + top;
+      top += b;
+      return p;
+    }
     void *p = dalloc(bytes);
-    ptrs.push_back(p);
+    if (!p) failed = true;
+    spill.push_back(p);
     return p;
   }
-  bool ok() const {
-    for (void *p : ptrs) if (!p) return false;
-    return true;
+  bool ok() const { return !failed; }
+  ~Scratch() {
+    top = base;
+    for (void *p : spill) dfree(p);
+    if (need > cap) want = std::max(want, need + need / 4);
   }
-  ~Scratch() { for (void *p : ptrs) dfree(p); }
 };
+uint8_t *Scratch::arena = nullptr;
+size_t Scratch::cap = 0, Scratch::top = 0, Scratch::want = 1 << 20;
+cudaStream_t Scratch::stream = nullptr;
 
 unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
 
@@ -836,27 +876,53 @@ int check_op(int op) {
   return RS_OK;
 }
 
-int upload_pairs(Scratch &S, const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
-                 uint64_t npairs, uint32_t **dia, uint32_t **dib) {
-  *dia = nullptr;
-  *dib = nullptr;
+int check_pairs(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib, uint64_t npairs) {
   if (!ia && npairs > A->nb) { set_error("identity pairing needs npairs <= len(A)"); return RS_EARG; }
   if (!ib && npairs > B->nb) { set_error("identity pairing needs npairs <= len(B)"); return RS_EARG; }
   for (uint64_t p = 0; ia && p < npairs; p++)
     if (ia[p] >= A->nb) { set_error("pair index out of range (A)"); return RS_EARG; }
   for (uint64_t p = 0; ib && p < npairs; p++)
     if (ib[p] >= B->nb) { set_error("pair index out of range (B)"); return RS_EARG; }
-  if (ia) {
-    *dia = (uint32_t *)S.get(npairs * 4);
-    if (!*dia) { set_error("device allocation failed"); return RS_ENOMEM; }
-    RS_TRY(h2d(*dia, ia, npairs * 4));
-  }
-  if (ib) {
-    *dib = (uint32_t *)S.get(npairs * 4);
-    if (!*dib) { set_error("device allocation failed"); return RS_ENOMEM; }
-    RS_TRY(h2d(*dib, ib, npairs * 4));
-  }
   return RS_OK;
+}
+
+// An op's small host-side inputs (pair indices, per-pair merge bases, zeroed
+// counters) gathered into one block and sent up as ONE copy through pinned
+// staging, instead of a pageable copy and a memset each.
+struct Upload {
+  static constexpr size_t NONE = ~(size_t)0;
+  std::vector<uint8_t> h;
+  uint8_t *d = nullptr;
+  size_t add(const void *src, size_t bytes) {  // src == nullptr: zeros
+    const size_t o = h.size();
+    h.resize(o + ((bytes + 15) & ~(size_t)15), 0);
+    if (src && bytes) memcpy(h.data() + o, src, bytes);
+    return o;
+  }
+  int commit(Scratch &S) {
+    if (h.empty()) return RS_OK;
+    d = (uint8_t *)S.get(h.size());
+    if (!d) { set_error("device allocation failed (upload)"); return RS_ENOMEM; }
+    return h2d_staged(d, h.data(), h.size());
+  }
+  template <typename T> T *at(size_t o) const { return o == NONE ? nullptr : (T *)(d + o); }
+};
+
+// mbase[p] = exclusive prefix of the per-pair merged key counts (na + nb, or
+// na for the count path), summed on the host (which holds bm_start) for small
+// pair lists; false = use the device size kernel + scan instead.
+bool pair_bases_host(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib, uint64_t npairs,
+                     int count_mode, std::vector<uint64_t> &h) {
+  if (npairs > 16384) return false;
+  h.resize(npairs + 1);
+  uint64_t acc = 0;
+  for (uint64_t p = 0; p < npairs; p++) {
+    h[p] = acc;
+    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+    acc += (A->h_bm_start[a + 1] - A->h_bm_start[a]) + (count_mode ? 0 : (B->h_bm_start[b + 1] - B->h_bm_start[b]));
+  }
+  h[npairs] = acc;
+  return true;
 }
 
 // Which work classes can occur between batches with these container-type
@@ -961,25 +1027,9 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   return RS_OK;
 }
 
-// mbase[p] = exclusive prefix of the per-pair merged key counts (na + nb, or
-// na for the count path).  Small pair lists are summed on the host (which
-// already holds bm_start) and uploaded; large ones use a size kernel + scan.
-int pair_bases(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib, uint64_t npairs,
-               DevBatch dA, DevBatch dB, const uint32_t *dia, const uint32_t *dib, int count_mode, uint64_t *msz,
-               uint64_t *mbase) {
-  if (npairs <= 16384) {
-    std::vector<uint64_t> h(npairs + 1);
-    uint64_t acc = 0;
-    for (uint64_t p = 0; p < npairs; p++) {
-      h[p] = acc;
-      uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
-      acc += (A->h_bm_start[a + 1] - A->h_bm_start[a]) +
-             (count_mode ? 0 : (B->h_bm_start[b + 1] - B->h_bm_start[b]));
-    }
-    h[npairs] = acc;
-    RS_CK(cudaMemcpyAsync(mbase, h.data(), (npairs + 1) * 8, cudaMemcpyHostToDevice, g_stream));
-    return RS_OK;
-  }
+// device path of the merge bases for large pair lists: size kernel + scan
+int pair_bases_device(uint64_t npairs, DevBatch dA, DevBatch dB, const uint32_t *dia, const uint32_t *dib,
+                      int count_mode, uint64_t *msz, uint64_t *mbase) {
   RS_LAUNCH(k_pair_msize, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, count_mode, msz);
   return scan_exclusive<uint64_t>(msz, mbase, npairs + 1);
 }
@@ -1030,9 +1080,8 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   *out = nullptr;
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
+  RS_TRY(check_pairs(A, B, ia, ib, npairs));
   Scratch S;
-  uint32_t *dia, *dib;
-  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
   uint64_t M = 0, Ecap = 0;
   for (uint64_t p = 0; p < npairs; p++) {
     uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
@@ -1044,7 +1093,14 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   // container costs at most ~2x the inputs' pools; else size exactly.
   const bool ub_mode = env_int("RS_EXACT_ALLOC", 0) == 0 &&
                        8192.0 * (double)Ecap <= 2.0 * (double)(A->pool_bytes + B->pool_bytes) + 64e6;
-  uint64_t *msz = (uint64_t *)S.get((npairs + 1) * 8), *mbase = (uint64_t *)S.get((npairs + 1) * 8);
+  Upload U;
+  const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
+  std::vector<uint64_t> hb;
+  const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 0, hb);
+  const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
+  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint16_t *mkey = (uint16_t *)S.get((M + 1) * 2);
   uint32_t *mca = (uint32_t *)S.get((M + 1) * 4), *mcb = (uint32_t *)S.get((M + 1) * 4),
            *mpair = (uint32_t *)S.get((M + 1) * 4), *keep = (uint32_t *)S.get((M + 1) * 4),
@@ -1057,13 +1113,17 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   En.pair = (uint32_t *)S.get((M + 1) * 4);
   En.off = (uint64_t *)S.get((M + 1) * 8);
   Lists L = make_lists(S, M);
-  uint64_t *tot = (uint64_t *)S.get(4 * 8);
   if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
+  RS_TRY(U.commit(S));
+  const uint32_t *dia = U.at<uint32_t>(o_ia), *dib = U.at<uint32_t>(o_ib);
+  L.cnt = U.at<uint32_t>(o_cnt);
   DevBatch dA = A->dev(), dB = B->dev();
-  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
-  RS_CK(cudaMemsetAsync(keep + M, 0, 4, g_stream));
-  RS_CK(cudaMemsetAsync(ub + M, 0, 8, g_stream));
-  RS_TRY(pair_bases(A, B, ia, ib, npairs, dA, dB, dia, dib, 0, msz, mbase));
+  if (hbases) mbase = U.at<uint64_t>(o_mb);
+  else RS_TRY(pair_bases_device(npairs, dA, dB, dia, dib, 0, msz, mbase));
+  if (M == 0) {  // k_merge writes these sentinels otherwise
+    RS_CK(cudaMemsetAsync(keep, 0, 4, g_stream));
+    RS_CK(cudaMemsetAsync(ub, 0, 8, g_stream));
+  }
   RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
@@ -1077,7 +1137,6 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_CK(cudaMemcpyAsync(&h.P, uoff + M, 8, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaMemcpyAsync(h.cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
   RS_CK(cudaStreamSynchronize(g_stream));
-  (void)tot;
   return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, nullptr, mbase, epos, npairs, out);
 }
 
@@ -1089,9 +1148,11 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
   RS_TRY(check_single_containers(A, B, ia, ib, npairs));
+  RS_TRY(check_pairs(A, B, ia, ib, npairs));
   Scratch S;
-  uint32_t *dia, *dib;
-  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
+  Upload U;
+  const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
+  const size_t o_cnt = U.add(nullptr, NCLS * 4);
   Entries En;
   En.key = (uint16_t *)S.get((npairs + 1) * 2);
   En.ca = (uint32_t *)S.get((npairs + 1) * 4);
@@ -1101,7 +1162,9 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   uint64_t *ub = (uint64_t *)S.get((npairs + 1) * 8);
   Lists L = make_lists(S, npairs);
   if (!S.ok()) { set_error("device allocation failed (container op)"); return RS_ENOMEM; }
-  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
+  RS_TRY(U.commit(S));
+  const uint32_t *dia = U.at<uint32_t>(o_ia), *dib = U.at<uint32_t>(o_ib);
+  L.cnt = U.at<uint32_t>(o_cnt);
   DevBatch dA = A->dev(), dB = B->dev();
   RS_LAUNCH(k_cont_entries, grid_for(npairs + 1, 256), 256, 0, npairs, dA, dB, dia, dib, op, En, ub, L);
   RS_TRY(scan_exclusive<uint64_t>(ub, En.off, npairs + 1));
@@ -1170,24 +1233,35 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
     RS_TRY(resolve_pending(A));
     RS_TRY(resolve_pending(B));
   }
+  RS_TRY(check_pairs(A, B, ia, ib, npairs));
   Scratch S;
-  uint32_t *dia, *dib;
-  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
   uint64_t Ma = 0;
   for (uint64_t p = 0; p < npairs; p++) {
     uint32_t a = ia ? ia[p] : (uint32_t)p;
     Ma += A->h_bm_start[a + 1] - A->h_bm_start[a];
   }
-  uint64_t *msz = (uint64_t *)S.get((npairs + 1) * 8), *mbase = (uint64_t *)S.get((npairs + 1) * 8);
+  Upload U;
+  const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
+  std::vector<uint64_t> hb;
+  const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 1, hb);
+  const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
+  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
+  uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   Lists L = make_lists(S, Ma);
   uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);
-  uint64_t *inter = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *inter = o_inter == Upload::NONE ? (uint64_t *)S.get((npairs + 1) * 8) : nullptr;
   uint64_t *dout = counts_on_device ? counts : (uint64_t *)S.get((npairs + 1) * 8);
   if (!S.ok()) { set_error("device allocation failed (count)"); return RS_ENOMEM; }
+  RS_TRY(U.commit(S));
+  const uint32_t *dia = U.at<uint32_t>(o_ia), *dib = U.at<uint32_t>(o_ib);
+  L.cnt = U.at<uint32_t>(o_cnt);
+  if (inter) RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
+  else inter = U.at<uint64_t>(o_inter);
   DevBatch dA = A->dev(), dB = B->dev();
-  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
-  RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
-  RS_TRY(pair_bases(A, B, ia, ib, npairs, dA, dB, dia, dib, 1, msz, mbase));
+  if (hbases) mbase = U.at<uint64_t>(o_mb);
+  else RS_TRY(pair_bases_device(npairs, dA, dB, dia, dib, 1, msz, mbase));
   RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
   RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
   RS_LAUNCH(k_formula, grid_for(npairs, 256), 256, 0, npairs, op, A->d_bm_card, B->d_bm_card, dia, dib, inter, dout);
@@ -1207,17 +1281,23 @@ extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, cons
     RS_TRY(resolve_pending(B));
   }
   RS_TRY(check_single_containers(A, B, ia, ib, npairs));
+  RS_TRY(check_pairs(A, B, ia, ib, npairs));
   Scratch S;
-  uint32_t *dia, *dib;
-  RS_TRY(upload_pairs(S, A, B, ia, ib, npairs, &dia, &dib));
+  Upload U;
+  const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
+  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   Lists L = make_lists(S, npairs);
   uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);
-  uint64_t *inter = (uint64_t *)S.get((npairs + 1) * 8);
+  uint64_t *inter = o_inter == Upload::NONE ? (uint64_t *)S.get((npairs + 1) * 8) : nullptr;
   uint64_t *dout = counts_on_device ? counts : (uint64_t *)S.get((npairs + 1) * 8);
   if (!S.ok()) { set_error("device allocation failed (count)"); return RS_ENOMEM; }
+  RS_TRY(U.commit(S));
+  const uint32_t *dia = U.at<uint32_t>(o_ia), *dib = U.at<uint32_t>(o_ib);
+  L.cnt = U.at<uint32_t>(o_cnt);
+  if (inter) RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
+  else inter = U.at<uint64_t>(o_inter);
   DevBatch dA = A->dev(), dB = B->dev();
-  RS_CK(cudaMemsetAsync(L.cnt, 0, NCLS * 4, g_stream));
-  RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
   RS_LAUNCH(k_cont_list, grid_for(npairs, 256), 256, 0, npairs, dA, dB, dia, dib, L, lcb, lpair);
   RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
   RS_LAUNCH(k_formula_containers, grid_for(npairs, 256), 256, 0, npairs, op, dA, dB, dia, dib, inter, dout);
