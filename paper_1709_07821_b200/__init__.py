@@ -11,8 +11,9 @@ hand-written CUDA kernels behind the C ABI of include/roaring_b200.h.
 
 from .batch import BitmapBatch
 from .bitmap import RoaringBitmap
-from .containers import (ArrayContainer, BitsetContainer, RunContainer, container_pairwise,
-                         container_pairwise_cardinality)
+from .containers import (ArrayContainer, BitsetContainer, RunContainer, container_add, container_contains,
+                         container_normalize, container_pairwise, container_pairwise_cardinality,
+                         container_remove)
 from .serde import DecodeError, deserialize, serialize
 from ._lib import RoaringCudaError
 
@@ -22,6 +23,7 @@ __all__ = [
     "RoaringBitmap", "BitmapBatch",
     "ArrayContainer", "BitsetContainer", "RunContainer",
     "container_pairwise", "container_pairwise_cardinality",
+    "container_add", "container_remove", "container_contains", "container_normalize",
     "serialize", "deserialize", "DecodeError", "RoaringCudaError",
     "__version__",
 ]

@@ -166,3 +166,66 @@ def container_pairwise_cardinality(op: str, a: Container, b: Container) -> int:
     A = BitmapBatch.from_wire([_single(a)])
     B = BitmapBatch.from_wire([_single(b)])
     return int(A.container_pairwise_cardinality(op, B)[0])
+
+
+# ------------------------------------------------- single-container helpers
+# The reference's element-level container functions (containers.py:208-367),
+# for drop-in completeness.  Each runs as a one-container GPU batch; the
+# batched forms are BitmapBatch.contains / pairwise.
+
+def _canonical(c: Container) -> bool:
+    n = len(c)
+    if isinstance(c, ArrayContainer):
+        return 1 <= n <= ARRAY_MAX and bool(np.all(np.diff(c.values.astype(np.int64)) > 0))
+    if isinstance(c, BitsetContainer):
+        return n > ARRAY_MAX
+    nr = len(c.runs)
+    return nr > 0 and (nr <= RUN_MAX_RUNS if n > ARRAY_MAX else 2 * nr < n)
+
+
+def _batch_of(c: Container):
+    from .batch import BitmapBatch
+    if _canonical(c):
+        return BitmapBatch.from_wire([_single(c)])
+    return BitmapBatch.from_values([container_positions(c).astype(np.uint32)])
+
+
+def container_normalize(c: Container, consider_run: bool = False) -> Container:
+    """containers.py:208-241: the canonical form; `c` itself when unchanged.
+    Run candidacy applies to run inputs always and to others on request."""
+    from .batch import BitmapBatch
+    if len(c) == 0:
+        return c if isinstance(c, ArrayContainer) else ArrayContainer()
+    B = BitmapBatch.from_values([container_positions(c).astype(np.uint32)])
+    if consider_run or isinstance(c, RunContainer):
+        B.run_optimize()
+    _, conts = chunks_from_wire(B.to_wire_list()[0])
+    n = conts[0]
+    return c if type(n) is type(c) and n == c else n
+
+
+def container_contains(c: Container, v: int) -> bool:
+    """containers.py:258-268."""
+    if len(c) == 0 or not 0 <= int(v) <= 0xFFFF:
+        return False
+    return bool(_batch_of(c).contains([int(v)])[0])
+
+
+def container_add(c: Container, v: int):
+    """containers.py:271-319: (container, changed); the re-typing is the OR
+    rule with {v} (array full -> bitset, runs re-checked)."""
+    if container_contains(c, v):
+        return c, False
+    one = ArrayContainer(np.array([int(v)], dtype=np.uint16))
+    if len(c) == 0:
+        return one, True
+    return container_pairwise("or", container_normalize(c) if not _canonical(c) else c, one), True
+
+
+def container_remove(c: Container, v: int):
+    """containers.py:322-367: (container, changed); the re-typing is the
+    ANDNOT rule with {v} (bitset at 4096 -> array, runs re-checked)."""
+    if not container_contains(c, v):
+        return c, False
+    one = ArrayContainer(np.array([int(v)], dtype=np.uint16))
+    return container_pairwise("andnot", container_normalize(c) if not _canonical(c) else c, one), True

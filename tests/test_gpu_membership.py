@@ -136,3 +136,67 @@ def test_run_optimize_and_shrink_never_grow_memory(pkg):
     assert reclaimed >= 0 and after_mem <= before_mem
     assert np.array_equal(rb.to_array(), before)
     rb.validate()
+
+
+# ---------------------------------------- container-level element functions
+# test_containers.py:55-135 known answers (container_add/remove/contains/normalize)
+
+def _arr(pkg, vals):
+    return pkg.ArrayContainer(np.array(sorted(vals), dtype=np.uint16))
+
+
+def _run(pkg, ivs):
+    return pkg.RunContainer(np.array(ivs, dtype=np.uint16))
+
+
+def _bitset(pkg, vals):
+    w = np.zeros(1024, dtype=np.uint64)
+    for v in vals:
+        w[v >> 6] |= np.uint64(1) << np.uint64(v & 63)
+    return pkg.BitsetContainer(w, len(vals))
+
+
+def test_container_add_remove_contains(pkg):
+    c, changed = pkg.container_add(_arr(pkg, [1, 3, 5]), 7)
+    assert changed and c.values.tolist() == [1, 3, 5, 7]
+    c, changed = pkg.container_add(_arr(pkg, [1, 3, 5]), 3)
+    assert not changed and c.values.tolist() == [1, 3, 5]
+    full = pkg.ArrayContainer(np.arange(4096, dtype=np.uint16))
+    c, changed = pkg.container_add(full, 4096)
+    assert changed and isinstance(c, pkg.BitsetContainer) and len(c) == 4097
+    c, changed = pkg.container_remove(_arr(pkg, [1, 3, 5]), 3)
+    assert changed and c.values.tolist() == [1, 5]
+    big = _bitset(pkg, range(4097))
+    c, changed = pkg.container_remove(big, 17)
+    assert changed and isinstance(c, pkg.ArrayContainer) and len(c) == 4096
+    r, changed = pkg.container_remove(_run(pkg, [(100, 100)]), 150)
+    assert changed and isinstance(r, pkg.RunContainer)
+    assert r.runs.tolist() == [[100, 49], [151, 49]]
+    r = _run(pkg, [(0, 99), (101, 99), (300, 99)])
+    assert not pkg.container_contains(r, 100) and pkg.container_contains(r, 200)
+    b = _bitset(pkg, [0] + list(range(100, 4200)))
+    assert pkg.container_contains(b, 0) and not pkg.container_contains(b, 1)
+    base = pkg.ArrayContainer(np.arange(4096, dtype=np.uint16))
+    c, _ = pkg.container_add(base.copy(), 5000)
+    assert isinstance(c, pkg.BitsetContainer)
+    c, _ = pkg.container_remove(c, 5000)
+    assert c == base
+
+
+def test_container_normalize_rules(pkg):
+    evens = _run(pkg, [(v, 0) for v in range(0, 65536, 2)])
+    n = pkg.container_normalize(evens)
+    assert isinstance(n, pkg.BitsetContainer) and len(n) == 32768
+    one_run = _run(pkg, [(0, 999)])
+    assert pkg.container_normalize(one_run) is one_run
+    assert len(pkg.container_normalize(pkg.ArrayContainer())) == 0
+    n = pkg.container_normalize(_run(pkg, [(0, 1), (10, 1)]))   # strict tie goes to the array
+    assert isinstance(n, pkg.ArrayContainer) and n.values.tolist() == [0, 1, 10, 11]
+    c = _arr(pkg, range(0, 1000))
+    assert pkg.container_normalize(c) is c
+    opt = pkg.container_normalize(c, consider_run=True)
+    assert isinstance(opt, pkg.RunContainer) and opt.runs.tolist() == [[0, 999]]
+    r = _run(pkg, [(i * 4, 1) for i in range(3000)])             # 6000 values, 3000 runs
+    assert isinstance(pkg.container_normalize(r), pkg.BitsetContainer)
+    r = _run(pkg, [(i * 32, 20) for i in range(2000)])           # 42000 values, 2000 runs
+    assert pkg.container_normalize(r) is r
