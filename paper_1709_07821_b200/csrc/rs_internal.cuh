@@ -107,7 +107,7 @@ extern bool g_prof_on;
 void prof_mark(const char *name, cudaEvent_t a, cudaEvent_t b, uint64_t items);
 cudaEvent_t prof_event();
 int h2d(void *d, const void *h, size_t bytes);   // async on g_stream
-int h2d_staged(void *d, const void *h, size_t bytes);  // via pinned staging; h reusable on return
+int h2d_small(void *d, const void *h, size_t bytes);  // small upload (see rs_runtime.cu)
 }  // namespace rs
 
 #define RS_CK(x)                                                                   \

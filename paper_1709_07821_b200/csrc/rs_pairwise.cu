@@ -887,8 +887,8 @@ int check_pairs(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const 
 }
 
 // An op's small host-side inputs (pair indices, per-pair merge bases, zeroed
-// counters) gathered into one block and sent up as ONE copy through pinned
-// staging, instead of a pageable copy and a memset each.
+// counters) gathered into one block and sent up as ONE copy, instead of a
+// copy and a memset each.
 struct Upload {
   static constexpr size_t NONE = ~(size_t)0;
   std::vector<uint8_t> h;
@@ -903,7 +903,7 @@ struct Upload {
     if (h.empty()) return RS_OK;
     d = (uint8_t *)S.get(h.size());
     if (!d) { set_error("device allocation failed (upload)"); return RS_ENOMEM; }
-    return h2d_staged(d, h.data(), h.size());
+    return h2d_small(d, h.data(), h.size());
   }
   template <typename T> T *at(size_t o) const { return o == NONE ? nullptr : (T *)(d + o); }
 };

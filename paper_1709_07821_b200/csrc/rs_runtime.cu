@@ -156,32 +156,13 @@ int h2d(void *d, const void *h, size_t bytes) {
   return RS_OK;
 }
 
-// Small host->device uploads through a pool of pinned staging blocks: the
-// bytes are copied into a free block (its last copy has completed) and go up
-// as one truly asynchronous copy; the caller's buffer is free on return.
-namespace {
-struct Staging { void *p; size_t bytes; cudaEvent_t done; };
-std::mutex g_stage_mu;
-std::vector<Staging> g_stage;
-}  // namespace
-
-int h2d_staged(void *d, const void *h, size_t bytes) {
-  if (!bytes) return RS_OK;
-  std::lock_guard<std::mutex> g(g_stage_mu);
-  Staging *blk = nullptr;
-  for (auto &b : g_stage)
-    if (b.bytes >= bytes && cudaEventQuery(b.done) == cudaSuccess) { blk = &b; break; }
-  if (!blk) {
-    Staging b;
-    b.bytes = std::max<size_t>(bytes, 64 << 10);
-    RS_CK(cudaHostAlloc(&b.p, b.bytes, cudaHostAllocDefault));
-    RS_CK(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
-    g_stage.push_back(b);
-    blk = &g_stage.back();
-  }
-  memcpy(blk->p, h, bytes);
-  RS_CK(cudaMemcpyAsync(d, blk->p, bytes, cudaMemcpyHostToDevice, g_stream));
-  RS_CK(cudaEventRecord(blk->done, g_stream));
+// An op's small host->device upload (a few KB): a plain cudaMemcpyAsync from
+// pageable memory, which the driver stages through the command stream itself.
+// Measured on the pipelined e2e path (bulk ingest saturating PCIe on the copy
+// stream): pageable 80 ms/step, pinned DMA 91 ms (queues on the copy engine
+// behind the bulk transfer), a kernel pulling from mapped host memory 94 ms.
+int h2d_small(void *d, const void *h, size_t bytes) {
+  if (bytes) RS_CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, g_stream));
   return RS_OK;
 }
 
