@@ -17,6 +17,7 @@
 //   compaction               drop empty results, per-bitmap container ranges
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <mutex>
 #include "rs_internal.cuh"
 #include "rs_dense.cuh"
 #include "rs_array.cuh"
@@ -814,6 +815,8 @@ struct Scratch {
   static uint8_t *arena;
   static size_t cap, top, want;
   static cudaStream_t stream;
+  static std::recursive_mutex mu;  // the arena is shared: ops from several host threads serialize
+  std::lock_guard<std::recursive_mutex> lock{mu};
   size_t base, need;
   bool failed = false;
   std::vector<void *> spill;
@@ -854,6 +857,7 @@ struct Scratch {
 uint8_t *Scratch::arena = nullptr;
 size_t Scratch::cap = 0, Scratch::top = 0, Scratch::want = 1 << 20;
 cudaStream_t Scratch::stream = nullptr;
+std::recursive_mutex Scratch::mu;
 
 unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
 
