@@ -28,7 +28,7 @@ using namespace rs;
 
 namespace {
 
-enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, NCLS = 6 };
+enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, CLS_PRB = 6, NCLS = 7 };
 
 struct Entries {
   uint16_t *key;
@@ -58,10 +58,16 @@ __device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { ret
 // bitset kernel wins for everything above 256 (RS_AA_LARGE_MIN overrides).
 __constant__ uint32_t c_aa_large_min = 256;
 
-__device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb) {
+// `op` is the materialized op, or AND for the intersection counts.  An
+// array against a bitset or runs under AND (either side), or an array minus a
+// bitset or runs, keeps a subset of the array: bit / interval probes of its
+// values (CLS_PRB) instead of densifying both sides.
+__device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb, int op) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
   if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY)
     return na + nb <= 256 ? CLS_AAS : na + nb <= c_aa_large_min ? CLS_AAM : CLS_AAL;
+  if (op == RS_OP_AND && (ta == RS_TAG_ARRAY || tb == RS_TAG_ARRAY)) return CLS_PRB;
+  if (op == RS_OP_ANDNOT && ta == RS_TAG_ARRAY) return CLS_PRB;
   return CLS_GEN;
 }
 
@@ -190,7 +196,7 @@ __global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict_
 __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ epos,
                        const uint64_t *__restrict__ uoff, const uint16_t *__restrict__ mkey,
                        const uint32_t *__restrict__ mca, const uint32_t *__restrict__ mcb,
-                       const uint32_t *__restrict__ mpair, DevBatch A, DevBatch B, Entries E, Lists L) {
+                       const uint32_t *__restrict__ mpair, DevBatch A, DevBatch B, Entries E, Lists L, int op) {
   uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   bool active = t < M && keep[t];
   int cls = CLS_COPY;
@@ -204,7 +210,7 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
     E.cb[e] = cb;
     E.pair[e] = mpair[t];
     E.off[e] = uoff[t];
-    cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
+    cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
     if (tma_class(cls)) {
       ao = A.off[ca];
       bo = B.off[cb];
@@ -620,6 +626,139 @@ int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch
   return RS_OK;
 }
 
+// ---------------------------------------- array x {bitset, runs}: probes
+//
+// array AND {bitset, runs} (either side) and array ANDNOT {bitset, runs}: the
+// result is the subset of the array's values that are (not) members of the
+// other container -- already sorted, always an array (App. A) -- so only the
+// other side is materialized: one warp per pair copies the bitset (or sets the
+// runs' bits) into a warp-private 8 KB shared-memory bitset, then its lanes
+// bit-test 32 array values at a time (_bitset_probe containers.py:181-186,
+// _values_in_runs :189-197) and a ballot compacts the kept ones into
+// consecutive output slots.  No extraction, no block barriers.
+constexpr int PRB_WARPS = 4;
+
+__device__ __forceinline__ void warp_load_member_set(uint64_t *W, uint8_t type, const uint8_t *payload, uint32_t n,
+                                                      int lane) {
+  if (type == RS_TAG_BITSET) {
+    const uint4 *src = (const uint4 *)payload;
+    uint4 *dst = (uint4 *)W;
+#pragma unroll 4
+    for (int k = lane; k < RS_WORDS / 2; k += 32) dst[k] = src[k];
+  } else {
+    for (int k = lane; k < RS_WORDS; k += 32) W[k] = 0;
+    __syncwarp();
+    uint32_t *W32 = (uint32_t *)W;
+    const uint32_t *r32 = (const uint32_t *)payload;
+    for (uint32_t r = lane; r < n; r += 32) {
+      const uint32_t sl = r32[r];
+      const uint32_t s = sl & 0xFFFF, e = s + (sl >> 16);
+      const uint32_t ws = s >> 5, we = e >> 5;
+      const uint32_t first = ~0u << (s & 31), last = ~0u >> (31 - (e & 31));
+      if (ws == we) {
+        atomicOr(&W32[ws], first & last);
+      } else {
+        atomicOr(&W32[ws], first);
+        atomicOr(&W32[we], last);
+        for (uint32_t w = ws + 1; w < we; w++) W32[w] = ~0u;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32 * PRB_WARPS) k_probe(int op, const uint32_t *__restrict__ list,
+                                                          const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                                                          Entries E, OutDesc O, uint8_t *__restrict__ opool,
+                                                          uint64_t *__restrict__ res_card) {
+  __shared__ __align__(16) uint64_t Xs[PRB_WARPS][RS_WORDS];
+  const int lane = threadIdx.x & 31;
+  uint64_t *W = Xs[threadIdx.x >> 5];
+  const uint32_t total = *cnt, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nw) {
+    const uint32_t e = list[i], ca = E.ca[e], cb = E.cb[e];
+    const bool from_a = op != RS_OP_AND || A.type[ca] == RS_TAG_ARRAY;  // the array side
+    const DevBatch &V = from_a ? A : B, &X = from_a ? B : A;
+    const uint32_t cv = from_a ? ca : cb, cx = from_a ? cb : ca;
+    const uint16_t *vals = (const uint16_t *)(V.pool + V.off[cv]);
+    const uint32_t n = V.n[cv];
+    warp_load_member_set(W, X.type[cx], X.pool + X.off[cx], X.n[cx], lane);
+    const uint32_t want = op == RS_OP_AND ? 1u : 0u;
+    uint16_t *out = (uint16_t *)(opool + E.off[e]);
+    // lane l takes values [256c + 8l, 256c + 8l + 8) with one 16-byte load
+    // (payloads are 16-byte aligned and zero-padded); a warp scan of the
+    // per-lane kept counts keeps the output in value order
+    uint32_t base = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += 256) {
+      const uint32_t j = c0 + 8 * lane;
+      uint4 q = make_uint4(0, 0, 0, 0);
+      if (j < n) q = *(const uint4 *)(vals + j);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+      uint32_t keepm = 0;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t v = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
+        if (j + k < n && ((W[v >> 6] >> (v & 63)) & 1) == want) keepm |= 1u << k;
+      }
+      const uint32_t c = __popc(keepm);
+      uint32_t x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      uint32_t pos = base + x - c;
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if (keepm >> k & 1) out[pos++] = (uint16_t)((w[k >> 1] >> (16 * (k & 1))) & 0xFFFF);
+      base += __shfl_sync(0xffffffffu, x, 31);
+    }
+    const uint32_t padded = (uint32_t)(rs_pad16(2ull * base) >> 1);
+    for (uint32_t k = base + lane; k < padded; k += 32) out[k] = 0;
+    if (lane == 0) {
+      O.type[e] = RS_TAG_ARRAY;
+      O.card[e] = base;
+      O.n[e] = base;
+      if (base) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)base);
+    }
+    __syncwarp();  // W is rebuilt for the next pair
+  }
+}
+
+// |array AND {bitset, runs}| for the counts: the same probes, counted
+__global__ void __launch_bounds__(32 * PRB_WARPS) k_probe_count(const uint32_t *__restrict__ lca,
+                                                                const uint32_t *__restrict__ lcb,
+                                                                const uint32_t *__restrict__ lpair,
+                                                                const uint32_t *__restrict__ cnt, DevBatch A,
+                                                                DevBatch B, uint64_t *__restrict__ acc) {
+  __shared__ __align__(16) uint64_t Xs[PRB_WARPS][RS_WORDS];
+  const int lane = threadIdx.x & 31;
+  uint64_t *W = Xs[threadIdx.x >> 5];
+  const uint32_t total = *cnt, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nw) {
+    const uint32_t ca = lca[i], cb = lcb[i];
+    const bool from_a = A.type[ca] == RS_TAG_ARRAY;
+    const DevBatch &V = from_a ? A : B, &X = from_a ? B : A;
+    const uint32_t cv = from_a ? ca : cb, cx = from_a ? cb : ca;
+    const uint16_t *vals = (const uint16_t *)(V.pool + V.off[cv]);
+    const uint32_t n = V.n[cv];
+    warp_load_member_set(W, X.type[cx], X.pool + X.off[cx], X.n[cx], lane);
+    uint32_t c = 0;
+    for (uint32_t j = 8 * lane; j < n; j += 256) {
+      const uint4 q = *(const uint4 *)(vals + j);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t v = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
+        c += j + k < n ? (uint32_t)((W[v >> 6] >> (v & 63)) & 1) : 0u;
+      }
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0 && c) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)c);
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------- array x array (merge path)
 
 // Materialized array x array pairs: one group of GT threads per pair
@@ -738,7 +877,7 @@ __global__ void k_match(uint64_t Ma, uint64_t npairs, const uint64_t *__restrict
       ca = (uint32_t)(a0 + l);
       cb = (uint32_t)(b0 + j);
       p32 = (uint32_t)p;
-      cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
+      cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], RS_OP_AND);
     }
   }
   count_append(L, cls, active, ca, cb, p32, lcb_base, lpair_base, A, B);
@@ -778,7 +917,7 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
     E.cb[p] = cb;
     E.pair[p] = (uint32_t)p;
     ub[p] = rs_pad16(rs_result_ub(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op));
-    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
+    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
     if (tma_class(cls)) {
       ao = A.off[ca];
       bo = B.off[cb];
@@ -799,7 +938,7 @@ __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint3
   if (active) {
     ca = (uint32_t)A.bm_start[pair_a(ia, p)];
     cb = (uint32_t)B.bm_start[pair_a(ib, p)];
-    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb]);
+    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], RS_OP_AND);
   }
   count_append(L, cls, active, ca, cb, (uint32_t)p, lcb_base, lpair_base, A, B);
 }
@@ -932,14 +1071,20 @@ bool pair_bases_host(const rs_batch *A, const rs_batch *B, const uint32_t *ia, c
 // Which work classes can occur between batches with these container-type
 // masks (bit t = type t present)?  Impossible classes are never launched.
 struct ClassMask {
-  bool bb, aa, gen;
+  bool bb, aa, gen, prb;
 };
-ClassMask class_mask(uint8_t ma, uint8_t mb) {
+// which type-pair classes can occur (op: the materialized op, or AND for counts)
+ClassMask class_mask(uint8_t ma, uint8_t mb, int op) {
   const uint8_t AR = 1 << RS_TAG_ARRAY, BS = 1 << RS_TAG_BITSET, RN = 1 << RS_TAG_RUN;
   ClassMask m;
   m.bb = (ma & BS) && (mb & BS);
   m.aa = (ma & AR) && (mb & AR);
-  m.gen = ((ma | mb) & RN) || ((ma & AR) && (mb & BS)) || ((ma & BS) && (mb & AR));
+  const bool a_x = (ma & AR) && (mb & (BS | RN)), x_a = (ma & (BS | RN)) && (mb & AR);
+  m.prb = op == RS_OP_AND ? (a_x || x_a) : op == RS_OP_ANDNOT ? a_x : false;
+  const bool gen_all = ((ma | mb) & RN) || a_x || x_a;
+  m.gen = op == RS_OP_AND ? (ma & (BS | RN)) && (mb & (BS | RN)) && ((ma | mb) & RN)
+        : op == RS_OP_ANDNOT ? x_a || ((ma & (BS | RN)) && (mb & (BS | RN)) && ((ma | mb) & RN))
+        : gen_all;
   return m;
 }
 
@@ -980,7 +1125,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   b->type_mask = result_mask(A->type_mask, B->type_mask);
   RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
   DevBatch dA = A->dev(), dB = B->dev();
-  const ClassMask cm = class_mask(A->type_mask, B->type_mask);
+  const ClassMask cm = class_mask(A->type_mask, B->type_mask, op);
   const unsigned sms = sm_count();
   auto want = [&](int c, bool possible) -> uint64_t {  // 0 = skip, else capacity for the grid
     if (hcnt) return hcnt[c];
@@ -1020,6 +1165,10 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   if (uint64_t n = want(CLS_GEN, cm.gen))
     RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 8), DT, 0, op,
                    L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  if (uint64_t n = want(CLS_PRB, cm.prb))
+    RS_LAUNCH_PROF("probe_pair", hcnt ? n : 0, k_probe, std::min<uint64_t>(grid_for(n, PRB_WARPS), sms * 12),
+                   32 * PRB_WARPS, 0, op,
+                   L.list[CLS_PRB], L.cnt + CLS_PRB, dA, dB, En, O, b->d_pool, b->d_bm_card);
   // compaction: drop empty results (bitmap.py:185-188)
   RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, dE, O.card, keep2);
   RS_TRY(scan_exclusive<uint32_t>(keep2, fpos, E + 1));
@@ -1131,7 +1280,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
-  RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L);
+  RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L, op);
   if (ub_mode)
     return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr, epos + M,
                                    mbase, epos, npairs, out);
@@ -1193,7 +1342,7 @@ namespace {
 int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, uint32_t *lcb, uint32_t *lpair,
                   uint64_t *inter) {
   DevBatch dA = A->dev(), dB = B->dev();
-  const ClassMask cm = class_mask(A->type_mask, B->type_mask);
+  const ClassMask cm = class_mask(A->type_mask, B->type_mask, RS_OP_AND);
   const unsigned pg = sm_count() * 8;
   if (cm.bb) {
     if (bb_kernel_choice() == 0) {
@@ -1223,6 +1372,10 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
   if (cm.gen)
     RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN],
                    lcb + CLS_GEN * L.cap, lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
+  if (cm.prb)
+    RS_LAUNCH_PROF("probe_count", 0, k_probe_count, sm_count() * 12, 32 * PRB_WARPS, 0, L.list[CLS_PRB],
+                   lcb + CLS_PRB * L.cap,
+                   lpair + CLS_PRB * L.cap, L.cnt + CLS_PRB, dA, dB, inter);
   return RS_OK;
 }
 }  // namespace

@@ -8,7 +8,7 @@ from paper_1709_07821_b200 import _lib, synth
 buf, offs = synth.config4(nbitmaps=200)
 Bt = rb.BitmapBatch.from_wire((buf, offs))
 ia, ib = np.arange(199), np.arange(1, 200)
-names = ["bitset_pair", "array_pair_s", "array_pair_m", "array_pair_l", "generic_pair", "copy", "union_fold"]
+names = ["bitset_pair", "array_pair_s", "array_pair_m", "array_pair_l", "generic_pair", "probe_pair", "copy", "union_fold"]
 for op in ("and", "or", "xor", "andnot"):
     Bt.pairwise(op, Bt, ia, ib); _lib.synchronize()
     _lib.profile_reset(); _lib.profile(True)
