@@ -108,6 +108,17 @@ void prof_mark(const char *name, cudaEvent_t a, cudaEvent_t b, uint64_t items);
 cudaEvent_t prof_event();
 int h2d(void *d, const void *h, size_t bytes);   // async on g_stream
 int h2d_small(void *d, const void *h, size_t bytes);  // small upload (see rs_runtime.cu)
+// Fork/join of independent launches onto side streams: begin(n) forks n
+// streams off the library stream, next() points g_stream at the next one (no
+// allocation may happen until end()), end() joins them back and restores it.
+struct Fork {
+  cudaStream_t saved = nullptr;
+  int n = 0, used = 0;
+  int begin(int nside);
+  void next();
+  int end();
+  ~Fork() { end(); }  // an early error return still joins and restores the stream
+};
 }  // namespace rs
 
 #define RS_CK(x)                                                                   \

@@ -1131,13 +1131,23 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     if (hcnt) return hcnt[c];
     return possible ? L.cap : 0;
   };
+  // the class kernels are independent (disjoint lists and output slots): with
+  // more than one of them they run concurrently on side streams
+  const uint64_t n_copy = want(CLS_COPY, op != RS_OP_AND), n_bb = want(CLS_BB, cm.bb),
+                 n_aas = want(CLS_AAS, cm.aa), n_aam = want(CLS_AAM, cm.aa && aa_medium_possible()),
+                 n_aal = want(CLS_AAL, cm.aa), n_gen = want(CLS_GEN, cm.gen), n_prb = want(CLS_PRB, cm.prb);
+  const int nk = (n_copy > 0) + (n_bb > 0) + (n_aas > 0) + (n_aam > 0) + (n_aal > 0) + (n_gen > 0) + (n_prb > 0);
+  Fork F;  // (tiny ops are host-bound: the fork's event calls would cost more than they overlap)
+  if (nk > 1 && E >= 16384) RS_TRY(F.begin(nk));
   // copies: persistent warps over the list (8 warps per CTA)
-  if (uint64_t n = want(CLS_COPY, op != RS_OP_AND)) {
+  if (uint64_t n = n_copy) {
+    F.next();
     unsigned g = std::min<uint64_t>(grid_for(n, 8), sms * 16);
     RS_LAUNCH_PROF("copy", hcnt ? n : 0, k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O,
                    b->d_pool, b->d_bm_card);
   }
-  if (uint64_t n = want(CLS_BB, cm.bb)) {
+  if (uint64_t n = n_bb) {
+    F.next();
     if (bb_kernel_choice() == 0) {
       RS_LAUNCH_PROF("bitset_pair", hcnt ? n : 0, k_pair_dense<false>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
                      L.list[CLS_BB], L.cnt + CLS_BB, dA, dB, En, O, b->d_pool, b->d_bm_card);
@@ -1149,26 +1159,36 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
       }
     }
   }
-  if (uint64_t n = want(CLS_AAS, cm.aa))
+  if (uint64_t n = n_aas) {
+    F.next();
     RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
                    0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  if (uint64_t n = want(CLS_AAM, cm.aa && aa_medium_possible()))
+  }
+  if (uint64_t n = n_aam) {
+    F.next();
     RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
                    256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  if (uint64_t n = want(CLS_AAL, cm.aa)) {
+  }
+  if (uint64_t n = n_aal) {
+    F.next();
     if (env_int("RS_AA_LARGE_MERGE", 0))
       RS_LAUNCH_PROF("array_pair_l", hcnt ? n : 0, (k_aa_pair<256, 32>), std::min<uint64_t>(n, sms * 8), 256, 0, op,
                      L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
     else
       RS_TRY(launch_aa_large_op(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card, hcnt != nullptr));
   }
-  if (uint64_t n = want(CLS_GEN, cm.gen))
+  if (uint64_t n = n_gen) {
+    F.next();
     RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 8), DT, 0, op,
                    L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, b->d_bm_card);
-  if (uint64_t n = want(CLS_PRB, cm.prb))
+  }
+  if (uint64_t n = n_prb) {
+    F.next();
     RS_LAUNCH_PROF("probe_pair", hcnt ? n : 0, k_probe, std::min<uint64_t>(grid_for(n, PRB_WARPS), sms * 12),
                    32 * PRB_WARPS, 0, op,
                    L.list[CLS_PRB], L.cnt + CLS_PRB, dA, dB, En, O, b->d_pool, b->d_bm_card);
+  }
+  RS_TRY(F.end());
   // compaction: drop empty results (bitmap.py:185-188)
   RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, dE, O.card, keep2);
   RS_TRY(scan_exclusive<uint32_t>(keep2, fpos, E + 1));
@@ -1344,7 +1364,11 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
   DevBatch dA = A->dev(), dB = B->dev();
   const ClassMask cm = class_mask(A->type_mask, B->type_mask, RS_OP_AND);
   const unsigned pg = sm_count() * 8;
+  const int nk = cm.bb + cm.aa + cm.gen + cm.prb;  // independent: concurrent on side streams
+  Fork F;
+  if (nk > 1 && L.cap >= 16384) RS_TRY(F.begin(nk));
   if (cm.bb) {
+    F.next();
     if (bb_kernel_choice() == 0) {
       RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB],
                      lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap, L.cnt + CLS_BB, dA, dB, inter);
@@ -1358,6 +1382,7 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
     }
   }
   if (cm.aa) {
+    F.next();
     RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
                    lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
     if (aa_medium_possible())
@@ -1369,14 +1394,18 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
     else
       RS_TRY(launch_aa_large_count(L, lpair + CLS_AAL * L.cap, dA, dB, inter));
   }
-  if (cm.gen)
+  if (cm.gen) {
+    F.next();
     RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN],
                    lcb + CLS_GEN * L.cap, lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
-  if (cm.prb)
+  }
+  if (cm.prb) {
+    F.next();
     RS_LAUNCH_PROF("probe_count", 0, k_probe_count, sm_count() * 12, 32 * PRB_WARPS, 0, L.list[CLS_PRB],
                    lcb + CLS_PRB * L.cap,
                    lpair + CLS_PRB * L.cap, L.cnt + CLS_PRB, dA, dB, inter);
-  return RS_OK;
+  }
+  return F.end();
 }
 }  // namespace
 

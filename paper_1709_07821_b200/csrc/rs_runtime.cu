@@ -156,6 +156,56 @@ int h2d(void *d, const void *h, size_t bytes) {
   return RS_OK;
 }
 
+// Fork/join of independent launches (the per-type-pair class kernels of one
+// op): side streams wait on an event recorded on the library stream, the
+// library stream waits on an event recorded on every side stream used.
+namespace {
+std::vector<cudaStream_t> g_side;
+std::vector<cudaEvent_t> g_side_ev;
+cudaEvent_t g_fork_ev = nullptr;
+int g_side_dev = -1;
+}  // namespace
+
+int Fork::begin(int nside) {
+  int dev = 0;
+  RS_CK(cudaGetDevice(&dev));
+  if (g_side_dev != dev) {  // streams and events belong to a device
+    g_side.clear();
+    g_side_ev.clear();
+    RS_CK(cudaEventCreateWithFlags(&g_fork_ev, cudaEventDisableTiming));
+    g_side_dev = dev;
+  }
+  while ((int)g_side.size() < nside) {
+    cudaStream_t st;
+    cudaEvent_t ev;
+    RS_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    RS_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    g_side.push_back(st);
+    g_side_ev.push_back(ev);
+  }
+  saved = g_stream;
+  n = nside;
+  used = 0;
+  RS_CK(cudaEventRecord(g_fork_ev, saved));
+  for (int i = 0; i < n; i++) RS_CK(cudaStreamWaitEvent(g_side[i], g_fork_ev, 0));
+  return RS_OK;
+}
+
+void Fork::next() {
+  if (n && used < n) g_stream = g_side[used++];
+}
+
+int Fork::end() {
+  if (!n) return RS_OK;
+  g_stream = saved;
+  for (int i = 0; i < used; i++) {
+    RS_CK(cudaEventRecord(g_side_ev[i], g_side[i]));
+    RS_CK(cudaStreamWaitEvent(saved, g_side_ev[i], 0));
+  }
+  n = 0;
+  return RS_OK;
+}
+
 // An op's small host->device upload (a few KB): a plain cudaMemcpyAsync from
 // pageable memory, which the driver stages through the command stream itself.
 // Measured on the pipelined e2e path (bulk ingest saturating PCIe on the copy
