@@ -142,6 +142,50 @@ __device__ __forceinline__ uint32_t upper_bound16(const uint16_t *__restrict__ k
 // t owns one key of one side of one pair.  A keys land at i + #(B < key), B
 // keys at j + #(A <= key), so a matched B key sits right after its A partner
 // and is marked as a duplicate.  keep/ub are written at the merged position.
+// One merged position t of pair p (local index l): A's key l, or B's key
+// l - na; keys come from kA / kB (global memory or a CTA's smem copy).
+__device__ __forceinline__ void merge_position(uint64_t base, uint32_t l, uint32_t p, uint64_t a0, uint64_t b0,
+                                               uint32_t na, uint32_t nb, const uint16_t *kA, const uint16_t *kB,
+                                               const DevBatch &A, const DevBatch &B, int op, uint16_t *mkey,
+                                               uint32_t *mca, uint32_t *mcb, uint32_t *mpair, uint32_t *keep,
+                                               uint64_t *ub) {
+  const bool keep_a = op != RS_OP_AND;                        // _KEEP_A, bitmap.py:21
+  const bool keep_b = op == RS_OP_OR || op == RS_OP_XOR;      // _KEEP_B, bitmap.py:22
+  if (l < na) {
+    uint16_t key = kA[l];
+    uint32_t j = lower_bound16(kB, nb, key);
+    bool matched = j < nb && kB[j] == key;
+    uint64_t pos = base + l + j;
+    uint64_t ca = a0 + l;
+    mkey[pos] = key;
+    mca[pos] = (uint32_t)ca;
+    mcb[pos] = matched ? (uint32_t)(b0 + j) : RS_NONE;
+    mpair[pos] = p;
+    bool k = matched || keep_a;
+    keep[pos] = k;
+    uint32_t u = 0;
+    if (matched) u = rs_result_ub(A.type[ca], A.card[ca], B.type[b0 + j], B.card[b0 + j], op);
+    else if (k) u = rs_payload_bytes(A.type[ca], A.n[ca]);
+    ub[pos] = rs_pad16(u);
+  } else {
+    uint32_t j = l - na;
+    uint16_t key = kB[j];
+    uint32_t i = upper_bound16(kA, na, key);
+    bool matched = i > 0 && kA[i - 1] == key;
+    uint64_t pos = base + i + j;
+    bool k = !matched && keep_b;
+    keep[pos] = k;
+    ub[pos] = k ? rs_pad16(rs_payload_bytes(B.type[b0 + j], B.n[b0 + j])) : 0;
+    if (k) {
+      mkey[pos] = key;
+      mca[pos] = RS_NONE;
+      mcb[pos] = (uint32_t)(b0 + j);
+      mpair[pos] = p;
+    }
+  }
+}
+
+// thread per merged position, keys searched in global memory (any sizes)
 __global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict__ mbase, DevBatch A, DevBatch B,
                         const uint32_t *ia, const uint32_t *ib, int op, uint16_t *__restrict__ mkey,
                         uint32_t *__restrict__ mca, uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
@@ -152,45 +196,38 @@ __global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict_
     ub[M] = 0;
   }
   if (t >= M) return;
-  const bool keep_a = op != RS_OP_AND;                        // _KEEP_A, bitmap.py:21
-  const bool keep_b = op == RS_OP_OR || op == RS_OP_XOR;      // _KEEP_B, bitmap.py:22
   uint64_t p = find_pair(mbase, npairs, t);
   uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
   uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
   uint32_t na = (uint32_t)(A.bm_start[a + 1] - a0), nb = (uint32_t)(B.bm_start[b + 1] - b0);
-  uint32_t l = (uint32_t)(t - mbase[p]);
-  if (l < na) {
-    uint16_t key = A.key[a0 + l];
-    uint32_t j = lower_bound16(B.key + b0, nb, key);
-    bool matched = j < nb && B.key[b0 + j] == key;
-    uint64_t pos = mbase[p] + l + j;
-    uint64_t ca = a0 + l;
-    mkey[pos] = key;
-    mca[pos] = (uint32_t)ca;
-    mcb[pos] = matched ? (uint32_t)(b0 + j) : RS_NONE;
-    mpair[pos] = (uint32_t)p;
-    bool k = matched || keep_a;
-    keep[pos] = k;
-    uint32_t u = 0;
-    if (matched) u = rs_result_ub(A.type[ca], A.card[ca], B.type[b0 + j], B.card[b0 + j], op);
-    else if (k) u = rs_payload_bytes(A.type[ca], A.n[ca]);
-    ub[pos] = rs_pad16(u);
-  } else {
-    uint32_t j = l - na;
-    uint16_t key = B.key[b0 + j];
-    uint32_t i = upper_bound16(A.key + a0, na, key);
-    bool matched = i > 0 && A.key[a0 + i - 1] == key;
-    uint64_t pos = mbase[p] + i + j;
-    bool k = !matched && keep_b;
-    keep[pos] = k;
-    ub[pos] = k ? rs_pad16(rs_payload_bytes(B.type[b0 + j], B.n[b0 + j])) : 0;
-    if (k) {
-      mkey[pos] = key;
-      mca[pos] = RS_NONE;
-      mcb[pos] = (uint32_t)(b0 + j);
-      mpair[pos] = (uint32_t)p;
-    }
+  merge_position(mbase[p], (uint32_t)(t - mbase[p]), (uint32_t)p, a0, b0, na, nb, A.key + a0, B.key + b0, A, B, op,
+                 mkey, mca, mcb, mpair, keep, ub);
+}
+
+// CTA per pair when every bitmap has at most MERGE_SMEM_KEYS containers: both
+// key lists staged in shared memory, so the binary searches of the join hit
+// smem instead of chaining global loads (and no search for the pair index)
+constexpr uint32_t MERGE_SMEM_KEYS = 2048;
+__global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, const uint64_t *__restrict__ mbase, DevBatch A,
+                                                    DevBatch B, const uint32_t *ia, const uint32_t *ib, int op,
+                                                    uint16_t *__restrict__ mkey, uint32_t *__restrict__ mca,
+                                                    uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
+                                                    uint32_t *__restrict__ keep, uint64_t *__restrict__ ub) {
+  __shared__ uint16_t kA[MERGE_SMEM_KEYS], kB[MERGE_SMEM_KEYS];
+  const uint32_t p = blockIdx.x;
+  if (p == 0 && threadIdx.x == 0) {
+    keep[M] = 0;
+    ub[M] = 0;
   }
+  const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+  const uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
+  const uint32_t na = (uint32_t)(A.bm_start[a + 1] - a0), nb = (uint32_t)(B.bm_start[b + 1] - b0);
+  for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) kA[i] = A.key[a0 + i];
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) kB[i] = B.key[b0 + i];
+  __syncthreads();
+  const uint64_t base = mbase[p];
+  for (uint32_t l = threadIdx.x; l < na + nb; l += blockDim.x)
+    merge_position(base, l, p, a0, b0, na, nb, kA, kB, A, B, op, mkey, mca, mcb, mpair, keep, ub);
 }
 
 __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ epos,
@@ -883,6 +920,38 @@ __global__ void k_match(uint64_t Ma, uint64_t npairs, const uint64_t *__restrict
   count_append(L, cls, active, ca, cb, p32, lcb_base, lpair_base, A, B);
 }
 
+// CTA per pair with B's keys in shared memory (every bitmap at most
+// MERGE_SMEM_KEYS containers); the warp-aggregated list appends need whole
+// warps, so each warp walks A's keys in steps of 32
+__global__ void __launch_bounds__(256) k_match_pair(const uint64_t *__restrict__ mbase, DevBatch A, DevBatch B,
+                                                    const uint32_t *ia, const uint32_t *ib, Lists L,
+                                                    uint32_t *__restrict__ lcb_base, uint32_t *__restrict__ lpair_base) {
+  __shared__ uint16_t kB[MERGE_SMEM_KEYS];
+  const uint32_t p = blockIdx.x;
+  const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+  const uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
+  const uint32_t na = (uint32_t)(A.bm_start[a + 1] - a0), nb = (uint32_t)(B.bm_start[b + 1] - b0);
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) kB[i] = B.key[b0 + i];
+  __syncthreads();
+  for (uint32_t l0 = threadIdx.x & ~31u; l0 < na; l0 += blockDim.x) {
+    const uint32_t l = l0 + (threadIdx.x & 31);
+    bool active = false;
+    int cls = CLS_GEN;
+    uint32_t ca = 0, cb = 0;
+    if (l < na) {
+      const uint16_t key = A.key[a0 + l];
+      const uint32_t j = lower_bound16(kB, nb, key);
+      if (j < nb && kB[j] == key) {
+        active = true;
+        ca = (uint32_t)(a0 + l);
+        cb = (uint32_t)(b0 + j);
+        cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], RS_OP_AND);
+      }
+    }
+    count_append(L, cls, active, ca, cb, p, lcb_base, lpair_base, A, B);
+  }
+}
+
 // bitmap.py:235-241: every count from |A ∩ B|
 __global__ void k_formula(uint64_t npairs, int op, const uint64_t *__restrict__ cardA, const uint64_t *__restrict__ cardB,
                           const uint32_t *ia, const uint32_t *ib, const uint64_t *__restrict__ inter,
@@ -1255,12 +1324,13 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_TRY(fetch_host_meta(B));
   RS_TRY(check_pairs(A, B, ia, ib, npairs));
   Scratch S;
-  uint64_t M = 0, Ecap = 0;
+  uint64_t M = 0, Ecap = 0, maxk = 0;
   for (uint64_t p = 0; p < npairs; p++) {
     uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
     uint64_t na = A->h_bm_start[a + 1] - A->h_bm_start[a], nb = B->h_bm_start[b + 1] - B->h_bm_start[b];
     M += na + nb;
     Ecap += op == RS_OP_AND ? std::min(na, nb) : op == RS_OP_ANDNOT ? na : na + nb;
+    maxk = std::max(maxk, std::max(na, nb));
   }
   // Upper-bound mode (no host sync) when an 8 KB slot per possible output
   // container costs at most ~2x the inputs' pools; else size exactly.
@@ -1297,7 +1367,11 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
     RS_CK(cudaMemsetAsync(keep, 0, 4, g_stream));
     RS_CK(cudaMemsetAsync(ub, 0, 8, g_stream));
   }
-  RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
+  if (M && maxk <= MERGE_SMEM_KEYS)
+    RS_LAUNCH(k_merge_pair, (unsigned)npairs, 256, 0, M, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
+  else
+    RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep,
+              ub);
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
   RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L, op);
@@ -1421,10 +1495,12 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   }
   RS_TRY(check_pairs(A, B, ia, ib, npairs));
   Scratch S;
-  uint64_t Ma = 0;
+  uint64_t Ma = 0, maxk = 0;
   for (uint64_t p = 0; p < npairs; p++) {
-    uint32_t a = ia ? ia[p] : (uint32_t)p;
-    Ma += A->h_bm_start[a + 1] - A->h_bm_start[a];
+    uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
+    const uint64_t na = A->h_bm_start[a + 1] - A->h_bm_start[a];
+    Ma += na;
+    maxk = std::max(maxk, std::max(na, B->h_bm_start[b + 1] - B->h_bm_start[b]));
   }
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
@@ -1448,7 +1524,10 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   DevBatch dA = A->dev(), dB = B->dev();
   if (hbases) mbase = U.at<uint64_t>(o_mb);
   else RS_TRY(pair_bases_device(npairs, dA, dB, dia, dib, 1, msz, mbase));
-  RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
+  if (Ma && maxk <= MERGE_SMEM_KEYS)
+    RS_LAUNCH(k_match_pair, (unsigned)npairs, 256, 0, mbase, dA, dB, dia, dib, L, lcb, lpair);
+  else
+    RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
   RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
   RS_LAUNCH(k_formula, grid_for(npairs, 256), 256, 0, npairs, op, A->d_bm_card, B->d_bm_card, dia, dib, inter, dout);
   if (!counts_on_device) RS_TRY(d2h(counts, dout, npairs * 8));
