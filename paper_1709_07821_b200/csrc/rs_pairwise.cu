@@ -528,12 +528,22 @@ int bb_stages() {
   return s;
 }
 
+inline int env_int_(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
 template <typename K>
 unsigned persistent_grid(K kernel, size_t smem, uint64_t count) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, rsb::BT, smem);
+  // 4 CTAs per SM (of the 5 that fit) measured best for both bitset kernels:
+  // C2 step 7.18 -> 6.96 ms, op kernel 5.95 -> 6.21 TB/s, count 6.99 -> 7.08
+  // TB/s -- fewer concurrent 8 KB streams per SM; RS_BB_CTAS overrides
+  static int cap = -1;
+  if (cap < 0) cap = env_int_("RS_BB_CTAS", 4);
+  if (cap > 0 && cap < per) per = cap;
   uint64_t g = (uint64_t)sms * (per > 0 ? per : 1);
   return (unsigned)(count < g ? count : g);
 }
