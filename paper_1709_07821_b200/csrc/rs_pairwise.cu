@@ -642,6 +642,8 @@ unsigned persistent_grid_t(K kernel, int threads, size_t smem, uint64_t count) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  static const int cap = env_int_("RS_AAL_CTAS", 0);  // CTAs per SM cap (tuning)
+  if (cap > 0 && cap < per) per = cap;
   uint64_t g = (uint64_t)sms * (per > 0 ? per : 1);
   return (unsigned)(count < g ? count : g);
 }
@@ -1217,11 +1219,13 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
                  n_aal = want(CLS_AAL, cm.aa), n_gen = want(CLS_GEN, cm.gen), n_prb = want(CLS_PRB, cm.prb);
   const int nk = (n_copy > 0) + (n_bb > 0) + (n_aas > 0) + (n_aam > 0) + (n_aal > 0) + (n_gen > 0) + (n_prb > 0);
   Fork F;  // (tiny ops are host-bound: the fork's event calls would cost more than they overlap)
-  if (nk > 1 && E >= 16384) RS_TRY(F.begin(nk));
+  static const int nofork = env_int_("RS_NO_FORK", 0);
+  if (nk > 1 && E >= 16384 && !nofork) RS_TRY(F.begin(nk));
   // copies: persistent warps over the list (8 warps per CTA)
   if (uint64_t n = n_copy) {
     F.next();
-    unsigned g = std::min<uint64_t>(grid_for(n, 8), sms * 16);
+    static const int copy_cta = env_int_("RS_COPY_CTAS", 16);  // CTAs per SM (tuning)
+    unsigned g = std::min<uint64_t>(grid_for(n, 8), sms * copy_cta);
     RS_LAUNCH_PROF("copy", hcnt ? n : 0, k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O,
                    b->d_pool, b->d_bm_card);
   }
