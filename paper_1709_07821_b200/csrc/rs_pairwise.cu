@@ -533,16 +533,18 @@ inline int env_int_(const char *name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 template <typename K>
-unsigned persistent_grid(K kernel, size_t smem, uint64_t count) {
+unsigned persistent_grid(K kernel, size_t smem, uint64_t count, int want_per_sm = 4) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, rsb::BT, smem);
-  // 4 CTAs per SM (of the 5 that fit) measured best for both bitset kernels:
-  // C2 step 7.18 -> 6.96 ms, op kernel 5.95 -> 6.21 TB/s, count 6.99 -> 7.08
-  // TB/s -- fewer concurrent 8 KB streams per SM; RS_BB_CTAS overrides
-  static int cap = -1;
-  if (cap < 0) cap = env_int_("RS_BB_CTAS", 4);
+  // 4 CTAs per SM (of the 5 that fit) measured best for the streaming bitset
+  // kernels (OR/ANDNOT/XOR and the counts: C2 step 7.18 -> 6.96 ms, op kernel
+  // 5.95 -> 6.21 TB/s, count 6.99 -> 7.08 TB/s -- fewer concurrent 8 KB
+  // streams per SM); AND, whose array extraction is instruction-heavy, keeps
+  // 5.  RS_BB_CTAS overrides both.
+  static const int env_cap = env_int_("RS_BB_CTAS", 0);
+  const int cap = env_cap > 0 ? env_cap : want_per_sm;
   if (cap > 0 && cap < per) per = cap;
   uint64_t g = (uint64_t)sms * (per > 0 ? per : 1);
   return (unsigned)(count < g ? count : g);
@@ -557,7 +559,7 @@ int launch_bb_op(int op, const Lists &L, uint64_t count, DevBatch dA, DevBatch d
     RS_CK(cudaFuncSetAttribute(k_bb_op<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  RS_LAUNCH_PROF("bitset_pair", 0, k_bb_op<S>, persistent_grid(k_bb_op<S>, smem, count), rsb::BT, smem, op,
+  RS_LAUNCH_PROF("bitset_pair", 0, k_bb_op<S>, persistent_grid(k_bb_op<S>, smem, count, op == RS_OP_AND ? 5 : 4), rsb::BT, smem, op,
                  L.list[CLS_BB], L.aoff, L.boff, L.cnt + CLS_BB, dA, dB, En, O, pool, res_card);
   return RS_OK;
 }
