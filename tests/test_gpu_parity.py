@@ -445,3 +445,27 @@ def test_random_pairs_vs_oracle(pkg):
         assert not bad, (op, bad[:5])
         cards = A.pairwise_cardinality(op, B).tolist()
         assert cards == [orc.op_cardinality(op, x, y) for x, y in zip(wa, wb)], op
+
+
+def test_maximum_key_counts(pkg):
+    """Bitmaps spanning all 65,536 chunk keys (one value per chunk, or full
+    chunks as single runs) against sparse ones: the key join's global-memory
+    path (more than 2,048 containers per bitmap), 65,536-entry results, and
+    full-chunk runs, byte for byte against the oracle."""
+    rng = np.random.default_rng(65536)
+    every_key = (np.arange(65536, dtype=np.uint64) << 16) + rng.integers(0, 65536, 65536).astype(np.uint64)
+    w_every = orc.from_values(every_key)
+    full_chunks = np.concatenate([np.arange(k << 16, (k + 1) << 16, dtype=np.uint64)
+                                  for k in rng.choice(65536, 24, replace=False)])
+    w_full = orc.run_optimize(orc.from_values(full_chunks))[0]
+    w_sparse = orc.from_values(np.unique(rng.integers(0, 1 << 32, 5000)).astype(np.uint64))
+    ws = [w_every, w_full, w_sparse]
+    A = pkg.BitmapBatch.from_wire(ws)
+    ia, ib = [0, 0, 1, 2, 1], [1, 2, 2, 0, 0]
+    for op in OPS:
+        got = A.pairwise(op, A, ia, ib).to_wire_list()
+        for k, (a, b) in enumerate(zip(ia, ib)):
+            assert got[k] == orc.op(op, ws[a], ws[b]), (op, a, b)
+        cards = A.pairwise_cardinality(op, A, ia, ib).tolist()
+        assert cards == [orc.op_cardinality(op, ws[a], ws[b]) for a, b in zip(ia, ib)], op
+    assert np.array_equal(A.to_arrays()[0], np.sort(every_key).astype(np.uint32))
