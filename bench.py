@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 OPS = ("and", "or", "andnot", "xor")
 NPAIRS = 1024
 NCHUNKS = 256
-E2E_CHUNKS = 8  # e2e pipeline depth: chunks of pairs whose transfer overlaps the previous chunk
+E2E_CHUNKS = 16  # e2e pipeline depth: chunks of pairs whose transfer overlaps the previous chunk
 METRIC = "container-pair set ops/sec (AND/OR/ANDNOT/XOR + cardinality counts)"
 UNIT = "container-pairs/s"
 NOMINAL_HBM_GBS = 8000.0
