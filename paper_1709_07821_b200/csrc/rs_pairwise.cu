@@ -733,7 +733,11 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe(int op, const uint32_t
     const uint32_t cv = from_a ? ca : cb, cx = from_a ? cb : ca;
     const uint16_t *vals = (const uint16_t *)(V.pool + V.off[cv]);
     const uint32_t n = V.n[cv];
-    warp_load_member_set(W, X.type[cx], X.pool + X.off[cx], X.n[cx], lane);
+    // a bitset is probed where it lies (independent 64-bit loads, mostly L2
+    // hits); runs are first set into the warp's smem bitset
+    const uint8_t xt = X.type[cx];
+    const uint64_t *M = xt == RS_TAG_BITSET ? (const uint64_t *)(X.pool + X.off[cx]) : W;
+    if (xt != RS_TAG_BITSET) warp_load_member_set(W, xt, X.pool + X.off[cx], X.n[cx], lane);
     const uint32_t want = op == RS_OP_AND ? 1u : 0u;
     uint16_t *out = (uint16_t *)(opool + E.off[e]);
     // lane l takes values [256c + 8l, 256c + 8l + 8) with one 16-byte load
@@ -749,7 +753,7 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe(int op, const uint32_t
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         const uint32_t v = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
-        if (j + k < n && ((W[v >> 6] >> (v & 63)) & 1) == want) keepm |= 1u << k;
+        if (j + k < n && ((M[v >> 6] >> (v & 63)) & 1) == want) keepm |= 1u << k;
       }
       const uint32_t c = __popc(keepm);
       uint32_t x = c;
@@ -793,7 +797,9 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe_count(const uint32_t *
     const uint32_t cv = from_a ? ca : cb, cx = from_a ? cb : ca;
     const uint16_t *vals = (const uint16_t *)(V.pool + V.off[cv]);
     const uint32_t n = V.n[cv];
-    warp_load_member_set(W, X.type[cx], X.pool + X.off[cx], X.n[cx], lane);
+    const uint8_t xt = X.type[cx];
+    const uint64_t *M = xt == RS_TAG_BITSET ? (const uint64_t *)(X.pool + X.off[cx]) : W;
+    if (xt != RS_TAG_BITSET) warp_load_member_set(W, xt, X.pool + X.off[cx], X.n[cx], lane);
     uint32_t c = 0;
     for (uint32_t j = 8 * lane; j < n; j += 256) {
       const uint4 q = *(const uint4 *)(vals + j);
@@ -801,7 +807,7 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe_count(const uint32_t *
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         const uint32_t v = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
-        c += j + k < n ? (uint32_t)((W[v >> 6] >> (v & 63)) & 1) : 0u;
+        c += j + k < n ? (uint32_t)((M[v >> 6] >> (v & 63)) & 1) : 0u;
       }
     }
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
