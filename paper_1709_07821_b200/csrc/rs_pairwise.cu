@@ -208,16 +208,20 @@ __global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict_
 // key lists staged in shared memory, so the binary searches of the join hit
 // smem instead of chaining global loads (and no search for the pair index)
 constexpr uint32_t MERGE_SMEM_KEYS = 2048;
-__global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, const uint64_t *__restrict__ mbase, DevBatch A,
-                                                    DevBatch B, const uint32_t *ia, const uint32_t *ib, int op,
-                                                    uint16_t *__restrict__ mkey, uint32_t *__restrict__ mca,
+__global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, uint64_t npairs, const uint64_t *__restrict__ mbase,
+                                                    DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib,
+                                                    int op, uint16_t *__restrict__ mkey, uint32_t *__restrict__ mca,
                                                     uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
-                                                    uint32_t *__restrict__ keep, uint64_t *__restrict__ ub) {
+                                                    uint32_t *__restrict__ keep, uint64_t *__restrict__ ub,
+                                                    uint32_t *__restrict__ pk, uint64_t *__restrict__ pu) {
   __shared__ uint16_t kA[MERGE_SMEM_KEYS], kB[MERGE_SMEM_KEYS];
+  __shared__ uint64_t red[8];
   const uint32_t p = blockIdx.x;
   if (p == 0 && threadIdx.x == 0) {
     keep[M] = 0;
     ub[M] = 0;
+    pk[npairs] = 0;  // sentinels of the scans over pairs
+    pu[npairs] = 0;
   }
   const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
   const uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
@@ -228,25 +232,38 @@ __global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, const uint64_t *
   const uint64_t base = mbase[p];
   for (uint32_t l = threadIdx.x; l < na + nb; l += blockDim.x)
     merge_position(base, l, p, a0, b0, na, nb, kA, kB, A, B, op, mkey, mca, mcb, mpair, keep, ub);
+  // per-pair totals of keep and ub (packed: keep count << 40 | ub bytes)
+  __syncthreads();
+  uint64_t v = 0;
+  for (uint32_t l = threadIdx.x; l < na + nb; l += blockDim.x) v += ((uint64_t)keep[base + l] << 40) + ub[base + l];
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+    for (int w = 0; w < 8; w++) s += red[w];
+    pk[p] = (uint32_t)(s >> 40);
+    pu[p] = s & ((1ull << 40) - 1);
+  }
 }
 
-__global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ epos,
-                       const uint64_t *__restrict__ uoff, const uint16_t *__restrict__ mkey,
-                       const uint32_t *__restrict__ mca, const uint32_t *__restrict__ mcb,
-                       const uint32_t *__restrict__ mpair, DevBatch A, DevBatch B, Entries E, Lists L, int op) {
-  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  bool active = t < M && keep[t];
+// One kept merged position becomes entry e with result slot `off`: the
+// entry record and its per-type-pair work list (whole warps must call this:
+// list_append aggregates with ballots).
+__device__ __forceinline__ void emit_entry(bool active, uint32_t e, uint64_t off, uint64_t t,
+                                           const uint16_t *__restrict__ mkey, const uint32_t *__restrict__ mca,
+                                           const uint32_t *__restrict__ mcb, const uint32_t *__restrict__ mpair,
+                                           const DevBatch &A, const DevBatch &B, Entries E, Lists L, int op) {
   int cls = CLS_COPY;
-  uint32_t e = 0, nab = 0;
+  uint32_t nab = 0;
   uint64_t ao = 0, bo = 0;
   if (active) {
-    e = epos[t];
     uint32_t ca = mca[t], cb = mcb[t];
     E.key[e] = mkey[t];
     E.ca[e] = ca;
     E.cb[e] = cb;
     E.pair[e] = mpair[t];
-    E.off[e] = uoff[t];
+    E.off[e] = off;
     cls = (ca == RS_NONE || cb == RS_NONE) ? CLS_COPY : classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
     if (tma_class(cls)) {
       ao = A.off[ca];
@@ -255,6 +272,46 @@ __global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint
     }
   }
   list_append(L, cls, active, e, ao, bo, nab);
+}
+
+__global__ void k_emit(uint64_t M, const uint32_t *__restrict__ keep, const uint32_t *__restrict__ epos,
+                       const uint64_t *__restrict__ uoff, const uint16_t *__restrict__ mkey,
+                       const uint32_t *__restrict__ mca, const uint32_t *__restrict__ mcb,
+                       const uint32_t *__restrict__ mpair, DevBatch A, DevBatch B, Entries E, Lists L, int op) {
+  uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const bool active = t < M && keep[t];
+  emit_entry(active, active ? epos[t] : 0, active ? uoff[t] : 0, t, mkey, mca, mcb, mpair, A, B, E, L, op);
+}
+
+// CTA per pair (the per-pair join path): entry indices and result slots from
+// the pair's bases (a scan over pairs) plus a block scan of the pair's own
+// positions -- no scan over every merged position.  keep (<= 256 per tile)
+// and ub (< 2^23 per tile) share one packed 64-bit block scan.
+__global__ void __launch_bounds__(256) k_emit_pair(const uint64_t *__restrict__ mbase, const uint32_t *__restrict__ keep,
+                                                   const uint64_t *__restrict__ ub, const uint32_t *__restrict__ pke,
+                                                   const uint64_t *__restrict__ pue, const uint16_t *__restrict__ mkey,
+                                                   const uint32_t *__restrict__ mca, const uint32_t *__restrict__ mcb,
+                                                   const uint32_t *__restrict__ mpair, DevBatch A, DevBatch B, Entries E,
+                                                   Lists L, int op) {
+  using BS = cub::BlockScan<uint64_t, 256>;
+  __shared__ typename BS::TempStorage ts;
+  const uint32_t p = blockIdx.x;
+  const uint64_t base = mbase[p], end = mbase[p + 1];
+  uint32_t ck = pke[p];
+  uint64_t cu = pue[p];
+  for (uint64_t t0 = base; t0 < end; t0 += blockDim.x) {
+    const uint64_t t = t0 + threadIdx.x;
+    const bool in = t < end;
+    const uint32_t k = in ? keep[t] : 0;
+    const uint64_t v = in ? (((uint64_t)k << 32) | ub[t]) : 0;
+    uint64_t ex, tot;
+    BS(ts).ExclusiveSum(v, ex, tot);
+    emit_entry(in && k, ck + (uint32_t)(ex >> 32), cu + (ex & 0xFFFFFFFFull), t, mkey, mca, mcb, mpair, A, B, E, L,
+               op);
+    ck += (uint32_t)(tot >> 32);
+    cu += tot & 0xFFFFFFFFull;
+    __syncthreads();  // ts reuse
+  }
 }
 
 
@@ -890,7 +947,9 @@ __global__ void k_compact(uint64_t E, const uint32_t *__restrict__ dE, const uin
 __global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ mbase, const uint32_t *__restrict__ epos,
                            const uint32_t *__restrict__ fpos, uint64_t *__restrict__ bm_start) {
   uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (p <= npairs) bm_start[p] = fpos[mbase ? epos[mbase[p]] : p];
+  // first entry of pair p: epos[mbase[p]] (key join), epos[p] (per-pair
+  // entry bases: mbase == nullptr, epos != nullptr), p (container ops)
+  if (p <= npairs) bm_start[p] = fpos[mbase ? epos[mbase[p]] : epos ? epos[p] : p];
 }
 
 // -------------------------------------------------- count-only join + formula
@@ -1389,9 +1448,33 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
     RS_CK(cudaMemsetAsync(keep, 0, 4, g_stream));
     RS_CK(cudaMemsetAsync(ub, 0, 8, g_stream));
   }
-  if (M && maxk <= MERGE_SMEM_KEYS)
-    RS_LAUNCH(k_merge_pair, (unsigned)npairs, 256, 0, M, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub);
-  else
+  // per-pair path (CTA per pair, keys in smem, scans over pairs): when the
+  // bitmaps are small enough for smem and there are enough pairs to fill the
+  // GPU (or few positions per pair); a handful of pairs with thousands of keys
+  // each (config 4) keep the thread-per-position join
+  const bool per_pair = M && maxk <= MERGE_SMEM_KEYS && (npairs >= 2 * sm_count() || M <= 1024 * npairs);
+  if (per_pair) {
+    // the join, then entry / slot bases from scans over pairs
+    uint32_t *pk = (uint32_t *)S.get((npairs + 1) * 4), *pke = (uint32_t *)S.get((npairs + 1) * 4);
+    uint64_t *pu = (uint64_t *)S.get((npairs + 1) * 8), *pue = (uint64_t *)S.get((npairs + 1) * 8);
+    if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
+    RS_LAUNCH(k_merge_pair, (unsigned)npairs, 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair,
+              keep, ub, pk, pu);
+    RS_TRY(scan_exclusive<uint32_t>(pk, pke, npairs + 1));
+    RS_TRY(scan_exclusive<uint64_t>(pu, pue, npairs + 1));
+    RS_LAUNCH(k_emit_pair, (unsigned)npairs, 256, 0, mbase, keep, ub, pke, pue, mkey, mca, mcb, mpair, dA, dB, En, L,
+              op);
+    if (ub_mode)
+      return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr,
+                                     pke + npairs, nullptr, pke, npairs, out);
+    struct { uint32_t E; uint32_t pad; uint64_t P; uint32_t cnt[NCLS]; } h;
+    RS_CK(cudaMemcpyAsync(&h.E, pke + npairs, 4, cudaMemcpyDeviceToHost, g_stream));
+    RS_CK(cudaMemcpyAsync(&h.P, pue + npairs, 8, cudaMemcpyDeviceToHost, g_stream));
+    RS_CK(cudaMemcpyAsync(h.cnt, L.cnt, NCLS * 4, cudaMemcpyDeviceToHost, g_stream));
+    RS_CK(cudaStreamSynchronize(g_stream));
+    return run_classes_and_compact(op, A, B, S, En, L, h.E, h.P, h.cnt, nullptr, nullptr, pke, npairs, out);
+  }
+  if (M)
     RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep,
               ub);
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
@@ -1546,7 +1629,7 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   DevBatch dA = A->dev(), dB = B->dev();
   if (hbases) mbase = U.at<uint64_t>(o_mb);
   else RS_TRY(pair_bases_device(npairs, dA, dB, dia, dib, 1, msz, mbase));
-  if (Ma && maxk <= MERGE_SMEM_KEYS)
+  if (Ma && maxk <= MERGE_SMEM_KEYS && (npairs >= 2 * sm_count() || Ma <= 512 * npairs))
     RS_LAUNCH(k_match_pair, (unsigned)npairs, 256, 0, mbase, dA, dB, dia, dib, L, lcb, lpair);
   else
     RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
