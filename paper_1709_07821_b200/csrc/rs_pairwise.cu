@@ -952,6 +952,57 @@ __global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ mbase, 
   if (p <= npairs) bm_start[p] = fpos[mbase ? epos[mbase[p]] : epos ? epos[p] : p];
 }
 
+// Per-pair compaction (entries of pair p are [pbase[p], pbase[p+1])): the
+// non-empty results per pair, then CTA per pair writes them at the pair's base
+// (a scan over pairs) plus an in-CTA scan -- no scan over every entry.
+__global__ void __launch_bounds__(256) k_pair_nonempty(uint64_t npairs, const uint32_t *__restrict__ pbase,
+                                                       const uint32_t *__restrict__ card, uint32_t *__restrict__ nz) {
+  __shared__ uint32_t red[8];
+  const uint32_t p = blockIdx.x;
+  if (p == 0 && threadIdx.x == 0) nz[npairs] = 0;
+  uint32_t c = 0;
+  for (uint32_t e = pbase[p] + threadIdx.x; e < pbase[p + 1]; e += blockDim.x) c += card[e] > 0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int w = 0; w < 8; w++) s += red[w];
+    nz[p] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uint32_t *__restrict__ pbase,
+                                                      const uint32_t *__restrict__ fbase, Entries En, OutDesc O,
+                                                      uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn,
+                                                      uint64_t *off, uint64_t *bm_start) {
+  using BS = cub::BlockScan<uint32_t, 256>;
+  __shared__ typename BS::TempStorage ts;
+  const uint32_t p = blockIdx.x;
+  uint32_t f = fbase[p];
+  if (threadIdx.x == 0) {
+    bm_start[p] = f;
+    if (p == 0) bm_start[npairs] = fbase[npairs];
+  }
+  const uint32_t e1 = pbase[p + 1];
+  for (uint32_t e0 = pbase[p]; e0 < e1; e0 += blockDim.x) {
+    const uint32_t e = e0 + threadIdx.x;
+    const uint32_t k = e < e1 && O.card[e] > 0;
+    uint32_t ex, tot;
+    BS(ts).ExclusiveSum(k, ex, tot);
+    if (k) {
+      const uint32_t d = f + ex;
+      key[d] = En.key[e];
+      type[d] = O.type[e];
+      card[d] = O.card[e];
+      nn[d] = O.n[e];
+      off[d] = En.off[e];
+    }
+    f += tot;
+    __syncthreads();
+  }
+}
+
 // -------------------------------------------------- count-only join + formula
 
 // count-path append: ca into the class list, cb / pair into parallel arrays
@@ -1340,6 +1391,17 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   }
   RS_TRY(F.end());
   // compaction: drop empty results (bitmap.py:185-188)
+  if (!mbase && epos && npairs) {  // per-pair entry bases: per-pair compaction
+    uint32_t *nz = (uint32_t *)S.get((npairs + 1) * 4), *fb = (uint32_t *)S.get((npairs + 1) * 4);
+    if (!S.ok()) { set_error("device allocation failed (compaction)"); return RS_ENOMEM; }
+    RS_LAUNCH(k_pair_nonempty, (unsigned)npairs, 256, 0, npairs, epos, O.card, nz);
+    RS_TRY(scan_exclusive<uint32_t>(nz, fb, npairs + 1));
+    RS_LAUNCH(k_compact_pair, (unsigned)npairs, 256, 0, npairs, epos, fb, En, O, b->d_key, b->d_type, b->d_card,
+              b->d_n, b->d_off, b->d_bm_start);
+    b->h_valid = false;
+    *out = b;
+    return RS_OK;
+  }
   RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, dE, O.card, keep2);
   RS_TRY(scan_exclusive<uint32_t>(keep2, fpos, E + 1));
   RS_LAUNCH(k_compact, grid_for(E, 256), 256, 0, E, dE, keep2, fpos, En, O, b->d_key, b->d_type, b->d_card, b->d_n,
