@@ -1,23 +1,28 @@
-// rs_array_large.cuh -- large array x array pairs (na + nb > 256) through an
-// 8 KB shared-memory bitset instead of a merge path.
+// rs_array_large.cuh -- large array x array pairs (na + nb > 256) through
+// shared-memory bitsets instead of a merge path.
 //
 // Same results as the two-pointer kernels (kernels/scalar.py:122-267) and
 // _container_from_values (containers.py:244-247):
-//   and     build X from A, keep the B values whose bit is set   (sorted: B order)
-//   andnot  build X from B, keep the A values whose bit is clear (sorted: A order)
-//   or/xor  build X from A, OR / XOR in B's bits (B values are distinct, so XOR
-//           flips each bit at most once), then popcount -> bitset if > 4096
-//           values, else extract the set bits in order.
+//   and / andnot  one bitset X built from the smaller side (and) or from B
+//                 (andnot); the other side is filtered through it with warp
+//                 ballots, so the result comes out sorted;
+//   or / xor      XA from A and XB from B; the result words XA op XB with a
+//                 popcount scan give the cardinality, and the result is the
+//                 words themselves (> 4096 values: a bitset container) or
+//                 their set bits in order (<= 4096: an array container).
+// AND / ANDNOT with one side at most 1/16 of the other skip the bitset and
+// binary-search the larger array (array_intersect_galloping's case,
+// kernels/scalar.py:149-176).
 //
 // CTA layout (warp-specialized): warps 0-7 are consumers (256 threads, one
 // pair at a time, synchronizing only among themselves with named barrier 1);
 // warp 8 is the producer.  The producer walks the CTA's items, loads each
 // item's metadata (operand offsets, sizes, output slot, pair) and streams both
-// arrays (variable sizes, 16-byte padded) into a 2-stage shared-memory ring
-// with cp.async.bulk completing on `full` mbarriers; consumers release a stage
-// through its `empty` mbarrier.  No consumer ever waits on a dependent global
-// load, and no consumer barrier waits on producer work (the stall profile of
-// the single-role version: 44 % of stalls at CTA barriers behind thread 0).
+// arrays (variable sizes, 16-byte padded) into a byte ring in shared memory
+// with cp.async.bulk completing on the item slot's `full` mbarrier.  Items
+// take only the bytes they need (a ~12 KB average item leaves room for two
+// more in flight behind it), and consumers hand an item's bytes back through
+// the slot's `empty` mbarrier as soon as its last value has been read.
 #pragma once
 #include "rs_internal.cuh"
 #include "rs_bitset.cuh"
@@ -26,22 +31,52 @@ namespace rsl {
 
 constexpr int LT = 256;               // consumer threads
 constexpr int LTHREADS = LT + 32;     // + one producer warp
-constexpr int LSTAGES = 2;
+constexpr int NSLOT = 8;              // items in flight (metadata + barrier slots)
 
 struct LargeMeta {
   uint32_t na, nb, e, pair;
   uint64_t dst;
+  uint32_t aoff, boff;  // ring offsets of the staged arrays
+};
+
+// Shared-memory layout (dynamic; carved at run time by large_layout):
+//   header | pad to 8 KB | XA (8 KB) | XB (8 KB) | byte ring (rest)
+// XA / XB sit on 8 KB boundaries of the shared window so a value's word
+// address is base | offset (see scatter).
+struct LargeHdr {
+  uint64_t full[NSLOT];
+  uint64_t empty[NSLOT];
+  LargeMeta meta[NSLOT];
+  uint32_t span[NSLOT];  // producer only: ring bytes each item holds (incl. the wrap skip)
+  uint32_t red[2][2][LT / 32];
 };
 
 struct LargeSmem {
-  uint16_t a[LSTAGES][RS_ARRAY_MAX];
-  uint16_t b[LSTAGES][RS_ARRAY_MAX];
-  uint64_t X[2][RS_WORDS];  // by pair parity: each pair clears its words after its last read
-  uint64_t full[LSTAGES];
-  uint64_t empty[LSTAGES];
-  LargeMeta meta[LSTAGES];
-  uint32_t red[2][2][LT / 32];
+  LargeHdr *h;
+  uint8_t *X;     // XA, XB, then the ring
+  uint32_t ring;  // ring bytes
+  __device__ __forceinline__ uint32_t *XA() const { return (uint32_t *)X; }
+  __device__ __forceinline__ uint32_t *XB() const { return (uint32_t *)(X + 8192); }
+  __device__ __forceinline__ uint8_t *R() const { return X + 16384; }
 };
+
+// 56 KB: four CTAs per SM (4 x (56 + 1 reserved) KB <= 228 KB).  The dynamic
+// window starts 1 KB into the CTA's shared window, so the header and the pad
+// to the first 8 KB boundary take 7 KB and the ring gets 33 KB; large_loop
+// traps if a toolchain ever places the window so that the ring is under
+// 32 KB (a 16 KB item wrapping around the end may hold up to 32 KB).
+constexpr size_t LARGE_SMEM_BYTES = 57344;
+
+__device__ __forceinline__ LargeSmem large_layout(uint8_t *raw) {
+  LargeSmem sm;
+  sm.h = (LargeHdr *)raw;
+  const uint32_t b = rsb::smem_u32(raw);
+  const uint32_t x = (b + (uint32_t)sizeof(LargeHdr) + 8191u) & ~8191u;
+  sm.X = raw + (x - b);
+  const uint32_t used = (x - b) + 16384u;
+  sm.ring = used < LARGE_SMEM_BYTES ? ((uint32_t)LARGE_SMEM_BYTES - used) & ~15u : 0u;
+  return sm;
+}
 
 __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(LT) : "memory"); }
 
@@ -108,59 +143,102 @@ __device__ __forceinline__ void cscan2(uint32_t v0, uint32_t v1, uint32_t (*red)
   }
 }
 
-// OR / XOR into X with one native 32-bit shared atomic per touched word
-// (64-bit shared atomics lower to ATOMS.CAST.SPIN.64 CAS loops)
-template <bool XOR>
-__device__ __forceinline__ void flush_word(uint32_t *X32, uint32_t w, uint32_t m) {
-  if (!m) return;
-  if (XOR) atomicXor(&X32[w], m);
-  else atomicOr(&X32[w], m);
+// Set bit v of X (32-bit words) for every value of a staged array: two
+// values per 32-bit shared load, one native shared OR per touched word (two
+// values in the same word share one).  Lanes read consecutive value pairs, so
+// the ORs of one warp instruction mostly hit distinct banks.  X is 8 KB
+// aligned in the shared window, so a value's word address is one LOP3:
+// X | ((v >> 3) & ~3); its bit is a wrapping funnel shift by v.
+__device__ __forceinline__ void red_or(uint32_t addr, uint32_t bit) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(bit) : "memory");
 }
 
-// Thread t owns the contiguous values [c*t, c*t + c) of an array, c =
-// ceil(n / 256) <= 16, so every consumer gets an equal share whatever the
-// array's size (the busiest thread sets each pair's critical path).  The
-// values land in registers as 8 packed words: two 128-bit shared loads for a
-// full 16-value share, single loads otherwise.
-__device__ __forceinline__ uint32_t load16(const uint16_t *v, uint32_t n, uint32_t w[8]) {
-  const uint32_t c = (n + LT - 1) / LT, base = c * threadIdx.x;
-  if (base >= n) return 0;
-  const uint32_t cnt = min(c, n - base);
-  if (c == 16) {
-    const uint4 *p = (const uint4 *)(v + base);
-    const uint4 q0 = p[0], q1 = p[1];
-    w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-    w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-    return cnt;
-  }
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const uint32_t lo = 2 * k < (int)cnt ? v[base + 2 * k] : 0, hi = 2 * k + 1 < (int)cnt ? v[base + 2 * k + 1] : 0;
-    w[k] = lo | (hi << 16);
-  }
-  return cnt;
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 
-__device__ __forceinline__ uint32_t val16(const uint32_t w[8], int k) { return (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF; }
+__device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t X) {
+  const uint32_t *w = (const uint32_t *)v;
+  const uint32_t nw = n >> 1;
+#pragma unroll 4
+  for (uint32_t i = threadIdx.x; i < nw; i += LT) {
+    const uint32_t x = w[i];
+    const uint32_t alo = X | ((x >> 3) & 0x1FFCu), ahi = X | ((x >> 19) & 0x1FFCu);
+    const uint32_t blo = __funnelshift_l(0u, 1u, x), bhi = __funnelshift_l(0u, 1u, x >> 16);
+    const bool same = alo == ahi;
+    red_or(alo, same ? blo | bhi : blo);
+    if (!same) red_or(ahi, bhi);
+  }
+  if ((n & 1) && threadIdx.x == LT - 1) {
+    const uint32_t x = v[n - 1];
+    red_or(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
+  }
+}
 
-template <bool XOR>
-__device__ __forceinline__ void set_bits16(const uint32_t w8[8], uint32_t c, uint64_t *X) {
-  if (!c) return;
-  uint32_t *X32 = (uint32_t *)X;
-  uint32_t w = val16(w8, 0) >> 5, m = 0;
+// Keep the values of P (np, sorted) whose bit in X equals `want`, in order:
+// warp w probes a contiguous run of P (up to 8 rounds of 32 value pairs), the
+// kept flags become ballots, a CTA scan of the warp totals places each run,
+// and the kept values go straight to dst with 16-bit stores (consecutive
+// lanes write consecutive values).  Returns the kept count on every consumer.
+__device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np, uint32_t X, uint32_t want,
+                                                 uint16_t *dst, uint32_t (*red2)[LT / 32], uint64_t *release) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t *P32 = (const uint32_t *)P;
+  const uint32_t np2 = (np + 1) >> 1;
+  const uint32_t cw = (np2 + 255) / 256 * 32;  // value pairs per warp, <= 256
+  const uint32_t beg = w * cw;
+  uint32_t BL[8], BH[8], XV[8], tot = 0;
 #pragma unroll
-  for (int k = 0; k < 16; k++) {
-    const uint32_t x = val16(w8, k);
-    if ((uint32_t)k < c) {
-      if ((x >> 5) != w) {
-        flush_word<XOR>(X32, w, m);
-        w = x >> 5;
-        m = 0;
+  for (int r = 0; r < 8; r++) {
+    BL[r] = BH[r] = XV[r] = 0;
+    if (32u * r < cw) {
+      const uint32_t i = beg + 32u * r + lane;
+      bool klo = false, khi = false;
+      if (i < np2) {
+        const uint32_t x = P32[i];
+        XV[r] = x;
+        const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
+        klo = (__funnelshift_r(wl, 0u, x) & 1u) == want;
+        khi = 2 * i + 1 < np && (__funnelshift_r(wh, 0u, x >> 16) & 1u) == want;
       }
-      m |= 1u << (x & 31);
+      BL[r] = __ballot_sync(0xffffffffu, klo);
+      BH[r] = __ballot_sync(0xffffffffu, khi);
+      tot += __popc(BL[r]) + __popc(BH[r]);
     }
   }
-  flush_word<XOR>(X32, w, m);
+  uint32_t *red = red2[0];
+  if (lane == 0) red[w] = tot;
+  cbar();
+  if (threadIdx.x == 0) mbar_arrive(release);  // P's values are in registers
+  uint32_t base = 0, total = 0;
+#pragma unroll
+  for (int k = 0; k < LT / 32; k++) {
+    const uint32_t s = red[k];
+    base += k < w ? s : 0;
+    total += s;
+  }
+  if (dst && total) {
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      if (32u * r < cw) {
+        const uint32_t bl = BL[r], bh = BH[r];
+        const uint32_t klo = (bl >> lane) & 1u, khi = (bh >> lane) & 1u;
+        if (klo | khi) {
+          const uint32_t x = XV[r];
+          const uint32_t pos = base + __popc(bl & lt) + __popc(bh & lt);
+          if (klo) dst[pos] = (uint16_t)x;
+          if (khi) dst[pos + klo] = (uint16_t)(x >> 16);
+        }
+        base += __popc(bl) + __popc(bh);
+      }
+    }
+    const uint32_t padded = (total + 7u) & ~7u;
+    if (threadIdx.x < 8 && total + threadIdx.x < padded) dst[total + threadIdx.x] = 0;
+  }
+  return total;
 }
 
 // Copy `total` staged u16 values to dst with 128-bit stores (16-byte zero pad).
@@ -183,20 +261,21 @@ __device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_
   return n && v[lo] == x;
 }
 
-// One pair (consumers only).  `stage` (the ring slot's A buffer) is free once
-// the values are in registers and doubles as the output staging buffer; the
-// slot goes back to the producer only after the next pair's first barrier.
-//
-// AND (and ANDNOT with a small A) on very unequal sizes -- the smaller side
-// at most 1/16 of the larger, so at most 256 values -- skips the bitset: one
-// thread per small-side value binary-searches the larger array in shared
-// memory (array_intersect_galloping's case, kernels/scalar.py:149-176).
-// Otherwise AND builds X from the smaller side and probes the larger one (the
-// probed side's order is the output order).
-__device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_t na, const uint16_t *B,
+// One pair (consumers only).  `release` (the item's ring slot) is arrived on
+// exactly once, after the barrier that follows the last read of the staged
+// values.
+//   and / andnot: X (XA / XB alternate by pair parity) is cleared after the
+//     scan barrier; the next pair uses the other one.
+//   or / xor: each thread reads and clears the words it owns (t + 256q)
+//     before the scan barrier, which every consumer passes before the next
+//     pair's scatter; array results are staged in XA (re-zeroed behind a
+//     barrier).
+__device__ uint32_t large_pair(const LargeSmem &sm, int op, const uint16_t *A, uint32_t na, const uint16_t *B,
                                uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
-                               uint16_t *stage, uint64_t *release) {
+                               uint64_t *release) {
   const int t = threadIdx.x;
+  uint32_t *XA = sm.XA(), *XB = sm.XB();
+  type = RS_TAG_ARRAY;
   if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
     const bool is_and = op == RS_OP_AND;
     const bool a_small = is_and ? na <= nb : true;
@@ -209,84 +288,53 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
         keep = bsearch16(L, nl, v) == is_and;
       }
       uint32_t total;
-      const uint32_t base = cscan(keep, sm.red[parity], total);
-      if (t == 0 && release) mbar_arrive(release);
-      type = RS_TAG_ARRAY;
+      const uint32_t base = cscan(keep, sm.h->red[parity], total);
+      if (t == 0) mbar_arrive(release);
       nout = total;
       if (dst && total) {
-        if (keep) stage[base] = (uint16_t)v;
-        flush_stage(stage, total, dst);
+        uint16_t *d = (uint16_t *)dst;
+        if (keep) d[base] = (uint16_t)v;
+        const uint32_t padded = (total + 7u) & ~7u;
+        if (t < 8 && total + t < padded) d[total + t] = 0;
       }
       return total;
     }
-  }
-  // X (this pair's parity) is all zero on entry: zeroed at kernel start, and
-  // every pair clears the words it owns after its last read of them; the
-  // other parity's buffer separates that clear from the next pair's scatter.
-  uint64_t *X = sm.X[parity];
-  uint32_t *X32 = (uint32_t *)X;
-  uint32_t xa[8], xb[8];
-  const uint32_t ca = load16(A, na, xa), cb = load16(B, nb, xb);
-  if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
-    const bool build_b = op == RS_OP_ANDNOT || (op == RS_OP_AND && nb < na);
-    if (build_b) set_bits16<false>(xb, cb, X);
-    else set_bits16<false>(xa, ca, X);
+    // and: build the smaller side, filter the larger; andnot: build B, filter A
+    const bool build_a = is_and && na <= nb;
+    uint32_t *X = parity ? XB : XA;
+    const uint32_t xs = rsb::smem_u32(X);
+    scatter(build_a ? A : B, build_a ? na : nb, xs);
     cbar();
-    // every consumer has finished the previous pair: its ring slot may refill
-    if (t == 0 && release) mbar_arrive(release);
-    const bool probe_b = !build_b;
-    uint32_t P[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) P[k] = probe_b ? xb[k] : xa[k];
-    const uint32_t cp = probe_b ? cb : ca;
-    const uint32_t want = op == RS_OP_AND ? 1u : 0u;
-    uint32_t keep = 0;
-#pragma unroll
-    for (int k = 0; k < 16; k++) {
-      const uint32_t x = val16(P, k);
-      if ((uint32_t)k < cp && ((X32[x >> 5] >> (x & 31)) & 1u) == want) keep |= 1u << k;
-    }
-    uint32_t total;
-    uint32_t base = cscan((uint32_t)__popc(keep), sm.red[parity], total);
-#pragma unroll
-    for (int q = 0; q < 4; q++) X[t + LT * q] = 0;  // every probe of this pair is done
-    type = RS_TAG_ARRAY;
+    const uint32_t total = probe_filter(build_a ? B : A, build_a ? nb : na, xs, is_and ? 1u : 0u,
+                                        (uint16_t *)dst, sm.h->red[parity], release);
+    // every probe of X is done (scan barrier above): clear it for pair + 2
+    ((uint4 *)X)[t] = make_uint4(0, 0, 0, 0);
+    ((uint4 *)X)[t + LT] = make_uint4(0, 0, 0, 0);
     nout = total;
-    if (dst && total) {
-#pragma unroll
-      for (int k = 0; k < 16; k++)
-        if (keep >> k & 1) stage[base++] = (uint16_t)val16(P, k);
-      flush_stage(stage, total, dst);
-    }
     return total;
   }
-  // OR / XOR: both arrays in one scatter phase (the updates commute; each
-  // side's values are distinct, so XOR flips a bit once per side)
-  if (op == RS_OP_OR) {
-    set_bits16<false>(xa, ca, X);
-    set_bits16<false>(xb, cb, X);
-  } else {
-    set_bits16<true>(xa, ca, X);
-    set_bits16<true>(xb, cb, X);
-  }
+  scatter(A, na, rsb::smem_u32(XA));
+  scatter(B, nb, rsb::smem_u32(XB));
   cbar();
-  if (t == 0 && release) mbar_arrive(release);
+  if (t == 0) mbar_arrive(release);
   // result words t + 256q (conflict-free), positions by a packed row scan
+  uint64_t *XA64 = (uint64_t *)XA, *XB64 = (uint64_t *)XB;
   uint64_t r[4];
   uint32_t pq[4];
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    r[q] = X[t + LT * q];
-    X[t + LT * q] = 0;
+    const uint64_t x = XA64[t + LT * q], y = XB64[t + LT * q];
+    XA64[t + LT * q] = 0;
+    XB64[t + LT * q] = 0;
+    r[q] = op == RS_OP_OR ? x | y : x ^ y;
     pq[q] = __popcll(r[q]);
   }
   const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
   uint32_t e0, e1, T0, T1;
-  cscan2(pk0, pk1, sm.red[parity], e0, e1, T0, T1);
+  cscan2(pk0, pk1, sm.h->red[parity], e0, e1, T0, T1);
   const uint32_t r0 = T0 & 0xFFFFu, r1 = T0 >> 16, r2 = T1 & 0xFFFFu;
   const uint32_t card = r0 + r1 + r2 + (T1 >> 16);
   if (!dst || card == 0) {
-    type = RS_TAG_ARRAY;
     nout = card;
     return card;
   }
@@ -298,6 +346,7 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
     nout = RS_WORDS;
     return card;
   }
+  uint16_t *stage = (uint16_t *)XA;
   const uint32_t end[4] = {(e0 & 0xFFFFu) + pq[0], r0 + (e0 >> 16) + pq[1], r0 + r1 + (e1 & 0xFFFFu) + pq[2],
                            r0 + r1 + r2 + (e1 >> 16) + pq[3]};
 #pragma unroll
@@ -316,46 +365,67 @@ __device__ uint32_t large_pair(LargeSmem &sm, int op, const uint16_t *A, uint32_
     }
   }
   flush_stage(stage, card, dst);
-  type = RS_TAG_ARRAY;
+  const uint32_t nvec = (2 * card + 15) >> 4;
+  for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)stage)[v] = make_uint4(0, 0, 0, 0);
+  cbar();  // XA is zero again before any consumer's next scatter
   nout = card;
   return card;
 }
 
-// Persistent, warp-specialized ring over items i = blockIdx.x + k*gridDim.x.
+// Persistent, warp-specialized byte ring over items i = blockIdx.x + k*gridDim.x.
 // meta_of(i, aoff, boff) -> LargeMeta (runs on the producer lane only);
 // sink(meta, card, type, n) runs on every consumer thread after the pair.
 template <typename MetaOf, typename Sink>
-__device__ void large_loop(LargeSmem &sm, uint32_t count, int op, const uint8_t *poolA, const uint8_t *poolB,
+__device__ void large_loop(uint8_t *raw, uint32_t count, int op, const uint8_t *poolA, const uint8_t *poolB,
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
   const int t = threadIdx.x;
+  const LargeSmem sm = large_layout(raw);
+  if (sm.ring < 4u * 8192u) __trap();  // a wrapped 16 KB item may span up to 32 KB
   if (t == 0) {
-    for (int s = 0; s < LSTAGES; s++) {
-      rsb::mbar_init(&sm.full[s], 1);
-      rsb::mbar_init(&sm.empty[s], 1);
+    for (int s = 0; s < NSLOT; s++) {
+      rsb::mbar_init(&sm.h->full[s], 1);
+      rsb::mbar_init(&sm.h->empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int w = t; w < 2 * RS_WORDS; w += LTHREADS) (&sm.X[0][0])[w] = 0;
+  for (int w = t; w < 4 * RS_WORDS; w += LTHREADS) sm.XA()[w] = 0;  // XA and XB
   __syncthreads();
   if (t >= LT) {  // ---------------- producer warp (one elected lane)
     if (t == LT) {
       uint64_t ao, bo;
       LargeMeta m;
       if (blockIdx.x < count) m = meta_of(blockIdx.x, ao, bo);
+      uint32_t phys = 0, occ = 0, oldest = 0;  // next free ring byte, bytes held, oldest unreleased item
       for (uint32_t j = 0;; j++) {
         const uint32_t i = blockIdx.x + j * gridDim.x;
         if (i >= count) break;
-        const int s = j % LSTAGES;
-        // metadata of the next item is fetched before waiting for a free slot
+        const int s = j % NSLOT;
+        // metadata of the next item is fetched before waiting for ring space
         uint64_t nao = 0, nbo = 0;
         LargeMeta nm = m;
         if (i + gridDim.x < count) nm = meta_of(i + gridDim.x, nao, nbo);
-        if (j >= LSTAGES) mbar_wait_backoff(&sm.empty[s], ((j / LSTAGES) - 1) & 1);
-        sm.meta[s] = m;
         const uint32_t ba = (uint32_t)rs_pad16(2ull * m.na), bb = (uint32_t)rs_pad16(2ull * m.nb);
-        rsb::mbar_expect_tx(&sm.full[s], ba + bb);
-        rsb::bulk_g2s(sm.a[s], poolA + ao, ba, &sm.full[s]);
-        rsb::bulk_g2s(sm.b[s], poolB + bo, bb, &sm.full[s]);
+        const uint32_t need = ba + bb;
+        uint32_t pos = phys, skip = 0;
+        if (phys + need > sm.ring) {  // wrap: the item starts at 0, the tail bytes go with it
+          skip = sm.ring - phys;
+          pos = 0;
+        }
+        const uint32_t span = need + skip;
+        while (j - oldest >= (uint32_t)NSLOT || occ + span > sm.ring) {
+          mbar_wait_backoff(&sm.h->empty[oldest % NSLOT], (oldest / NSLOT) & 1);
+          occ -= sm.h->span[oldest % NSLOT];
+          oldest++;
+        }
+        sm.h->span[s] = span;
+        occ += span;
+        phys = pos + need;
+        m.aoff = pos;
+        m.boff = pos + ba;
+        sm.h->meta[s] = m;
+        rsb::mbar_expect_tx(&sm.h->full[s], need);
+        if (ba) rsb::bulk_g2s(sm.R() + pos, poolA + ao, ba, &sm.h->full[s]);
+        if (bb) rsb::bulk_g2s(sm.R() + pos + ba, poolB + bo, bb, &sm.h->full[s]);
         m = nm;
         ao = nao;
         bo = nbo;
@@ -366,14 +436,14 @@ __device__ void large_loop(LargeSmem &sm, uint32_t count, int op, const uint8_t 
   for (uint32_t k = 0;; k++) {  // ---------------- consumers
     const uint32_t i = blockIdx.x + k * gridDim.x;
     if (i >= count) break;
-    const int s = k % LSTAGES;
-    rsb::mbar_wait(&sm.full[s], (k / LSTAGES) & 1);
-    const LargeMeta m = sm.meta[s];
+    const int s = k % NSLOT;
+    rsb::mbar_wait(&sm.h->full[s], (k / NSLOT) & 1);
+    const LargeMeta m = sm.h->meta[s];
     uint8_t type;
     uint32_t n;
-    uint64_t *release = k ? &sm.empty[(k - 1) % LSTAGES] : nullptr;
-    const uint32_t card = large_pair(sm, op, sm.a[s], m.na, sm.b[s], m.nb, opool ? opool + m.dst : nullptr, k & 1,
-                                     type, n, sm.a[s], release);
+    const uint32_t card = large_pair(sm, op, (const uint16_t *)(sm.R() + m.aoff), m.na,
+                                     (const uint16_t *)(sm.R() + m.boff), m.nb, opool ? opool + m.dst : nullptr,
+                                     k & 1, type, n, &sm.h->empty[s]);
     sink(m, card, type, n);
   }
 }

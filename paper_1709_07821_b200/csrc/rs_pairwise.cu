@@ -645,7 +645,6 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(int op, const 
                                                                uint8_t *__restrict__ opool,
                                                                uint64_t *__restrict__ res_card) {
   extern __shared__ __align__(128) uint8_t smraw[];
-  auto &sm = *reinterpret_cast<rsl::LargeSmem *>(smraw);
   auto meta_of = [&](uint32_t i, uint64_t &ao, uint64_t &bo) {
     rsl::LargeMeta m;
     ao = laoff[i];
@@ -666,7 +665,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(int op, const 
       if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
     }
   };
-  rsl::large_loop(sm, *cnt, op, A.pool, B.pool, opool, meta_of, sink);
+  rsl::large_loop(smraw, *cnt, op, A.pool, B.pool, opool, meta_of, sink);
 }
 
 __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint64_t *__restrict__ laoff,
@@ -676,7 +675,6 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint6
                                                                   const uint32_t *__restrict__ cnt, DevBatch A,
                                                                   DevBatch B, uint64_t *__restrict__ acc) {
   extern __shared__ __align__(128) uint8_t smraw[];
-  auto &sm = *reinterpret_cast<rsl::LargeSmem *>(smraw);
   auto meta_of = [&](uint32_t i, uint64_t &ao, uint64_t &bo) {
     rsl::LargeMeta m;
     ao = laoff[i];
@@ -692,7 +690,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint6
   auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t, uint32_t) {
     if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);
   };
-  rsl::large_loop(sm, *cnt, RS_OP_AND, A.pool, B.pool, nullptr, meta_of, sink);
+  rsl::large_loop(smraw, *cnt, RS_OP_AND, A.pool, B.pool, nullptr, meta_of, sink);
 }
 
 template <typename K>
@@ -709,7 +707,7 @@ unsigned persistent_grid_t(K kernel, int threads, size_t smem, uint64_t count) {
 
 int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
                        uint8_t *pool, uint64_t *res_card, bool exact) {
-  const size_t smem = sizeof(rsl::LargeSmem);
+  const size_t smem = rsl::LARGE_SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     RS_CK(cudaFuncSetAttribute(k_aa_large_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -722,7 +720,7 @@ int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch
 }
 
 int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch dB, uint64_t *inter) {
-  const size_t smem = sizeof(rsl::LargeSmem);
+  const size_t smem = rsl::LARGE_SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     RS_CK(cudaFuncSetAttribute(k_aa_large_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
