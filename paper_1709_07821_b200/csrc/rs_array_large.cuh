@@ -329,11 +329,16 @@ __device__ uint32_t large_pair(const LargeSmem &sm, int op, const uint16_t *A, u
     r[q] = op == RS_OP_OR ? x | y : x ^ y;
     pq[q] = __popcll(r[q]);
   }
-  const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
-  uint32_t e0, e1, T0, T1;
-  cscan2(pk0, pk1, sm.h->red[parity], e0, e1, T0, T1);
-  const uint32_t r0 = T0 & 0xFFFFu, r1 = T0 >> 16, r2 = T1 & 0xFFFFu;
-  const uint32_t card = r0 + r1 + r2 + (T1 >> 16);
+  // cardinality first (one warp reduction); the position scan only for an
+  // array result
+  uint32_t *red = sm.h->red[parity][0];
+  const int lane = t & 31, w = t >> 5;
+  const uint32_t wsum = __reduce_add_sync(0xffffffffu, pq[0] + pq[1] + pq[2] + pq[3]);
+  if (lane == 0) red[w] = wsum;
+  cbar();
+  uint32_t card = 0;
+#pragma unroll
+  for (int k = 0; k < LT / 32; k++) card += red[k];
   if (!dst || card == 0) {
     nout = card;
     return card;
@@ -346,6 +351,10 @@ __device__ uint32_t large_pair(const LargeSmem &sm, int op, const uint16_t *A, u
     nout = RS_WORDS;
     return card;
   }
+  const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
+  uint32_t e0, e1, T0, T1;
+  cscan2(pk0, pk1, sm.h->red[parity ^ 1], e0, e1, T0, T1);
+  const uint32_t r0 = T0 & 0xFFFFu, r1 = T0 >> 16, r2 = T1 & 0xFFFFu;
   uint16_t *stage = (uint16_t *)XA;
   const uint32_t end[4] = {(e0 & 0xFFFFu) + pq[0], r0 + (e0 >> 16) + pq[1], r0 + r1 + (e1 & 0xFFFFu) + pq[2],
                            r0 + r1 + r2 + (e1 >> 16) + pq[3]};
