@@ -1,28 +1,39 @@
 // rs_umma.cuh -- all-pairs |A AND B| of one chunk key's containers on the
-// 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
+// 5th-generation tensor cores (tcgen05.mma kind::mxf4, accumulators in TMEM).
 //
 // Config 5 asks for op_cardinality("and") over every bitmap pair
 // (bitmap.py:212-241 -> container_pairwise_cardinality, containers.py:532-570).
 // Grouped by chunk key, the containers of one key form m bit-rows of 65,536
 // bits (densified to 8 KB), and all their pairwise intersection counts are the
 // Gram matrix G = X X^T over {0,1}: a GEMM.  On CUDA cores this is bound by
-// the POPC issue rate (16/clk/SM); the tensor cores multiply 0/1 bytes.  Each
+// the POPC issue rate (16/clk/SM); the tensor cores multiply 0/1 values
+// packed as 4-bit E2M1 (bit -> nibble 0x2 = 1.0) with unit E8M0 block scales,
+// K = 64 per instruction -- twice the K of kind::i8 at the same issue rate
+// (N/2 cycles per 128 x N MMA, tools/umma_rate_probe.cu), and half the
+// expanded shared-memory bytes.  Products and sums of 0/1 are exact in the f32
+// accumulator (counts <= 65,536 < 2^24).  Each
 // CTA owns one tile: A = 128 rows starting at r0, B = NB <= 256 rows starting
 // at c0, both of one key.  When r0 == c0 the A rows are the first 128 rows of
 // the B operand -- one expansion feeds both descriptors -- so a key with
 // m <= 256 containers is one tile (pairs u < v with u < 128) plus, past 128,
 // a small corner left to the CUDA-core tiles.
-//   * warps 0-7 (producers) stream 256-bit K chunks of the rows from HBM (4
-//     chunks prefetched in registers), expand bits to bytes {0,1} in shared
-//     memory in the canonical K-major SWIZZLE_128B layout, and arrive on the
-//     stage's `full` mbarrier;
-//   * warp 8 lane 0 issues 8 x tcgen05.mma (M=128, N=NB, K=32) per chunk into
-//     an s32 accumulator in TMEM and frees the stage with tcgen05.commit ->
-//     `empty`;
+//   * warp 9 lane 0 streams the raw rows with 2D tensor TMA (box: 128 rows x
+//     128 bytes = four 256-bit K chunks, SWIZZLE_128B) into a raw ring;
+//   * warps 0-7 (producers) each expand whole chunks (warp c % 8 takes chunk
+//     c, so eight chunks are in flight): per row, the 32 raw bytes (two
+//     conflict-free 128-bit loads) become one 128-byte K-major SWIZZLE_128B
+//     atom row of nibbles (nib32: 7 integer ops per 32 bits), then the warp
+//     arrives on the stage's `full` mbarrier;
+//   * warp 8 lane 0 issues 4 x tcgen05.mma (M=128, N=NB, K=64) per chunk into
+//     an f32 accumulator in TMEM and frees the stage with tcgen05.commit ->
+//     `empty`; the block scales are 0x7F bytes filled once into TMEM columns
+//     256..287 (every scale-factor layout then reads 1.0);
 //   * after the last chunk every warp reads a quarter of the accumulator rows
 //     (TMEM lanes 32(w%4)..) and half of the columns back with tcgen05.ld and
 //     adds the upper-triangle counts into the N x N matrix.
-// Counts are exact: at most 65,536 per pair, accumulated in s32.
+// Counts are exact: at most 65,536 per pair.  Within each 32-bit word the K
+// order is permuted (see nib32), identically for every row, which a dot
+// product does not see.
 #pragma once
 #include "rs_internal.cuh"
 
@@ -31,13 +42,17 @@ namespace rsu {
 constexpr int UM = 128;                 // tile rows (A operand, TMEM lanes)
 constexpr int UNMAX = 256;              // tile columns (B operand rows), at most
 constexpr int UKC = 256;                // K bits per smem chunk
-constexpr int UACH = UM * UKC;          // expanded separate-A bytes per chunk (32 KB)
-constexpr int URING = 192 * 1024;       // stage ring: as many stages as fit (<= UMAXST)
-constexpr int UMAXST = 6;
-constexpr int UPF = 4;                  // raw chunks prefetched in registers
+constexpr int UROWB = UKC / 2;          // expanded bytes per row and chunk (one 128-byte atom row)
+constexpr int UACH = UM * UROWB;        // expanded separate-A bytes per chunk (16 KB)
+constexpr int UTMEM = 512;              // TMEM columns: accumulator (<= 256) + block scales at 256..287
+constexpr int URING = 192 * 1024;       // raw + expanded stages: as many as fit (<= UMAXST each)
+constexpr int UMAXST = 8;               // expanded stages (raw stages: 2-3)
+constexpr int UBOXR = 128;              // raw TMA box: rows
+constexpr int UBOXB = 128;              // raw TMA box: bytes of K (4 chunks)
+constexpr int UBOX = UBOXR * UBOXB;     // 16 KB
 constexpr int UPROD = 256;              // producer threads
-constexpr int UTHREADS = UPROD + 32;    // + the MMA-issuer warp
-constexpr size_t USMEM = (size_t)URING + 256;
+constexpr int UTHREADS = UPROD + 64;    // + the MMA-issuer warp + the TMA warp
+constexpr size_t USMEM = (size_t)URING + 2048;  // + alignment slack and the barriers
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -52,9 +67,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
   return d;
 }
 
-// Instruction descriptor, kind::i8: D s32, A and B unsigned 8-bit, K-major.
-__host__ __device__ constexpr uint32_t idesc_u8(int m, int n) {
-  return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+// Instruction descriptor, kind::mxf4 block-scaled: A and B E2M1 (MXF4 format
+// 1), E8M0 scales, K-major, dense K = 64, scale-factor ids 0; D is f32.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int m, int n) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) | ((uint32_t)(m >> 4) << 24);
 }
 
 // Byte offset of (row, k) in one operand chunk of `rows` rows:
@@ -63,9 +79,6 @@ __host__ __device__ constexpr uint32_t idesc_u8(int m, int n) {
 __device__ __forceinline__ uint32_t sw_off(int row, int k, int rows) {
   return (k >> 7) * (rows * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((((k & 127) >> 4) ^ (row & 7)) << 4);
 }
-
-// 4 bits -> 4 bytes {0,1} (the four shifted copies never overlap)
-__device__ __forceinline__ uint32_t spread4(uint32_t n) { return ((n & 0xF) * 0x00204081u) & 0x01010101u; }
 
 __device__ __forceinline__ void ubar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count) : "memory");
@@ -85,18 +98,19 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                : "memory");
 }
 
-// Expand NW consecutive words (bits k0 ..) of one row into `dst`.
-template <int NW>
-__device__ __forceinline__ void expand_words(uint8_t *dst, int row, int rows, int k0, const uint64_t *x) {
+// 32 bits -> 32 nibbles {0, 0x2 = E2M1 1.0} in one 16-byte unit: nibble j of
+// word i holds bit 4j + i (a fixed K permutation within the word).
+__device__ __forceinline__ uint4 nib32(uint32_t x) {
+  constexpr uint32_t M2 = 0x22222222u;
+  return make_uint4((x << 1) & M2, x & M2, (x >> 1) & M2, (x >> 2) & M2);
+}
+
+// Expand one row's 256-bit chunk (two 16-byte raw units) into its 128-byte
+// atom row of an operand chunk of `rows` rows.
+__device__ __forceinline__ void expand_row(uint8_t *dst, int row, int rows, uint4 lo, uint4 hi) {
+  const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
-  for (int w = 0; w < NW; w++) {
-#pragma unroll
-    for (int h = 0; h < 4; h++) {
-      const uint32_t s = (uint32_t)(x[w] >> (16 * h));
-      *(uint4 *)(dst + sw_off(row, k0 + w * 64 + h * 16, rows)) =
-          make_uint4(spread4(s), spread4(s >> 4), spread4(s >> 8), spread4(s >> 12));
-    }
-  }
+  for (int u = 0; u < 8; u++) *(uint4 *)(dst + sw_off(row, 16 * u, rows)) = nib32(w[u]);
 }
 
 }  // namespace rsu

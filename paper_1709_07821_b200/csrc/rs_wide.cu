@@ -9,6 +9,7 @@
 #include "rs_internal.cuh"
 #include "rs_dense.cuh"
 #include "rs_umma.cuh"
+#include <cudaTypedefs.h>
 
 using namespace rs;
 using namespace rsd;
@@ -164,6 +165,32 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
   }
 }
 
+// D (T densified 8 KB rows) as a 2D uint8 tensor for TMA: boxes of 128 rows x
+// 128 bytes, SWIZZLE_128B, rows past T read as zero.  The encoder comes from
+// the driver through the runtime (no libcuda link).
+static int rows_tensor_map(CUtensorMap *tm, const void *D, uint64_t T) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode) {
+      encode = nullptr;
+      set_error("cuTensorMapEncodeTiled unavailable");
+      return RS_ECUDA;
+    }
+  }
+  const cuuint64_t dims[2] = {8192, T ? T : 1}, strides[1] = {8192};
+  const cuuint32_t box[2] = {(cuuint32_t)rsu::UBOXB, (cuuint32_t)rsu::UBOXR}, es[2] = {1, 1};
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(D), dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return RS_ECUDA;
+  }
+  return RS_OK;
+}
+
 // ------------------------------------------------------------ all pairs
 
 // densify every grouped container into its own 8 KB slot.  Thread t owns
@@ -195,40 +222,51 @@ __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__re
 
 // One CTA per tensor-core tile (see rs_umma.cuh): A = rows [r0, r0+128),
 // B = rows [c0, c0+nb) of one key segment; counts of pairs u < v go into the
-// same N x N matrix as the CUDA-core tiles.
+// same N x N matrix as the CUDA-core tiles.  tmD maps D as a 2D tensor
+// (8192 bytes x T rows).
 __global__ void __launch_bounds__(rsu::UTHREADS, 1)
     k_allpairs_umma(const uint32_t *__restrict__ tp_seg, const uint16_t *__restrict__ tp_r0,
                     const uint16_t *__restrict__ tp_c0, const uint16_t *__restrict__ tp_nb,
-                    const uint32_t *__restrict__ seg_start, const uint64_t *__restrict__ D,
-                    const uint32_t *__restrict__ item_bm, uint64_t N, unsigned long long *__restrict__ Mx,
-                    int maxst) {
+                    const uint32_t *__restrict__ seg_start, const __grid_constant__ CUtensorMap tmD,
+                    const uint32_t *__restrict__ item_bm, uint64_t N, unsigned long long *__restrict__ Mx) {
   using namespace rsu;
-  extern __shared__ __align__(1024) uint8_t usm[];
-  uint64_t *full = (uint64_t *)(usm + URING), *empty = full + UMAXST, *done = empty + UMAXST;
+  extern __shared__ __align__(1024) uint8_t usm_raw[];
+  // 1024-byte alignment for the swizzled TMA boxes and operand atoms
+  uint8_t *usm = (uint8_t *)(((uintptr_t)usm_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(usm + URING), *empty = full + UMAXST, *rfull = empty + UMAXST,
+           *rempty = rfull + 4, *done = rempty + 4;
   uint32_t *tslot = (uint32_t *)(done + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const uint32_t seg = tp_seg[blockIdx.x];
   const uint32_t s0 = seg_start[seg], m = seg_start[seg + 1] - s0;
   const uint32_t r0 = tp_r0[blockIdx.x], c0 = tp_c0[blockIdx.x], nb = tp_nb[blockIdx.x];
   const bool shared_a = r0 == c0;  // A = the first 128 rows of the B operand
-  // stage layout: B operand (rows_b rows, >= the 128 rows A reads when shared),
-  // then a separate A operand; as many stages as fit in the ring
-  const uint32_t rows_b = max(nb, (uint32_t)UM);
-  const uint32_t bbytes = rows_b * (UKC / 8) * 8, sbytes = bbytes + (shared_a ? 0 : UACH);
-  const int nst = min(maxst, (int)(URING / sbytes));
-  // rows never written below (past m, past nb) must read as zero
-  for (uint32_t i = t; i < URING / 16; i += UTHREADS) ((uint4 *)usm)[i] = make_uint4(0, 0, 0, 0);
+  // raw stage: the B boxes (128 rows each) then a separate A box; expanded
+  // stage: the B operand (rows_b rows, >= the 128 rows A reads when shared),
+  // then a separate A operand
+  const uint32_t rows_b = max(nb, (uint32_t)UM), nbox = (rows_b + UBOXR - 1) / UBOXR;
+  const uint32_t rbytes = nbox * UBOX + (shared_a ? 0 : UBOX);
+  const uint32_t bbytes = rows_b * UROWB, sbytes = bbytes + (shared_a ? 0 : UACH);
+  const int nraw = rbytes <= (uint32_t)UBOX ? 3 : 2;
+  const int nst = min(UMAXST, (int)((URING - nraw * rbytes) / sbytes));
+  uint8_t *raw = usm, *xst = usm + nraw * rbytes;
+  // expanded rows never written below (past m, past nb) must read as zero
+  for (uint32_t i = t; i < nst * sbytes / 16; i += UTHREADS) ((uint4 *)xst)[i] = make_uint4(0, 0, 0, 0);
   if (t == 0) {
     for (int i = 0; i < nst; i++) {
-      ubar_init(&full[i], UPROD / 32);
+      ubar_init(&full[i], 1);
       ubar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < nraw; i++) {
+      ubar_init(&rfull[i], 1);
+      ubar_init(&rempty[i], UBOXB * 8 / UKC);  // the warps of the box's chunks
     }
     ubar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
-                 "r"(UNMAX)
+                 "r"(UTMEM)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -237,27 +275,58 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  constexpr int NCH = RS_WORDS * 64 / UKC;
-  if (warp == UPROD / 32) {  // ------------------------------ MMA issuer
+  if (warp < 4) {  // unit block scales: 0x7F (E8M0 2^0) in columns 256..287 of every lane
+    const uint32_t one = 0x7F7F7F7Fu;
+    for (int c = 0; c < 32; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       tmem + ((uint32_t)(32 * warp) << 16) + 256 + c),
+                   "r"(one)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  constexpr int NCH = RS_WORDS * 64 / UKC;   // 256-bit chunks per row
+  constexpr int NRAW = 8192 / UBOXB;         // raw boxes per row
+  constexpr int CPB = UBOXB * 8 / UKC;       // chunks per raw box (4)
+  if (warp == UPROD / 32 + 1) {  // ------------------------------ TMA (raw rows)
+    if (lane == 0) {
+      for (int r = 0; r < NRAW; r++) {
+        const int st = r % nraw;
+        if (r >= nraw) ubar_wait(&rempty[st], ((r - nraw) / nraw) & 1);
+        uint8_t *dst = raw + st * rbytes;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[st])), "r"(rbytes)
+                     : "memory");
+        for (uint32_t bx = 0; bx <= nbox - (shared_a ? 1u : 0u); bx++) {
+          const uint32_t row = bx < nbox ? s0 + c0 + bx * UBOXR : s0 + r0;  // the last box is A when separate
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+              "[%4];" ::"r"(su32(dst + bx * UBOX)),
+              "l"((uint64_t)&tmD), "r"(r * UBOXB), "r"(row), "r"(su32(&rfull[st]))
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == UPROD / 32) {  // ------------------------------ MMA issuer
     // the whole warp walks the stages (no lane diverges into a spin-wait
     // while lane 0 issues); lane 0 issues the MMAs and the commits
-    const uint32_t idesc = idesc_u8(UM, (int)nb);
+    const uint32_t idesc = idesc_mxf4(UM, (int)nb);
     for (int c = 0; c < NCH; c++) {
       const int b = c % nst;
       ubar_wait(&full[b], (c / nst) & 1);
       if (lane == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t bb = su32(usm + b * sbytes), ba = shared_a ? bb : bb + bbytes;
-        const uint32_t astride = shared_a ? rows_b * 128 : UM * 128;
+        const uint32_t bb = su32(xst + b * sbytes), ba = shared_a ? bb : bb + bbytes;
 #pragma unroll
-        for (int k = 0; k < UKC / 32; k++) {
-          const uint64_t da = sw128_desc(ba + (k >> 2) * astride + (k & 3) * 32);
-          const uint64_t db = sw128_desc(bb + (k >> 2) * (rows_b * 128) + (k & 3) * 32);
+        for (int k = 0; k < UKC / 64; k++) {  // K = 64 nibbles = 32 bytes of the 128-byte atom row
+          const uint64_t da = sw128_desc(ba + k * 32);
+          const uint64_t db = sw128_desc(bb + k * 32);
           const uint32_t acc = (c | k) ? 1u : 0u;
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc)
+              "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
+              ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(tmem + 256u), "r"(tmem + 272u)
               : "memory");
         }
         umma_commit(&empty[b]);
@@ -266,35 +335,35 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
       __syncwarp();
     }
   } else {  // ------------------------------------------- producers
-    // B: thread t expands row c0 + t (all 4 words of a chunk); a separate A:
-    // thread t expands half of row r0 + (t & 127)
-    const int arow = t & (UM - 1), ahalf = t >> 7;
-    const uint64_t *pb = (uint32_t)t < nb && c0 + t < m ? D + (uint64_t)(s0 + c0 + t) * RS_WORDS : nullptr;
-    const uint64_t *pa = !shared_a && r0 + arow < m ? D + (uint64_t)(s0 + r0 + arow) * RS_WORDS + ahalf * 2 : nullptr;
-    uint64_t xb[UPF][4], xa[UPF][2];
-#pragma unroll
-    for (int q = 0; q < UPF; q++) {
-#pragma unroll
-      for (int w = 0; w < 4; w++) xb[q][w] = pb ? pb[q * (UKC / 64) + w] : 0;
-#pragma unroll
-      for (int w = 0; w < 2; w++) xa[q][w] = pa ? pa[q * (UKC / 64) + w] : 0;
-    }
-    for (int cc = 0; cc < NCH; cc += UPF) {
-#pragma unroll
-      for (int q = 0; q < UPF; q++) {
-        const int c = cc + q, b = c % nst;
-        if (c >= nst) ubar_wait(&empty[b], ((c - nst) / nst) & 1);
-        uint8_t *sb = usm + b * sbytes;
-        if (pb) expand_words<4>(sb, t, rows_b, 0, xb[q]);
-        if (pa) expand_words<2>(sb + bbytes, arow, UM, ahalf * (UKC / 2), xa[q]);
-        const bool more = c + UPF < NCH;
-#pragma unroll
-        for (int w = 0; w < 4; w++) xb[q][w] = pb && more ? pb[(c + UPF) * (UKC / 64) + w] : 0;
-#pragma unroll
-        for (int w = 0; w < 2; w++) xa[q][w] = pa && more ? pa[(c + UPF) * (UKC / 64) + w] : 0;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) ubar_arrive(&full[b]);
+    // warp c % nst expands chunk c (so each stage has one producer and its
+    // mbarrier phases are waited in order): every B row (and a separate A's
+    // rows) from the raw box, whose 128-byte rows have their 16-byte units
+    // XOR-swizzled by row % 8 (conflict-free: eight consecutive rows hit
+    // eight units).  nst is 8 for 128-row tiles, 4 otherwise.
+    const uint32_t nrow_b = c0 < m ? min(nb, m - c0) : 0u, nrow_a = shared_a ? 0u : min((uint32_t)UM, m - r0);
+    for (int c = warp; warp < nst && c < NCH; c += nst) {
+      const int r = c / CPB, q = c % CPB, st = r % nraw, b = c % nst;
+      ubar_wait(&rfull[st], (r / nraw) & 1);
+      if (c >= nst) ubar_wait(&empty[b], ((c - nst) / nst) & 1);
+      const uint8_t *rs = raw + st * rbytes;
+      uint8_t *sb = xst + b * sbytes;
+      for (uint32_t row = lane; row < nrow_b; row += 32) {
+        const uint8_t *p = rs + (row / UBOXR) * UBOX + (row & (UBOXR - 1)) * UBOXB;
+        const uint32_t sw = row & 7;
+        expand_row(sb, (int)row, (int)rows_b, *(const uint4 *)(p + (((2 * q) ^ sw) << 4)),
+                   *(const uint4 *)(p + (((2 * q + 1) ^ sw) << 4)));
+      }
+      for (uint32_t row = lane; row < nrow_a; row += 32) {
+        const uint8_t *p = rs + nbox * UBOX + row * UBOXB;
+        const uint32_t sw = row & 7;
+        expand_row(sb + bbytes, (int)row, UM, *(const uint4 *)(p + (((2 * q) ^ sw) << 4)),
+                   *(const uint4 *)(p + (((2 * q + 1) ^ sw) << 4)));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        ubar_arrive(&full[b]);
+        ubar_arrive(&rempty[st]);  // this chunk's reads of the raw box are done
       }
     }
   }
@@ -322,10 +391,11 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; j++) {
             const uint32_t vc = c0 + cb + j;
-            if (v[j] && vc < m && u < vc) {
+            const uint32_t cnt = (uint32_t)__uint_as_float(v[j]);  // exact: an integer <= 65,536
+            if (cnt && vc < m && u < vc) {
               const uint32_t bv = item_bm[s0 + vc];
               const uint32_t lo = min(bu, bv), hi = max(bu, bv);
-              atomicAdd(&Mx[(uint64_t)lo * N + hi], (unsigned long long)v[j]);
+              atomicAdd(&Mx[(uint64_t)lo * N + hi], (unsigned long long)cnt);
             }
           }
         }
@@ -335,7 +405,7 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(UNMAX) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(UTMEM) : "memory");
 }
 
 constexpr int AP_TILE = 16;   // containers per tile side
@@ -604,8 +674,6 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   const bool use_umma = !(uv && *uv == '0');
   const char *mv = getenv("RS_ALLPAIRS_UMMA_MIN");
   const uint32_t umma_min = mv && *mv ? (uint32_t)atoi(mv) : 48;
-  const char *sv = getenv("RS_UMMA_STAGES");
-  const int umma_stages = sv && *sv ? std::max(2, std::min(rsu::UMAXST, atoi(sv))) : 2;
   std::vector<uint32_t> hseg(g.G + 1);
   RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
   std::vector<uint32_t> tseg, useg;
@@ -667,8 +735,10 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
       RS_CK(cudaFuncSetAttribute(k_allpairs_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsu::USMEM));
       attr = true;
     }
+    CUtensorMap tmD;
+    RS_TRY(rows_tensor_map(&tmD, D, g.T));
     RS_LAUNCH_PROF("allpairs_umma", nup, k_allpairs_umma, (unsigned)nup, rsu::UTHREADS, rsu::USMEM, d_useg, d_ur0,
-                   d_uc0, d_unb, g.seg_start, D, item_bm, N, Mx, umma_stages);
+                   d_uc0, d_unb, g.seg_start, tmD, item_bm, N, Mx);
   }
   if (!ntp) {
   } else if (tiles2)

@@ -9,6 +9,12 @@
 #include <vector>
 #include <cuda_runtime.h>
 
+#ifndef FP8
+#define FP8 0
+#endif
+#ifndef MXF4
+#define MXF4 0   // packed E2M1 (1.0 = 0x2 per nibble), kind::mxf4 with unit E8M0 block scales
+#endif
 constexpr int M = 128;          // rows (A) = cols (B): Gram tile
 #ifndef KCH
 #define KCH 256
@@ -18,7 +24,7 @@ constexpr int M = 128;          // rows (A) = cols (B): Gram tile
 #endif
 constexpr int KC = KCH;         // K elements (bits) per smem chunk
 constexpr int NS = NST;         // smem stages
-constexpr int CHUNK_BYTES = M * KC;   // u8 expanded: 32 KB
+constexpr int CHUNK_BYTES = MXF4 ? M * KC / 2 : M * KC;   // u8 expanded: 32 KB (4-bit: 16 KB)
 constexpr int NT = 256;         // threads: thread t expands half of row t & 127
 constexpr int PF = 4;           // chunks of raw words prefetched in registers
 
@@ -44,8 +50,15 @@ __device__ __forceinline__ uint32_t koff(int row, int k) {
 }
 
 // kind::i8 instruction descriptor: D s32, A/B unsigned 8-bit, K-major, N, M
+// (FP8: kind::f8f6f4, D f32, A/B E4M3)
+__host__ __device__ constexpr uint32_t idesc_mxf4(int m, int n) {
+  return (1u << 7) | (1u << 10)          // a/b format: MXF4 E2M1
+         | ((uint32_t)(n >> 3) << 17)    // N >> 3
+         | (1u << 23)                    // scale format E8M0
+         | ((uint32_t)(m >> 4) << 24);   // M >> 4 (sf ids 0, K64)
+}
 __host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
-  return (2u << 4)                      // c_format S32
+  return ((FP8 ? 1u : 2u) << 4)         // c_format S32 (F32 for FP8)
          | (0u << 7) | (0u << 10)       // a/b format: unsigned 8-bit
          | (0u << 15) | (0u << 16)      // K-major A and B
          | ((uint32_t)(n >> 3) << 17)   // N >> 3
@@ -82,8 +95,11 @@ __device__ __forceinline__ void mbar_sleep(uint64_t *bar, uint32_t phase) {
   }
 }
 
-// expand 4 bits n -> 4 bytes {0,1}
-__device__ __forceinline__ uint32_t spread4(uint32_t n) { return ((n & 0xF) * 0x00204081u) & 0x01010101u; }
+// expand 4 bits n -> 4 bytes {0,1} (FP8: {0, 0x38 = E4M3 1.0})
+__device__ __forceinline__ uint32_t spread4(uint32_t n) {
+  const uint32_t b = ((n & 0xF) * 0x00204081u) & 0x01010101u;
+  return FP8 ? b * 0x38u : b;
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -104,7 +120,7 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(128)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(MXF4 ? 512 : 128)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -112,10 +128,23 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
+#if MXF4
+  if (warp < 4) {  // unit E8M0 scales (0x7F = 2^0) in columns 256..287 of every lane
+    const uint32_t one = 0x7F7F7F7Fu;
+    for (int c = 0; c < 32; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       tmem + ((uint32_t)(32 * warp) << 16) + 256 + c), "r"(one)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#endif
   const int nchunks = kwords * 64 / KC;
   if (warp == NT / 32) {  // ---------------- MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = idesc_i8(M, M);
+      const uint32_t idesc = MXF4 ? idesc_mxf4(M, M) : idesc_i8(M, M);
       for (int c = 0; c < nchunks; c++) {
         const int b = c % NS;
         if (mode & 16) mbar_spin(&full[b], (c / NS) & 1);
@@ -123,15 +152,25 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
         if (!(mode & 64)) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = smem_u32(sm + b * CHUNK_BYTES);
 #pragma unroll
-        for (int s = 0; s < ((mode & 2) ? 1 : KC / 32); s++) {
+        for (int s = 0; s < ((mode & 2) ? 1 : (MXF4 ? KC / 64 : KC / 32)); s++) {
           const uint64_t da = SW128 ? sdesc(base + (s >> 2) * (M * 128) + (s & 3) * 32, 16, 1024)
                                     : sdesc(base + s * 256, 128, (KC / 16) * 128);
           const uint32_t acc = (c | s) ? 1u : 0u;
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+#if MXF4
+              "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
+              ::"r"(tmem), "l"(da), "l"(da), "r"(idesc), "r"(acc), "r"(tmem + 256), "r"(tmem + 272)
+              : "memory");
+#else
+#if FP8
+              "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+#else
               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+#endif
               "l"(da), "l"(da), "r"(idesc), "r"(acc)
               : "memory");
+#endif
         }
         if (!(mode & 32))
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -169,12 +208,27 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
 #pragma unroll
           for (int w = 0; w < KC / 128; w++) {
             const uint64_t xv = x[p][w];
+#if MXF4
+            // 32 bits -> 32 nibbles (16 bytes); K order within the 8 bits is
+            // permuted (0,4,1,5,..), identically for every row
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const uint32_t s = (uint32_t)(xv >> (32 * h));
+              uint4 v;
+              v.x = (spread4(s) << 1) | (spread4(s >> 4) << 5);
+              v.y = (spread4(s >> 8) << 1) | (spread4(s >> 12) << 5);
+              v.z = (spread4(s >> 16) << 1) | (spread4(s >> 20) << 5);
+              v.w = (spread4(s >> 24) << 1) | (spread4(s >> 28) << 5);
+              *(uint4 *)(bufb + koff(row, (k0 + w * 64 + h * 32) / 2)) = v;  // koff takes a byte index
+            }
+#else
 #pragma unroll
             for (int h = 0; h < 4; h++) {
               const uint32_t s = (uint32_t)(xv >> (16 * h));
               uint4 v = make_uint4(spread4(s), spread4(s >> 4), spread4(s >> 8), spread4(s >> 12));
               *(uint4 *)(bufb + koff(row, k0 + w * 64 + h * 16)) = v;
             }
+#endif
             x[p][w] = c + PF < nchunks ? src[(c + PF) * (KC / 64) + w] : 0;
           }
         }
@@ -201,11 +255,11 @@ __global__ void __launch_bounds__(NT + 32, 1) k_gram(const uint64_t *__restrict_
           : "r"(ta));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 32; j++) out[t * M + c0 + j] = v[j];
+      for (int j = 0; j < 32; j++) out[t * M + c0 + j] = (FP8 || MXF4) ? (uint32_t)__uint_as_float(v[j]) : v[j];
     }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(MXF4 ? 512 : 128) : "memory");
 }
 
 int main(int argc, char **argv) {
