@@ -43,14 +43,16 @@ constexpr int UM = 128;                 // tile rows (A operand, TMEM lanes)
 constexpr int UNMAX = 256;              // tile columns (B operand rows), at most
 constexpr int UKC = 256;                // K bits per smem chunk
 constexpr int UROWB = UKC / 2;          // expanded bytes per row and chunk (one 128-byte atom row)
-constexpr int UACH = UM * UROWB;        // expanded separate-A bytes per chunk (16 KB)
-constexpr int UTMEM = 512;              // TMEM columns: accumulator (<= 256) + block scales at 256..287
-constexpr int URING = 192 * 1024;       // raw + expanded stages: as many as fit (<= UMAXST each)
-constexpr int UMAXST = 8;               // expanded stages (raw stages: 2-3)
-constexpr int UBOXR = 128;              // raw TMA box: rows
+constexpr int UTMEM = 512;              // TMEM columns: accumulator (<= 256), A stages, block scales
+constexpr int UACOL = 256;              // A operand stages: 32 columns (one 256-bit K chunk of 128 rows) each
+constexpr int USCOL = 480;              // unit block scales (SFA at 480, SFB at 496)
+constexpr int URING = 192 * 1024;       // expanded stages, then as many raw stages as fit
+constexpr int UNST = 4;                 // expanded stages = producer groups = TMEM A stages (256..383)
+constexpr int URAWMAX = 8;              // raw TMA stages in flight (barrier slots)
+constexpr int UBOXR = 32;               // raw TMA box: rows
 constexpr int UBOXB = 128;              // raw TMA box: bytes of K (4 chunks)
-constexpr int UBOX = UBOXR * UBOXB;     // 16 KB
-constexpr int UPROD = 256;              // producer threads
+constexpr int UBOX = UBOXR * UBOXB;     // 4 KB
+constexpr int UPROD = 512;              // producer threads: UNST groups of four warps
 constexpr int UTHREADS = UPROD + 64;    // + the MMA-issuer warp + the TMA warp
 constexpr size_t USMEM = (size_t)URING + 2048;  // + alignment slack and the barriers
 
@@ -103,6 +105,35 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
 __device__ __forceinline__ uint4 nib32(uint32_t x) {
   constexpr uint32_t M2 = 0x22222222u;
   return make_uint4((x << 1) & M2, x & M2, (x >> 1) & M2, (x >> 2) & M2);
+}
+
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(p));
+  return p != 0;
+}
+
+// D[tmem] (+)= A[ta] x B[db] (kind::mxf4, unit block scales at sfa / sfb)
+__device__ __forceinline__ void umma_mxf4(uint32_t tmem, uint32_t ta, uint64_t db, uint32_t idesc, uint32_t sfa,
+                                          uint32_t sfb, bool acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(tmem),
+      "r"(ta), "l"(db), "r"(idesc), "r"((uint32_t)acc), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+
+// 32 consecutive TMEM columns of this warp's 32 lanes (lane = thread) <- e
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&e)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(e[0]), "r"(e[1]), "r"(e[2]), "r"(e[3]), "r"(e[4]), "r"(e[5]), "r"(e[6]), "r"(e[7]), "r"(e[8]), "r"(e[9]),
+      "r"(e[10]), "r"(e[11]), "r"(e[12]), "r"(e[13]), "r"(e[14]), "r"(e[15]), "r"(e[16]), "r"(e[17]), "r"(e[18]),
+      "r"(e[19]), "r"(e[20]), "r"(e[21]), "r"(e[22]), "r"(e[23]), "r"(e[24]), "r"(e[25]), "r"(e[26]), "r"(e[27]),
+      "r"(e[28]), "r"(e[29]), "r"(e[30]), "r"(e[31])
+      : "memory");
 }
 
 // Expand one row's 256-bit chunk (two 16-byte raw units) into its 128-byte

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
   }
 }
 
-// D (T densified 8 KB rows) as a 2D uint8 tensor for TMA: boxes of 128 rows x
+// D (T densified 8 KB rows) as a 2D uint8 tensor for TMA: boxes of 32 rows x
 // 128 bytes, SWIZZLE_128B, rows past T read as zero.  The encoder comes from
 // the driver through the runtime (no libcuda link).
 static int rows_tensor_map(CUtensorMap *tm, const void *D, uint64_t T) {
@@ -180,7 +180,7 @@ static int rows_tensor_map(CUtensorMap *tm, const void *D, uint64_t T) {
     }
   }
   const cuuint64_t dims[2] = {8192, T ? T : 1}, strides[1] = {8192};
-  const cuuint32_t box[2] = {(cuuint32_t)rsu::UBOXB, (cuuint32_t)rsu::UBOXR}, es[2] = {1, 1};
+  const cuuint32_t box[2] = {(cuuint32_t)rsu::UBOXB, (cuuint32_t)rsu::UBOXR}, es[2] = {1, 1};  // 128 B x 32 rows
   const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(D), dims, strides, box, es,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -220,6 +220,14 @@ __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__re
   for (int q = 0; q < 4; q++) __stcs(dst + t + DT * q, X[t + DT * q]);
 }
 
+#ifdef RS_UMMA_TRACE  // timeline of CTA 0 (tools only): 6 events x 256 chunks
+__device__ long long g_umma_trace[6][256];
+#define UTR(e, i) \
+  if (blockIdx.x == 0) g_umma_trace[e][i] = clock64()
+#else
+#define UTR(e, i)
+#endif
+
 // One CTA per tensor-core tile (see rs_umma.cuh): A = rows [r0, r0+128),
 // B = rows [c0, c0+nb) of one key segment; counts of pairs u < v go into the
 // same N x N matrix as the CUDA-core tiles.  tmD maps D as a 2D tensor
@@ -233,33 +241,33 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   extern __shared__ __align__(1024) uint8_t usm_raw[];
   // 1024-byte alignment for the swizzled TMA boxes and operand atoms
   uint8_t *usm = (uint8_t *)(((uintptr_t)usm_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t *full = (uint64_t *)(usm + URING), *empty = full + UMAXST, *rfull = empty + UMAXST,
-           *rempty = rfull + 4, *done = rempty + 4;
+  uint64_t *full = (uint64_t *)(usm + URING), *empty = full + UNST, *rfull = empty + UNST,
+           *rempty = rfull + URAWMAX, *done = rempty + URAWMAX;
   uint32_t *tslot = (uint32_t *)(done + 1);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const uint32_t seg = tp_seg[blockIdx.x];
   const uint32_t s0 = seg_start[seg], m = seg_start[seg + 1] - s0;
   const uint32_t r0 = tp_r0[blockIdx.x], c0 = tp_c0[blockIdx.x], nb = tp_nb[blockIdx.x];
   const bool shared_a = r0 == c0;  // A = the first 128 rows of the B operand
-  // raw stage: the B boxes (128 rows each) then a separate A box; expanded
-  // stage: the B operand (rows_b rows, >= the 128 rows A reads when shared),
-  // then a separate A operand
+  // raw stage: the B rows in 32-row boxes, then a separate A's 128 rows
+  // (128 bytes per row either way, so raw row r sits at r * 128); expanded
+  // stage: the B operand (rows_b rows) in shared memory -- the A operand of
+  // the same stage sits in TMEM (32 columns per chunk from column UACOL)
   const uint32_t rows_b = max(nb, (uint32_t)UM), nbox = (rows_b + UBOXR - 1) / UBOXR;
-  const uint32_t rbytes = nbox * UBOX + (shared_a ? 0 : UBOX);
-  const uint32_t bbytes = rows_b * UROWB, sbytes = bbytes + (shared_a ? 0 : UACH);
-  const int nraw = rbytes <= (uint32_t)UBOX ? 3 : 2;
-  const int nst = min(UMAXST, (int)((URING - nraw * rbytes) / sbytes));
+  const uint32_t rbytes = nbox * UBOX + (shared_a ? 0u : (uint32_t)(UM * UBOXB));
+  const uint32_t sbytes = rows_b * UROWB;
+  const int nraw = min(URAWMAX, (int)((URING - UNST * sbytes) / rbytes));
   uint8_t *raw = usm, *xst = usm + nraw * rbytes;
   // expanded rows never written below (past m, past nb) must read as zero
-  for (uint32_t i = t; i < nst * sbytes / 16; i += UTHREADS) ((uint4 *)xst)[i] = make_uint4(0, 0, 0, 0);
+  for (uint32_t i = t; i < UNST * sbytes / 16; i += UTHREADS) ((uint4 *)xst)[i] = make_uint4(0, 0, 0, 0);
   if (t == 0) {
-    for (int i = 0; i < nst; i++) {
-      ubar_init(&full[i], 1);
+    for (int i = 0; i < UNST; i++) {
+      ubar_init(&full[i], 4);  // the four warps of the stage's producer group
       ubar_init(&empty[i], 1);
     }
     for (int i = 0; i < nraw; i++) {
       ubar_init(&rfull[i], 1);
-      ubar_init(&rempty[i], UBOXB * 8 / UKC);  // the warps of the box's chunks
+      ubar_init(&rempty[i], UPROD / 32);  // every producer warp reads each box
     }
     ubar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -275,11 +283,11 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
-  if (warp < 4) {  // unit block scales: 0x7F (E8M0 2^0) in columns 256..287 of every lane
+  if (warp < 4) {  // unit block scales: 0x7F (E8M0 2^0) in columns USCOL.. of every lane
     const uint32_t one = 0x7F7F7F7Fu;
     for (int c = 0; c < 32; c += 8)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                       tmem + ((uint32_t)(32 * warp) << 16) + 256 + c),
+                       tmem + ((uint32_t)(32 * warp) << 16) + USCOL + c),
                    "r"(one)
                    : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -288,82 +296,128 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   constexpr int NCH = RS_WORDS * 64 / UKC;   // 256-bit chunks per row
-  constexpr int NRAW = 8192 / UBOXB;         // raw boxes per row
-  constexpr int CPB = UBOXB * 8 / UKC;       // chunks per raw box (4)
+  constexpr int NRAW = 8192 / UBOXB;         // raw boxes per row (one K chunk per producer group)
+  static_assert(NCH == NRAW * UNST, "one chunk per producer group and raw box");
   if (warp == UPROD / 32 + 1) {  // ------------------------------ TMA (raw rows)
     if (lane == 0) {
+      uint32_t st = 0, ph = 0;
       for (int r = 0; r < NRAW; r++) {
-        const int st = r % nraw;
-        if (r >= nraw) ubar_wait(&rempty[st], ((r - nraw) / nraw) & 1);
+        if (r >= nraw) ubar_wait(&rempty[st], ph ^ 1u);
         uint8_t *dst = raw + st * rbytes;
+        UTR(4, r);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rfull[st])), "r"(rbytes)
                      : "memory");
-        for (uint32_t bx = 0; bx <= nbox - (shared_a ? 1u : 0u); bx++) {
-          const uint32_t row = bx < nbox ? s0 + c0 + bx * UBOXR : s0 + r0;  // the last box is A when separate
+        const uint32_t nload = nbox + (shared_a ? 0u : (uint32_t)(UM / UBOXR));
+        for (uint32_t bx = 0; bx < nload; bx++) {
+          // B boxes, then a separate A's
+          const uint32_t row = bx < nbox ? s0 + c0 + bx * UBOXR : s0 + r0 + (bx - nbox) * UBOXR;
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
               "[%4];" ::"r"(su32(dst + bx * UBOX)),
               "l"((uint64_t)&tmD), "r"(r * UBOXB), "r"(row), "r"(su32(&rfull[st]))
               : "memory");
         }
+        if (++st == (uint32_t)nraw) {
+          st = 0;
+          ph ^= 1u;
+        }
       }
     }
   } else if (warp == UPROD / 32) {  // ------------------------------ MMA issuer
-    // the whole warp walks the stages (no lane diverges into a spin-wait
-    // while lane 0 issues); lane 0 issues the MMAs and the commits
+    // The whole warp walks the stages with warp-uniform state (stage, phase,
+    // descriptors stay in uniform registers) and one elected lane issues: a
+    // single issuing thread is instruction-latency bound, so per chunk there
+    // is one wait, four MMAs and one commit, and nothing else.
     const uint32_t idesc = idesc_mxf4(UM, (int)nb);
+    const uint64_t db0 = sw128_desc(su32(xst));
+    const uint32_t sstep = sbytes >> 4;  // descriptor address units per stage
+    const uint32_t sfa = tmem + USCOL, sfb = tmem + USCOL + 16u;
+    uint32_t b = 0, ph = 0;
     for (int c = 0; c < NCH; c++) {
-      const int b = c % nst;
-      ubar_wait(&full[b], (c / nst) & 1);
-      if (lane == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t bb = su32(xst + b * sbytes), ba = shared_a ? bb : bb + bbytes;
-#pragma unroll
-        for (int k = 0; k < UKC / 64; k++) {  // K = 64 nibbles = 32 bytes of the 128-byte atom row
-          const uint64_t da = sw128_desc(ba + k * 32);
-          const uint64_t db = sw128_desc(bb + k * 32);
-          const uint32_t acc = (c | k) ? 1u : 0u;
-          asm volatile(
-              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n}\n"
-              ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(tmem + 256u), "r"(tmem + 272u)
-              : "memory");
-        }
+      ubar_wait(&full[b], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t db = db0 + (uint64_t)(b * sstep);
+      const uint32_t ta = tmem + UACOL + 32u * b;
+      if (elect_one()) {
+        UTR(2, c);
+        // K = 64 nibbles per MMA: 8 TMEM columns of A, 32 bytes (2 descriptor units) of the B atom row
+        umma_mxf4(tmem, ta, db, idesc, sfa, sfb, c > 0);
+        umma_mxf4(tmem, ta + 8u, db + 2, idesc, sfa, sfb, true);
+        umma_mxf4(tmem, ta + 16u, db + 4, idesc, sfa, sfb, true);
+        umma_mxf4(tmem, ta + 24u, db + 6, idesc, sfa, sfb, true);
         umma_commit(&empty[b]);
+        UTR(3, c);
         if (c == NCH - 1) umma_commit(done);
       }
       __syncwarp();
+      if (++b == (uint32_t)UNST) {
+        b = 0;
+        ph ^= 1u;
+      }
     }
   } else {  // ------------------------------------------- producers
-    // warp c % nst expands chunk c (so each stage has one producer and its
-    // mbarrier phases are waited in order): every B row (and a separate A's
-    // rows) from the raw box, whose 128-byte rows have their 16-byte units
-    // XOR-swizzled by row % 8 (conflict-free: eight consecutive rows hit
-    // eight units).  nst is 8 for 128-row tiles, 4 otherwise.
-    const uint32_t nrow_b = c0 < m ? min(nb, m - c0) : 0u, nrow_a = shared_a ? 0u : min((uint32_t)UM, m - r0);
-    for (int c = warp; warp < nst && c < NCH; c += nst) {
-      const int r = c / CPB, q = c % CPB, st = r % nraw, b = c % nst;
-      ubar_wait(&rfull[st], (r / nraw) & 1);
-      if (c >= nst) ubar_wait(&empty[b], ((c - nst) / nst) & 1);
+    // UNST groups of four warps; group g expands K chunk g of every raw box
+    // (chunk 4r + g) into its own stage g, so stage and phases advance by
+    // one per box with no arithmetic.  Warp q of a group owns rows 32q +
+    // lane (+128): it expands them from the raw box -- 128-byte rows whose
+    // 16-byte units are XOR-swizzled by row % 8 -- into the B atom rows in
+    // shared memory, and writes rows < 128 of A (B's own rows, or the
+    // separate A rows) into the stage's TMEM columns with one tcgen05.st
+    // (warp q reaches TMEM lanes 32q..32q+31 = those rows); rows past the key
+    // are zeros.
+    const int grp = warp >> 2, q = warp & 3;
+    const uint32_t nrow_b = c0 < m ? min(nb, m - c0) : 0u, nrow_a = shared_a ? nrow_b : min((uint32_t)UM, m - r0);
+    const uint32_t arow = 32 * q + lane, sw = arow & 7;
+    const uint32_t aoff = (shared_a ? 0u : nbox * UBOX) + arow * UBOXB;
+    const uint32_t u0 = ((2 * grp) ^ sw) << 4, u1 = ((2 * grp + 1) ^ sw) << 4;  // this chunk's two raw units
+    uint8_t *sb = xst + grp * sbytes;
+    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + UACOL + 32u * grp;
+    uint32_t st = 0, rph = 0, eph = 0;
+    for (int r = 0; r < NRAW; r++) {
+      const int c = 4 * r + grp;
+      ubar_wait(&rfull[st], rph);
+      UTR(5, c);
+      if (r) {
+        ubar_wait(&empty[grp], eph);
+        eph ^= 1u;
+      }
+      UTR(0, c);
       const uint8_t *rs = raw + st * rbytes;
-      uint8_t *sb = xst + b * sbytes;
-      for (uint32_t row = lane; row < nrow_b; row += 32) {
-        const uint8_t *p = rs + (row / UBOXR) * UBOX + (row & (UBOXR - 1)) * UBOXB;
-        const uint32_t sw = row & 7;
-        expand_row(sb, (int)row, (int)rows_b, *(const uint4 *)(p + (((2 * q) ^ sw) << 4)),
-                   *(const uint4 *)(p + (((2 * q + 1) ^ sw) << 4)));
+      uint32_t e[32];
+      {  // A row arow (and B row arow when shared)
+        uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
+        if (arow < nrow_a) {
+          lo = *(const uint4 *)(rs + aoff + u0);
+          hi = *(const uint4 *)(rs + aoff + u1);
+        }
+        const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const uint4 v = nib32(w[u]);
+          e[4 * u] = v.x; e[4 * u + 1] = v.y; e[4 * u + 2] = v.z; e[4 * u + 3] = v.w;
+          if (shared_a && arow < nrow_b) *(uint4 *)(sb + sw_off((int)arow, 16 * u, (int)rows_b)) = v;
+        }
       }
-      for (uint32_t row = lane; row < nrow_a; row += 32) {
-        const uint8_t *p = rs + nbox * UBOX + row * UBOXB;
-        const uint32_t sw = row & 7;
-        expand_row(sb + bbytes, (int)row, UM, *(const uint4 *)(p + (((2 * q) ^ sw) << 4)),
-                   *(const uint4 *)(p + (((2 * q + 1) ^ sw) << 4)));
+      tmem_st32(ta, e);
+      // the other B rows: all of them for a separate A, rows >= 128 otherwise
+      for (uint32_t row = shared_a ? UM + arow : arow; row < nrow_b; row += UM) {
+        const uint8_t *p = rs + row * UBOXB;
+        const uint32_t rsw = row & 7;
+        expand_row(sb, (int)row, (int)rows_b, *(const uint4 *)(p + (((2 * grp) ^ rsw) << 4)),
+                   *(const uint4 *)(p + (((2 * grp + 1) ^ rsw) << 4)));
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        ubar_arrive(&full[b]);
-        ubar_arrive(&rempty[st]);  // this chunk's reads of the raw box are done
+        UTR(1, c);
+        ubar_arrive(&full[grp]);
+        ubar_arrive(&rempty[st]);  // this warp's reads of the raw box are done
+      }
+      if (++st == (uint32_t)nraw) {
+        st = 0;
+        rph ^= 1u;
       }
     }
   }
@@ -739,6 +793,17 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
     RS_TRY(rows_tensor_map(&tmD, D, g.T));
     RS_LAUNCH_PROF("allpairs_umma", nup, k_allpairs_umma, (unsigned)nup, rsu::UTHREADS, rsu::USMEM, d_useg, d_ur0,
                    d_uc0, d_unb, g.seg_start, tmD, item_bm, N, Mx);
+#ifdef RS_UMMA_TRACE
+    {
+      long long h[6][256];
+      cudaStreamSynchronize(g_stream);
+      cudaMemcpyFromSymbol(h, g_umma_trace, sizeof h);
+      const long long t0 = h[4][0];
+      for (int c = 0; c < 256; c += 1)
+        fprintf(stderr, "c=%3d raw(box)=%7lld rfull=%7lld start=%7lld full=%7lld issue=%7lld commit=%7lld\n", c,
+                c < 64 ? h[4][c] - t0 : 0, h[5][c] - t0, h[0][c] - t0, h[1][c] - t0, h[2][c] - t0, h[3][c] - t0);
+    }
+#endif
   }
   if (!ntp) {
   } else if (tiles2)

@@ -31,14 +31,15 @@ __device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db, uin
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(128, 1) k_rate(int n, int reps, unsigned long long *cyc) {
+__global__ void __launch_bounds__(128, 1) k_rate(int n, int reps, unsigned long long *cyc, int commit_every, uint32_t fill) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tslot;
   const int t = threadIdx.x, warp = t >> 5;
-  for (int i = t; i < 64 * 1024 / 16; i += 128) ((uint4 *)sm)[i] = make_uint4(0, 0, 0, 0);
+  for (int i = t; i < 64 * 1024 / 16; i += 128) ((uint4 *)sm)[i] = make_uint4(fill, fill * 3u, fill ^ (i * 0x9E3779B9u), fill);
   if (t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(128, 1) k_rate(int n, int reps, unsigned long 
     for (int r = 0; r < reps; r++) {
 #pragma unroll
       for (int s = 0; s < 4; s++) mma<KIND>(tmem, da + 2 * s, db + 2 * s, idesc, (r | s) ? 1u : 0u);
+      if (commit_every && (r % commit_every) == commit_every - 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar2)) : "memory");
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
     asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(smem_u32(&bar)) : "memory");
@@ -83,27 +86,28 @@ __global__ void __launch_bounds__(128, 1) k_rate(int n, int reps, unsigned long 
 }
 
 template <int KIND>
-void run(const char *name, int kper) {
+void run(const char *name, int kper, int ce = 0, uint32_t fill = 0) {
   unsigned long long *d;
   cudaMalloc(&d, 8);
   cudaFuncSetAttribute(k_rate<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   for (int n : {128, 256}) {
     const int reps = 2000;
-    k_rate<KIND><<<148, 128, 64 * 1024>>>(n, reps, d);
+    k_rate<KIND><<<148, 128, 64 * 1024>>>(n, reps, d, ce, fill);
     cudaError_t e = cudaDeviceSynchronize();
     unsigned long long c = 0;
     cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
     const double per = (double)c / (reps * 4.0);
-    printf("%-8s N=%3d: %s  %.1f clk/MMA  %.0f MAC/clk/SM (M=128, K=%d)\n", name, n, cudaGetErrorString(e), per,
+    printf("%-8s fill=%08x commit/%d N=%3d: %s  %.1f clk/MMA  %.0f MAC/clk/SM (M=128, K=%d)\n", name, fill, ce, n, cudaGetErrorString(e), per,
            128.0 * n * kper / per, kper);
   }
   cudaFree(d);
 }
 
 int main() {
-  run<0>("i8", 32);
-  run<1>("e4m3", 32);
-  run<2>("mxf4", 64);
-  run<3>("bf16", 16);
+  run<2>("mxf4", 64, 0);
+  run<2>("mxf4", 64, 1);
+  run<2>("mxf4", 64, 4);
+  run<2>("mxf4", 64, 64);
+  run<2>("mxf4", 64, 1999);
   return 0;
 }
