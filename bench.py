@@ -49,47 +49,102 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + clock-event-reason sampling DURING the timed region (the
+    B200_PROFILING.md clocks line).  The C2 timed region is tens of ms, shorter
+    than one `nvidia-smi -lms 200` start-up, so the sampler is an NVML polling
+    thread (same counters nvidia-smi reads: clocks.sm, clocks.max.sm,
+    clocks_event_reasons.*) at ~2 ms; nvidia-smi is the fallback.  Rows from
+    several regions (device-timed and e2e) accumulate in one object."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason{HwSlowdown,HwThermalSlowdown,SwThermalSlowdown,SwPowerCap}
 
     def __init__(self, device: int):
-        self.device, self.rows, self._p = device, [], None
+        self.device, self.rows, self._p, self._nv, self.max_mhz = device, [], None, None, None
+        self.source = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(device)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._nv, self._h, self.source = pynvml, h, "nvml"
+        except Exception:
+            self._nv = None
+
+    def region(self):
+        return _ClockRegion(self)
+
+    def _poll_nvml(self, stop):
+        nv, h = self._nv, self._h
+        while True:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                self.rows.append((sm, rs))
+            except Exception:
+                return
+            if stop.wait(0.002):
+                return
+
+    def _read_smi(self, p):
+        for line in p.stdout:
+            r = [x.strip() for x in line.split(",")]
+            try:
+                bits = sum(b for b, v in zip(self.BITS, r[5:9]) if v.lower() == "active")
+                self.rows.append((float(r[1]), bits))
+                self.max_mhz = float(r[2])
+            except (ValueError, IndexError):
+                pass
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no clock samples"]}
+        reasons = sorted({n for _, rs in self.rows for n, b in zip(self.NAMES, self.BITS) if rs & b})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.rows), "sm_max_mhz": self.max_mhz,
+                "sm_min_mhz": min(sm for sm, _ in self.rows), "reasons": reasons, "samples": len(self.rows),
+                "source": self.source or "nvidia-smi"}
+
+
+class _ClockRegion:
+    def __init__(self, c: Clocks):
+        self.c, self._stop, self._t, self._p = c, threading.Event(), None, None
 
     def __enter__(self):
-        try:
-            self._p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+        c = self.c
+        if c._nv is not None:
+            self._t = threading.Thread(target=c._poll_nvml, args=(self._stop,), daemon=True)
+        else:
+            try:
+                self._p = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(c.device), f"--query-gpu={c.Q}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self._t = threading.Thread(target=c._read_smi, args=(self._p,), daemon=True)
+            except Exception:
+                self._p = None
+        if self._t:
             self._t.start()
-        except Exception:
-            self._p = None
-        return self
-
-    def _read(self):
-        for line in self._p.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+        return c
 
     def __exit__(self, *a):
+        self._stop.set()
         if self._p:
             self._p.terminate()
             try:
                 self._p.wait(timeout=5)
             except Exception:
                 self._p.kill()
-
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if self._t:
+            self._t.join(timeout=5)
 
 
 def dist_env():
@@ -251,7 +306,8 @@ def run_gpu(args):
     dist_barrier(dist)
     _lib.synchronize()
     k0 = _lib.kernel_launches()
-    with Clocks(local) as clk:
+    clk = Clocks(local)
+    with clk.region():
         e0 = _lib.Event()
         for _ in range(args.steps):
             step()
@@ -343,9 +399,10 @@ def run_gpu(args):
             _lib.synchronize()
             t0 = time.perf_counter()
             h2d = d2h = 0
-            for _ in range(n_e2e):
-                h2d, d2h = e2e_step(export)
-            _lib.synchronize()
+            with clk.region():
+                for _ in range(n_e2e):
+                    h2d, d2h = e2e_step(export)
+                _lib.synchronize()
             return dist_max(dist, (time.perf_counter() - t0) * 1e3 / n_e2e), h2d, d2h
 
         e2e_ms, h2d, d2h = e2e_time(False)
