@@ -285,8 +285,10 @@ class BitmapBatch:
         """(|B_i ∩ B_j|, |B_i ∪ B_j|) for all i<j in row-major order."""
         n = len(self)
         m = n * (n - 1) // 2
-        inter = np.zeros(max(m, 1), dtype=np.uint64)
-        uni = np.zeros(max(m, 1), dtype=np.uint64)
+        # every entry is written by the call; large results land in recycled
+        # page-locked memory (PCIe-rate readback, no first-touch faults)
+        inter = _lib.pinned_pool.empty(max(m, 1), np.uint64)
+        uni = _lib.pinned_pool.empty(max(m, 1), np.uint64)
         check(lib().rs_all_pairs_cardinality(self._h, inter.ctypes.data, uni.ctypes.data))
         return inter[:m], uni[:m]
 

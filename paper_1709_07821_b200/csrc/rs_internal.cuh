@@ -98,7 +98,8 @@ int materialize(const rs_batch *b);        // queue a deferred batch's unpack/ga
 void drop_staged(rs_batch *b);             // release an unused deferred batch's staging slot
 template <typename T> int scan_exclusive(const T *in, T *out, uint64_t n);
 template <typename T> int scan_inclusive(const T *in, T *out, uint64_t n);
-int sort_u64(uint64_t *keys, uint64_t n, int end_bit);
+// LSD radix sort of bits [begin_bit, end_bit) (stable: equal keys keep their order)
+int sort_u64(uint64_t *keys, uint64_t n, int end_bit, int begin_bit = 0);
 int d2h(void *h, const void *d, size_t bytes);   // synchronous on g_stream
 // RS_TRACE=1: synchronize and print host wall time per phase (diagnostics only)
 void trace(const char *phase);

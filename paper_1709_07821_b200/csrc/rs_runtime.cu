@@ -273,17 +273,17 @@ template int scan_exclusive<uint64_t>(const uint64_t *, uint64_t *, uint64_t);
 template int scan_inclusive<uint32_t>(const uint32_t *, uint32_t *, uint64_t);
 template int scan_inclusive<uint64_t>(const uint64_t *, uint64_t *, uint64_t);
 
-int sort_u64(uint64_t *keys, uint64_t n, int end_bit) {
+int sort_u64(uint64_t *keys, uint64_t n, int end_bit, int begin_bit) {
   if (n <= 1) return RS_OK;
   uint64_t *alt = (uint64_t *)dalloc(n * 8);
   if (!alt) { set_error("device allocation failed (sort)"); return RS_ENOMEM; }
   cub::DoubleBuffer<uint64_t> db(keys, alt);
   size_t tmp = 0;
-  RS_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)n, 0, end_bit, g_stream));
+  RS_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)n, begin_bit, end_bit, g_stream));
   void *t = dalloc(tmp);
   if (!t) { dfree(alt); set_error("device allocation failed (sort)"); return RS_ENOMEM; }
-  RS_CK(cub::DeviceRadixSort::SortKeys(t, tmp, db, (int64_t)n, 0, end_bit, g_stream));
-  g_launches += (end_bit + 7) / 8 + 2;
+  RS_CK(cub::DeviceRadixSort::SortKeys(t, tmp, db, (int64_t)n, begin_bit, end_bit, g_stream));
+  g_launches += (end_bit - begin_bit + 7) / 8 + 2;
   if (db.Current() != keys)
     RS_CK(cudaMemcpyAsync(keys, db.Current(), n * 8, cudaMemcpyDeviceToDevice, g_stream));
   dfree(t);

@@ -18,6 +18,11 @@ namespace {
 
 unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
 
+bool env_flag_(const char *name) {
+  const char *v = getenv(name);
+  return v && *v == '1';
+}
+
 // item t of the ordered selection -> container index; sort key = key << 40 | t
 __global__ void k_group_keys(uint64_t T, uint64_t nsel, const uint64_t *__restrict__ qbase,
                              const uint64_t *__restrict__ qsrc, DevBatch S, uint64_t *__restrict__ keys,
@@ -218,6 +223,97 @@ __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__re
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < 4; q++) __stcs(dst + t + DT * q, X[t + DT * q]);
+}
+
+// The same rows, one WARP per container (persistent over the items, with the
+// next item's metadata loaded before the current row is built).  k_densify's
+// CTA per 8 KB row was latency-bound (125 k CTAs of dependent metadata loads,
+// two block barriers each: 2.9 TB/s of row writes on config 5).  Here a
+// bitset row is 16 independent 16-byte loads per lane then 16 streaming
+// stores; an array / run row is built in the warp's own 8 KB of shared
+// memory (16-byte zeroing, 16-byte value loads masked to n, native shared
+// ORs) and streamed out with 16-byte stores.  No block barriers.
+constexpr int DW_WARPS = 4;  // 4 x 8 KB rows of shared memory per CTA; 6 CTAs per SM (80 registers)
+__global__ void __launch_bounds__(32 * DW_WARPS) k_densify_warp(uint64_t T, const uint32_t *__restrict__ item_c,
+                                                                DevBatch S, uint64_t *__restrict__ D) {
+  __shared__ __align__(16) uint4 Xs[DW_WARPS][RS_WORDS / 2];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint4 *X = Xs[wib];
+  uint32_t *X32 = (uint32_t *)X;
+  const uint64_t step = (uint64_t)gridDim.x * DW_WARPS;
+  uint64_t i = (uint64_t)blockIdx.x * DW_WARPS + wib;
+  if (i >= T) return;
+  uint32_t c = item_c[i];
+  uint8_t type = S.type[c];
+  uint64_t off = S.off[c];
+  uint32_t n = S.n[c];
+  for (;;) {
+    // next item's metadata first: its dependent loads overlap this row
+    const uint64_t ni = i + step;
+    uint32_t nc = 0, nn = 0;
+    uint8_t ntype = 0;
+    uint64_t noff = 0;
+    if (ni < T) {
+      nc = item_c[ni];
+      ntype = S.type[nc];
+      noff = S.off[nc];
+      nn = S.n[nc];
+    }
+    uint4 *dst = (uint4 *)(D + i * RS_WORDS);
+    if (type == RS_TAG_BITSET) {
+      const uint4 *src = (const uint4 *)(S.pool + off);
+      uint4 r[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) r[q] = __ldcs(src + lane + 32 * q);
+#pragma unroll
+      for (int q = 0; q < 16; q++) __stcs(dst + lane + 32 * q, r[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; q++) X[lane + 32 * q] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      if (type == RS_TAG_ARRAY) {
+        const uint4 *v = (const uint4 *)(S.pool + off);
+        const uint32_t nv = (n + 7) >> 3;
+        for (uint32_t k = lane; k < nv; k += 32) {
+          const uint4 x = v[k];
+          const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+          const uint32_t left = n - 8 * k;  // values of this vector inside the array
+#pragma unroll
+          for (int h = 0; h < 8; h++) {
+            if ((uint32_t)h < left) {
+              const uint32_t val = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+              atomicOr(&X32[val >> 5], 1u << (val & 31));
+            }
+          }
+        }
+      } else {  // runs (_words_from_runs, containers.py:122-135): edge words by atomics, interior by stores
+        const uint32_t *r32 = (const uint32_t *)(S.pool + off);
+        for (uint32_t r = lane; r < n; r += 32) {
+          const uint32_t sl = r32[r];
+          const uint32_t s = sl & 0xFFFF, e = s + (sl >> 16);
+          const uint32_t ws = s >> 5, we = e >> 5;
+          const uint32_t first = ~0u << (s & 31), last = ~0u >> (31 - (e & 31));
+          if (ws == we) {
+            atomicOr(&X32[ws], first & last);
+          } else {
+            atomicOr(&X32[ws], first);
+            atomicOr(&X32[we], last);
+            for (uint32_t w = ws + 1; w < we; w++) X32[w] = ~0u;
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 16; q++) __stcs(dst + lane + 32 * q, X[lane + 32 * q]);
+      __syncwarp();  // the row is read out before the next item zeroes it
+    }
+    if (ni >= T) break;
+    i = ni;
+    c = nc;
+    type = ntype;
+    off = noff;
+    n = nn;
+  }
 }
 
 #ifdef RS_UMMA_TRACE  // timeline of CTA 0 (tools only): 6 events x 256 chunks
@@ -646,7 +742,9 @@ int group_by_key(const rs_batch *in, const std::vector<uint64_t> &sel, Grouped &
   RS_TRY(h2d(d_qb, qbase.data(), (n + 1) * 8));
   RS_TRY(h2d(d_qs, qsrc.data(), (n + 1) * 8));
   RS_LAUNCH(k_group_keys, grid_for(T, 256), 256, 0, T, n, d_qb, d_qs, in->dev(), g.keys, g.item_c);
-  RS_TRY(sort_u64(g.keys, T, 56));
+  // the low 40 bits (item index) are already ascending: a stable sort of the
+  // 16-bit key field alone gives the full order (2 radix passes instead of 7)
+  RS_TRY(sort_u64(g.keys, T, 56, 40));
   // item index after the sort comes from the low 40 bits: reorder item_c
   RS_LAUNCH(k_seg_flags, grid_for(T + 1, 256), 256, 0, T, g.keys, flag);
   RS_TRY(scan_exclusive<uint32_t>(flag, pos, T + 1));
@@ -781,8 +879,19 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
   RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
   trace("allpairs: uploads + memset + item_bm");
-  RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
+  if (env_flag_("RS_DENSIFY_CTA")) {  // the CTA-per-row kernel (A/B only)
+    RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
+  } else {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t g_need = (g.T + DW_WARPS - 1) / DW_WARPS;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g_need, (uint64_t)sms * 6));
+    RS_LAUNCH_PROF("densify", g.T, k_densify_warp, grid, 32 * DW_WARPS, 0, g.T, g.item_c, in->dev(), D);
+  }
   trace("allpairs: densify");
+  // (running the tensor-core and CUDA-core tiles concurrently on side streams
+  // measured no faster: 1.078 vs 1.087 ms, the umma tiles slowing 0.44 -> 0.50)
   if (nup) {
     static bool attr = false;
     if (!attr) {
@@ -818,8 +927,8 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   ++g_launches;
   RS_CK(cudaGetLastError());
   trace("allpairs: upper triangle");
-  RS_TRY(d2h(inter, d_inter, npairs * 8));
-  if (uni) RS_TRY(d2h(uni, d_uni, npairs * 8));
+  if (uni) RS_CK(cudaMemcpyAsync(uni, d_uni, npairs * 8, cudaMemcpyDeviceToHost, g_stream));
+  RS_TRY(d2h(inter, d_inter, npairs * 8));  // one synchronization for both
   trace("allpairs: readback");
   dfree(D); dfree(item_bm); dfree(d_tseg); dfree(d_ti); dfree(d_tj); dfree(Mx); dfree(d_inter); dfree(d_uni);
   dfree(d_useg); dfree(d_ur0); dfree(d_uc0); dfree(d_unb);

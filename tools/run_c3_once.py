@@ -7,7 +7,7 @@ n = 1_000_000
 buf, offs = synth.config3(npairs=n)
 A = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, 0, n))
 B = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, n, 2 * n))
-for op in ("and", "or", "and", "or"):
+for op in os.environ.get("RUN_OPS", "and,or,and,or").split(","):
     A.container_pairwise(op, B)
 _lib.synchronize()
 print("ok")
