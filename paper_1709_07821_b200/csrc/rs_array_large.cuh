@@ -177,34 +177,33 @@ __device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t 
   }
 }
 
-// Keep the values of P (np, sorted) whose bit in X equals `want`, in order:
+// Keep the values of P (np, sorted) whose bit in X equals WANT, in order:
 // warp w probes a contiguous run of P (up to 8 rounds of 32 value pairs), the
 // kept flags become ballots, a CTA scan of the warp totals places each run,
 // and the kept values go straight to dst with 16-bit stores (consecutive
 // lanes write consecutive values).  Returns the kept count on every consumer.
-__device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np, uint32_t X, uint32_t want,
-                                                 uint16_t *dst, uint32_t (*red2)[LT / 32], uint64_t *release) {
+// The round count is CTA-uniform and the reads are clamped into P, so a round
+// has no divergent branch (lanes past the end only drop out of the ballots).
+template <uint32_t WANT>
+__device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np, uint32_t X, uint16_t *dst,
+                                                 uint32_t (*red2)[LT / 32], uint64_t *release) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t *P32 = (const uint32_t *)P;
   const uint32_t np2 = (np + 1) >> 1;
-  const uint32_t cw = (np2 + 255) / 256 * 32;  // value pairs per warp, <= 256
-  const uint32_t beg = w * cw;
+  const uint32_t nr = (np2 + 255) >> 8;  // rounds of 32 value pairs per warp, <= 8
+  const uint32_t beg = w * nr * 32u + lane, last = np2 ? np2 - 1 : 0;
   uint32_t BL[8], BH[8], XV[8], tot = 0;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
     BL[r] = BH[r] = XV[r] = 0;
-    if (32u * r < cw) {
-      const uint32_t i = beg + 32u * r + lane;
-      bool klo = false, khi = false;
-      if (i < np2) {
-        const uint32_t x = P32[i];
-        XV[r] = x;
-        const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
-        klo = (__funnelshift_r(wl, 0u, x) & 1u) == want;
-        khi = 2 * i + 1 < np && (__funnelshift_r(wh, 0u, x >> 16) & 1u) == want;
-      }
-      BL[r] = __ballot_sync(0xffffffffu, klo);
-      BH[r] = __ballot_sync(0xffffffffu, khi);
+    if ((uint32_t)r < nr) {
+      const uint32_t i = beg + 32u * r;
+      const uint32_t x = P32[min(i, last)];
+      XV[r] = x;
+      const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
+      const uint32_t bl = __funnelshift_r(wl, 0u, x) & 1u, bh = __funnelshift_r(wh, 0u, x >> 16) & 1u;
+      BL[r] = __ballot_sync(0xffffffffu, (bl == WANT) & (i < np2));
+      BH[r] = __ballot_sync(0xffffffffu, (bh == WANT) & (2 * i + 1 < np));
       tot += __popc(BL[r]) + __popc(BH[r]);
     }
   }
@@ -223,15 +222,13 @@ __device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np,
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
     for (int r = 0; r < 8; r++) {
-      if (32u * r < cw) {
+      if ((uint32_t)r < nr) {
         const uint32_t bl = BL[r], bh = BH[r];
         const uint32_t klo = (bl >> lane) & 1u, khi = (bh >> lane) & 1u;
-        if (klo | khi) {
-          const uint32_t x = XV[r];
-          const uint32_t pos = base + __popc(bl & lt) + __popc(bh & lt);
-          if (klo) dst[pos] = (uint16_t)x;
-          if (khi) dst[pos + klo] = (uint16_t)(x >> 16);
-        }
+        const uint32_t x = XV[r];
+        const uint32_t pos = base + __popc(bl & lt) + __popc(bh & lt);
+        if (klo) dst[pos] = (uint16_t)x;
+        if (khi) dst[pos + klo] = (uint16_t)(x >> 16);
         base += __popc(bl) + __popc(bh);
       }
     }
@@ -270,14 +267,15 @@ __device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_
 //     before the scan barrier, which every consumer passes before the next
 //     pair's scatter; array results are staged in XA (re-zeroed behind a
 //     barrier).
-__device__ uint32_t large_pair(const LargeSmem &sm, int op, const uint16_t *A, uint32_t na, const uint16_t *B,
+template <int op>
+__device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, const uint16_t *A, uint32_t na, const uint16_t *B,
                                uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
                                uint64_t *release) {
   const int t = threadIdx.x;
   uint32_t *XA = sm.XA(), *XB = sm.XB();
   type = RS_TAG_ARRAY;
-  if (op == RS_OP_AND || op == RS_OP_ANDNOT) {
-    const bool is_and = op == RS_OP_AND;
+  if constexpr (op == RS_OP_AND || op == RS_OP_ANDNOT) {
+    constexpr bool is_and = op == RS_OP_AND;
     const bool a_small = is_and ? na <= nb : true;
     const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
     if (16 * ns <= nl) {
@@ -305,8 +303,8 @@ __device__ uint32_t large_pair(const LargeSmem &sm, int op, const uint16_t *A, u
     const uint32_t xs = rsb::smem_u32(X);
     scatter(build_a ? A : B, build_a ? na : nb, xs);
     cbar();
-    const uint32_t total = probe_filter(build_a ? B : A, build_a ? nb : na, xs, is_and ? 1u : 0u,
-                                        (uint16_t *)dst, sm.h->red[parity], release);
+    const uint32_t total = probe_filter<is_and ? 1u : 0u>(build_a ? B : A, build_a ? nb : na, xs, (uint16_t *)dst,
+                                                           sm.h->red[parity], release);
     // every probe of X is done (scan barrier above): clear it for pair + 2
     ((uint4 *)X)[t] = make_uint4(0, 0, 0, 0);
     ((uint4 *)X)[t + LT] = make_uint4(0, 0, 0, 0);
@@ -384,8 +382,8 @@ __device__ uint32_t large_pair(const LargeSmem &sm, int op, const uint16_t *A, u
 // Persistent, warp-specialized byte ring over items i = blockIdx.x + k*gridDim.x.
 // meta_of(i, aoff, boff) -> LargeMeta (runs on the producer lane only);
 // sink(meta, card, type, n) runs on every consumer thread after the pair.
-template <typename MetaOf, typename Sink>
-__device__ void large_loop(uint8_t *raw, uint32_t count, int op, const uint8_t *poolA, const uint8_t *poolB,
+template <int op, typename MetaOf, typename Sink>
+__device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, const uint8_t *poolB,
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
   const int t = threadIdx.x;
   const LargeSmem sm = large_layout(raw);
@@ -450,7 +448,7 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, int op, const uint8_t *
     const LargeMeta m = sm.h->meta[s];
     uint8_t type;
     uint32_t n;
-    const uint32_t card = large_pair(sm, op, (const uint16_t *)(sm.R() + m.aoff), m.na,
+    const uint32_t card = large_pair<op>(sm, (const uint16_t *)(sm.R() + m.aoff), m.na,
                                      (const uint16_t *)(sm.R() + m.boff), m.nb, opool ? opool + m.dst : nullptr,
                                      k & 1, type, n, &sm.h->empty[s]);
     sink(m, card, type, n);

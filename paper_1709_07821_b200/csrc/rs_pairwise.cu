@@ -636,7 +636,8 @@ int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBat
 
 // ------------------------------------ large array x array (smem bitset + TMA)
 
-__global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(int op, const uint32_t *__restrict__ list,
+template <int OP>
+__global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(const uint32_t *__restrict__ list,
                                                                const uint64_t *__restrict__ laoff,
                                                                const uint64_t *__restrict__ lboff,
                                                                const uint32_t *__restrict__ lnab,
@@ -665,7 +666,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(int op, const 
       if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
     }
   };
-  rsl::large_loop(smraw, *cnt, op, A.pool, B.pool, opool, meta_of, sink);
+  rsl::large_loop<OP>(smraw, *cnt, A.pool, B.pool, opool, meta_of, sink);
 }
 
 __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint64_t *__restrict__ laoff,
@@ -690,7 +691,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint6
   auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t, uint32_t) {
     if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);
   };
-  rsl::large_loop(smraw, *cnt, RS_OP_AND, A.pool, B.pool, nullptr, meta_of, sink);
+  rsl::large_loop<RS_OP_AND>(smraw, *cnt, A.pool, B.pool, nullptr, meta_of, sink);
 }
 
 template <typename K>
@@ -705,18 +706,29 @@ unsigned persistent_grid_t(K kernel, int threads, size_t smem, uint64_t count) {
   return (unsigned)(count < g ? count : g);
 }
 
-int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
-                       uint8_t *pool, uint64_t *res_card, bool exact) {
+template <int OP>
+int launch_aa_large_op_t(const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O, uint8_t *pool,
+                         uint64_t *res_card, bool exact) {
   const size_t smem = rsl::LARGE_SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
-    RS_CK(cudaFuncSetAttribute(k_aa_large_op, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RS_CK(cudaFuncSetAttribute(k_aa_large_op<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  RS_LAUNCH_PROF("array_pair_l", exact ? n : 0, k_aa_large_op,
-                 persistent_grid_t(k_aa_large_op, rsl::LTHREADS, smem, n), rsl::LTHREADS, smem, op, L.list[CLS_AAL],
+  RS_LAUNCH_PROF("array_pair_l", exact ? n : 0, k_aa_large_op<OP>,
+                 persistent_grid_t(k_aa_large_op<OP>, rsl::LTHREADS, smem, n), rsl::LTHREADS, smem, L.list[CLS_AAL],
                  L.aoff + L.cap, L.boff + L.cap, L.nab, L.cnt + CLS_AAL, dA, dB, En, O, pool, res_card);
   return RS_OK;
+}
+
+int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O,
+                       uint8_t *pool, uint64_t *res_card, bool exact) {
+  switch (op) {  // one instantiation per op: no per-value op tests in the kernel
+    case RS_OP_AND: return launch_aa_large_op_t<RS_OP_AND>(L, n, dA, dB, En, O, pool, res_card, exact);
+    case RS_OP_OR: return launch_aa_large_op_t<RS_OP_OR>(L, n, dA, dB, En, O, pool, res_card, exact);
+    case RS_OP_ANDNOT: return launch_aa_large_op_t<RS_OP_ANDNOT>(L, n, dA, dB, En, O, pool, res_card, exact);
+    default: return launch_aa_large_op_t<RS_OP_XOR>(L, n, dA, dB, En, O, pool, res_card, exact);
+  }
 }
 
 int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch dB, uint64_t *inter) {
