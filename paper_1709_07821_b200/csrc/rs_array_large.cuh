@@ -178,34 +178,32 @@ __device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t 
 }
 
 // Keep the values of P (np, sorted) whose bit in X equals WANT, in order:
-// warp w probes a contiguous run of P (up to 8 rounds of 32 value pairs), the
-// kept flags become ballots, a CTA scan of the warp totals places each run,
-// and the kept values go straight to dst with 16-bit stores (consecutive
-// lanes write consecutive values).  Returns the kept count on every consumer.
-// The round count is CTA-uniform and the reads are clamped into P, so a round
-// has no divergent branch (lanes past the end only drop out of the ballots).
-template <uint32_t WANT>
-__device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np, uint32_t X, uint16_t *dst,
-                                                 uint32_t (*red2)[LT / 32], uint64_t *release) {
+// warp w probes a contiguous run of P (NR rounds of 32 value pairs), the kept
+// flags become ballots, a CTA scan of the warp totals places each run, and
+// the kept values go straight to dst with 16-bit stores (consecutive lanes
+// write consecutive values).  Returns the kept count on every consumer.  NR
+// (<= 8) is a template parameter -- probe_filter dispatches on it once per
+// pair -- so the rounds are straight-line code (guarded rounds cost ~90
+// instructions per warp per pair in branches alone); the reads are clamped
+// into P, so lanes past the end only drop out of the ballots.
+template <uint32_t WANT, int NR>
+__device__ __forceinline__ uint32_t probe_filter_n(const uint16_t *P, uint32_t np, uint32_t X, uint16_t *dst,
+                                                   uint32_t (*red2)[LT / 32], uint64_t *release) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t *P32 = (const uint32_t *)P;
   const uint32_t np2 = (np + 1) >> 1;
-  const uint32_t nr = (np2 + 255) >> 8;  // rounds of 32 value pairs per warp, <= 8
-  const uint32_t beg = w * nr * 32u + lane, last = np2 ? np2 - 1 : 0;
-  uint32_t BL[8], BH[8], XV[8], tot = 0;
+  const uint32_t beg = w * NR * 32u + lane, last = np2 - 1;
+  uint32_t BL[NR], BH[NR], XV[NR], tot = 0;
 #pragma unroll
-  for (int r = 0; r < 8; r++) {
-    BL[r] = BH[r] = XV[r] = 0;
-    if ((uint32_t)r < nr) {
-      const uint32_t i = beg + 32u * r;
-      const uint32_t x = P32[min(i, last)];
-      XV[r] = x;
-      const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
-      const uint32_t bl = __funnelshift_r(wl, 0u, x) & 1u, bh = __funnelshift_r(wh, 0u, x >> 16) & 1u;
-      BL[r] = __ballot_sync(0xffffffffu, (bl == WANT) & (i < np2));
-      BH[r] = __ballot_sync(0xffffffffu, (bh == WANT) & (2 * i + 1 < np));
-      tot += __popc(BL[r]) + __popc(BH[r]);
-    }
+  for (int r = 0; r < NR; r++) {
+    const uint32_t i = beg + 32u * r;
+    const uint32_t x = P32[min(i, last)];
+    XV[r] = x;
+    const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
+    const uint32_t bl = __funnelshift_r(wl, 0u, x) & 1u, bh = __funnelshift_r(wh, 0u, x >> 16) & 1u;
+    BL[r] = __ballot_sync(0xffffffffu, (bl == WANT) & (i < np2));
+    BH[r] = __ballot_sync(0xffffffffu, (bh == WANT) & (2 * i + 1 < np));
+    tot += __popc(BL[r]) + __popc(BH[r]);
   }
   uint32_t *red = red2[0];
   if (lane == 0) red[w] = tot;
@@ -221,21 +219,34 @@ __device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np,
   if (dst && total) {
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-      if ((uint32_t)r < nr) {
-        const uint32_t bl = BL[r], bh = BH[r];
-        const uint32_t klo = (bl >> lane) & 1u, khi = (bh >> lane) & 1u;
-        const uint32_t x = XV[r];
-        const uint32_t pos = base + __popc(bl & lt) + __popc(bh & lt);
-        if (klo) dst[pos] = (uint16_t)x;
-        if (khi) dst[pos + klo] = (uint16_t)(x >> 16);
-        base += __popc(bl) + __popc(bh);
-      }
+    for (int r = 0; r < NR; r++) {
+      const uint32_t bl = BL[r], bh = BH[r];
+      const uint32_t klo = (bl >> lane) & 1u, khi = (bh >> lane) & 1u;
+      const uint32_t x = XV[r];
+      const uint32_t pos = base + __popc(bl & lt) + __popc(bh & lt);
+      if (klo) dst[pos] = (uint16_t)x;
+      if (khi) dst[pos + klo] = (uint16_t)(x >> 16);
+      base += __popc(bl) + __popc(bh);
     }
     const uint32_t padded = (total + 7u) & ~7u;
     if (threadIdx.x < 8 && total + threadIdx.x < padded) dst[total + threadIdx.x] = 0;
   }
   return total;
+}
+
+template <uint32_t WANT>
+__device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np, uint32_t X, uint16_t *dst,
+                                                 uint32_t (*red2)[LT / 32], uint64_t *release) {
+  switch ((((np + 1) >> 1) + 255) >> 8) {  // rounds of 32 value pairs per warp (np >= 1)
+    case 1: return probe_filter_n<WANT, 1>(P, np, X, dst, red2, release);
+    case 2: return probe_filter_n<WANT, 2>(P, np, X, dst, red2, release);
+    case 3: return probe_filter_n<WANT, 3>(P, np, X, dst, red2, release);
+    case 4: return probe_filter_n<WANT, 4>(P, np, X, dst, red2, release);
+    case 5: return probe_filter_n<WANT, 5>(P, np, X, dst, red2, release);
+    case 6: return probe_filter_n<WANT, 6>(P, np, X, dst, red2, release);
+    case 7: return probe_filter_n<WANT, 7>(P, np, X, dst, red2, release);
+    default: return probe_filter_n<WANT, 8>(P, np, X, dst, red2, release);
+  }
 }
 
 // Copy `total` staged u16 values to dst with 128-bit stores (16-byte zero pad).
