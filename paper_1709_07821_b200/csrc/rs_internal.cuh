@@ -102,6 +102,11 @@ template <typename T> int scan_inclusive(const T *in, T *out, uint64_t n);
 int sort_u64(uint64_t *keys, uint64_t n, int end_bit, int begin_bit = 0);
 int d2h(void *h, const void *d, size_t bytes);   // synchronous on g_stream
 // RS_TRACE=1: synchronize and print host wall time per phase (diagnostics only)
+// cached cudaOccupancyMaxActiveBlocksPerMultiprocessor (+ the device's SM count)
+int occupancy_per_sm(const void *kernel, int threads, size_t smem, int *sms_out);
+// RS_HOST_TRACE=1: accumulated host nanoseconds between numbered points of
+// the per-op host path, printed at exit (diagnostics only; no synchronization)
+void host_mark(int point);
 void trace(const char *phase);
 // live per-kernel timing (bench roofline): events around tagged launches
 extern bool g_prof_on;

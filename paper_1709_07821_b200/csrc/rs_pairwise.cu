@@ -208,12 +208,51 @@ __global__ void k_merge(uint64_t M, uint64_t npairs, const uint64_t *__restrict_
 // key lists staged in shared memory, so the binary searches of the join hit
 // smem instead of chaining global loads (and no search for the pair index)
 constexpr uint32_t MERGE_SMEM_KEYS = 2048;
+// Scans over pairs fused into the kernel that produces their inputs ("last
+// block" pattern): every CTA publishes its per-pair value, fences, and bumps a
+// zeroed counter; the CTA that arrives last scans all of them.  Used when the
+// pairs fit one CTA's serial chunks (npairs <= FUSED_SCAN_MAX); it removes a
+// launch per scan, which is most of a small batch's host time (config 1:
+// ~3 us per launch, 10 launches per op).
+constexpr uint64_t FUSED_SCAN_MAX = 4096;
+
+__device__ __forceinline__ bool last_block_arrives(uint32_t *done, uint64_t nblocks) {
+  __shared__ bool last;
+  __syncthreads();  // every thread's writes of this CTA precede the fence below
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == (uint32_t)(nblocks - 1);
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// exclusive scan of in[0, n) into out (in[n-1] is the zero sentinel, so
+// out[n-1] is the total); one CTA of 256 threads, 256 values per round
+template <typename T>
+__device__ void block_exclusive_scan(const T *in, T *out, uint64_t n) {
+  using BS = cub::BlockScan<T, 256>;
+  __shared__ typename BS::TempStorage ts;
+  T carry = 0;
+  for (uint64_t b0 = 0; b0 < n; b0 += 256) {
+    const uint64_t i = b0 + threadIdx.x;
+    const T v = i < n ? __ldcg(in + i) : (T)0;  // other CTAs' writes: read through L2
+    T ex, agg;
+    BS(ts).ExclusiveSum(v, ex, agg);
+    if (i < n) out[i] = carry + ex;
+    carry += agg;
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, uint64_t npairs, const uint64_t *__restrict__ mbase,
                                                     DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib,
                                                     int op, uint16_t *__restrict__ mkey, uint32_t *__restrict__ mca,
                                                     uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
                                                     uint32_t *__restrict__ keep, uint64_t *__restrict__ ub,
-                                                    uint32_t *__restrict__ pk, uint64_t *__restrict__ pu) {
+                                                    uint32_t *__restrict__ pk, uint64_t *__restrict__ pu,
+                                                    uint32_t *done, uint32_t *pke, uint64_t *pue) {
   __shared__ uint16_t kA[MERGE_SMEM_KEYS], kB[MERGE_SMEM_KEYS];
   __shared__ uint64_t red[8];
   const uint32_t p = blockIdx.x;
@@ -244,6 +283,10 @@ __global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, uint64_t npairs,
     for (int w = 0; w < 8; w++) s += red[w];
     pk[p] = (uint32_t)(s >> 40);
     pu[p] = s & ((1ull << 40) - 1);
+  }
+  if (done && last_block_arrives(done, npairs)) {  // fused scans over pairs
+    block_exclusive_scan<uint32_t>(pk, pke, npairs + 1);
+    block_exclusive_scan<uint64_t>(pu, pue, npairs + 1);
   }
 }
 
@@ -591,10 +634,8 @@ inline int env_int_(const char *name, int dflt) {
 }
 template <typename K>
 unsigned persistent_grid(K kernel, size_t smem, uint64_t count, int want_per_sm = 4) {
-  int dev = 0, sms = 148, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, rsb::BT, smem);
+  int sms = 148;
+  int per = occupancy_per_sm((const void *)kernel, rsb::BT, smem, &sms);
   // 4 CTAs per SM (of the 5 that fit) measured best for the streaming bitset
   // kernels (OR/ANDNOT/XOR and the counts: C2 step 7.18 -> 6.96 ms, op kernel
   // 5.95 -> 6.21 TB/s, count 6.99 -> 7.08 TB/s -- fewer concurrent 8 KB
@@ -696,10 +737,8 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint6
 
 template <typename K>
 unsigned persistent_grid_t(K kernel, int threads, size_t smem, uint64_t count) {
-  int dev = 0, sms = 148, per = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  int sms = 148;
+  int per = occupancy_per_sm((const void *)kernel, threads, smem, &sms);
   static const int cap = env_int_("RS_AAL_CTAS", 0);  // CTAs per SM cap (tuning)
   if (cap > 0 && cap < per) per = cap;
   uint64_t g = (uint64_t)sms * (per > 0 ? per : 1);
@@ -966,7 +1005,8 @@ __global__ void k_bm_start(uint64_t npairs, const uint64_t *__restrict__ mbase, 
 // non-empty results per pair, then CTA per pair writes them at the pair's base
 // (a scan over pairs) plus an in-CTA scan -- no scan over every entry.
 __global__ void __launch_bounds__(256) k_pair_nonempty(uint64_t npairs, const uint32_t *__restrict__ pbase,
-                                                       const uint32_t *__restrict__ card, uint32_t *__restrict__ nz) {
+                                                       const uint32_t *__restrict__ card, uint32_t *__restrict__ nz,
+                                                       uint32_t *done, uint32_t *fb) {
   __shared__ uint32_t red[8];
   const uint32_t p = blockIdx.x;
   if (p == 0 && threadIdx.x == 0) nz[npairs] = 0;
@@ -980,6 +1020,7 @@ __global__ void __launch_bounds__(256) k_pair_nonempty(uint64_t npairs, const ui
     for (int w = 0; w < 8; w++) s += red[w];
     nz[p] = s;
   }
+  if (done && last_block_arrives(done, npairs)) block_exclusive_scan<uint32_t>(nz, fb, npairs + 1);
 }
 
 __global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uint32_t *__restrict__ pbase,
@@ -1328,11 +1369,14 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   O.n = (uint32_t *)S.get((E + 1) * 4);
   uint32_t *keep2 = (uint32_t *)S.get((E + 1) * 4), *fpos = (uint32_t *)S.get((E + 1) * 4);
   if (!S.ok()) { set_error("device allocation failed (op scratch)"); return RS_ENOMEM; }
+  host_mark(5);
   rs_batch *b = new rs_batch();
   int rc = batch_alloc(b, npairs, E, P);
   if (rc) { rs_batch_free(b); return rc; }
   b->type_mask = result_mask(A->type_mask, B->type_mask);
+  host_mark(6);
   RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
+  host_mark(7);
   DevBatch dA = A->dev(), dB = B->dev();
   const ClassMask cm = class_mask(A->type_mask, B->type_mask, op);
   const unsigned sms = sm_count();
@@ -1400,16 +1444,20 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
                    L.list[CLS_PRB], L.cnt + CLS_PRB, dA, dB, En, O, b->d_pool, b->d_bm_card);
   }
   RS_TRY(F.end());
+  host_mark(8);
   // compaction: drop empty results (bitmap.py:185-188)
   if (!mbase && epos && npairs) {  // per-pair entry bases: per-pair compaction
     uint32_t *nz = (uint32_t *)S.get((npairs + 1) * 4), *fb = (uint32_t *)S.get((npairs + 1) * 4);
     if (!S.ok()) { set_error("device allocation failed (compaction)"); return RS_ENOMEM; }
-    RS_LAUNCH(k_pair_nonempty, (unsigned)npairs, 256, 0, npairs, epos, O.card, nz);
-    RS_TRY(scan_exclusive<uint32_t>(nz, fb, npairs + 1));
+    const bool fuse = npairs <= FUSED_SCAN_MAX;
+    RS_LAUNCH(k_pair_nonempty, (unsigned)npairs, 256, 0, npairs, epos, O.card, nz, fuse ? L.cnt + NCLS + 1 : nullptr,
+              fb);
+    if (!fuse) RS_TRY(scan_exclusive<uint32_t>(nz, fb, npairs + 1));
     RS_LAUNCH(k_compact_pair, (unsigned)npairs, 256, 0, npairs, epos, fb, En, O, b->d_key, b->d_type, b->d_card,
               b->d_n, b->d_off, b->d_bm_start);
     b->h_valid = false;
     *out = b;
+    host_mark(9);
     return RS_OK;
   }
   RS_LAUNCH(k_keep_nonempty, grid_for(E + 1, 256), 256, 0, E, dE, O.card, keep2);
@@ -1459,7 +1507,7 @@ Lists make_lists(Scratch &S, uint64_t cap) {
   Lists L;
   L.cap = cap ? cap : 1;
   for (int c = 0; c < NCLS; c++) L.list[c] = (uint32_t *)S.get(L.cap * 4);
-  L.cnt = (uint32_t *)S.get(NCLS * 4);
+  L.cnt = (uint32_t *)S.get((NCLS + 2) * 4);  // + the fused-scan arrival counters
   L.aoff = (uint64_t *)S.get(2 * L.cap * 8);  // [0,cap): bitset class, [cap,2cap): large-array class
   L.boff = (uint64_t *)S.get(2 * L.cap * 8);
   L.nab = (uint32_t *)S.get(L.cap * 4);
@@ -1470,12 +1518,14 @@ Lists make_lists(Scratch &S, uint64_t cap) {
 
 extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
                            uint64_t npairs, rs_batch **out) {
+  host_mark(0);
   RS_TRY(check_op(op));
   RS_TRY(ensure_device());
   *out = nullptr;
   RS_TRY(fetch_host_meta(A));
   RS_TRY(fetch_host_meta(B));
   RS_TRY(check_pairs(A, B, ia, ib, npairs));
+  host_mark(1);
   Scratch S;
   uint64_t M = 0, Ecap = 0, maxk = 0;
   for (uint64_t p = 0; p < npairs; p++) {
@@ -1494,7 +1544,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   std::vector<uint64_t> hb;
   const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 0, hb);
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint16_t *mkey = (uint16_t *)S.get((M + 1) * 2);
@@ -1510,7 +1560,9 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   En.off = (uint64_t *)S.get((M + 1) * 8);
   Lists L = make_lists(S, M);
   if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
+  host_mark(2);
   RS_TRY(U.commit(S));
+  host_mark(3);
   const uint32_t *dia = U.at<uint32_t>(o_ia), *dib = U.at<uint32_t>(o_ib);
   L.cnt = U.at<uint32_t>(o_cnt);
   DevBatch dA = A->dev(), dB = B->dev();
@@ -1524,18 +1576,24 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   // bitmaps are small enough for smem and there are enough pairs to fill the
   // GPU (or few positions per pair); a handful of pairs with thousands of keys
   // each (config 4) keep the thread-per-position join
-  const bool per_pair = M && maxk <= MERGE_SMEM_KEYS && (npairs >= 2 * sm_count() || M <= 1024 * npairs);
+  static const int force_pp = env_int("RS_PER_PAIR", -1);  // A/B: 1 forces, 0 disables the per-pair join
+  const bool per_pair = M && maxk <= MERGE_SMEM_KEYS &&
+                        (force_pp >= 0 ? force_pp == 1 : (npairs >= 2 * sm_count() || M <= 1024 * npairs));
   if (per_pair) {
     // the join, then entry / slot bases from scans over pairs
     uint32_t *pk = (uint32_t *)S.get((npairs + 1) * 4), *pke = (uint32_t *)S.get((npairs + 1) * 4);
     uint64_t *pu = (uint64_t *)S.get((npairs + 1) * 8), *pue = (uint64_t *)S.get((npairs + 1) * 8);
     if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
+    const bool fuse = npairs <= FUSED_SCAN_MAX;
     RS_LAUNCH(k_merge_pair, (unsigned)npairs, 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair,
-              keep, ub, pk, pu);
-    RS_TRY(scan_exclusive<uint32_t>(pk, pke, npairs + 1));
-    RS_TRY(scan_exclusive<uint64_t>(pu, pue, npairs + 1));
+              keep, ub, pk, pu, fuse ? L.cnt + NCLS : nullptr, pke, pue);
+    if (!fuse) {
+      RS_TRY(scan_exclusive<uint32_t>(pk, pke, npairs + 1));
+      RS_TRY(scan_exclusive<uint64_t>(pu, pue, npairs + 1));
+    }
     RS_LAUNCH(k_emit_pair, (unsigned)npairs, 256, 0, mbase, keep, ub, pke, pue, mkey, mca, mcb, mpair, dA, dB, En, L,
               op);
+    host_mark(4);
     if (ub_mode)
       return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr,
                                      pke + npairs, nullptr, pke, npairs, out);
@@ -1576,7 +1634,7 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   Scratch S;
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
   Entries En;
   En.key = (uint16_t *)S.get((npairs + 1) * 2);
   En.ca = (uint32_t *)S.get((npairs + 1) * 4);
@@ -1684,7 +1742,7 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   std::vector<uint64_t> hb;
   const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 1, hb);
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
@@ -1727,7 +1785,7 @@ extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, cons
   Scratch S;
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, NCLS * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   Lists L = make_lists(S, npairs);
   uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);

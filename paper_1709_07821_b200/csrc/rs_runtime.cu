@@ -3,12 +3,14 @@
 #include <cub/cub.cuh>
 #include <chrono>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <unordered_map>
 #include <cstring>
 #include "rs_internal.cuh"
 
 namespace rs {
+uint64_t g_dalloc_stats[2] = {0, 0};  // stream switches, cache misses (RS_HOST_TRACE)
 cudaStream_t g_stream = nullptr;
 uint64_t g_launches = 0;
 static thread_local std::string t_err;
@@ -29,6 +31,70 @@ cudaEvent_t prof_event() {
 }
 void prof_mark(const char *name, cudaEvent_t a, cudaEvent_t b, uint64_t items) {
   g_prof.push_back({name, a, b, items});
+}
+
+// Occupancy of a kernel per (device, kernel, threads, smem), computed once:
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor and the attribute queries
+// cost microseconds of host time per launch, which small batches (config 1:
+// ~10 launches per op) paid on every call.
+int occupancy_per_sm(const void *kernel, int threads, size_t smem, int *sms_out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void *, int, size_t>, int> cache;
+  static std::map<int, int> sms;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto si = sms.find(dev);
+  if (si == sms.end()) {
+    int n = 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    si = sms.emplace(dev, n).first;
+  }
+  if (sms_out) *sms_out = si->second;
+  const auto key = std::make_tuple(dev, kernel, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int per = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess || per <= 0) {
+    cudaGetLastError();
+    per = 1;
+  }
+  cache.emplace(key, per);
+  return per;
+}
+
+namespace {
+struct HostTrace {
+  int on = -1;
+  std::chrono::steady_clock::time_point last;
+  double ns[32] = {0};
+  uint64_t n[32] = {0};
+  ~HostTrace() { dump(); }
+  void dump() {
+    if (on != 1) return;
+    fprintf(stderr, "[rs_host] dalloc stream switches %llu, cache misses %llu\n",
+            (unsigned long long)g_dalloc_stats[0], (unsigned long long)g_dalloc_stats[1]);
+    for (int i = 0; i < 32; i++)
+      if (n[i]) fprintf(stderr, "[rs_host] point %2d: %8.2f us avg over %llu\n", i, ns[i] / n[i] * 1e-3,
+                        (unsigned long long)n[i]);
+  }
+} g_ht;
+}  // namespace
+
+extern "C" void rs_host_trace_dump(void) { g_ht.dump(); }
+
+void host_mark(int point) {
+  if (g_ht.on < 0) {
+    const char *v = getenv("RS_HOST_TRACE");
+    g_ht.on = v && *v == '1';
+  }
+  if (!g_ht.on) return;
+  auto now = std::chrono::steady_clock::now();
+  if (point > 0 && point < 32) {
+    g_ht.ns[point] += std::chrono::duration<double, std::nano>(now - g_ht.last).count();
+    g_ht.n[point]++;
+  }
+  g_ht.last = now;
 }
 
 void trace(const char *phase) {
@@ -110,6 +176,7 @@ static void release_cached_locked() {
 void *dalloc(size_t bytes) {
   std::lock_guard<std::mutex> g(g_alloc_mu);
   if (g_alloc_stream != g_stream) {  // cached blocks are ordered on the old stream
+    g_dalloc_stats[0]++;
     cudaStreamSynchronize(g_alloc_stream);
     g_alloc_stream = g_stream;
   }
@@ -121,6 +188,7 @@ void *dalloc(size_t bytes) {
     return p;
   }
   void *p = nullptr;
+  g_dalloc_stats[1]++;
   if (cudaMallocAsync(&p, r, g_stream) != cudaSuccess) {
     cudaGetLastError();
     release_cached_locked();
@@ -466,8 +534,10 @@ int rs_profile_query(const char *name, double *total_ms, uint64_t *launches, uin
 
 int rs_batch_free(rs_batch *b) {
   if (!b) return RS_OK;
+  host_mark(0);
   batch_release(b);
   delete b;
+  host_mark(20);
   return RS_OK;
 }
 
