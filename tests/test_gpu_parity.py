@@ -469,3 +469,37 @@ def test_maximum_key_counts(pkg):
         cards = A.pairwise_cardinality(op, A, ia, ib).tolist()
         assert cards == [orc.op_cardinality(op, ws[a], ws[b]) for a, b in zip(ia, ib)], op
     assert np.array_equal(A.to_arrays()[0], np.sort(every_key).astype(np.uint32))
+
+
+@pytest.mark.parametrize("npairs", [1, 4096, 4097])
+def test_scan_over_pairs_fused_and_separate(pkg, npairs):
+    """The per-pair join scans over pairs inside k_merge_pair / k_pair_nonempty
+    (last-CTA pattern) up to 4096 pairs and with separate scan launches above:
+    both sides of the boundary, byte for byte against the oracle.  Small seeded
+    bitmaps (a few chunks each, some pairs with empty results so per-pair
+    compaction drops entries)."""
+    rng = np.random.default_rng(4097 + npairs)
+    pool = []
+    for _ in range(64):
+        keys = rng.choice(24, size=int(rng.integers(1, 6)), replace=False)
+        v = np.concatenate([(int(k) << 16) + np.unique(rng.integers(0, 1 << 16, size=int(rng.integers(1, 6000))))
+                            for k in keys]).astype(np.uint64)
+        pool.append(orc.from_values(np.sort(v)))
+    ia = rng.integers(0, 64, size=npairs).astype(np.uint32)
+    ib = rng.integers(0, 64, size=npairs).astype(np.uint32)
+    P = pkg.BitmapBatch.from_wire(pool)
+    want_card = {}
+    for op in OPS:
+        got = P.pairwise(op, P, ia, ib).to_wire_list()
+        memo = {}
+        for p in range(npairs):
+            key = (int(ia[p]), int(ib[p]))
+            if key not in memo:
+                memo[key] = orc.op(op, pool[key[0]], pool[key[1]])
+            assert got[p] == memo[key], (op, p)
+        cards = P.pairwise_cardinality(op, P, ia, ib).tolist()
+        for p in range(npairs):
+            key = (op, int(ia[p]), int(ib[p]))
+            if key not in want_card:
+                want_card[key] = orc.op_cardinality(op, pool[key[1]], pool[key[2]])
+            assert cards[p] == want_card[key], (op, p)
