@@ -6,8 +6,8 @@
 //   and / andnot  one bitset X built from the smaller side (and) or from B
 //                 (andnot); the other side is filtered through it with warp
 //                 ballots, so the result comes out sorted;
-//   or / xor      XA from A and XB from B; the result words XA op XB with a
-//                 popcount scan give the cardinality, and the result is the
+//   or / xor      both sides scattered into XA (shared OR, resp. XOR); the
+//                 result words with a popcount scan give the cardinality, and the result is the
 //                 words themselves (> 4096 values: a bitset container) or
 //                 their set bits in order (<= 4096: an array container).
 // AND / ANDNOT with one side at most 1/16 of the other skip the bitset and
@@ -152,6 +152,14 @@ __device__ __forceinline__ void cscan2(uint32_t v0, uint32_t v1, uint32_t (*red)
 __device__ __forceinline__ void red_or(uint32_t addr, uint32_t bit) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(bit) : "memory");
 }
+__device__ __forceinline__ void red_xor(uint32_t addr, uint32_t bit) {
+  asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr), "r"(bit) : "memory");
+}
+template <bool XOR>
+__device__ __forceinline__ void red_set(uint32_t addr, uint32_t bit) {
+  if constexpr (XOR) red_xor(addr, bit);
+  else red_or(addr, bit);
+}
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -159,6 +167,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   return v;
 }
 
+// XOR: the bits go in with shared XORs instead of ORs, so scattering both
+// arrays of a pair into one bitset leaves exactly the symmetric difference
+// (a value of both sides toggles twice; two values of one side sharing a word
+// have distinct bits, so their combined mask is the same either way).
+template <bool XOR = false>
 __device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t X) {
   const uint32_t *w = (const uint32_t *)v;
   const uint32_t nw = n >> 1;
@@ -168,12 +181,12 @@ __device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t 
     const uint32_t alo = X | ((x >> 3) & 0x1FFCu), ahi = X | ((x >> 19) & 0x1FFCu);
     const uint32_t blo = __funnelshift_l(0u, 1u, x), bhi = __funnelshift_l(0u, 1u, x >> 16);
     const bool same = alo == ahi;
-    red_or(alo, same ? blo | bhi : blo);
-    if (!same) red_or(ahi, bhi);
+    red_set<XOR>(alo, same ? blo | bhi : blo);
+    if (!same) red_set<XOR>(ahi, bhi);
   }
   if ((n & 1) && threadIdx.x == LT - 1) {
     const uint32_t x = v[n - 1];
-    red_or(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
+    red_set<XOR>(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
   }
 }
 
@@ -274,10 +287,10 @@ __device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_
 // values.
 //   and / andnot: X (XA / XB alternate by pair parity) is cleared after the
 //     scan barrier; the next pair uses the other one.
-//   or / xor: each thread reads and clears the words it owns (t + 256q)
-//     before the scan barrier, which every consumer passes before the next
-//     pair's scatter; array results are staged in XA (re-zeroed behind a
-//     barrier).
+//   or / xor: XA only; each thread reads and clears the words it owns
+//     (t + 256q) before the scan barrier, which every consumer passes before
+//     the next pair's scatter; array results are staged in XA (re-zeroed
+//     behind a barrier).
 template <int op>
 __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, const uint16_t *A, uint32_t na, const uint16_t *B,
                                uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
@@ -322,20 +335,21 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, const uint16
     nout = total;
     return total;
   }
-  scatter(A, na, rsb::smem_u32(XA));
-  scatter(B, nb, rsb::smem_u32(XB));
+  // or / xor: both arrays into one bitset (shared OR / XOR), so the result
+  // words are read (and cleared) once
+  constexpr bool is_xor = op == RS_OP_XOR;
+  scatter<is_xor>(A, na, rsb::smem_u32(XA));
+  scatter<is_xor>(B, nb, rsb::smem_u32(XA));
   cbar();
   if (t == 0) mbar_arrive(release);
   // result words t + 256q (conflict-free), positions by a packed row scan
-  uint64_t *XA64 = (uint64_t *)XA, *XB64 = (uint64_t *)XB;
+  uint64_t *XA64 = (uint64_t *)XA;
   uint64_t r[4];
   uint32_t pq[4];
 #pragma unroll
   for (int q = 0; q < 4; q++) {
-    const uint64_t x = XA64[t + LT * q], y = XB64[t + LT * q];
+    r[q] = XA64[t + LT * q];
     XA64[t + LT * q] = 0;
-    XB64[t + LT * q] = 0;
-    r[q] = op == RS_OP_OR ? x | y : x ^ y;
     pq[q] = __popcll(r[q]);
   }
   // cardinality first (one warp reduction); the position scan only for an
