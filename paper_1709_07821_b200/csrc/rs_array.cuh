@@ -118,6 +118,36 @@ __device__ __forceinline__ void stage(uint16_t *dst, const uint8_t *src, int n, 
 // One pair through the group.  count_only: returns the kept count, writes
 // nothing.  Otherwise writes the result container at dst and returns its
 // (type, card, n) through the out-parameters (identical on every thread).
+// One tiny pair by ONE thread: the textbook two-pointer merge
+// (kernels/scalar.py:122-267; the same keep rules as merge_walk) reading the
+// values straight from the pools and writing the result array to dst with
+// its 16-byte zero pad.  Returns the kept count (always an array result:
+// at most na + nb values).
+__device__ __forceinline__ uint32_t aa_pair_thread(int op, const uint16_t *A, uint32_t na, const uint16_t *B,
+                                                   uint32_t nb, uint16_t *dst) {
+  uint32_t i = 0, j = 0, k = 0;
+  uint32_t a = na ? __ldg(A) : 0u, b = nb ? __ldg(B) : 0u;
+  const bool keep_a = op != RS_OP_AND, keep_b = op == RS_OP_OR || op == RS_OP_XOR,
+             keep_both = op == RS_OP_AND || op == RS_OP_OR;
+  while (i < na || j < nb) {
+    const bool take_a = j >= nb || (i < na && a < b), take_b = i >= na || (j < nb && b < a);
+    uint32_t v;
+    bool keep;
+    if (take_a) { v = a; keep = keep_a; }
+    else if (take_b) { v = b; keep = keep_b; }
+    else { v = a; keep = keep_both; }
+    if (keep) {
+      if (dst) dst[k] = (uint16_t)v;
+      k++;
+    }
+    if (!take_b) { i++; a = i < na ? __ldg(A + i) : 0u; }
+    if (!take_a) { j++; b = j < nb ? __ldg(B + j) : 0u; }
+  }
+  if (dst)
+    for (uint32_t p = k; p & 7; p++) dst[p] = 0;
+  return k;
+}
+
 template <int GT, int VT>
 __device__ uint32_t aa_pair(int op, bool count_only, const uint8_t *pa, int na, const uint8_t *pb, int nb,
                             AASmem<GT, VT> &sm, int gid, uint8_t *dst, uint8_t &type, uint32_t &nout) {

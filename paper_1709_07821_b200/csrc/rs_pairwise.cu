@@ -926,6 +926,65 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe_count(const uint32_t *
 
 // Materialized array x array pairs: one group of GT threads per pair
 // (array_intersect/union/difference/xor + _container_from_values).
+// Small array x array pairs (na + nb <= 256), 32 list items per warp at a
+// time: a lane takes item (batch + lane) alone when it is tiny (na + nb <=
+// c_aa_tiny: a scalar two-pointer merge, ~10 thread instructions per value,
+// 32 pairs per warp instruction), and the warp then runs the merge path on
+// the batch's remaining items one by one.  Config 3's Zipf sizes make ~85 %
+// of the small pairs tiny; the warp-per-pair kernel spent ~350 warp
+// instructions on each of them whatever its size.
+__constant__ uint32_t c_aa_tiny = 64;
+
+__global__ void __launch_bounds__(256) k_aa_small(int op, const uint32_t *__restrict__ list,
+                                                  const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B, Entries E,
+                                                  OutDesc O, uint8_t *__restrict__ opool,
+                                                  uint64_t *__restrict__ res_card) {
+  __shared__ __align__(16) rsa::AASmem<32, 8> sm[8];
+  const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t total = *cnt, tiny = c_aa_tiny;
+  for (uint32_t b0 = (blockIdx.x * 8 + gid) * 32; b0 < total; b0 += gridDim.x * 8 * 32) {
+    const uint32_t it = b0 + lane;
+    const bool valid = it < total;
+    uint32_t e = 0, ca = 0, cb = 0, na = 0, nb = 0;
+    if (valid) {
+      e = list[it];
+      ca = E.ca[e];
+      cb = E.cb[e];
+      na = A.card[ca];
+      nb = B.card[cb];
+    }
+    const bool is_tiny = valid && na + nb <= tiny;
+    if (is_tiny) {
+      const uint32_t card = rsa::aa_pair_thread(op, (const uint16_t *)(A.pool + A.off[ca]), na,
+                                                (const uint16_t *)(B.pool + B.off[cb]), nb,
+                                                (uint16_t *)(opool + E.off[e]));
+      O.type[e] = RS_TAG_ARRAY;
+      O.card[e] = card;
+      O.n[e] = card;
+      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+    uint32_t rest = __ballot_sync(0xffffffffu, valid && !is_tiny);
+    while (rest) {  // the batch's larger items through the warp merge path
+      const int src = __ffs(rest) - 1;
+      rest &= rest - 1;
+      const uint32_t e1 = __shfl_sync(0xffffffffu, e, src), ca1 = __shfl_sync(0xffffffffu, ca, src),
+                     cb1 = __shfl_sync(0xffffffffu, cb, src), na1 = __shfl_sync(0xffffffffu, na, src),
+                     nb1 = __shfl_sync(0xffffffffu, nb, src);
+      uint8_t type;
+      uint32_t n;
+      const uint32_t card = rsa::aa_pair<32, 8>(op, false, A.pool + A.off[ca1], (int)na1, B.pool + B.off[cb1],
+                                                (int)nb1, sm[gid], gid, opool + E.off[e1], type, n);
+      if (lane == 0) {
+        O.type[e1] = type;
+        O.card[e1] = card;
+        O.n[e1] = n;
+        if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e1]], (unsigned long long)card);
+      }
+      __syncwarp();
+    }
+  }
+}
+
 template <int GT, int VT>
 __global__ void __launch_bounds__(256) k_aa_pair(int op, const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
                                                  DevBatch A, DevBatch B, Entries E, OutDesc O,
@@ -1264,6 +1323,8 @@ int check_op(int op) {
     uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 256);
     g_aa_large_min = v;
     RS_CK(cudaMemcpyToSymbol(c_aa_large_min, &v, sizeof v));
+    const uint32_t tiny = (uint32_t)env_int("RS_AA_TINY", 64);  // tuning: largest pair merged by one thread
+    RS_CK(cudaMemcpyToSymbol(c_aa_tiny, &tiny, sizeof tiny));
     tuned = 1;
   }
   return RS_OK;
@@ -1416,8 +1477,12 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   }
   if (uint64_t n = n_aas) {
     F.next();
-    RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
-                   0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
+    if (env_int_("RS_AA_SMALL_PLAIN", 0))  // the warp-per-pair kernel (A/B only)
+      RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
+                     256, 0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
+    else
+      RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, k_aa_small, std::min<uint64_t>(grid_for(n, 256), sms * 8), 256,
+                     0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
   }
   if (uint64_t n = n_aam) {
     F.next();
