@@ -1010,6 +1010,48 @@ __global__ void __launch_bounds__(256) k_aa_pair(int op, const uint32_t *__restr
 }
 
 // |a ∩ b| of array x array pairs (array_intersect count_only).
+// |A n B| of small pairs, laid out like k_aa_small: tiny pairs one per lane
+// (scalar intersection count), the rest through the warp merge path.
+__global__ void __launch_bounds__(256) k_aa_count_small(const uint32_t *__restrict__ lca,
+                                                        const uint32_t *__restrict__ lcb,
+                                                        const uint32_t *__restrict__ lpair,
+                                                        const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                                                        uint64_t *__restrict__ acc) {
+  __shared__ __align__(16) rsa::AASmem<32, 8> sm[8];
+  const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t total = *cnt, tiny = c_aa_tiny;
+  for (uint32_t b0 = (blockIdx.x * 8 + gid) * 32; b0 < total; b0 += gridDim.x * 8 * 32) {
+    const uint32_t it = b0 + lane;
+    const bool valid = it < total;
+    uint32_t ca = 0, cb = 0, na = 0, nb = 0;
+    if (valid) {
+      ca = lca[it];
+      cb = lcb[it];
+      na = A.card[ca];
+      nb = B.card[cb];
+    }
+    const bool is_tiny = valid && na + nb <= tiny;
+    if (is_tiny) {
+      const uint32_t c = rsa::aa_pair_thread(RS_OP_AND, (const uint16_t *)(A.pool + A.off[ca]), na,
+                                             (const uint16_t *)(B.pool + B.off[cb]), nb, nullptr);
+      if (c) atomicAdd((unsigned long long *)&acc[lpair[it]], (unsigned long long)c);
+    }
+    uint32_t rest = __ballot_sync(0xffffffffu, valid && !is_tiny);
+    while (rest) {
+      const int src = __ffs(rest) - 1;
+      rest &= rest - 1;
+      const uint32_t ca1 = __shfl_sync(0xffffffffu, ca, src), cb1 = __shfl_sync(0xffffffffu, cb, src),
+                     na1 = __shfl_sync(0xffffffffu, na, src), nb1 = __shfl_sync(0xffffffffu, nb, src);
+      uint8_t type;
+      uint32_t n;
+      const uint32_t c = rsa::aa_pair<32, 8>(RS_OP_AND, true, A.pool + A.off[ca1], (int)na1, B.pool + B.off[cb1],
+                                             (int)nb1, sm[gid], gid, nullptr, type, n);
+      if (lane == 0 && c) atomicAdd((unsigned long long *)&acc[lpair[b0 + src]], (unsigned long long)c);
+      __syncwarp();
+    }
+  }
+}
+
 template <int GT, int VT>
 __global__ void __launch_bounds__(256) k_aa_count(const uint32_t *__restrict__ lca, const uint32_t *__restrict__ lcb,
                                                   const uint32_t *__restrict__ lpair, const uint32_t *__restrict__ cnt,
@@ -1757,8 +1799,12 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
   }
   if (cm.aa) {
     F.next();
-    RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
-                   lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
+    if (env_int_("RS_AA_SMALL_PLAIN", 0))  // the warp-per-pair kernel (A/B only)
+      RS_LAUNCH_PROF("array_count_s", 0, (k_aa_count<32, 8>), pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
+                     lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
+    else
+      RS_LAUNCH_PROF("array_count_s", 0, k_aa_count_small, pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
+                     lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
     if (aa_medium_possible())
       RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
                      lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
