@@ -53,10 +53,15 @@ __device__ __forceinline__ bool tma_class(int c) { return c == 1 /*CLS_BB*/ || c
 
 __device__ __forceinline__ uint32_t pair_a(const uint32_t *ia, uint64_t p) { return ia ? ia[p] : (uint32_t)p; }
 
-// array x array size classes: <= 256 merged items -> warp merge path; <= c_aa_large_min
-// -> 128-thread merge path; above -> smem-bitset kernel.  Measured on C3 the
-// bitset kernel wins for everything above 256 (RS_AA_LARGE_MIN overrides).
+// array x array size classes: <= 256 merged items -> small-pair kernel; up to
+// the op's medium bound -> a warp merge path per pair (16 items per lane);
+// above -> smem-bitset kernel.  Measured on C3: for AND / ANDNOT (and the
+// counts) the bitset kernel -- its filter needs no result sweep, and very
+// unequal AND pairs binary-search -- wins for everything above 256
+// (RS_AA_LARGE_MIN); for OR / XOR the warp merge path wins up to 512 items
+// (RS_AA_UNION_MEDIUM; OR 2.07 -> 1.93 ms, XOR 2.07 -> 1.99 ms).
 __constant__ uint32_t c_aa_large_min = 256;
+__constant__ uint32_t c_aa_union_medium = 512;
 
 // `op` is the materialized op, or AND for the intersection counts.  An
 // array against a bitset or runs under AND (either side), or an array minus a
@@ -65,7 +70,9 @@ __constant__ uint32_t c_aa_large_min = 256;
 __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb, int op) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
   if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY)
-    return na + nb <= 256 ? CLS_AAS : na + nb <= c_aa_large_min ? CLS_AAM : CLS_AAL;
+    return na + nb <= 256 ? CLS_AAS
+           : na + nb <= (op == RS_OP_OR || op == RS_OP_XOR ? c_aa_union_medium : c_aa_large_min) ? CLS_AAM
+                                                                                                : CLS_AAL;
   if (op == RS_OP_AND && (ta == RS_TAG_ARRAY || tb == RS_TAG_ARRAY)) return CLS_PRB;
   if (op == RS_OP_ANDNOT && ta == RS_TAG_ARRAY) return CLS_PRB;
   return CLS_GEN;
@@ -1351,8 +1358,10 @@ std::recursive_mutex Scratch::mu;
 
 unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
 
-uint32_t g_aa_large_min = 256;
-bool aa_medium_possible() { return g_aa_large_min > 256; }
+uint32_t g_aa_large_min = 256, g_aa_union_medium = 512;
+// medium bound of the op's array x array pairs (host mirror of classify())
+uint32_t aa_medium_max(int op) { return op == RS_OP_OR || op == RS_OP_XOR ? g_aa_union_medium : g_aa_large_min; }
+bool aa_medium_possible(int op = RS_OP_AND) { return aa_medium_max(op) > 256; }
 
 int check_op(int op) {
   if (op < 0 || op > 3) {
@@ -1365,6 +1374,9 @@ int check_op(int op) {
     uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 256);
     g_aa_large_min = v;
     RS_CK(cudaMemcpyToSymbol(c_aa_large_min, &v, sizeof v));
+    const uint32_t um = (uint32_t)env_int("RS_AA_UNION_MEDIUM", 512);
+    g_aa_union_medium = um;
+    RS_CK(cudaMemcpyToSymbol(c_aa_union_medium, &um, sizeof um));
     const uint32_t tiny = (uint32_t)env_int("RS_AA_TINY", 64);  // tuning: largest pair merged by one thread
     RS_CK(cudaMemcpyToSymbol(c_aa_tiny, &tiny, sizeof tiny));
     tuned = 1;
@@ -1490,7 +1502,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   // the class kernels are independent (disjoint lists and output slots): with
   // more than one of them they run concurrently on side streams
   const uint64_t n_copy = want(CLS_COPY, op != RS_OP_AND), n_bb = want(CLS_BB, cm.bb),
-                 n_aas = want(CLS_AAS, cm.aa), n_aam = want(CLS_AAM, cm.aa && aa_medium_possible()),
+                 n_aas = want(CLS_AAS, cm.aa), n_aam = want(CLS_AAM, cm.aa && aa_medium_possible(op)),
                  n_aal = want(CLS_AAL, cm.aa), n_gen = want(CLS_GEN, cm.gen), n_prb = want(CLS_PRB, cm.prb);
   const int nk = (n_copy > 0) + (n_bb > 0) + (n_aas > 0) + (n_aam > 0) + (n_aal > 0) + (n_gen > 0) + (n_prb > 0);
   Fork F;  // (tiny ops are host-bound: the fork's event calls would cost more than they overlap)
@@ -1528,8 +1540,14 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   }
   if (uint64_t n = n_aam) {
     F.next();
-    RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
-                   256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
+    // medium pairs: a warp per pair (16 items per lane) up to 512 items, else
+    // the 128-thread groups
+    if (aa_medium_max(op) <= 512)
+      RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<32, 16>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
+                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
+    else
+      RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
+                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
   }
   if (uint64_t n = n_aal) {
     F.next();
@@ -1806,8 +1824,14 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
       RS_LAUNCH_PROF("array_count_s", 0, k_aa_count_small, pg, 256, 0, L.list[CLS_AAS], lcb + CLS_AAS * L.cap,
                      lpair + CLS_AAS * L.cap, L.cnt + CLS_AAS, dA, dB, inter);
     if (aa_medium_possible())
-      RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
-                     lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
+    {
+      if (g_aa_large_min <= 512)
+        RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<32, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
+                       lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
+      else
+        RS_LAUNCH_PROF("array_count_m", 0, (k_aa_count<128, 16>), pg, 256, 0, L.list[CLS_AAM], lcb + CLS_AAM * L.cap,
+                       lpair + CLS_AAM * L.cap, L.cnt + CLS_AAM, dA, dB, inter);
+    }
     if (env_int("RS_AA_LARGE_MERGE", 0))
       RS_LAUNCH_PROF("array_count_l", 0, (k_aa_count<256, 32>), pg, 256, 0, L.list[CLS_AAL], lcb + CLS_AAL * L.cap,
                      lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
