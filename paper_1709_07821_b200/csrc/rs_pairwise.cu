@@ -949,8 +949,14 @@ __global__ void __launch_bounds__(256) k_aa_small(int op, const uint32_t *__rest
   __shared__ __align__(16) rsa::AASmem<32, 8> sm[8];
   const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t total = *cnt, tiny = c_aa_tiny;
-  for (uint32_t b0 = (blockIdx.x * 8 + gid) * 32; b0 < total; b0 += gridDim.x * 8 * 32) {
-    const uint32_t it = b0 + lane;
+  // A long list is cut into 32 consecutive items per warp (coalesced list /
+  // entry loads); a short one (fewer than 32 per warp) is strided so that it
+  // still spreads over every warp: warp w owns w, w + W, w + 2W, ...
+  const uint32_t W = gridDim.x * 8, gw = blockIdx.x * 8 + gid;
+  const bool wide = total >= 32u * W;
+  const uint32_t first = wide ? 32 * gw : gw, lstep = wide ? 1u : W;
+  for (uint32_t b0 = first; b0 < total; b0 += 32 * W) {
+    const uint32_t it = b0 + lane * lstep;
     const bool valid = it < total;
     uint32_t e = 0, ca = 0, cb = 0, na = 0, nb = 0;
     if (valid) {
@@ -1027,8 +1033,11 @@ __global__ void __launch_bounds__(256) k_aa_count_small(const uint32_t *__restri
   __shared__ __align__(16) rsa::AASmem<32, 8> sm[8];
   const int gid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t total = *cnt, tiny = c_aa_tiny;
-  for (uint32_t b0 = (blockIdx.x * 8 + gid) * 32; b0 < total; b0 += gridDim.x * 8 * 32) {
-    const uint32_t it = b0 + lane;
+  const uint32_t W = gridDim.x * 8, gw = blockIdx.x * 8 + gid;  // item layout as in k_aa_small
+  const bool wide = total >= 32u * W;
+  const uint32_t first = wide ? 32 * gw : gw, lstep = wide ? 1u : W;
+  for (uint32_t b0 = first; b0 < total; b0 += 32 * W) {
+    const uint32_t it = b0 + lane * lstep;
     const bool valid = it < total;
     uint32_t ca = 0, cb = 0, na = 0, nb = 0;
     if (valid) {
@@ -1053,7 +1062,7 @@ __global__ void __launch_bounds__(256) k_aa_count_small(const uint32_t *__restri
       uint32_t n;
       const uint32_t c = rsa::aa_pair<32, 8>(RS_OP_AND, true, A.pool + A.off[ca1], (int)na1, B.pool + B.off[cb1],
                                              (int)nb1, sm[gid], gid, nullptr, type, n);
-      if (lane == 0 && c) atomicAdd((unsigned long long *)&acc[lpair[b0 + src]], (unsigned long long)c);
+      if (lane == 0 && c) atomicAdd((unsigned long long *)&acc[lpair[b0 + src * lstep]], (unsigned long long)c);
       __syncwarp();
     }
   }
@@ -1535,7 +1544,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
       RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
                      256, 0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
     else
-      RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, k_aa_small, std::min<uint64_t>(grid_for(n, 256), sms * 8), 256,
+      RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, k_aa_small, std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
                      0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
   }
   if (uint64_t n = n_aam) {
