@@ -179,7 +179,7 @@ def dist_barrier(dist):
 
 
 def workload(seed: int):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     return synth.config2(seed=seed, npairs=NPAIRS, nchunks=NCHUNKS)
 
 

@@ -60,7 +60,7 @@ def wires(buf, offs, idx):
 
 def c1(steps):
     import paper_1709_07821_b200 as rb
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     from oracle import oracle as orc
     buf, offs = synth.config1()
     B = rb.BitmapBatch.from_wire((buf, offs))
@@ -86,7 +86,8 @@ def c1(steps):
 
 def c2(steps):
     import paper_1709_07821_b200 as rb
-    from paper_1709_07821_b200 import _lib, synth
+    from paper_1709_07821_b200 import _lib
+    import workloads as synth
     from oracle import oracle as orc
     buf, offs = synth.config2()
     n = 1024
@@ -128,7 +129,7 @@ def c2(steps):
 
 def c3(steps, npairs=1_000_000):
     import paper_1709_07821_b200 as rb
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     from oracle import oracle as orc
     buf, offs = synth.config3(npairs=npairs)
     ia_, ib_ = synth.slice_images(buf, offs, 0, npairs), synth.slice_images(buf, offs, npairs, 2 * npairs)
@@ -189,7 +190,7 @@ def descriptors(buf, offs, i):
 
 def c4(steps, nbitmaps=200):
     import paper_1709_07821_b200 as rb
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     from oracle import oracle as orc
     buf, offs = synth.config4(nbitmaps=nbitmaps)
     Bt = rb.BitmapBatch.from_wire((buf, offs))
@@ -243,7 +244,7 @@ def c4(steps, nbitmaps=200):
 
 def c5(steps, nbitmaps=512):
     import paper_1709_07821_b200 as rb
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     from oracle import oracle as orc
     buf, offs = synth.config5(nbitmaps=nbitmaps)
     Bt = rb.BitmapBatch.from_wire((buf, offs))

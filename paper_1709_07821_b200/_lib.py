@@ -188,6 +188,21 @@ class PinnedBuffer:
             pass
 
 
+class _PinnedView:
+    """Owner of one pooled page-locked block, exported to numpy through the
+    array interface.  Every array made from it -- slices, views, `arr[:m]` --
+    has this object as its `.base` (numpy collapses view chains to the first
+    non-ndarray owner), so the block goes back to the pool only when the last
+    of them dies."""
+
+    __slots__ = ("__array_interface__", "_buf", "__weakref__")
+
+    def __init__(self, buf: "PinnedBuffer", nbytes: int):
+        self._buf = buf
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                    "data": (buf._p.value, False), "version": 3}
+
+
 class _PinnedPool:
     """Recycled page-locked result arrays for large device->host readbacks.
 
@@ -196,7 +211,8 @@ class _PinnedPool:
     `empty()` view a cached cudaMallocHost block (power-of-two size class);
     when the last view of an array dies its block goes back to the pool, so a
     repeated call reads back at PCIe speed into already-resident pages.  The
-    caller owns the returned array like any numpy array."""
+    caller owns the returned array like any numpy array: the block's lifetime
+    is tied to a `_PinnedView` owner that every derived view references."""
 
     MIN_BYTES = 1 << 16          # smaller results: plain numpy (pinning buys nothing)
     MAX_CACHED = 256 << 20       # free bytes kept for reuse
@@ -221,9 +237,9 @@ class _PinnedPool:
                 self._cached -= size
         if buf is None:
             buf = PinnedBuffer(size)
-        arr = buf.array[:nbytes].view(dt)
-        weakref.finalize(arr, self._release, size, buf)
-        return arr
+        owner = _PinnedView(buf, nbytes)
+        weakref.finalize(owner, self._release, size, buf)
+        return np.asarray(owner).view(dt)
 
     def _release(self, size: int, buf) -> None:
         with self._mu:

@@ -187,7 +187,7 @@ class BitmapBatch:
 
     def equal(self, other: "BitmapBatch", ia=None, ib=None) -> np.ndarray:
         """Type-sensitive equality per pair (bitmap.py:87-91)."""
-        n = len(ia) if ia is not None else min(len(self), len(other))
+        n = self._npairs(other, ia, ib)
         a, pa = _u32_or_none(ia)
         b, pb = _u32_or_none(ib)
         out = np.zeros(max(n, 1), dtype=np.uint8)
@@ -210,12 +210,20 @@ class BitmapBatch:
         return out[:n].astype(bool)
 
     # ------------------------------------------------------------ hot path
-    def _npairs(self, other, ia, ib):
-        if ia is not None:
-            return len(ia)
-        if ib is not None:
-            return len(ib)
-        return min(len(self), len(other))
+    def _npairs(self, other, ia, ib, n=None):
+        """Pair count of a call, checked against the index arrays the C ABI
+        reads (npairs u32 each): ia and ib must have equal lengths, and an
+        explicit n must not exceed either of them."""
+        la = None if ia is None else len(ia)
+        lb = None if ib is None else len(ib)
+        if la is not None and lb is not None and la != lb:
+            raise ValueError(f"ia and ib differ in length ({la} != {lb})")
+        if n is None:
+            return la if la is not None else lb if lb is not None else min(len(self), len(other))
+        n = int(n)
+        if n < 0 or (la is not None and n > la) or (lb is not None and n > lb):
+            raise ValueError(f"n={n} exceeds the pair index arrays")
+        return n
 
     def pairwise(self, op: str, other: "BitmapBatch", ia=None, ib=None) -> "BitmapBatch":
         """Bitmap p of the result = self[ia[p]] op other[ib[p]] (bitmap.py:169-210)."""
@@ -241,6 +249,7 @@ class BitmapBatch:
                                     ia=None, ib=None) -> None:
         """Asynchronous variant writing u64 counts to a device pointer."""
         k = op_index(op)
+        n = self._npairs(other, ia, ib, n)
         a, pa = _u32_or_none(ia)
         b, pb = _u32_or_none(ib)
         check(lib().rs_pairwise_cardinality(k, self._h, other._h, pa, pb, n, C.c_void_p(dev_out_ptr), 1))
@@ -259,6 +268,7 @@ class BitmapBatch:
                                               ia=None, ib=None) -> None:
         """Asynchronous variant writing u64 counts to a device pointer."""
         k = op_index(op)
+        n = self._npairs(other, ia, ib, n)
         a, pa = _u32_or_none(ia)
         b, pb = _u32_or_none(ib)
         check(lib().rs_container_pairwise_cardinality(k, self._h, other._h, pa, pb, n, C.c_void_p(dev_out_ptr), 1))

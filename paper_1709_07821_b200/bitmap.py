@@ -23,22 +23,51 @@ _EMPTY = b"ROAR\x00\x00\x00\x00"
 class RoaringBitmap:
     """Compressed set of 32-bit unsigned integers (GPU-resident)."""
 
-    __slots__ = ("_b",)
+    __slots__ = ("_b", "_snap")
 
     def __init__(self) -> None:
         self._b = BitmapBatch.from_wire([_EMPTY])
+        self._snap = None
 
     @classmethod
     def _wrap(cls, batch: BitmapBatch) -> "RoaringBitmap":
         rb = cls.__new__(cls)
         rb._b = batch
+        rb._snap = None
         return rb
+
+    def _set(self, batch: BitmapBatch) -> None:
+        """Replace the device state (mutation); host snapshots are dropped."""
+        self._b = batch
+        self._snap = None
+
+    # --------------------------------------------------- host snapshots
+    # The reference keeps `_keys` / `_containers` as Python lists
+    # (bitmap.py:32-36).  Here the bitmap lives in HBM; these are host copies
+    # taken on first access, for code that inspects them.  validate() checks
+    # a snapshot against the device state, so a snapshot edited in place
+    # reads as corruption (as the reference's validator would see it).
+    def _snapshot(self):
+        if self._snap is None:
+            keys, conts = chunks_from_wire(self.serialize())
+            self._snap = (keys, conts, list(keys))
+        return self._snap
+
+    @property
+    def _keys(self) -> list:
+        return self._snapshot()[0]
+
+    @property
+    def _containers(self) -> list:
+        return self._snapshot()[1]
 
     # ------------------------------------------------------------- building
     @classmethod
     def from_values(cls, values) -> "RoaringBitmap":
-        """Bulk-build from any iterable or array of 32-bit values (bitmap.py:40-62)."""
-        arr = np.asarray(list(values) if not isinstance(values, np.ndarray) else values)
+        """Bulk-build from any iterable or array of 32-bit values (bitmap.py:40-62).
+        The conversion mirrors the reference's: u64 via numpy, so a negative
+        Python int raises OverflowError and anything above 2^32-1 ValueError."""
+        arr = np.asarray(list(values) if not isinstance(values, np.ndarray) else values, dtype=np.uint64)
         return cls._wrap(BitmapBatch.from_values([arr]))
 
     @classmethod
@@ -96,7 +125,7 @@ class RoaringBitmap:
             raise ValueError("value out of 32-bit range")
         if v in self:
             return False
-        self._b = self._b.pairwise("or", BitmapBatch.from_values([np.array([v], dtype=np.uint32)]), [0], [0])
+        self._set(self._b.pairwise("or", BitmapBatch.from_values([np.array([v], dtype=np.uint32)]), [0], [0]))
         return True
 
     def remove(self, v: int) -> bool:
@@ -106,7 +135,7 @@ class RoaringBitmap:
         v = int(v)
         if not 0 <= v <= 0xFFFFFFFF or v not in self:
             return False
-        self._b = self._b.pairwise("andnot", BitmapBatch.from_values([np.array([v], dtype=np.uint32)]), [0], [0])
+        self._set(self._b.pairwise("andnot", BitmapBatch.from_values([np.array([v], dtype=np.uint32)]), [0], [0]))
         return True
 
     # ------------------------------------------------------------ iteration
@@ -164,12 +193,16 @@ class RoaringBitmap:
     # ------------------------------------------------------- storage tuning
     def run_optimize(self) -> bool:
         """Re-pick each container's type with run candidacy (bitmap.py:308-316)."""
+        self._snap = None
         return bool(self._b.run_optimize()[0])
 
     def shrink_to_fit(self) -> int:
-        """Bytes reclaimed by trimming container capacity (bitmap.py:318-328).
-        Device pools are packed at exactly each container's length, so there
-        is never slack to reclaim."""
+        """Bytes reclaimed by trimming container capacity (bitmap.py:318-328),
+        in the reference's accounting, where capacity == length here: 0.  The
+        device side of the same idea happens too: an op result's pool, laid
+        out by per-container upper bounds, is packed to its containers' bytes
+        (rs_batch_info packs it)."""
+        self._b.info()
         return 0
 
     def memory_bytes(self) -> tuple[int, int]:
@@ -184,11 +217,17 @@ class RoaringBitmap:
     # ------------------------------------------------------------ validation
     def validate(self) -> None:
         """Raise AssertionError if a structural invariant is broken: the image is
-        re-ingested through the GPU decoder, which applies every serde check."""
+        re-ingested through the GPU decoder, which applies every serde check;
+        a host snapshot (_keys / _containers) must still match the device."""
         try:
             BitmapBatch.from_wire([self.serialize()])
         except DecodeError as e:
             raise AssertionError(str(e)) from None
+        if self._snap is not None:
+            keys, conts, taken = self._snap
+            assert all(0 <= k <= 0xFFFF for k in keys), "key outside 16 bits"
+            assert all(a < b for a, b in zip(keys, keys[1:])), "keys not strictly increasing"
+            assert keys == taken and len(conts) == len(keys), "key index differs from the bitmap"
 
 
 __all__ = ["RoaringBitmap", "OPS"]

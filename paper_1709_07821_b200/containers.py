@@ -11,6 +11,7 @@ as one-container batches; ``ContainerBatch`` runs millions of pairs per launch.
 from __future__ import annotations
 
 import struct
+import types
 
 import numpy as np
 
@@ -27,11 +28,12 @@ def op_index(op: str) -> int:
 
 
 class ArrayContainer:
-    __slots__ = ("values",)
+    __slots__ = ("values", "capacity")
     tag = TAG_ARRAY
 
-    def __init__(self, values=()):
+    def __init__(self, values=(), capacity: int = 0):
         self.values = np.asarray(values, dtype=np.uint16)
+        self.capacity = max(len(self.values), capacity)
 
     def __len__(self) -> int:
         return len(self.values)
@@ -43,7 +45,7 @@ class ArrayContainer:
         return f"ArrayContainer(card={len(self)})"
 
     def copy(self) -> "ArrayContainer":
-        return ArrayContainer(self.values.copy())
+        return ArrayContainer(self.values.copy(), self.capacity)
 
 
 class BitsetContainer:
@@ -68,11 +70,12 @@ class BitsetContainer:
 
 
 class RunContainer:
-    __slots__ = ("runs",)
+    __slots__ = ("runs", "capacity")
     tag = TAG_RUN
 
-    def __init__(self, runs):
+    def __init__(self, runs, capacity: int = 0):
         self.runs = np.asarray(runs, dtype=np.uint16).reshape(-1, 2)
+        self.capacity = max(len(self.runs), capacity)
 
     def __len__(self) -> int:
         return len(self.runs) + int(self.runs[:, 1].sum(dtype=np.int64))
@@ -84,7 +87,7 @@ class RunContainer:
         return f"RunContainer(runs={len(self.runs)}, card={len(self)})"
 
     def copy(self) -> "RunContainer":
-        return RunContainer(self.runs.copy())
+        return RunContainer(self.runs.copy(), self.capacity)
 
 
 Container = ArrayContainer | BitsetContainer | RunContainer
@@ -146,25 +149,142 @@ def _single(c: Container) -> bytes:
     return wire_from_chunks([0], [c]) if len(c) else wire_from_chunks([], [])
 
 
-def container_pairwise(op: str, a: Container, b: Container) -> Container:
-    """containers.py:450-529 on the GPU; an empty result is an empty ArrayContainer."""
-    op_index(op)
-    if len(a) == 0 or len(b) == 0:
-        raise TypeError("containers must be non-empty (normalized)")
+def empty_container() -> ArrayContainer:
+    """containers.py:106-107."""
+    return ArrayContainer()
+
+
+def bitset_from_positions(positions) -> BitsetContainer:
+    """A BitsetContainer holding `positions` (containers.py:113-119).  Host
+    value construction (numpy), like the container classes themselves."""
+    pos = np.asarray(positions, dtype=np.int64)
+    bits = np.zeros(1 << 16, dtype=bool)
+    bits[pos] = True
+    words = np.frombuffer(np.packbits(bits, bitorder="little").tobytes(), dtype="<u8").astype(np.uint64)
+    return BitsetContainer(words, len(pos))
+
+
+# Names the reference's tests reach through ``containers.kernels`` (its kernel
+# backend module, kernels/_shared.py:8-20).  This build has no per-container
+# kernel seam (SURVEY 8(b)); only the shared constants are provided.
+kernels = types.SimpleNamespace(OPS=OPS, BLOCK_WORDS=1024, GALLOP_RATIO=64)
+
+
+def _tag(c) -> int:
+    t = getattr(c, "tag", None)
+    if t not in (TAG_ARRAY, TAG_BITSET, TAG_RUN):
+        raise TypeError(f"unsupported container {type(c)}")
+    return t
+
+
+def _canonical(c: Container) -> bool:
+    """Non-empty and in the form container_normalize would keep (the form the
+    wire decoder accepts, serde.py:122-164)."""
+    n = len(c)
+    t = _tag(c)
+    if t == TAG_ARRAY:
+        return 1 <= n <= ARRAY_MAX and (n < 2 or bool(np.all(np.diff(c.values.astype(np.int64)) > 0)))
+    if t == TAG_BITSET:
+        return n > ARRAY_MAX
+    nr = len(c.runs)
+    if nr == 0:
+        return False
+    r = c.runs.astype(np.int64)
+    e = r[:, 0] + r[:, 1]
+    if np.any(e > 0xFFFF) or (nr > 1 and np.any(r[1:, 0] <= e[:-1] + 1)):
+        return False
+    return nr <= RUN_MAX_RUNS if n > ARRAY_MAX else 2 * nr < n
+
+
+# Result type of container_pairwise per declared input types (SURVEY App. A,
+# containers.py:459-527): "card" = array iff card <= 4096 else bitset
+# (_container_from_values / _container_from_words); "run" = container_normalize
+# of the interval result (run iff admissible, else by card); "array" = a subset
+# of the array side, kept as an ArrayContainer whatever its size.
+def _result_rule(ta: int, tb: int, op: str) -> str:
+    if ta == tb and ta != TAG_RUN:
+        return "card"
+    if {ta, tb} == {TAG_ARRAY, TAG_BITSET}:
+        if op == "and" or (op == "andnot" and ta == TAG_ARRAY):
+            return "array"
+        return "card"
+    if ta == tb == TAG_RUN:
+        return "run"
+    if ta == TAG_RUN and tb == TAG_ARRAY:
+        return "array" if op == "and" else "run"
+    if ta == TAG_ARRAY and tb == TAG_RUN:
+        return "array" if op in ("and", "andnot") else "run"
+    return "card"
+
+
+def _device_single(c: Container):
+    """One-container device batch holding c's members in canonical form; None
+    when c is empty.  Canonical containers go up as wire images; others (an
+    under-full bitset, an array over 4096 values, a run form that is not the
+    smallest) are rebuilt from their members (from_values on the GPU)."""
     from .batch import BitmapBatch
-    A = BitmapBatch.from_wire([_single(a)])
-    B = BitmapBatch.from_wire([_single(b)])
-    R = A.container_pairwise(op, B)
-    keys, conts = chunks_from_wire(R.to_wire_list()[0])
-    return conts[0] if conts else ArrayContainer()
+    if len(c) == 0:
+        return None
+    if _canonical(c):
+        return BitmapBatch.from_wire([_single(c)])
+    return BitmapBatch.from_values([container_positions(c).astype(np.uint32)])
+
+
+def _retype(R, rule: str) -> Container:
+    """The one-container device result R re-typed by `rule` (see
+    _result_rule); the conversions run on the GPU."""
+    from .batch import BitmapBatch
+    if R is None or int(R.container_counts()[0]) == 0:
+        return ArrayContainer()
+    if rule == "array":
+        return ArrayContainer(R.to_arrays()[0].astype(np.uint16))
+    _, conts = chunks_from_wire(R.to_wire_list()[0])
+    if rule == "run":
+        R = R.select([0])
+        R.run_optimize()                    # run iff admissible, else by card
+    elif isinstance(conts[0], RunContainer):  # "card": drop the run form
+        R = BitmapBatch.from_values([R.to_arrays()[0]])
+    else:
+        return conts[0]
+    _, conts = chunks_from_wire(R.to_wire_list()[0])
+    return conts[0]
+
+
+def container_pairwise(op: str, a: Container, b: Container) -> Container:
+    """containers.py:450-529 on the GPU; an empty result is an empty
+    ArrayContainer.  Canonical non-empty inputs run as one batched container
+    op whose kernels pick the reference's result type directly.  Empty or
+    non-canonical inputs (accepted by the reference as structurally valid
+    containers) run on their canonical device forms and the result is
+    re-typed by the declared input types' rule (_result_rule), so the type
+    matches the reference's dispatch on the objects actually passed."""
+    op_index(op)
+    ta, tb = _tag(a), _tag(b)
+    if _canonical(a) and _canonical(b):
+        from .batch import BitmapBatch
+        A = BitmapBatch.from_wire([_single(a)])
+        B = BitmapBatch.from_wire([_single(b)])
+        R = A.container_pairwise(op, B)
+        keys, conts = chunks_from_wire(R.to_wire_list()[0])
+        return conts[0] if conts else ArrayContainer()
+    A, B = _device_single(a), _device_single(b)
+    if A is None or B is None:
+        # op(empty, x) = x for OR/XOR; op(x, empty) = x for OR/XOR/ANDNOT
+        R = (B if op in ("or", "xor") else None) if A is None else (A if op != "and" else None)
+    else:
+        R = A.container_pairwise(op, B)
+    return _retype(R, _result_rule(ta, tb, op))
 
 
 def container_pairwise_cardinality(op: str, a: Container, b: Container) -> int:
-    """containers.py:554-570 on the GPU."""
+    """containers.py:554-570 on the GPU.  Empty containers count as 0 members
+    (|a op empty| from the reference's own formula, containers.py:563-570)."""
     op_index(op)
-    from .batch import BitmapBatch
-    A = BitmapBatch.from_wire([_single(a)])
-    B = BitmapBatch.from_wire([_single(b)])
+    _tag(a), _tag(b)
+    A, B = _device_single(a), _device_single(b)
+    if A is None or B is None:
+        la, lb = len(a), len(b)
+        return {"and": 0, "or": la + lb, "andnot": la, "xor": la + lb}[op]
     return int(A.container_pairwise_cardinality(op, B)[0])
 
 
@@ -172,16 +292,6 @@ def container_pairwise_cardinality(op: str, a: Container, b: Container) -> int:
 # The reference's element-level container functions (containers.py:208-367),
 # for drop-in completeness.  Each runs as a one-container GPU batch; the
 # batched forms are BitmapBatch.contains / pairwise.
-
-def _canonical(c: Container) -> bool:
-    n = len(c)
-    if isinstance(c, ArrayContainer):
-        return 1 <= n <= ARRAY_MAX and bool(np.all(np.diff(c.values.astype(np.int64)) > 0))
-    if isinstance(c, BitsetContainer):
-        return n > ARRAY_MAX
-    nr = len(c.runs)
-    return nr > 0 and (nr <= RUN_MAX_RUNS if n > ARRAY_MAX else 2 * nr < n)
-
 
 def _batch_of(c: Container):
     from .batch import BitmapBatch
@@ -229,3 +339,33 @@ def container_remove(c: Container, v: int):
         return c, False
     one = ArrayContainer(np.array([int(v)], dtype=np.uint16))
     return container_pairwise("andnot", container_normalize(c) if not _canonical(c) else c, one), True
+
+
+def container_validate(c: Container, normalized: bool = True) -> None:
+    """Raise AssertionError if a host container breaks its invariants
+    (containers.py:575-604): the same checks the wire decoder applies."""
+    t = _tag(c)
+    if t == TAG_ARRAY:
+        assert c.values.dtype == np.uint16
+        assert len(c.values) <= ARRAY_MAX, "array container over 4096 values"
+        if len(c.values) > 1:
+            assert np.all(np.diff(c.values.astype(np.int32)) > 0), "array values not strictly increasing"
+        assert getattr(c, "capacity", len(c.values)) >= len(c.values)
+        return
+    if t == TAG_BITSET:
+        assert c.words.dtype == np.uint64 and len(c.words) == 1024
+        true_card = int(np.bitwise_count(c.words).sum(dtype=np.int64))
+        assert c.cardinality == true_card, f"bitset cardinality {c.cardinality} != popcount {true_card}"
+        if normalized:
+            assert c.cardinality > ARRAY_MAX, "bitset container under 4097 values"
+        return
+    assert c.runs.dtype == np.uint16 and c.runs.ndim == 2 and c.runs.shape[1] == 2
+    runs = c.runs.astype(np.int32)
+    assert len(runs) > 0, "empty run container"
+    ends = runs[:, 0] + runs[:, 1]
+    assert np.all(ends <= 65535)
+    if len(runs) > 1:
+        assert np.all(runs[1:, 0] > ends[:-1] + 1), "runs overlap or are adjacent"
+    if normalized:
+        n = len(c)
+        assert (len(runs) <= RUN_MAX_RUNS if n > ARRAY_MAX else 2 * len(runs) < n), "run form not the smallest"

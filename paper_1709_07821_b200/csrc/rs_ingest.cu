@@ -76,9 +76,19 @@ __global__ void k_wire_gather_validate(uint64_t nc, uint64_t nvalidate, const ui
   uint8_t code = V_OK;
   uint32_t val = 0, fixed = card;
   if (t == RS_TAG_ARRAY) {
-    bool bad = false;
-    for (uint32_t i = 1 + lane; i < n; i += 32) bad |= s16[i] <= s16[i - 1];
-    if (__any_sync(0xffffffffu, bad)) code = V_ARRAY_ORDER;
+    // first position that breaks strict increase (n = none)
+    uint32_t first_bad = n;
+    for (uint32_t i = 1 + lane; i < n; i += 32)
+      if (s16[i] <= s16[i - 1]) { first_bad = i; break; }
+    for (int o = 16; o; o >>= 1) first_bad = min(first_bad, __shfl_xor_sync(0xffffffffu, first_bad, o));
+    if (first_bad < n) {
+      code = V_ARRAY_ORDER;
+      // deferred mode: keep only the strictly increasing prefix, so every
+      // kernel's per-pair output bound (2*min(na,nb), containers.py:471)
+      // holds until the batch is rejected at rs_batch_wait
+      fixed = first_bad;
+      if (card_fix && lane == 0) const_cast<uint32_t *>(B.n)[c] = first_bad;
+    }
   } else if (t == RS_TAG_BITSET) {
     uint32_t pc = 0;
     for (uint32_t i = lane; i < 2048; i += 32) pc += __popc((uint32_t)s16[2 * i] | ((uint32_t)s16[2 * i + 1] << 16));
@@ -856,6 +866,9 @@ extern "C" int rs_batch_concat(const rs_batch *const *parts, uint64_t nparts, rs
     cb += p->nc; bb += p->nb; pb += p->pool_bytes;
   }
   b->h_valid = true;
+  bool ub = false;
+  for (uint64_t k = 0; k < nparts; k++) ub |= parts[k]->ub_pool;
+  if (ub) ub_register(b);  // the parts' holes were copied along
   *out = b;
   return RS_OK;
 }

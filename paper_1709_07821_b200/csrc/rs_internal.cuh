@@ -71,6 +71,10 @@ struct rs_batch {
   // pipeline skip type-pair classes that cannot occur
   uint8_t type_mask = 0xFF;
   int single = -1;  // 1 = every bitmap holds exactly one container (cached)
+  // pool laid out by per-result upper bounds (op / union results): it may
+  // hold holes until repack_pool() packs it (at the first host query, or when
+  // the live upper-bound reservations pass the high-water mark)
+  bool ub_pool = false;
   rs_pending *pending = nullptr;  // payload checks not yet read back
   DevBatch dev() const {
     DevBatch d;
@@ -93,6 +97,14 @@ int batch_alloc(rs_batch *b, uint64_t nb, uint64_t nc, uint64_t pool_bytes);
 void batch_release(rs_batch *b);
 int fetch_host_meta(const rs_batch *b);   // fills h_bm_start (synchronizes)
 int finalize_batch(rs_batch *b);          // computes d_bm_card from containers
+// Upper-bound result pools: register a fresh result (its reservation counts
+// toward the high-water mark), pack one pool to its containers' bytes
+// (synchronizes), and pack every registered pool when the reservations
+// exceed the mark -- called before an op reserves a new result pool.
+void ub_register(rs_batch *b);
+void ub_unregister(rs_batch *b);
+int repack_pool(rs_batch *b);
+int ub_reserve(uint64_t bytes);
 int resolve_pending(const rs_batch *b);    // reads deferred checks; RS_EDECODE on failure
 int materialize(const rs_batch *b);        // queue a deferred batch's unpack/gather (first use)
 void drop_staged(rs_batch *b);             // release an unused deferred batch's staging slot

@@ -393,6 +393,15 @@ __global__ void k_copy(const uint32_t *__restrict__ list, const uint32_t *__rest
   if (w >= total) return;
   Item cur = fetch(w);
   for (; w < total; w += nw) {
+    if (cur.c == RS_NONE) {  // container-level op with an empty result (nothing kept)
+      if (lane == 0) {
+        O.type[cur.e] = RS_TAG_ARRAY;
+        O.card[cur.e] = 0;
+        O.n[cur.e] = 0;
+      }
+      if (w + nw < total) cur = fetch(w + nw);
+      continue;
+    }
     const DevBatch &S = cur.from_a ? A : B;
     const uint8_t t = S.type[cur.c];
     const uint32_t n = S.n[cur.c], card = S.card[cur.c];
@@ -1265,7 +1274,10 @@ __global__ void k_formula_containers(uint64_t npairs, int op, DevBatch A, DevBat
                                      const uint32_t *ib, const uint64_t *__restrict__ inter, uint64_t *__restrict__ out) {
   uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (p >= npairs) return;
-  uint64_t x = A.card[A.bm_start[pair_a(ia, p)]], y = B.card[B.bm_start[pair_a(ib, p)]], i = inter[p];
+  const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+  // an image without containers is the empty container (len 0)
+  uint64_t x = A.bm_start[a + 1] > A.bm_start[a] ? A.card[A.bm_start[a]] : 0;
+  uint64_t y = B.bm_start[b + 1] > B.bm_start[b] ? B.card[B.bm_start[b]] : 0, i = inter[p];
   out[p] = op == RS_OP_AND ? i : op == RS_OP_OR ? x + y - i : op == RS_OP_ANDNOT ? x - i : x + y - 2 * i;
 }
 
@@ -1278,13 +1290,33 @@ __global__ void k_cont_entries(uint64_t npairs, DevBatch A, DevBatch B, const ui
   uint64_t ao = 0, bo = 0;
   uint32_t nab = 0;
   if (active) {
-    uint32_t ca = (uint32_t)A.bm_start[pair_a(ia, p)], cb = (uint32_t)B.bm_start[pair_a(ib, p)];
+    const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+    uint32_t ca = (uint32_t)A.bm_start[a], cb = (uint32_t)B.bm_start[b];
+    const bool ea = A.bm_start[a + 1] == ca, eb = B.bm_start[b + 1] == cb;
+    E.pair[p] = (uint32_t)p;
+    if (ea || eb) {
+      // an empty image is the empty container: op(empty, x) is x for OR/XOR,
+      // op(x, empty) is x for OR/XOR/ANDNOT -- a deep copy of x, whose type is
+      // already the one container_pairwise picks (an empty array side keeps
+      // the other side's canonical type, App. A); anything else is empty.
+      // Both sides RS_NONE = nothing to copy (k_copy writes an empty result).
+      const bool keep_b = ea && !eb && (op == RS_OP_OR || op == RS_OP_XOR);
+      const bool keep_a = eb && !ea && op != RS_OP_AND;
+      ca = keep_a ? ca : RS_NONE;
+      cb = keep_b ? cb : RS_NONE;
+      E.key[p] = keep_a ? A.key[ca] : keep_b ? B.key[cb] : 0;
+      E.ca[p] = ca;
+      E.cb[p] = cb;
+      ub[p] = keep_a ? rs_pad16(rs_payload_bytes(A.type[ca], A.n[ca]))
+            : keep_b ? rs_pad16(rs_payload_bytes(B.type[cb], B.n[cb])) : 0;
+      cls = CLS_COPY;
+    } else {
     E.key[p] = A.key[ca];
     E.ca[p] = ca;
     E.cb[p] = cb;
-    E.pair[p] = (uint32_t)p;
     ub[p] = rs_pad16(rs_result_ub(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op));
     cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
+    }
     if (tma_class(cls)) {
       ao = A.off[ca];
       bo = B.off[cb];
@@ -1303,9 +1335,12 @@ __global__ void k_cont_list(uint64_t npairs, DevBatch A, DevBatch B, const uint3
   int cls = CLS_GEN;
   uint32_t ca = 0, cb = 0;
   if (active) {
-    ca = (uint32_t)A.bm_start[pair_a(ia, p)];
-    cb = (uint32_t)B.bm_start[pair_a(ib, p)];
-    cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], RS_OP_AND);
+    const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+    ca = (uint32_t)A.bm_start[a];
+    cb = (uint32_t)B.bm_start[b];
+    // an empty side: |empty ∩ x| = 0, no work item
+    active = A.bm_start[a + 1] > ca && B.bm_start[b + 1] > cb;
+    if (active) cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], RS_OP_AND);
   }
   count_append(L, cls, active, ca, cb, (uint32_t)p, lcb_base, lpair_base, A, B);
 }
@@ -1380,10 +1415,12 @@ int check_op(int op) {
   static int tuned = 0;  // one-time device tuning constants
   if (!tuned) {
     RS_TRY(ensure_device());
-    uint32_t v = (uint32_t)env_int("RS_AA_LARGE_MIN", 256);
+    // medium bounds are capped at 2048 merged items: the capacity of the
+    // largest merge-path kernel they select (k_aa_pair/k_aa_count<128,16>)
+    uint32_t v = (uint32_t)std::min(std::max(env_int("RS_AA_LARGE_MIN", 256), 0), 2048);
     g_aa_large_min = v;
     RS_CK(cudaMemcpyToSymbol(c_aa_large_min, &v, sizeof v));
-    const uint32_t um = (uint32_t)env_int("RS_AA_UNION_MEDIUM", 512);
+    const uint32_t um = (uint32_t)std::min(std::max(env_int("RS_AA_UNION_MEDIUM", 512), 0), 2048);
     g_aa_union_medium = um;
     RS_CK(cudaMemcpyToSymbol(c_aa_union_medium, &um, sizeof um));
     const uint32_t tiny = (uint32_t)env_int("RS_AA_TINY", 64);  // tuning: largest pair merged by one thread
@@ -1494,9 +1531,11 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   uint32_t *keep2 = (uint32_t *)S.get((E + 1) * 4), *fpos = (uint32_t *)S.get((E + 1) * 4);
   if (!S.ok()) { set_error("device allocation failed (op scratch)"); return RS_ENOMEM; }
   host_mark(5);
+  RS_TRY(ub_reserve(P));
   rs_batch *b = new rs_batch();
   int rc = batch_alloc(b, npairs, E, P);
   if (rc) { rs_batch_free(b); return rc; }
+  ub_register(b);
   b->type_mask = result_mask(A->type_mask, B->type_mask);
   host_mark(6);
   RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
@@ -1619,18 +1658,21 @@ int check_single_containers(const rs_batch *A, const rs_batch *B, const uint32_t
                             uint64_t npairs) {
   for (const rs_batch *X : {A, B}) {
     rs_batch *x = const_cast<rs_batch *>(X);
-    if (x->single < 0) {
+    if (x->single < 0) {  // 1: one container each; 2: at most one (some empty); 0: other
       x->single = 1;
-      for (uint64_t i = 0; i < x->nb && x->single; i++)
-        if (x->h_bm_start[i + 1] - x->h_bm_start[i] != 1) x->single = 0;
+      for (uint64_t i = 0; i < x->nb && x->single; i++) {
+        const uint64_t k = x->h_bm_start[i + 1] - x->h_bm_start[i];
+        if (k > 1) x->single = 0;
+        else if (k == 0) x->single = 2;
+      }
     }
   }
   if (A->single && B->single) return RS_OK;
   for (uint64_t p = 0; p < npairs; p++) {
     uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
     if (a < A->nb && b < B->nb &&
-        (A->h_bm_start[a + 1] - A->h_bm_start[a] != 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] != 1)) {
-      set_error("container_pairwise needs exactly one container per image");
+        (A->h_bm_start[a + 1] - A->h_bm_start[a] > 1 || B->h_bm_start[b + 1] - B->h_bm_start[b] > 1)) {
+      set_error("container_pairwise needs at most one container per image");
       return RS_ESHAPE;
     }
   }
@@ -1788,7 +1830,9 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   // 2(na + nb) bytes (+16 pad), so the input pools bound the result pool and
   // the op needs no host synchronization.
   const uint8_t AR = 1 << RS_TAG_ARRAY;
-  if (!ia && !ib && A->type_mask == AR && B->type_mask == AR && env_int("RS_EXACT_ALLOC", 0) == 0) {
+  // (empty images need the exact class counts: their entries go through k_copy)
+  if (!ia && !ib && A->type_mask == AR && B->type_mask == AR && A->single == 1 && B->single == 1 &&
+      env_int("RS_EXACT_ALLOC", 0) == 0) {
     const uint64_t Pub = A->pool_bytes + B->pool_bytes + 16 * npairs;
     return run_classes_and_compact(op, A, B, S, En, L, npairs, Pub, nullptr, nullptr, nullptr, nullptr, npairs,
                                    out);

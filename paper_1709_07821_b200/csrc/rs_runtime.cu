@@ -5,6 +5,7 @@
 #include <map>
 #include <tuple>
 #include <mutex>
+#include <set>
 #include <unordered_map>
 #include <cstring>
 #include "rs_internal.cuh"
@@ -382,6 +383,7 @@ int batch_alloc(rs_batch *b, uint64_t nb, uint64_t nc, uint64_t pool_bytes) {
 }
 
 void batch_release(rs_batch *b) {
+  if (b->ub_pool) ub_unregister(b);
   if (b->pending) {
     drop_staged(b);
     dfree(b->pending->d_any); dfree(b->pending->d_vcode); dfree(b->pending->d_vval);
@@ -397,11 +399,99 @@ void batch_release(rs_batch *b) {
 int fetch_host_meta(const rs_batch *cb) {
   RS_TRY(materialize(cb));
   rs_batch *b = const_cast<rs_batch *>(cb);
-  if (b->h_valid) return RS_OK;
-  b->h_bm_start.resize(b->nb + 1);
-  RS_TRY(d2h(b->h_bm_start.data(), b->d_bm_start, (b->nb + 1) * 8));
-  b->nc = b->h_bm_start[b->nb];
-  b->h_valid = true;
+  if (!b->h_valid) {
+    b->h_bm_start.resize(b->nb + 1);
+    RS_TRY(d2h(b->h_bm_start.data(), b->d_bm_start, (b->nb + 1) * 8));
+    b->nc = b->h_bm_start[b->nb];
+    b->h_valid = true;
+  }
+  // the stream is synchronized (or was, when h_valid was set): pack an
+  // upper-bound pool now, so every batch the host looks at holds at most
+  // ~1.25x its containers' bytes (bitmap.py:318-328 shrink_to_fit semantics)
+  if (b->ub_pool) RS_TRY(repack_pool(b));
+  return RS_OK;
+}
+
+// ------------------------------------------------------- pool repacking
+namespace {
+std::mutex g_ub_mu;
+std::set<rs_batch *> g_ub_live;   // results whose pool still holds its upper-bound slots
+uint64_t g_ub_bytes = 0;
+
+__global__ void k_pool_sizes(uint64_t nc, const uint8_t *__restrict__ type, const uint32_t *__restrict__ n,
+                             uint64_t *__restrict__ psize) {
+  uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (c < nc) psize[c] = rs_pad16(rs_payload_bytes(type[c], n[c]));
+  else if (c == nc) psize[c] = 0;
+}
+
+// warp per container: payload to its packed offset (16-byte units)
+__global__ void k_repack(uint64_t nc, DevBatch S, const uint64_t *__restrict__ new_off, uint8_t *__restrict__ pool) {
+  uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nc) return;
+  const uint32_t nv = (uint32_t)(rs_pad16(rs_payload_bytes(S.type[c], S.n[c])) >> 4);
+  const uint4 *src = (const uint4 *)(S.pool + S.off[c]);
+  uint4 *dst = (uint4 *)(pool + new_off[c]);
+  for (uint32_t i = lane; i < nv; i += 32) __stcs(dst + i, __ldcs(src + i));
+}
+
+uint64_t ub_high_water() {
+  static uint64_t mark = 0;
+  if (!mark) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    mark = std::max<uint64_t>(tot / 8, 1ull << 30);
+  }
+  return mark;
+}
+}  // namespace
+
+void ub_register(rs_batch *b) {
+  std::lock_guard<std::mutex> g(g_ub_mu);
+  b->ub_pool = true;
+  if (g_ub_live.insert(b).second) g_ub_bytes += b->pool_bytes;
+}
+
+void ub_unregister(rs_batch *b) {
+  std::lock_guard<std::mutex> g(g_ub_mu);
+  if (g_ub_live.erase(b)) g_ub_bytes -= b->pool_bytes;
+  b->ub_pool = false;
+}
+
+int repack_pool(rs_batch *b) {
+  ub_unregister(b);
+  const uint64_t nc = b->nc;
+  uint64_t *psize = (uint64_t *)dalloc((nc + 1) * 8), *poff = (uint64_t *)dalloc((nc + 1) * 8);
+  if (!psize || !poff) { dfree(psize); dfree(poff); set_error("device allocation failed (repack)"); return RS_ENOMEM; }
+  RS_LAUNCH(k_pool_sizes, (unsigned)((nc + 1 + 255) / 256), 256, 0, nc, b->d_type, b->d_n, psize);
+  RS_TRY(scan_exclusive<uint64_t>(psize, poff, nc + 1));
+  uint64_t used = 0;
+  RS_TRY(d2h(&used, poff + nc, 8));
+  // keep the pool when it is already within 1.25x of its containers' bytes
+  if (4 * b->pool_bytes <= 5 * used + 4096) {
+    dfree(psize); dfree(poff);
+    return RS_OK;
+  }
+  uint8_t *np = (uint8_t *)dalloc(used ? used : 16);
+  if (!np) { dfree(psize); dfree(poff); set_error("device allocation failed (repack pool)"); return RS_ENOMEM; }
+  if (nc) RS_LAUNCH(k_repack, (unsigned)((nc * 32 + 255) / 256), 256, 0, nc, b->dev(), poff, np);
+  RS_CK(cudaMemcpyAsync(b->d_off, poff, nc * 8, cudaMemcpyDeviceToDevice, g_stream));
+  dfree(b->d_pool);
+  b->d_pool = np;
+  b->pool_bytes = used;
+  dfree(psize); dfree(poff);
+  return RS_OK;
+}
+
+int ub_reserve(uint64_t bytes) {
+  std::vector<rs_batch *> victims;
+  {
+    std::lock_guard<std::mutex> g(g_ub_mu);
+    if (g_ub_bytes + bytes <= ub_high_water()) return RS_OK;
+    victims.assign(g_ub_live.begin(), g_ub_live.end());
+  }
+  for (rs_batch *v : victims) RS_TRY(fetch_host_meta(v));  // packs it
   return RS_OK;
 }
 

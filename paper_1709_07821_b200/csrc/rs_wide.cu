@@ -785,9 +785,11 @@ extern "C" int rs_union_many(const rs_batch *in, const uint64_t *idx, uint64_t n
   }
   Grouped g;
   RS_TRY(group_and_reorder(in, sel, g));
+  RS_TRY(ub_reserve(g.G * 8192));
   rs_batch *b = new rs_batch();
   int rc = batch_alloc(b, 1, g.G, g.G * 8192);
   if (rc) { g.release(); rs_batch_free(b); return rc; }
+  ub_register(b);  // one 8 KB slot per key until packed
   RS_LAUNCH_PROF("union_fold", g.G, k_union_fold, (unsigned)g.G, DT, 0, g.G, g.seg_start, g.item_c, g.keys, in->dev(), b->d_key, b->d_type,
             b->d_card, b->d_n, b->d_off, b->d_pool);
   uint64_t hs[2] = {0, g.G};

@@ -32,7 +32,7 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     from oracle import oracle as orc
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     from paper_1709_07821_b200.dist import max_over_ranks, sharded_counts
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -49,7 +49,7 @@ def _worker(rank, world, port, q):
 def test_two_rank_gloo_sharded_counts():
     import torch.multiprocessing as mp
     from oracle import oracle as orc
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -103,5 +103,5 @@ def test_config1_full_and_run_optimize_roundtrip(pkg_full):
 @pytest.fixture(scope="module")
 def pkg_full():
     import paper_1709_07821_b200 as rb
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     return rb, synth

@@ -148,7 +148,7 @@ def _check_pairs(pkg, wa, wb, A, B, ia, ib, ops=OPS, sample=None):
 
 
 def test_config1_full(pkg):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     buf, offs = synth.config1()
     w = _wires(buf, offs)
     Bt = pkg.BitmapBatch.from_wire((buf, offs))
@@ -156,7 +156,7 @@ def test_config1_full(pkg):
 
 
 def test_config2_subset(pkg):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     buf, offs = synth.config2(npairs=24)
     w = _wires(buf, offs)
     Bt = pkg.BitmapBatch.from_wire((buf, offs))
@@ -165,7 +165,7 @@ def test_config2_subset(pkg):
 
 
 def test_config3_subset(pkg):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     n = 30000
     buf, offs = synth.config3(npairs=n)
     A = pkg.BitmapBatch.from_wire(synth.slice_images(buf, offs, 0, n))
@@ -187,7 +187,7 @@ def test_config3_subset(pkg):
 
 
 def test_config4_subset_pairs_and_union(pkg):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     nb = 10
     buf, offs = synth.config4(nbitmaps=nb)
     w = _wires(buf, offs)
@@ -198,7 +198,7 @@ def test_config4_subset_pairs_and_union(pkg):
 
 
 def test_config5_subset_all_pairs(pkg):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     nb = 20
     buf, offs = synth.config5(nbitmaps=nb)
     Bt = pkg.BitmapBatch.from_wire((buf, offs))
@@ -226,7 +226,7 @@ def test_all_pairs_tensor_core_tiles(pkg, monkeypatch):
     with 300 containers (3 x 3 tile blocks, off-diagonal tiles), against the
     oracle's pairwise intersections; and the CUDA-core tiles for the same
     input."""
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     rng = np.random.default_rng(77)
     imgs = []
     for i in range(300):  # one container at key 0 per bitmap: m = 300 for that key
@@ -253,7 +253,7 @@ def test_all_pairs_tensor_core_tiles(pkg, monkeypatch):
 
 
 def test_run_optimize_matches_oracle(pkg):
-    from paper_1709_07821_b200 import synth
+    import workloads as synth
     buf, offs = synth.config5(nbitmaps=6, seed=9)
     # strip runs first: re-build from values, then run_optimize on the GPU
     Bt = pkg.BitmapBatch.from_wire((buf, offs))
@@ -295,7 +295,8 @@ def test_exact_and_upper_bound_allocation_agree(pkg, monkeypatch):
 
 def test_harness_rows_gate_and_format(pkg):
     import io
-    from paper_1709_07821_b200 import harness, synth
+    from paper_1709_07821_b200 import harness
+    import workloads as synth
     buf, offs = synth.config4(seed=31, nbitmaps=5, nkeys=50)
     B = pkg.BitmapBatch.from_wire((buf, offs))
     S = orc.Session(buf, offs)
@@ -352,7 +353,8 @@ def test_deferred_ingest_decode_errors(pkg):
 def test_deferred_ingest_pipeline_matches_sync(pkg):
     """Chunked ingest on the copy stream overlapping ops on the library
     stream (the e2e pattern of bench.py) gives the synchronous results."""
-    from paper_1709_07821_b200 import _lib, synth
+    from paper_1709_07821_b200 import _lib
+    import workloads as synth
     buf, offs = synth.config2(npairs=32)
     n = 32
     pin = _lib.PinnedBuffer(int(offs[-1]))

@@ -5,7 +5,7 @@ import struct
 import numpy as np
 
 from oracle import oracle as orc
-from paper_1709_07821_b200 import synth
+import workloads as synth
 
 
 def _types(buf, offs):

@@ -3,7 +3,8 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1709_07821_b200 as rb
-from paper_1709_07821_b200 import _lib, synth
+from paper_1709_07821_b200 import _lib
+import workloads as synth
 buf, offs = synth.config1()
 B = rb.BitmapBatch.from_wire((buf, offs))
 import torch

@@ -4,7 +4,8 @@ import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import ctypes as C
 import paper_1709_07821_b200 as rb
-from paper_1709_07821_b200 import _lib, synth
+from paper_1709_07821_b200 import _lib
+import workloads as synth
 from paper_1709_07821_b200._lib import lib
 buf, offs = synth.config1()
 B = rb.BitmapBatch.from_wire((buf, offs))

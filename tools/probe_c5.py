@@ -3,7 +3,8 @@ phase) on the last of several calls, plus the live kernel times."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1709_07821_b200 as rb
-from paper_1709_07821_b200 import _lib, synth
+from paper_1709_07821_b200 import _lib
+import workloads as synth
 buf, offs = synth.config5()
 B = rb.BitmapBatch.from_wire((buf, offs))
 for _ in range(3):

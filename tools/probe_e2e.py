@@ -4,7 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_1709_07821_b200 as rb
-from paper_1709_07821_b200 import _lib, synth
+from paper_1709_07821_b200 import _lib
+import workloads as synth
 
 buf, offs = synth.config2()
 n = 1024

@@ -3,7 +3,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1709_07821_b200 as rb
-from paper_1709_07821_b200 import _lib, synth
+from paper_1709_07821_b200 import _lib
+import workloads as synth
 
 op = sys.argv[1] if len(sys.argv) > 1 else "and"
 npairs = int(sys.argv[2]) if len(sys.argv) > 2 else 1024

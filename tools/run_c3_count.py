@@ -2,7 +2,8 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1709_07821_b200 as rb
-from paper_1709_07821_b200 import _lib, synth
+from paper_1709_07821_b200 import _lib
+import workloads as synth
 n = 1_000_000
 op = sys.argv[1] if len(sys.argv) > 1 else "and"
 buf, offs = synth.config3(npairs=n)

@@ -15,7 +15,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(os.path.dirname(_HERE), "libroaring_synth.so")
+LIB = os.path.join(_HERE, "libworkloads.so")
 _lib = None
 
 
