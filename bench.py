@@ -211,7 +211,66 @@ def cpu_baseline(buf, offs, max_seconds: float = 25.0, min_seconds: float = 5.0)
                       f"oracle/roaring_oracle.c restatement, {threads} threads, {t_total:.1f} s"}
 
 
+def python_reference_row(buf, offs, seconds: float = 6.0):
+    """Secondary row: the REAL reference package (pure Python + numpy, its
+    default `auto` -> accelerated backend, kernels/__init__.py:31-48), from the
+    pod-local install baseline/_ref, on a sample of C2 pairs: 1 core, and one
+    process per host core over independent pairs (the reference
+    itself is single-threaded)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "roaringset")):
+        return {"unavailable": "baseline/_ref not installed (tools/install_reference.sh)"}
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    ncores = os.cpu_count() or 1
+    # one bitmap pair per task: 4 ops + 4 op_cardinality over 256 container pairs
+    tasks = [(buf[int(offs[p]):int(offs[p + 1])].tobytes(), buf[int(offs[NPAIRS + p]):int(offs[NPAIRS + p + 1])].tobytes())
+             for p in range(min(NPAIRS, 4 * ncores))]
+    t0 = time.perf_counter()
+    done1 = 0
+    with ctx.Pool(1, initializer=_pyref_init, initargs=(ref,)) as pool:
+        pool.apply(_pyref_pair, (tasks[0],))  # import + warm-up
+        t0 = time.perf_counter()
+        while done1 < len(tasks) and time.perf_counter() - t0 < seconds / 2:
+            pool.apply(_pyref_pair, (tasks[done1],))
+            done1 += 1
+        t1 = time.perf_counter() - t0
+    with ctx.Pool(ncores, initializer=_pyref_init, initargs=(ref,)) as pool:
+        pool.map(_pyref_pair, tasks[:ncores])  # imports + warm-up in every worker
+        t0 = time.perf_counter()
+        pool.map(_pyref_pair, tasks)
+        tn = time.perf_counter() - t0
+    units = 8 * NCHUNKS
+    return {"kind": "python reference (baseline/_ref roaringset 0.1.0, accelerated backend)", "unit": UNIT,
+            "value_1core": units * done1 / t1, "value_ncores": units * len(tasks) / tn, "cores": ncores,
+            "sample": f"1 core: {done1} C2 bitmap pairs x (4 ops + 4 counts) in {t1:.1f} s; {ncores} processes: "
+                      f"{len(tasks)} pairs in {tn:.1f} s (each task deserializes its two images, then runs the 8 calls)"}
+
+
+_PYREF = {}
+
+
+def _pyref_init(ref):
+    sys.path.insert(0, ref)
+    import roaringset  # noqa: F401  (the reference, not this repo)
+    _PYREF["rs"] = roaringset
+
+
+def _pyref_pair(task):
+    rs = _PYREF["rs"]
+    a, b = rs.deserialize(task[0]), rs.deserialize(task[1])
+    for op in OPS:
+        a.op(op, b)
+        a.op_cardinality(op, b)
+    return 0
+
+
 def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path on this
+    box's host cores -- the oracle port (oracle/roaring_oracle.c, the C
+    restatement of the reference algorithm, -O3 x86-64-v3, all host threads
+    over independent pairs), on the SAME workload as the GPU arm: all 1024
+    C2 bitmap pairs x (4 ops + 4 op_cardinality) per step."""
     ws, rank, local = dist_env()
     if rank != 0:
         return 0
@@ -219,34 +278,35 @@ def run_reference(args):
     buf, offs = workload(seed=2)
     threads = orc.num_threads()
     S = orc.Session(buf, offs, threads)
-    sample = 32  # bitmap pairs per step (8,192 container pairs x 8)
+    ia = np.arange(NPAIRS)
 
-    def step(k):
-        lo = (k * sample) % NPAIRS
-        ia = np.arange(lo, lo + sample)
+    def step():
         for op in OPS:
             S.run(op, "op", S, ia, ia + NPAIRS, threads)
             S.run(op, "op_cardinality", S, ia, ia + NPAIRS, threads)
 
-    for k in range(args.warmup):
-        step(k)
+    for _ in range(args.warmup):
+        step()
     t0 = time.perf_counter()
-    for k in range(args.steps):
-        step(args.warmup + k)
+    for _ in range(args.steps):
+        step()
     dt = time.perf_counter() - t0
-    units = args.steps * sample * NCHUNKS * 8
+    units = args.steps * NPAIRS * NCHUNKS * 8
     value = units / dt
+    pyref = None if args.no_pyref else python_reference_row(buf, offs)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (seeded, BASELINE.json configs[1] shape)",
-        "config": {"workload": f"C2 sample: {sample} of {NPAIRS} bitmap pairs x {NCHUNKS} bitset chunks per step, "
-                               "4 ops + 4 op_cardinality", "seed": 2},
+        "data": "synthetic (seeded, BASELINE.json configs[1] shape)", "same_config": True,
+        "config": {"workload": f"C2: {NPAIRS} bitmap pairs x {NCHUNKS} bitset chunks (8 KB), 4 ops + 4 "
+                               "op_cardinality per step", "seed": 2},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} bitmap pairs per step (oracle/roaring_oracle.c restatement of "
-                                   "the reference algorithm, in-memory bitmaps)"},
+                         "sample": f"all {NPAIRS} pairs per step x {args.steps} steps (oracle/roaring_oracle.c "
+                                   "restatement of the reference algorithm, in-memory bitmaps, -O3 x86-64-v3, "
+                                   f"{threads} threads)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "python_reference": pyref,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -278,21 +338,24 @@ def run_gpu(args):
         for op in OPS:
             A.pairwise_cardinality_device(op, B, counts.data_ptr(), NPAIRS)
 
-    # oracle-checked warm-up (harness.py:230-235): sampled pairs, bytes + counts
+    # oracle-checked warm-up (harness.py:230-235) over the FULL results: the
+    # content digest of every result bitmap (computed on the device) and every
+    # count, folded and compared with the oracle's (tests/golden/config_digests.json)
+    from bench_configs import Parity
+    from paper_1709_07821_b200.batch import fold_digests
+    par = Parity("C2")
     out_bytes = {}
     for op in OPS:
         R = A.pairwise(op, B)
         pb, db, _ = R.stats()
         out_bytes[op] = pb + db
-        if rank == 0 and not args.no_check:
-            from oracle import oracle as orc
-            got = R.select([0, NPAIRS - 1]).to_wire_list()
-            for k, p in enumerate((0, NPAIRS - 1)):
-                wa = A_img[0][int(A_img[1][p]):int(A_img[1][p + 1])].tobytes()
-                wb = B_img[0][int(B_img[1][p]):int(B_img[1][p + 1])].tobytes()
-                if got[k] != orc.op(op, wa, wb):
-                    raise SystemExit(f"parity failure in warm-up: op {op} pair {p}")
+        if not args.no_check and seed == 2:
+            par.check(op, fold_digests(R.digests()))
+            par.check(op + "_count", fold_digests(A.pairwise_cardinality(op, B)))
         del R
+    parity = par.result("every result bitmap of all 1024 pairs x 4 ops (content digests) and all 4 x 1024 counts")
+    if par.bad:
+        raise SystemExit(f"parity failure in warm-up: {par.bad}")
     for _ in range(args.warmup):
         step()
     _lib.synchronize()
@@ -423,6 +486,22 @@ def run_gpu(args):
         base = cpu_baseline(buf, offs, max_seconds=args.cpu_seconds)  # rank 0: seed 2 = this workload
 
     value = ws * units_per_step * args.steps / (ms_max * 1e-3)
+    step_ms = ms_max / args.steps
+    step_bytes = 4 * in_bytes + sum(out_bytes.values()) + 4 * (in_bytes + 8 * NPAIRS)
+    configs = None
+    if rank == 0 and not args.no_configs:
+        # every BASELINE.json config, measured the same way (bench_configs.py);
+        # C2 is this line's own step
+        from bench_configs import measure
+        configs = {"C2": {
+            "workload": f"C2: {NPAIRS} bitmap pairs x {NCHUNKS} bitset chunks, 4 ops + 4 counts (this line's step)",
+            "units_per_step": units_per_step, "ms": step_ms, "value": units_per_step / (step_ms * 1e-3),
+            "unit": UNIT, "algorithmic_GBps": step_bytes / (step_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "frac": step_bytes / (step_ms * 1e-3) / 1e9 / hbm, "peak": hbm,
+                         "peak_kind": peak_kind},
+            "cpu_baseline": base, "parity": parity}}
+        configs.update(measure([c for c in ("C1", "C3", "C4", "C5") if c in args.configs.split(",")],
+                               cpu_seconds=args.cpu_seconds_config))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -446,6 +525,8 @@ def run_gpu(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": base,
+        "parity": parity,
+        "configs": configs,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -464,6 +545,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config block (C1, C3, C4, C5)")
+    ap.add_argument("--no-pyref", action="store_true", help="reference arm: skip the real Python reference row")
+    ap.add_argument("--configs", default="C1,C3,C4,C5")
+    ap.add_argument("--cpu-seconds-config", type=float, default=3.0)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "gpu":
         print("note: warm-up raised to 3 (timing rules)", file=sys.stderr)

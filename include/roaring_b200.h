@@ -130,6 +130,13 @@ int rs_batch_to_wire(const rs_batch *b, uint8_t *buf, uint64_t cap, uint64_t *of
 /* RoaringBitmap.to_array (bitmap.py:136-144): all bitmaps' values into host
  * out (capacity cap values) with offs[0..n] out. */
 int rs_batch_to_u32(const rs_batch *b, uint32_t *out, uint64_t cap, uint64_t *offs);
+/* Content digest of every bitmap: a 64-bit hash of exactly what its wire
+ * image holds (keys, container types, cardinalities, payloads), computed on
+ * the device -- equal bitmaps (bitmap.py:87-91) have equal digests.  For
+ * checking results at full size against another implementation without
+ * moving them (the definition is in DESIGN.md section 5).  digests: host
+ * u64[n] (synchronizes) or, with on_device != 0, device u64[n]. */
+int rs_batch_digests(const rs_batch *b, uint64_t *digests, int on_device);
 /* Bitmap-level equality (bitmap.py:87-91): eq[p] = A[ia[p]] == B[ib[p]], host u8 out. */
 int rs_batch_equal(const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
                    uint64_t npairs, uint8_t *eq);

@@ -71,6 +71,9 @@ def lib():
         L.orc_batch_load.restype = P
         L.orc_batch_free.argtypes = [P]
         L.orc_batch_run.argtypes = [C.c_int, C.c_int, P, P, P, P, I64, P, C.c_int]
+        L.orc_digest_images.argtypes = [P, P, I64, P, C.c_int]
+        L.orc_batch_digest.argtypes = [C.c_int, C.c_int, P, P, P, P, I64, P, C.c_int]
+        L.orc_union_digest.argtypes = [P, P]
         _lib = L
     return _lib
 
@@ -271,8 +274,34 @@ class Session:
                             ib.ctypes.data, ia.size, out.ctypes.data, threads)
         return out[:ia.size]
 
+    def digests(self, op_name: str, kind: str, other: "Session", ia, ib, threads: int = 0) -> np.ndarray:
+        """Content digests (roaring_oracle.c "content digests") of the results
+        of op / container_pairwise over the pairs, without serializing them."""
+        ia, ib = _i64(ia), _i64(ib)
+        out = np.zeros(max(ia.size, 1), dtype=np.uint64)
+        lib().orc_batch_digest(_op_index(op_name), self.KINDS[kind], self._h, other._h, ia.ctypes.data,
+                               ib.ctypes.data, ia.size, out.ctypes.data, threads)
+        return out[:ia.size]
+
+    def union_digest(self) -> int:
+        out = np.zeros(1, dtype=np.uint64)
+        lib().orc_union_digest(self._h, out.ctypes.data)
+        return int(out[0])
+
     def __del__(self):
         try:
             lib().orc_batch_free(self._h)
         except Exception:
             pass
+
+
+def digest_images(buf, offs, threads: int = 0) -> np.ndarray:
+    """Content digest of each wire image (roaring_oracle.c "content digests")."""
+    buf = np.ascontiguousarray(buf, dtype=np.uint8)
+    offs = np.ascontiguousarray(offs, dtype=np.uint64)
+    n = len(offs) - 1
+    out = np.zeros(max(n, 1), dtype=np.uint64)
+    rc = lib().orc_digest_images(buf.ctypes.data, offs.ctypes.data, n, out.ctypes.data, threads)
+    if rc:
+        _raise(-1)
+    return out[:n]

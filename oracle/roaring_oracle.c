@@ -1295,3 +1295,101 @@ int orc_batch_run(int op, int kind, void *ha, void *hb, const int64_t *ia, const
     }
     return 0;
 }
+
+/* ------------------------------------------------ content digests (parity at scale)
+ * A 64-bit digest of a bitmap's exact content -- keys, container types,
+ * cardinalities and payloads, i.e. everything its wire image
+ * (serde.py:3-10) holds -- so full-size results can be compared with the
+ * GPU's (rs_batch_digest, include/roaring_b200.h) without moving them.
+ * Definition (identical in csrc/rs_egress.cu):
+ *   mix(z)      = SplitMix64 finalizer
+ *   h(c)        = mix(key<<48 | tag<<40 | card) + sum_i term_i
+ *     array:    term_i = mix((i<<16 | v_i) + K_ARRAY)
+ *     bitset:   term_w = mix(word_w + w * K_BITSET)
+ *     run:      term_r = mix((r<<32 | start_r<<16 | len_r) + K_RUN)
+ *   digest(bm)  = sum_j mix(h(c_j) + (j+1) * K_POS)     (0 for the empty bitmap)
+ * Sums are mod 2^64. */
+#define DG_K_ARRAY 0x243F6A8885A308D3ull
+#define DG_K_BITSET 0x13198A2E03707344ull
+#define DG_K_RUN 0xA4093822299F31D0ull
+#define DG_K_POS 0x082EFA98EC4E6C89ull
+
+static inline uint64_t dg_mix(uint64_t z) {
+    z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27; z *= 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static uint64_t dg_container(uint16_t key, const oc_t *c) {
+    uint64_t card = (uint64_t)oc_len(c);
+    uint64_t h = dg_mix(((uint64_t)key << 48) | ((uint64_t)c->type << 40) | card);
+    if (c->type == TAG_ARRAY) {
+        for (int32_t i = 0; i < c->n; i++) h += dg_mix((((uint64_t)i << 16) | c->v[i]) + DG_K_ARRAY);
+    } else if (c->type == TAG_BITSET) {
+        for (int w = 0; w < BLOCK_WORDS; w++) h += dg_mix(c->w[w] + (uint64_t)w * DG_K_BITSET);
+    } else {
+        for (int32_t r = 0; r < c->n; r++)
+            h += dg_mix((((uint64_t)r << 32) | ((uint64_t)c->v[2 * r] << 16) | c->v[2 * r + 1]) + DG_K_RUN);
+    }
+    return h;
+}
+
+static uint64_t dg_bitmap(const obm_t *b) {
+    uint64_t d = 0;
+    for (int32_t j = 0; j < b->n; j++) d += dg_mix(dg_container(b->keys[j], &b->c[j]) + (uint64_t)(j + 1) * DG_K_POS);
+    return d;
+}
+
+/* digests of n wire images */
+int orc_digest_images(const uint8_t *buf, const uint64_t *offs, int64_t n, uint64_t *out, int nthreads) {
+    int err = 0;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 4) num_threads(nthreads) reduction(|:err)
+#endif
+    for (int64_t i = 0; i < n; i++) {
+        obm_t b;
+        char m[256]; int64_t eo;
+        if (deserialize(buf + offs[i], offs[i + 1] - offs[i], &b, &eo, m, sizeof m)) { err |= 1; continue; }
+        out[i] = dg_bitmap(&b);
+        bm_free(&b);
+    }
+    return err ? -1 : 0;
+}
+
+/* digests of the results of a batched op (kind 0: RoaringBitmap.op; kind 2:
+ * container_pairwise over one-container bitmaps, result at key 0 of A's key)
+ * on in-memory sessions, without serializing the results */
+int orc_batch_digest(int op, int kind, void *ha, void *hb, const int64_t *ia, const int64_t *ib, int64_t npairs,
+                     uint64_t *out, int nthreads) {
+    obatch_t *A = ha, *B = hb;
+#ifdef _OPENMP
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#endif
+    for (int64_t p = 0; p < npairs; p++) {
+        const obm_t *a = &A->bm[ia[p]], *b = &B->bm[ib[p]];
+        if (kind == 0) {
+            obm_t R = bm_op(op, a, b);
+            out[p] = dg_bitmap(&R);
+            bm_free(&R);
+        } else {
+            oc_t r = container_pairwise(op, &a->c[0], &b->c[0]);
+            out[p] = oc_len(&r) ? dg_mix(dg_container(a->keys[0], &r) + DG_K_POS) : 0;
+            oc_free(&r);
+        }
+    }
+    return 0;
+}
+
+/* digest of union_many over all images of a session, in order */
+int orc_union_digest(void *ha, uint64_t *out) {
+    obatch_t *A = ha;
+    const obm_t **pp = xmalloc(sizeof(obm_t *) * (size_t)(A->n ? A->n : 1));
+    for (int64_t i = 0; i < A->n; i++) pp[i] = &A->bm[i];
+    obm_t R = bm_union_many(pp, (int32_t)A->n);
+    *out = dg_bitmap(&R);
+    bm_free(&R);
+    free(pp);
+    return 0;
+}

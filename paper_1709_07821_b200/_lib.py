@@ -66,6 +66,7 @@ def _declare(L):
         "rs_batch_to_wire": ([P, P, U64, P], I32),
         "rs_batch_to_u32": ([P, P, U64, P], I32),
         "rs_batch_equal": ([P, P, P, P, U64, P], I32),
+        "rs_batch_digests": ([P, P, I32], I32),
         "rs_batch_contains": ([P, P, P, U64, P], I32),
         "rs_pairwise": ([I32, P, P, P, P, U64, pp], I32),
         "rs_pairwise_cardinality": ([I32, P, P, P, P, U64, P, I32], I32),
@@ -191,9 +192,8 @@ class PinnedBuffer:
 class _PinnedView:
     """Owner of one pooled page-locked block, exported to numpy through the
     array interface.  Every array made from it -- slices, views, `arr[:m]` --
-    has this object as its `.base` (numpy collapses view chains to the first
-    non-ndarray owner), so the block goes back to the pool only when the last
-    of them dies."""
+    reaches this object through its `.base` chain, so the block goes back to
+    the pool only when the last of them dies."""
 
     __slots__ = ("__array_interface__", "_buf", "__weakref__")
 

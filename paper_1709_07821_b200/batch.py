@@ -41,6 +41,24 @@ def _images(images):
     return buf, offs
 
 
+_FOLD_K = np.uint64(0x9E3779B97F4A7C15)
+
+
+def fold_digests(values) -> int:
+    """One 64-bit digest of an ordered sequence of u64 (per-bitmap content
+    digests, or counts): sum_i mix(v_i + (i+1) * K) mod 2^64, mix the
+    SplitMix64 finalizer -- order-sensitive, so a permuted batch differs."""
+    z = np.ascontiguousarray(values, dtype=np.uint64).copy()
+    with np.errstate(over="ignore"):
+        z += np.arange(1, len(z) + 1, dtype=np.uint64) * _FOLD_K
+        z ^= z >> np.uint64(30)
+        z *= np.uint64(0xBF58476D1CE4E5B9)
+        z ^= z >> np.uint64(27)
+        z *= np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(31)
+        return int(z.sum(dtype=np.uint64))
+
+
 class BitmapBatch:
     __slots__ = ("_h", "_keep", "__weakref__")
 
@@ -184,6 +202,18 @@ class BitmapBatch:
     def to_arrays(self) -> list[np.ndarray]:
         vals, offs = self.to_arrays_flat()
         return [vals[int(offs[i]):int(offs[i + 1])] for i in range(len(offs) - 1)]
+
+    def digests(self) -> np.ndarray:
+        """64-bit content digest per bitmap, computed on the device (equal
+        bitmaps, equal digests; rs_batch_digests)."""
+        out = np.zeros(max(len(self), 1), dtype=np.uint64)
+        check(lib().rs_batch_digests(self._h, out.ctypes.data, 0))
+        return out[:len(self)]
+
+    def digest(self) -> int:
+        """fold_digests of the per-bitmap content digests: one u64 for the
+        whole batch's exact content."""
+        return fold_digests(self.digests())
 
     def equal(self, other: "BitmapBatch", ia=None, ib=None) -> np.ndarray:
         """Type-sensitive equality per pair (bitmap.py:87-91)."""

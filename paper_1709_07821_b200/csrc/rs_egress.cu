@@ -392,3 +392,79 @@ extern "C" int rs_batch_contains(const rs_batch *b, const uint32_t *ibm, const u
   dfree(d_v); dfree(d_i); dfree(d_h);
   return RS_OK;
 }
+
+// ---------------------------------------------------------- content digests
+// A 64-bit digest of each bitmap's exact content (keys, types, cardinalities,
+// payloads: everything its wire image holds), for parity at full size without
+// moving results to the host.  The definition is shared with the oracle
+// (oracle/roaring_oracle.c "content digests"):
+//   h(c) = mix(key<<48 | tag<<40 | card) + sum of per-unit terms
+//   digest(bitmap) = sum_j mix(h(c_j) + (j+1) * K_POS)
+namespace {
+constexpr uint64_t DG_K_ARRAY = 0x243F6A8885A308D3ull, DG_K_BITSET = 0x13198A2E03707344ull,
+                   DG_K_RUN = 0xA4093822299F31D0ull, DG_K_POS = 0x082EFA98EC4E6C89ull;
+
+__device__ __forceinline__ uint64_t dg_mix(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27; z *= 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// warp per container: its positional term mix(h(c) + (j+1) K_POS)
+__global__ void k_digest_containers(uint64_t nc, uint64_t nb, DevBatch B, uint64_t *__restrict__ term) {
+  const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nc) return;
+  const uint8_t t = B.type[c];
+  const uint32_t n = B.n[c];
+  const uint8_t *p = B.pool + B.off[c];
+  uint64_t h = 0;
+  if (t == RS_TAG_ARRAY) {
+    const uint16_t *v = (const uint16_t *)p;
+    for (uint32_t i = lane; i < n; i += 32) h += dg_mix((((uint64_t)i << 16) | v[i]) + DG_K_ARRAY);
+  } else if (t == RS_TAG_BITSET) {
+    const uint64_t *w = (const uint64_t *)p;
+    for (uint32_t i = lane; i < RS_WORDS; i += 32) h += dg_mix(w[i] + (uint64_t)i * DG_K_BITSET);
+  } else {
+    const uint32_t *r = (const uint32_t *)p;  // (start, length) u16 pairs
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t x = r[i];
+      h += dg_mix((((uint64_t)i << 32) | ((uint64_t)(x & 0xFFFF) << 16) | (x >> 16)) + DG_K_RUN);
+    }
+  }
+  for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if (lane == 0) {
+    const uint64_t bm = bitmap_of(B.bm_start, nb, c);
+    h += dg_mix(((uint64_t)B.key[c] << 48) | ((uint64_t)t << 40) | B.card[c]);
+    term[c] = dg_mix(h + (c - B.bm_start[bm] + 1) * DG_K_POS);
+  }
+}
+
+__global__ void k_digest_bitmaps(uint64_t nb, const uint64_t *__restrict__ bm_start, const uint64_t *__restrict__ term,
+                                 uint64_t *__restrict__ out) {
+  const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nb) return;
+  uint64_t s = 0;
+  for (uint64_t c = bm_start[w] + lane; c < bm_start[w + 1]; c += 32) s += term[c];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s;
+}
+}  // namespace
+
+extern "C" int rs_batch_digests(const rs_batch *b, uint64_t *digests, int on_device) {
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(b));
+  if (!on_device) RS_TRY(resolve_pending(b));
+  uint64_t *term = (uint64_t *)dalloc((b->nc + 1) * 8);
+  uint64_t *dout = on_device ? digests : (uint64_t *)dalloc((b->nb + 1) * 8);
+  if (!term || !dout) { set_error("device allocation failed (digests)"); return RS_ENOMEM; }
+  RS_LAUNCH(k_digest_containers, grid_for(b->nc * 32, 256), 256, 0, b->nc, b->nb, b->dev(), term);
+  RS_LAUNCH(k_digest_bitmaps, grid_for(b->nb * 32, 256), 256, 0, b->nb, b->d_bm_start, term, dout);
+  if (!on_device) {
+    RS_TRY(d2h(digests, dout, b->nb * 8));
+    dfree(dout);
+  }
+  dfree(term);
+  return RS_OK;
+}

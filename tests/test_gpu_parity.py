@@ -505,3 +505,21 @@ def test_scan_over_pairs_fused_and_separate(pkg, npairs):
             if key not in want_card:
                 want_card[key] = orc.op_cardinality(op, pool[key[1]], pool[key[2]])
             assert cards[p] == want_card[key], (op, p)
+
+
+def test_device_content_digests_match_oracle(pkg):
+    """rs_batch_digests (device) == the oracle's content digest, on the
+    reference's golden inputs and on GPU op results of every container mix."""
+    g = load()
+    ws = [g.wire(a) for a in g["pair_a"]]
+    buf = np.frombuffer(b"".join(ws), np.uint8)
+    offs = np.concatenate([[0], np.cumsum([len(w) for w in ws])]).astype(np.uint64)
+    A = pkg.BitmapBatch.from_wire(ws)
+    assert np.array_equal(A.digests(), orc.digest_images(buf, offs))
+    B = pkg.BitmapBatch.from_wire([g.wire(b) for b in g["pair_b"]])
+    for op in OPS:
+        R = A.pairwise(op, B)
+        rw = R.to_wire_list()
+        rbuf = np.frombuffer(b"".join(rw), np.uint8)
+        roffs = np.concatenate([[0], np.cumsum([len(w) for w in rw])]).astype(np.uint64)
+        assert np.array_equal(R.digests(), orc.digest_images(rbuf, roffs)), op

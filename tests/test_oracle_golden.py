@@ -122,3 +122,51 @@ def test_point_mutation_is_op_with_singleton():
                 one = orc.from_values(np.array([v], dtype=np.uint64))
                 cur = orc.op("or" if kind == "add" else "andnot", cur, one)
             assert cur == g.wire(img), (kind, v)
+
+
+def _mix(z):
+    m = (1 << 64) - 1
+    z ^= z >> 30; z = (z * 0xBF58476D1CE4E5B9) & m
+    z ^= z >> 27; z = (z * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def digest_py(wire: bytes) -> int:
+    """Plain-Python restatement of the content digest (roaring_oracle.c
+    "content digests", rs_batch_digests)."""
+    import struct
+    m = (1 << 64) - 1
+    (count,) = struct.unpack_from("<I", wire, 4)
+    off = 8 + 8 * count
+    d = 0
+    for j in range(count):
+        key, tag, _pad, card = struct.unpack_from("<HBBI", wire, 8 + 8 * j)
+        h = _mix((key << 48) | (tag << 40) | card)
+        if tag == 1:
+            for i, v in enumerate(struct.unpack_from(f"<{card}H", wire, off)):
+                h += _mix((((i << 16) | v) + 0x243F6A8885A308D3) & m)
+            off += 2 * card
+        elif tag == 2:
+            for w, x in enumerate(struct.unpack_from("<1024Q", wire, off)):
+                h += _mix((x + w * 0x13198A2E03707344) & m)
+            off += 8192
+        else:
+            (nr,) = struct.unpack_from("<H", wire, off)
+            r = struct.unpack_from(f"<{2 * nr}H", wire, off + 2)
+            for k in range(nr):
+                h += _mix((((k << 32) | (r[2 * k] << 16) | r[2 * k + 1]) + 0xA4093822299F31D0) & m)
+            off += 2 + 4 * nr
+        d += _mix(((h & m) + (j + 1) * 0x082EFA98EC4E6C89) & m)
+    return d & m
+
+
+def test_content_digest_definition():
+    """The oracle's content digest equals its plain-Python restatement on the
+    reference's own images (all three container types)."""
+    g = load()
+    ws = [g.wire(i) for i in list(g["pair_a"][:12]) + list(g["pair_res"][:6, 1])]
+    buf = np.frombuffer(b"".join(ws), np.uint8)
+    offs = np.concatenate([[0], np.cumsum([len(w) for w in ws])]).astype(np.uint64)
+    got = orc.digest_images(buf, offs)
+    assert [int(x) for x in got] == [digest_py(w) for w in ws]
+    assert len(set(int(x) for x in got)) == len(set(ws))
