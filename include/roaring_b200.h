@@ -108,7 +108,11 @@ int rs_batch_free(rs_batch *b);
  * container count per type (u64[4], index = tag). */
 int rs_batch_stats(const rs_batch *b, uint64_t *payload_bytes, uint64_t *descriptor_bytes,
                    uint64_t *type_counts);
-/* Number of bitmaps, total containers, payload-pool bytes. */
+/* Number of bitmaps (host-side, never synchronizes). */
+uint64_t rs_batch_len(const rs_batch *b);
+/* Number of bitmaps, total containers, payload-pool bytes.  An op result's
+ * pool, laid out by per-container upper bounds, is packed here first, so
+ * pool_bytes is at most ~1.25x the containers' bytes. */
 int rs_batch_info(const rs_batch *b, uint64_t *n_bitmaps, uint64_t *n_containers,
                   uint64_t *pool_bytes);
 /* Per-bitmap cardinality (RoaringBitmap.__len__, bitmap.py:77-82) -> host u64[n]. */
@@ -127,6 +131,17 @@ int rs_batch_select(const rs_batch *b, const uint64_t *idx, uint64_t n, rs_batch
 int rs_batch_wire_sizes(const rs_batch *b, uint64_t *sizes);
 /* All images concatenated into host buf (capacity cap) with offs[0..n] out. */
 int rs_batch_to_wire(const rs_batch *b, uint8_t *buf, uint64_t cap, uint64_t *offs);
+/* Same images, asynchronously: the image sizes are read back (one
+ * synchronization of the library stream: offs[0..n] are valid on return),
+ * the images are assembled on the device and copied into buf on the
+ * library's export stream, and the call returns; *done is a CUDA event
+ * (rs_event_synchronize / rs_event_query / rs_event_destroy) that completes
+ * when the bytes have landed.  buf should be page-locked (rs_host_alloc) for
+ * the copy to overlap; the batch may be freed as soon as the call returns. */
+int rs_batch_to_wire_async(const rs_batch *b, uint8_t *buf, uint64_t cap, uint64_t *offs, void **done);
+int rs_event_synchronize(void *event);
+/* RS_OK when the event has completed, 1 while it is pending. */
+int rs_event_query(void *event);
 /* RoaringBitmap.to_array (bitmap.py:136-144): all bitmaps' values into host
  * out (capacity cap values) with offs[0..n] out. */
 int rs_batch_to_u32(const rs_batch *b, uint32_t *out, uint64_t cap, uint64_t *offs);

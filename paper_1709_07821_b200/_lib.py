@@ -57,6 +57,7 @@ def _declare(L):
         "rs_batch_from_u32": ([P, P, U64, I32, pp], I32),
         "rs_batch_free": ([P], I32),
         "rs_batch_info": ([P, P, P, P], I32),
+        "rs_batch_len": ([P], U64),
         "rs_batch_cardinalities": ([P, P], I32),
         "rs_batch_cardinalities_device": ([P, P], I32),
         "rs_batch_container_counts": ([P, P], I32),
@@ -64,6 +65,9 @@ def _declare(L):
         "rs_batch_select": ([P, P, U64, pp], I32),
         "rs_batch_wire_sizes": ([P, P], I32),
         "rs_batch_to_wire": ([P, P, U64, P], I32),
+        "rs_batch_to_wire_async": ([P, P, U64, P, pp], I32),
+        "rs_event_synchronize": ([P], I32),
+        "rs_event_query": ([P], I32),
         "rs_batch_to_u32": ([P, P, U64, P], I32),
         "rs_batch_equal": ([P, P, P, P, U64, P], I32),
         "rs_batch_digests": ([P, P, I32], I32),
@@ -161,6 +165,31 @@ class Event:
         ms = C.c_float()
         check(lib().rs_event_elapsed(self._e, later._e, C.byref(ms)))
         return float(ms.value)
+
+    def __del__(self):
+        try:
+            if self._e:
+                lib().rs_event_destroy(self._e)
+        except Exception:
+            pass
+
+
+class Completion:
+    """A CUDA event handed out by an asynchronous call (rs_batch_to_wire_async):
+    wait() blocks until the work behind it has finished; done() polls."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._e = handle
+
+    def wait(self) -> None:
+        check(lib().rs_event_synchronize(self._e))
+
+    def done(self) -> bool:
+        rc = lib().rs_event_query(self._e)
+        if rc == 1:
+            return False
+        check(rc)
+        return True
 
     def __del__(self):
         try:

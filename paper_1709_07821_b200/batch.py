@@ -147,7 +147,7 @@ class BitmapBatch:
         return int(nb.value), int(nc.value), int(pb.value)
 
     def __len__(self) -> int:
-        return self.info()[0]
+        return int(lib().rs_batch_len(self._h))
 
     def stats(self):
         """(payload bytes, descriptor bytes, {tag: count}) in the SURVEY 8(d) accounting."""
@@ -185,6 +185,18 @@ class BitmapBatch:
         offs = np.zeros(n + 1, dtype=np.uint64)
         check(lib().rs_batch_to_wire(self._h, buf.ctypes.data, buf.nbytes, offs.ctypes.data))
         return buf[:total], offs
+
+    def to_wire_async(self, out: np.ndarray):
+        """serde.serialize of every bitmap into `out` (uint8, ideally
+        page-locked: PinnedBuffer) without waiting for the transfer.
+        Returns (offsets, completion): offsets are final on return, the bytes
+        are in `out` once completion.wait() returns.  `out` must stay alive
+        until then; this batch may be freed at once."""
+        n = len(self)
+        offs = _lib.pinned_pool.empty(n + 1, np.uint64)
+        e = C.c_void_p()
+        check(lib().rs_batch_to_wire_async(self._h, out.ctypes.data, out.nbytes, offs.ctypes.data, C.byref(e)))
+        return offs, _lib.Completion(e)
 
     def to_wire_list(self) -> list[bytes]:
         buf, offs = self.to_wire()

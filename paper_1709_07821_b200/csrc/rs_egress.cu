@@ -231,7 +231,7 @@ static int wire_offsets(const rs_batch *b, uint64_t *&ps, uint64_t *&imgoff) {
 
 extern "C" int rs_batch_wire_sizes(const rs_batch *b, uint64_t *sizes) {
   RS_TRY(ensure_device());
-  RS_TRY(fetch_host_meta(b));
+  RS_TRY(fetch_host_meta_nopack(b));
   RS_TRY(resolve_pending(b));
   uint64_t *ps, *imgoff;
   RS_TRY(wire_offsets(b, ps, imgoff));
@@ -245,7 +245,7 @@ extern "C" int rs_batch_wire_sizes(const rs_batch *b, uint64_t *sizes) {
 
 extern "C" int rs_batch_to_wire(const rs_batch *b, uint8_t *buf, uint64_t cap, uint64_t *offs) {
   RS_TRY(ensure_device());
-  RS_TRY(fetch_host_meta(b));
+  RS_TRY(fetch_host_meta_nopack(b));
   RS_TRY(resolve_pending(b));
   uint64_t *ps, *imgoff;
   RS_TRY(wire_offsets(b, ps, imgoff));
@@ -262,6 +262,67 @@ extern "C" int rs_batch_to_wire(const rs_batch *b, uint8_t *buf, uint64_t cap, u
   RS_LAUNCH(k_wire_containers, grid_for(b->nc * 32, 256), 256, 0, b->nc, b->nb, b->dev(), ps, imgoff, dout);
   RS_TRY(d2h(buf, dout, total));
   dfree(dout); dfree(ps); dfree(imgoff);
+  return RS_OK;
+}
+
+// Asynchronous export: one host synchronization for the image sizes (the
+// layout), then the images are assembled in a stream-ordered device staging
+// block and copied to the caller's page-locked buffer on a dedicated export
+// stream, so the device->host transfer of one batch overlaps whatever the
+// library stream and the ingest copy stream do next (PCIe is full duplex).
+namespace {
+cudaStream_t g_export = nullptr;
+int g_export_dev = -1;
+}  // namespace
+
+extern "C" int rs_batch_to_wire_async(const rs_batch *b, uint8_t *buf, uint64_t cap, uint64_t *offs, void **done) {
+  RS_TRY(ensure_device());
+  if (!b || !offs || !done) { set_error("null batch/offs/done"); return RS_EARG; }
+  *done = nullptr;
+  RS_TRY(fetch_host_meta_nopack(b));
+  RS_TRY(resolve_pending(b));
+  int dev = 0;
+  RS_CK(cudaGetDevice(&dev));
+  if (!g_export || g_export_dev != dev) {
+    RS_CK(cudaStreamCreateWithFlags(&g_export, cudaStreamNonBlocking));
+    g_export_dev = dev;
+  }
+  uint64_t *ps, *imgoff;
+  RS_TRY(wire_offsets(b, ps, imgoff));
+  RS_TRY(d2h(offs, imgoff, (b->nb + 1) * 8));  // the layout: the one synchronization
+  const uint64_t total = offs[b->nb];
+  if (total > cap) {
+    dfree(ps); dfree(imgoff);
+    set_error("wire buffer too small: need " + std::to_string(total));
+    return RS_EARG;
+  }
+  uint8_t *stage = nullptr;
+  RS_CK(cudaMallocAsync((void **)&stage, total ? total : 16, g_stream));
+  RS_LAUNCH(k_wire_headers, grid_for(b->nb, 256), 256, 0, b->nb, b->d_bm_start, imgoff, stage);
+  RS_LAUNCH(k_wire_containers, grid_for(b->nc * 32, 256), 256, 0, b->nc, b->nb, b->dev(), ps, imgoff, stage);
+  dfree(ps); dfree(imgoff);
+  cudaEvent_t assembled, landed;
+  RS_CK(cudaEventCreateWithFlags(&assembled, cudaEventDisableTiming));
+  RS_CK(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
+  RS_CK(cudaEventRecord(assembled, g_stream));
+  RS_CK(cudaStreamWaitEvent(g_export, assembled, 0));
+  if (total) RS_CK(cudaMemcpyAsync(buf, stage, total, cudaMemcpyDeviceToHost, g_export));
+  RS_CK(cudaFreeAsync(stage, g_export));
+  RS_CK(cudaEventRecord(landed, g_export));
+  RS_CK(cudaEventDestroy(assembled));
+  *done = (void *)landed;
+  return RS_OK;
+}
+
+extern "C" int rs_event_synchronize(void *event) {
+  RS_CK(cudaEventSynchronize((cudaEvent_t)event));
+  return RS_OK;
+}
+
+extern "C" int rs_event_query(void *event) {
+  cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+  if (e == cudaErrorNotReady) { cudaGetLastError(); return 1; }
+  RS_CK(e);
   return RS_OK;
 }
 
@@ -454,7 +515,7 @@ __global__ void k_digest_bitmaps(uint64_t nb, const uint64_t *__restrict__ bm_st
 
 extern "C" int rs_batch_digests(const rs_batch *b, uint64_t *digests, int on_device) {
   RS_TRY(ensure_device());
-  RS_TRY(fetch_host_meta(b));
+  RS_TRY(fetch_host_meta_nopack(b));
   if (!on_device) RS_TRY(resolve_pending(b));
   uint64_t *term = (uint64_t *)dalloc((b->nc + 1) * 8);
   uint64_t *dout = on_device ? digests : (uint64_t *)dalloc((b->nb + 1) * 8);

@@ -95,7 +95,8 @@ void dfree(void *p);
 int ensure_device();
 int batch_alloc(rs_batch *b, uint64_t nb, uint64_t nc, uint64_t pool_bytes);
 void batch_release(rs_batch *b);
-int fetch_host_meta(const rs_batch *b);   // fills h_bm_start (synchronizes)
+int fetch_host_meta(const rs_batch *b);   // fills h_bm_start (synchronizes); packs an upper-bound pool
+int fetch_host_meta_nopack(const rs_batch *b);  // same, leaving the pool as it is (egress paths)
 int finalize_batch(rs_batch *b);          // computes d_bm_card from containers
 // Upper-bound result pools: register a fresh result (its reservation counts
 // toward the high-water mark), pack one pool to its containers' bytes

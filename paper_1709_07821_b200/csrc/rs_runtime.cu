@@ -396,7 +396,7 @@ void batch_release(rs_batch *b) {
   b->d_card = nullptr; b->d_n = nullptr; b->d_off = nullptr; b->d_pool = nullptr;
 }
 
-int fetch_host_meta(const rs_batch *cb) {
+int fetch_host_meta_nopack(const rs_batch *cb) {
   RS_TRY(materialize(cb));
   rs_batch *b = const_cast<rs_batch *>(cb);
   if (!b->h_valid) {
@@ -405,9 +405,16 @@ int fetch_host_meta(const rs_batch *cb) {
     b->nc = b->h_bm_start[b->nb];
     b->h_valid = true;
   }
+  return RS_OK;
+}
+
+int fetch_host_meta(const rs_batch *cb) {
+  RS_TRY(fetch_host_meta_nopack(cb));
   // the stream is synchronized (or was, when h_valid was set): pack an
-  // upper-bound pool now, so every batch the host looks at holds at most
-  // ~1.25x its containers' bytes (bitmap.py:318-328 shrink_to_fit semantics)
+  // upper-bound pool now, so a batch the host keeps using holds at most
+  // ~1.25x its containers' bytes (bitmap.py:318-328 shrink_to_fit semantics).
+  // Exports (wire images, digests) read the pool in place and skip this.
+  rs_batch *b = const_cast<rs_batch *>(cb);
   if (b->ub_pool) RS_TRY(repack_pool(b));
   return RS_OK;
 }
@@ -630,6 +637,8 @@ int rs_batch_free(rs_batch *b) {
   host_mark(20);
   return RS_OK;
 }
+
+uint64_t rs_batch_len(const rs_batch *b) { return b ? b->nb : 0; }
 
 int rs_batch_info(const rs_batch *b, uint64_t *n_bitmaps, uint64_t *n_containers,
                   uint64_t *pool_bytes) {

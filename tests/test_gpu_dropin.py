@@ -132,3 +132,26 @@ def test_deferred_ingest_of_duplicate_array_stays_in_bounds(pkg):
     # results were computed from the 2000-value prefix, nothing past the slots
     assert int(R.cardinalities()[0]) <= 2000
     assert int(R2.cardinalities()[0]) <= 4000
+
+
+def test_to_wire_async_matches_sync_export(pkg):
+    """rs_batch_to_wire_async: same images and offsets as rs_batch_to_wire,
+    landing in pinned memory behind a completion event; the result batch may
+    be freed before the copy finishes; too small a buffer is an error."""
+    from tests.golden_io import load
+    g = load()
+    A = pkg.BitmapBatch.from_wire([g.wire(a) for a in g["pair_a"]])
+    B = pkg.BitmapBatch.from_wire([g.wire(b) for b in g["pair_b"]])
+    pin = pkg._lib.PinnedBuffer(64 << 20)
+    for op in OPS:
+        R = A.pairwise(op, B)
+        want_buf, want_offs = R.to_wire()
+        offs, done = R.to_wire_async(pin.array)
+        del R  # freed while the copy may still be in flight
+        done.wait()
+        assert done.done()
+        assert np.array_equal(offs, want_offs), op
+        assert pin.array[:int(offs[-1])].tobytes() == want_buf.tobytes(), op
+    R = A.pairwise("or", B)
+    with pytest.raises(ValueError):
+        R.to_wire_async(np.zeros(16, np.uint8))
