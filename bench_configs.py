@@ -353,14 +353,9 @@ def c5(cpu_seconds=3.0, reps=5, nbitmaps=512):
     compulsory = int(offs[-1])  # every bitmap read once
     pi, pj = np.triu_indices(nbitmaps, 1)
     samp = np.arange(0, npairs, 4)[:8192]
-    t0 = time.perf_counter()
-    calls = 0
-    while True:
-        orc.all_pairs_and(buf, offs, pi[samp], pj[samp])
-        calls += 1
-        if time.perf_counter() - t0 >= cpu_seconds:
-            break
-    dt = time.perf_counter() - t0
+    S = orc.Session(buf, offs)  # in-memory bitmaps: |A and B| is op_cardinality (the union follows from it)
+    rate, dt, calls = cpu_rate(lambda: S.run("and", "op_cardinality", S, pi[samp], pj[samp]), len(samp),
+                               cpu_seconds)
     return {"workload": f"C5: all {npairs} pairs of {nbitmaps} clustered bitmaps on [0,2^26), |A and B| and "
                         "|A or B| (rs_all_pairs_cardinality: key grouping, densify, tcgen05 Gram tiles)",
             "units_per_step": npairs, "ms": ms, "value": npairs / (ms * 1e-3), "unit": "bitmap pairs/s",
@@ -370,7 +365,7 @@ def c5(cpu_seconds=3.0, reps=5, nbitmaps=512):
                          "umma_kernel_ms": um_ms / um_n if um_n else None,
                          "note": "all-pairs intersections are a Gram matrix per chunk key (tcgen05 kind::mxf4); "
                                  "compulsory bytes = every bitmap read once"},
-            "cpu_baseline": {"value": len(samp) * calls / dt, "unit": "bitmap pairs/s", "cores": orc.num_threads(),
+            "cpu_baseline": {"value": rate, "unit": "bitmap pairs/s", "cores": orc.num_threads(),
                              "kind": "port",
                              "sample": f"{len(samp)} of {npairs} pairs x{calls} ({dt:.1f} s), all host threads"},
             "parity": par.result(f"all {npairs} intersection and union counts")}
