@@ -35,6 +35,7 @@ OPS = ("and", "or", "andnot", "xor")
 NPAIRS = 1024
 NCHUNKS = 256
 E2E_CHUNKS = 16  # e2e pipeline depth: chunks of pairs whose transfer overlaps the previous chunk
+RING = 3         # e2e export: pinned result slots in flight (chunk i reuses chunk i-RING's)
 METRIC = "container-pair set ops/sec (AND/OR/ANDNOT/XOR + cardinality counts)"
 UNIT = "container-pairs/s"
 NOMINAL_HBM_GBS = 8000.0
@@ -406,11 +407,12 @@ def run_gpu(args):
         pin_b.array[:] = B_img[0]
         # one chunk's result images at a time (an OR of two 8 KB bitsets is at most 8 KB)
         # an op result of one chunk is at most the chunk's two inputs (OR of
-        # bitsets); 2 ring slots x 4 ops of pinned result buffers
+        # bitsets); RING slots x 4 ops of pinned result buffers
         out_cap = int((A_img[0].nbytes + B_img[0].nbytes) // E2E_CHUNKS + (1 << 20))
-        pin_out = _lib.PinnedBuffer(8 * out_cap)
-        ring = [[pin_out.array[(4 * s + k) * out_cap:(4 * s + k + 1) * out_cap] for k in range(4)] for s in (0, 1)]
-        pending = [[], []]
+        pin_out = _lib.PinnedBuffer(4 * RING * out_cap)
+        ring = [[pin_out.array[(4 * s + k) * out_cap:(4 * s + k + 1) * out_cap] for k in range(4)]
+                for s in range(RING)]
+        pending = [[] for _ in range(RING)]
         host_counts = np.zeros(NPAIRS, dtype=np.uint64)
 
         # Pipelined through the public API: chunk i+1's wire images go to HBM on
@@ -448,9 +450,9 @@ def run_gpu(args):
                     # every result bitmap back to the host as wire images, into a
                     # 2-deep ring of pinned slots: chunk i's device->host copy runs on
                     # the export stream while chunk i+1's ingest and ops proceed
-                    slot = i % 2
+                    slot = i % RING
                     for c in pending[slot]:
-                        c.wait()  # the slot's previous contents (chunk i-2) have landed
+                        c.wait()  # the slot's previous contents (chunk i-RING) have landed
                     pending[slot] = []
                 for k, R in enumerate(Rs):
                     if export:
@@ -461,7 +463,7 @@ def run_gpu(args):
                         R.cardinalities_device(base + (k * NPAIRS + i * cs) * 8)
                 del Rs
                 live += [AA, BB]
-            for slot in (0, 1):
+            for slot in range(RING):
                 for c in pending[slot]:
                     c.wait()
                 pending[slot] = []
@@ -497,7 +499,7 @@ def run_gpu(args):
             "value": ws * units_per_step / (x_ms * 1e-3), "ms_per_step": x_ms, "h2d_bytes_per_step": int(xh),
             "d2h_bytes_per_step": int(xd),
             "path": "as above, plus every result bitmap copied back as wire images: BitmapBatch.to_wire_async "
-                    "(rs_batch_to_wire_async) into a 2-deep ring of pinned slots; each chunk's device->host copy "
+                    "(rs_batch_to_wire_async) into a 3-deep ring of pinned slots; each chunk's device->host copy "
                     "runs on the export stream, overlapping the next chunk's host->device copy and ops"}
 
     base = None

@@ -126,6 +126,13 @@ int rs_batch_concat(const rs_batch *const *parts, uint64_t nparts, rs_batch **ou
 /* Copy of bitmaps idx[0..n) (host indices) into a new batch (RoaringBitmap.copy). */
 int rs_batch_select(const rs_batch *b, const uint64_t *idx, uint64_t n, rs_batch **out);
 
+/* Multi-GPU key-range sharding: a copy of every bitmap
+ * restricted to the chunk keys in [lo, hi) (0 <= lo <= hi <= 65536); and the
+ * number of containers per chunk key over the whole batch (host u64[65536]),
+ * to balance the ranges. */
+int rs_batch_key_range(const rs_batch *b, uint32_t lo, uint32_t hi, rs_batch **out);
+int rs_batch_key_histogram(const rs_batch *b, uint64_t *hist);
+
 /* ---- egress ------------------------------------------------------------- */
 /* serde.serialize (serde.py:69-84): wire size of every image -> host u64[n]. */
 int rs_batch_wire_sizes(const rs_batch *b, uint64_t *sizes);

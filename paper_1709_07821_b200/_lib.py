@@ -63,6 +63,8 @@ def _declare(L):
         "rs_batch_container_counts": ([P, P], I32),
         "rs_batch_concat": ([P, U64, pp], I32),
         "rs_batch_select": ([P, P, U64, pp], I32),
+        "rs_batch_key_range": ([P, C.c_uint32, C.c_uint32, pp], I32),
+        "rs_batch_key_histogram": ([P, P], I32),
         "rs_batch_wire_sizes": ([P, P], I32),
         "rs_batch_to_wire": ([P, P, U64, P], I32),
         "rs_batch_to_wire_async": ([P, P, U64, P, pp], I32),

@@ -140,6 +140,19 @@ class BitmapBatch:
         check(lib().rs_batch_select(self._h, a.ctypes.data, a.size, C.byref(h)))
         return BitmapBatch(h)
 
+    def key_range(self, lo: int, hi: int) -> "BitmapBatch":
+        """Every bitmap restricted to chunk keys [lo, hi) (multi-GPU key-range
+        sharding; dist.py)."""
+        h = C.c_void_p()
+        check(lib().rs_batch_key_range(self._h, int(lo), int(hi), C.byref(h)))
+        return BitmapBatch(h)
+
+    def key_histogram(self) -> np.ndarray:
+        """Containers per chunk key over the batch (u64[65536])."""
+        out = np.zeros(65536, dtype=np.uint64)
+        check(lib().rs_batch_key_histogram(self._h, out.ctypes.data))
+        return out
+
     # ------------------------------------------------------------- queries
     def info(self):
         nb, nc, pb = C.c_uint64(), C.c_uint64(), C.c_uint64()

@@ -906,3 +906,91 @@ extern "C" int rs_batch_select(const rs_batch *S, const uint64_t *idx, uint64_t 
   *out = b;
   return RS_OK;
 }
+
+// ------------------------------------------------------ key-range sharding
+// Multi-GPU: the 2^16 chunk keys are independent, so a single
+// bitmap pair, a wide union or the all-pairs counts shard by contiguous key
+// ranges -- each rank restricts its batches to [lo, hi) and the results
+// concatenate in key order (counts add up).
+namespace {
+__global__ void k_key_keep(uint64_t nc, const uint16_t *__restrict__ key, uint32_t lo, uint32_t hi,
+                           const uint8_t *__restrict__ type, const uint32_t *__restrict__ n,
+                           uint64_t *__restrict__ keep, uint64_t *__restrict__ psize) {
+  uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (c > nc) return;
+  const bool k = c < nc && key[c] >= lo && key[c] < hi;
+  keep[c] = k;
+  psize[c] = k ? rs_pad16(rs_payload_bytes(type[c], n[c])) : 0;
+}
+
+// warp per kept container: metadata + payload to the new batch
+__global__ void k_key_copy(uint64_t nc, DevBatch S, const uint64_t *__restrict__ keep, const uint64_t *__restrict__ pos,
+                           const uint64_t *__restrict__ poff, uint16_t *key, uint8_t *type, uint32_t *card,
+                           uint32_t *nn, uint64_t *off, uint8_t *__restrict__ pool) {
+  const uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= nc || !keep[c]) return;
+  const uint64_t j = pos[c];
+  const uint32_t nv = (uint32_t)(rs_pad16(rs_payload_bytes(S.type[c], S.n[c])) >> 4);
+  const uint4 *src = (const uint4 *)(S.pool + S.off[c]);
+  uint4 *dst = (uint4 *)(pool + poff[c]);
+  for (uint32_t i = lane; i < nv; i += 32) dst[i] = src[i];
+  if (lane == 0) {
+    key[j] = S.key[c]; type[j] = S.type[c]; card[j] = S.card[c]; nn[j] = S.n[c]; off[j] = poff[c];
+  }
+}
+
+__global__ void k_key_bm_start(uint64_t nb, const uint64_t *__restrict__ bm_start, const uint64_t *__restrict__ pos,
+                               uint64_t *__restrict__ out) {
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i <= nb) out[i] = pos[bm_start[i]];
+}
+
+__global__ void k_key_hist(uint64_t nc, const uint16_t *__restrict__ key, unsigned long long *__restrict__ h) {
+  uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (c < nc) atomicAdd(&h[key[c]], 1ull);
+}
+}  // namespace
+
+extern "C" int rs_batch_key_range(const rs_batch *S, uint32_t lo, uint32_t hi, rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  if (lo > hi || hi > 65536) { set_error("bad key range"); return RS_EARG; }
+  RS_TRY(fetch_host_meta(S));
+  RS_TRY(resolve_pending(S));
+  const uint64_t nc = S->nc, nb = S->nb;
+  uint64_t *keep = (uint64_t *)dalloc((nc + 1) * 8), *pos = (uint64_t *)dalloc((nc + 1) * 8);
+  uint64_t *psize = (uint64_t *)dalloc((nc + 1) * 8), *poff = (uint64_t *)dalloc((nc + 1) * 8);
+  if (!keep || !pos || !psize || !poff) { set_error("device allocation failed (key range)"); return RS_ENOMEM; }
+  RS_LAUNCH(k_key_keep, (unsigned)((nc + 1 + 255) / 256), 256, 0, nc, S->d_key, lo, hi, S->d_type, S->d_n, keep, psize);
+  RS_TRY(scan_exclusive<uint64_t>(keep, pos, nc + 1));
+  RS_TRY(scan_exclusive<uint64_t>(psize, poff, nc + 1));
+  uint64_t tot[2];
+  RS_TRY(d2h(&tot[0], pos + nc, 8));
+  RS_TRY(d2h(&tot[1], poff + nc, 8));
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, nb, tot[0], tot[1]);
+  if (rc) { rs_batch_free(b); return rc; }
+  RS_LAUNCH(k_key_copy, (unsigned)((nc * 32 + 255) / 256), 256, 0, nc, S->dev(), keep, pos, poff, b->d_key, b->d_type,
+            b->d_card, b->d_n, b->d_off, b->d_pool);
+  RS_LAUNCH(k_key_bm_start, (unsigned)((nb + 1 + 255) / 256), 256, 0, nb, S->d_bm_start, pos, b->d_bm_start);
+  dfree(keep); dfree(pos); dfree(psize); dfree(poff);
+  RS_TRY(finalize_batch(b));
+  b->type_mask = S->type_mask;
+  b->h_valid = false;
+  RS_TRY(fetch_host_meta(b));
+  *out = b;
+  return RS_OK;
+}
+
+extern "C" int rs_batch_key_histogram(const rs_batch *S, uint64_t *hist) {
+  RS_TRY(ensure_device());
+  RS_TRY(fetch_host_meta(S));
+  unsigned long long *h = (unsigned long long *)dalloc(65536 * 8);
+  if (!h) { set_error("device allocation failed (key histogram)"); return RS_ENOMEM; }
+  RS_CK(cudaMemsetAsync(h, 0, 65536 * 8, g_stream));
+  RS_LAUNCH(k_key_hist, (unsigned)((S->nc + 255) / 256), 256, 0, S->nc, S->d_key, h);
+  RS_TRY(d2h(hist, h, 65536 * 8));
+  dfree(h);
+  return RS_OK;
+}
