@@ -166,12 +166,25 @@ def dist_init(ws, local):
 
 
 def dist_max(dist, x: float) -> float:
-    if dist is None:
-        return x
-    import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    """Slowest rank's value (paper_1709_07821_b200/dist.py, NCCL all_reduce MAX)."""
+    from paper_1709_07821_b200.dist import max_over_ranks
+    return max_over_ranks(x)
+
+
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` without a torchrun environment: re-launch this
+    script as N ranks, one process per GPU (torch.distributed.run, rendezvous
+    on 127.0.0.1); rank 0 prints the JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_barrier(dist):
@@ -574,6 +587,9 @@ def main():
     if args.warmup < 3 and args.impl == "gpu":
         print("note: warm-up raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
     return run_reference(args) if args.impl == "reference" else run_gpu(args)
 
 
