@@ -525,7 +525,40 @@ __global__ void k_bm_card_thread(uint64_t nb, const uint64_t *__restrict__ bm_st
   out[i] = s;
 }
 
+// few bitmaps holding many containers (a wide union's result): a CTA per
+// bitmap instead of a lone warp walking tens of thousands of cards
+// few bitmaps holding many containers (a wide union's result): CTAs of 256
+// threads split each bitmap's cards (blockIdx.y) and add their block sums
+// into out, which is zeroed first
+__global__ void __launch_bounds__(256) k_bm_card_split(uint64_t nb, const uint64_t *__restrict__ bm_start,
+                                                       const uint32_t *__restrict__ card,
+                                                       unsigned long long *__restrict__ out) {
+  __shared__ uint64_t red[8];
+  const uint64_t b = blockIdx.x;
+  const uint64_t c0 = bm_start[b], c1 = bm_start[b + 1];
+  uint64_t s = 0;
+  for (uint64_t c = c0 + blockIdx.y * 256ull + threadIdx.x; c < c1; c += 256ull * gridDim.y) s += card[c];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t tot = 0;
+    for (int w = 0; w < 8; w++) tot += red[w];
+    if (tot) atomicAdd(&out[b], (unsigned long long)tot);
+  }
+}
+
 int finalize_batch(rs_batch *b) {
+  if (b->nb && b->nb <= 1024 && b->nc >= 256 * b->nb) {
+    const unsigned split = (unsigned)std::min<uint64_t>(std::max<uint64_t>(b->nc / b->nb / 2048, 1), 64);
+    RS_CK(cudaMemsetAsync(b->d_bm_card, 0, b->nb * 8, g_stream));
+    dim3 grid((unsigned)b->nb, split);
+    k_bm_card_split<<<grid, 256, 0, g_stream>>>(b->nb, b->d_bm_start, b->d_card,
+                                                (unsigned long long *)b->d_bm_card);
+    ++g_launches;
+    RS_CK(cudaGetLastError());
+    return RS_OK;
+  }
   if (b->nb && b->nc <= 4 * b->nb) {
     RS_LAUNCH(k_bm_card_thread, (unsigned)((b->nb + 255) / 256), 256, 0, b->nb, b->d_bm_start, b->d_card,
               b->d_bm_card);

@@ -18,6 +18,17 @@ namespace {
 
 unsigned grid_for(uint64_t n, unsigned block) { return (unsigned)((n + block - 1) / block); }
 
+unsigned sm_count_() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return (unsigned)sms;
+}
+
 bool env_flag_(const char *name) {
   const char *v = getenv(name);
   return v && *v == '1';
@@ -88,15 +99,25 @@ __device__ __forceinline__ void block_card_runs(const uint64_t *X, uint32_t &car
 //   ci bitset             -> acc becomes bitset(ci | acc)      (:288-296)
 //   both array/run        -> container_pairwise("or")         (:297-298)
 //                            = array/bitset by card, or norm(run) if a run is involved
-__global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *__restrict__ seg_start,
+// Runs over the keys in list[0..*cnt) (the keys without a bitset
+// contributor: their type can depend on the order, App. B), persistent.
+__global__ void __launch_bounds__(DT) k_union_fold(const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
+                                                   const uint32_t *__restrict__ seg_start,
                                                    const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ keys,
                                                    DevBatch S, uint16_t *okey, uint8_t *otype, uint32_t *ocard,
                                                    uint32_t *on, uint64_t *ooff, uint8_t *__restrict__ opool) {
   __shared__ __align__(16) DenseSmem sm;
   __shared__ uint32_t mc[DT];   // contributor container index
   __shared__ uint8_t mt[DT];    // contributor type
-  const uint64_t g = blockIdx.x;
-  if (g >= G) return;
+  __shared__ uint32_t next_li;
+  const uint32_t total = cnt[0];
+  for (;;) {
+  __syncthreads();  // the previous key's smem reads are done
+  if (threadIdx.x == 0) next_li = atomicAdd(const_cast<uint32_t *>(cnt) + 2, 1u);  // dynamic: keys differ in cost
+  __syncthreads();
+  const uint32_t li = next_li;
+  if (li >= total) break;
+  const uint64_t g = list[li];
   const int t = threadIdx.x;
   uint32_t s = seg_start[g], e = seg_start[g + 1];
   // metadata of the first DT contributors in one parallel round of loads
@@ -167,6 +188,233 @@ __global__ void __launch_bounds__(DT) k_union_fold(uint64_t G, const uint32_t *_
     ocard[g] = card;
     on[g] = n;
     ooff[g] = g * 8192;
+  }
+  }
+}
+
+// Keys of union_many by result rule: a key with at least one bitset
+// contributor ends as a bitset holding the OR of all its contributors,
+// whatever their order (App. B: once a bitset, always a bitset, and a
+// bitset contributor turns the accumulator into one; its cardinality is
+// >= 4097 from then on) -> list 0, an order-free streaming OR.  The other
+// keys replay the fold (list 1).
+__global__ void k_union_classify(uint64_t G, const uint32_t *__restrict__ seg_start,
+                                 const uint32_t *__restrict__ item_c, DevBatch S, uint32_t *__restrict__ list0,
+                                 uint32_t *__restrict__ list1, uint32_t *__restrict__ cnt) {
+  const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool bs = false;
+  if (g < G)
+    for (uint32_t i = seg_start[g]; i < seg_start[g + 1] && !bs; i++) bs = S.type[item_c[i]] == RS_TAG_BITSET;
+  const bool active = g < G;
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    const unsigned m = __ballot_sync(0xffffffffu, active && bs == (c == 0));
+    if (!m) continue;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if ((int)lane == leader) base = atomicAdd(&cnt[c], (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (active && bs == (c == 0)) (c == 0 ? list0 : list1)[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)g;
+  }
+}
+
+// The order-free keys: OR of every contributor, written as a bitset.
+// Persistent CTAs over list[0..*cnt); thread t owns words [4t, 4t+4).  The
+// key's contributors are handled in windows of up to DT: one round of
+// metadata loads (container, type, offset, size) into shared memory, then
+// every payload load of the window is independent of the others -- bitset
+// words go into registers (four contributors in flight per thread), array
+// values and runs are flattened over the window (thread f takes element f of
+// the concatenation) and scattered into a shared bitset with native shared
+// ORs, which is folded into the registers at the end and re-zeroed by its
+// owners.  A CTA-per-contributor-chain kernel spent most of its time in
+// dependent load chains (metadata -> payload per contributor).
+constexpr int UT = 128;  // k_union_or threads: thread t owns words [4t, 4t+4) and [4(t+UT), 4(t+UT)+4)
+__global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
+                                                 const uint32_t *__restrict__ seg_start,
+                                                 const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ keys,
+                                                 DevBatch S, uint16_t *okey, uint8_t *otype, uint32_t *ocard,
+                                                 uint32_t *on, uint64_t *ooff, uint8_t *__restrict__ opool) {
+  __shared__ __align__(16) uint64_t X[RS_WORDS];
+  __shared__ uint64_t moff[UT];          // bitset contributors' payload offsets (compacted)
+  __shared__ uint64_t eoff[UT];          // array / run contributors' payload offsets (compacted)
+  __shared__ uint32_t ebase[UT + 1];     // their 16-byte unit prefix; [UT] = slot counter
+  __shared__ uint8_t etype[UT];
+  __shared__ uint32_t eunits_n[UT];      // their value / run counts
+  __shared__ uint32_t nbits, nelem, next_li;
+  __shared__ uint32_t red[UT / 32];
+  const int t = threadIdx.x, lane = t & 31;
+  uint32_t *X32 = (uint32_t *)X;
+#pragma unroll
+  for (int k = 0; k < 8; k++) X[t + UT * k] = 0;
+  if (t == 0) {
+    ebase[UT] = 0;
+    next_li = atomicAdd(const_cast<uint32_t *>(cnt) + 2, 1u);  // dynamic: keys differ in cost
+  }
+  const uint32_t total = cnt[0];
+  __syncthreads();
+  for (;;) {
+    const uint32_t li = next_li;
+    if (li >= total) break;
+    const uint32_t g = list[li];
+    const uint32_t s = seg_start[g], e = seg_start[g + 1];
+    uint64_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t w0 = s; w0 < e; w0 += UT) {
+      // window metadata: thread t = contributor w0 + t
+      const bool have = w0 + t < e;
+      uint8_t ty = 0;
+      uint64_t of = 0;
+      uint32_t nn = 0;
+      if (have) {
+        const uint32_t c = item_c[w0 + t];
+        ty = S.type[c];
+        of = S.off[c];
+        nn = S.n[c];
+      }
+      if (t == 0) { nbits = 0; nelem = 0; }
+      __syncthreads();  // (every thread has read next_li)
+      if (t == 0 && w0 == s) next_li = atomicAdd(const_cast<uint32_t *>(cnt) + 2, 1u);  // the next key, early
+      // compact: bitset offsets to moff, array/run ones to eoff (an OR commutes:
+      // the order inside the window does not matter)
+      const bool isb = have && ty == RS_TAG_BITSET, ise = have && !isb;
+      {
+        const unsigned mb = __ballot_sync(0xffffffffu, isb);
+        uint32_t base = 0;
+        if (lane == 0 && mb) base = atomicAdd(&nbits, (uint32_t)__popc(mb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (isb) moff[base + __popc(mb & ((1u << lane) - 1))] = of;
+      }
+      {
+        const unsigned me = __ballot_sync(0xffffffffu, ise);
+        uint32_t base = 0;
+        if (lane == 0 && me) base = atomicAdd(&ebase[UT], (uint32_t)__popc(me));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (ise) {
+          const uint32_t slot = base + __popc(me & ((1u << lane) - 1));
+          eoff[slot] = of;
+          etype[slot] = ty;
+          eunits_n[slot] = nn;
+          ebase[slot] = ty == RS_TAG_ARRAY ? (nn + 7) >> 3 : (nn + 3) >> 2;  // 16-byte units
+        }
+      }
+      __syncthreads();
+      const uint32_t nb = nbits, ne = ebase[UT];
+      if (t < 32) {  // exclusive prefix of the unit counts (one warp)
+        uint32_t carry = 0;
+        for (uint32_t k0 = 0; k0 < ne; k0 += 32) {
+          const uint32_t k = k0 + lane;
+          const uint32_t v = k < ne ? ebase[k] : 0;
+          uint32_t x = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          if (k < ne) ebase[k] = carry + x - v;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) nelem = carry;
+      }
+      // bitset contributors: words straight into registers, 2 contributors
+      // (4 x 16-byte loads per thread) in flight
+      uint32_t k = 0;
+      for (; k + 2 <= nb; k += 2) {
+        uint64_t w[4][4];
+        ld_words(S.pool, moff[k], t, w[0]);
+        ld_words(S.pool, moff[k], t + UT, w[1]);
+        ld_words(S.pool, moff[k + 1], t, w[2]);
+        ld_words(S.pool, moff[k + 1], t + UT, w[3]);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          r[q] |= w[0][q] | w[2][q];
+          r[4 + q] |= w[1][q] | w[3][q];
+        }
+      }
+      if (k < nb) {
+        uint64_t w[2][4];
+        ld_words(S.pool, moff[k], t, w[0]);
+        ld_words(S.pool, moff[k], t + UT, w[1]);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          r[q] |= w[0][q];
+          r[4 + q] |= w[1][q];
+        }
+      }
+      __syncthreads();  // prefix and nelem visible
+      // array / run payloads, flattened over the window in 16-byte units
+      // (8 array values or 4 runs per load; every unit's load is independent)
+      const uint32_t tot = nelem;
+      for (uint32_t f = t; f < tot; f += UT) {
+        uint32_t lo = 0, hi = ne;  // contributor j with ebase[j] <= f < ebase[j+1]
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (ebase[mid] <= f) lo = mid; else hi = mid;
+        }
+        const uint32_t u = f - ebase[lo];
+        const uint4 q = __ldg((const uint4 *)(S.pool + eoff[lo]) + u);
+        const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t nv = eunits_n[lo];  // values (array) / runs (run) of the contributor
+        if (etype[lo] == RS_TAG_ARRAY) {
+          const uint32_t v0 = 8 * u;
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const uint32_t lo16 = x[j] & 0xFFFF, hi16 = x[j] >> 16;
+            const bool a = v0 + 2 * j < nv, b = v0 + 2 * j + 1 < nv;
+            const uint32_t wl = lo16 >> 5, wh = hi16 >> 5;
+            const uint32_t bl = 1u << (lo16 & 31), bh = 1u << (hi16 & 31);
+            if (a && b && wl == wh) {
+              atomicOr(&X32[wl], bl | bh);
+            } else {
+              if (a) atomicOr(&X32[wl], bl);
+              if (b) atomicOr(&X32[wh], bh);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            if (4 * u + j >= nv) break;
+            const uint32_t st = x[j] & 0xFFFF, en = st + (x[j] >> 16);
+            const uint32_t ws = st >> 5, we = en >> 5;
+            const uint32_t first = ~0u << (st & 31), last = ~0u >> (31 - (en & 31));
+            if (ws == we) {
+              atomicOr(&X32[ws], first & last);
+            } else {
+              atomicOr(&X32[ws], first);
+              atomicOr(&X32[we], last);
+              for (uint32_t w = ws + 1; w < we; w++) X32[w] = ~0u;  // all-ones commutes with the ORs
+            }
+          }
+        }
+      }
+      if (t == 0) ebase[UT] = 0;
+      __syncthreads();  // window done: its smem may be reused
+    }
+    uint32_t pc = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int wd = 4 * (t + UT * h) + q;
+        r[4 * h + q] |= X[wd];
+        X[wd] = 0;
+        pc += __popcll(r[4 * h + q]);
+      }
+    st_words(opool, (uint64_t)g * 8192, t, r);
+    st_words(opool, (uint64_t)g * 8192, t + UT, r + 4);
+    pc = __reduce_add_sync(0xffffffffu, pc);
+    if (lane == 0) red[t >> 5] = pc;
+    __syncthreads();  // also orders the X clears before the next key's scatter
+    if (t == 0) {
+      uint32_t card = 0;
+#pragma unroll
+      for (int w = 0; w < UT / 32; w++) card += red[w];
+      okey[g] = (uint16_t)(keys[s] >> 40);
+      otype[g] = RS_TAG_BITSET;
+      ocard[g] = card;
+      on[g] = RS_WORDS;
+      ooff[g] = (uint64_t)g * 8192;
+    }
   }
 }
 
@@ -790,8 +1038,34 @@ extern "C" int rs_union_many(const rs_batch *in, const uint64_t *idx, uint64_t n
   int rc = batch_alloc(b, 1, g.G, g.G * 8192);
   if (rc) { g.release(); rs_batch_free(b); return rc; }
   ub_register(b);  // one 8 KB slot per key until packed
-  RS_LAUNCH_PROF("union_fold", g.G, k_union_fold, (unsigned)g.G, DT, 0, g.G, g.seg_start, g.item_c, g.keys, in->dev(), b->d_key, b->d_type,
-            b->d_card, b->d_n, b->d_off, b->d_pool);
+  // keys by result rule: order-free bitset ORs and order-dependent folds,
+  // the two kernels concurrently on side streams
+  uint32_t *lists = (uint32_t *)dalloc((2 * g.G + 2) * 4), *cnt = (uint32_t *)dalloc(32);
+  if (!lists || !cnt) { g.release(); rs_batch_free(b); set_error("device allocation failed (union lists)"); return RS_ENOMEM; }
+  RS_CK(cudaMemsetAsync(cnt, 0, 32, g_stream));  // [0,1] list sizes, [2,3] work counters
+  RS_LAUNCH(k_union_classify, grid_for(g.G, 256), 256, 0, g.G, g.seg_start, g.item_c, in->dev(), lists,
+            lists + g.G + 1, cnt);
+  {
+    const unsigned sms = sm_count_();
+    Fork F;
+    RS_TRY(F.begin(2));
+    F.next();
+    int occ_or = 0, occ_fold = 0;
+    RS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_or, k_union_or, UT, 0));
+    RS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fold, k_union_fold, DT, 0));
+    // the two persistent kernels share the SMs: one resident wave of each
+    RS_LAUNCH_PROF("union_or", g.G, k_union_or, (unsigned)std::min<uint64_t>(g.G, sms * std::max(occ_or, 1)), UT, 0,
+                   lists, cnt,
+                   g.seg_start, g.item_c, g.keys, in->dev(), b->d_key, b->d_type, b->d_card, b->d_n, b->d_off,
+                   b->d_pool);
+    F.next();
+    RS_LAUNCH_PROF("union_fold", g.G, k_union_fold, (unsigned)std::min<uint64_t>(g.G, sms * std::max(occ_fold, 1)), DT, 0,
+                   lists + g.G + 1, cnt + 1, g.seg_start, g.item_c, g.keys, in->dev(), b->d_key, b->d_type, b->d_card,
+                   b->d_n, b->d_off, b->d_pool);
+    RS_TRY(F.end());
+  }
+  dfree(lists);
+  dfree(cnt);
   uint64_t hs[2] = {0, g.G};
   RS_TRY(h2d(b->d_bm_start, hs, 16));
   RS_TRY(finalize_batch(b));
