@@ -101,94 +101,139 @@ __device__ __forceinline__ void block_card_runs(const uint64_t *X, uint32_t &car
 //                            = array/bitset by card, or norm(run) if a run is involved
 // Runs over the keys in list[0..*cnt) (the keys without a bitset
 // contributor: their type can depend on the order, App. B), persistent.
+// Scatter one 16-byte unit u of an array (8 values) or run (4 runs)
+// payload holding nv values / runs into the shared bitset X32.
+__device__ __forceinline__ void scatter_unit(const uint4 q, uint32_t u, uint32_t nv, bool is_array, uint32_t *X32) {
+  const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+  if (is_array) {
+    const uint32_t v0 = 8 * u;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t lo16 = x[j] & 0xFFFF, hi16 = x[j] >> 16;
+      const bool a = v0 + 2 * j < nv, b = v0 + 2 * j + 1 < nv;
+      const uint32_t wl = lo16 >> 5, wh = hi16 >> 5;
+      const uint32_t bl = 1u << (lo16 & 31), bh = 1u << (hi16 & 31);
+      if (a && b && wl == wh) {
+        atomicOr(&X32[wl], bl | bh);
+      } else {
+        if (a) atomicOr(&X32[wl], bl);
+        if (b) atomicOr(&X32[wh], bh);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    if (4 * u + j >= nv) break;
+    const uint32_t st = x[j] & 0xFFFF, en = st + (x[j] >> 16);
+    const uint32_t ws = st >> 5, we = en >> 5;
+    const uint32_t first = ~0u << (st & 31), last = ~0u >> (31 - (en & 31));
+    if (ws == we) {
+      atomicOr(&X32[ws], first & last);
+    } else {
+      atomicOr(&X32[ws], first);
+      atomicOr(&X32[we], last);
+      for (uint32_t w = ws + 1; w < we; w++) X32[w] = ~0u;  // all-ones commutes with the ORs
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t units_of(uint8_t type, uint32_t n) {
+  return type == RS_TAG_ARRAY ? (n + 7) >> 3 : type == RS_TAG_RUN ? (n + 3) >> 2 : 512u;
+}
+
+// One CTA per key (persistent over the keys in list[0..*cnt), fetched
+// dynamically): the keys without a bitset contributor, whose result type can
+// depend on the order (App. B).  The fold replays the sequence:
+//   acc = copy(c0); per next ci: container_pairwise("or", acc, ci), i.e.
+//   array / bitset by card, or norm(run) when a run is involved
+//   (containers.py:459-527); once a bitset, the rest ORs in order-free
+//   (bitmap.py:278-287).
+// The contributors' metadata comes in one round of loads; each step's payload
+// (at most 8 KB: 512 16-byte units, two per thread) is loaded into registers
+// one step ahead, so a step is scatter + two barriers, with no global load on
+// its critical path.
 __global__ void __launch_bounds__(DT) k_union_fold(const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
                                                    const uint32_t *__restrict__ seg_start,
                                                    const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ keys,
                                                    DevBatch S, uint16_t *okey, uint8_t *otype, uint32_t *ocard,
                                                    uint32_t *on, uint64_t *ooff, uint8_t *__restrict__ opool) {
   __shared__ __align__(16) DenseSmem sm;
-  __shared__ uint32_t mc[DT];   // contributor container index
+  __shared__ uint64_t mo[DT];   // contributor payload offset
+  __shared__ uint32_t mn[DT];   // contributor n
   __shared__ uint8_t mt[DT];    // contributor type
   __shared__ uint32_t next_li;
+  const int t = threadIdx.x;
+  uint32_t *X32 = (uint32_t *)sm.X;
   const uint32_t total = cnt[0];
   for (;;) {
-  __syncthreads();  // the previous key's smem reads are done
-  if (threadIdx.x == 0) next_li = atomicAdd(const_cast<uint32_t *>(cnt) + 2, 1u);  // dynamic: keys differ in cost
-  __syncthreads();
-  const uint32_t li = next_li;
-  if (li >= total) break;
-  const uint64_t g = list[li];
-  const int t = threadIdx.x;
-  uint32_t s = seg_start[g], e = seg_start[g + 1];
-  // metadata of the first DT contributors in one parallel round of loads
-  if (s + t < e) {
-    const uint32_t c = item_c[s + t];
-    mc[t] = c;
-    mt[t] = S.type[c];
-  }
-#pragma unroll
-  for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
-  __syncthreads();
-  auto cont = [&](uint32_t i) { return i - s < DT ? mc[i - s] : item_c[i]; };
-  auto ctype = [&](uint32_t i, uint32_t c) { return i - s < DT ? mt[i - s] : S.type[c]; };
-  uint32_t c0 = cont(s);
-  uint8_t acc = ctype(s, c0);
-  or_into(S, c0, acc, sm.X);
-  __syncthreads();
-  uint32_t i = s + 1;
-  // Sequential replay while the accumulator's type can still change: only
-  // array/run steps re-decide it from the running union's card / run count.
-  for (; i < e && acc != RS_TAG_BITSET; i++) {
-    uint32_t ci = cont(i);
-    uint8_t ti = ctype(i, ci);
-    or_into(S, ci, ti, sm.X);
+    __syncthreads();  // the previous key's smem reads are done
+    if (t == 0) next_li = atomicAdd(const_cast<uint32_t *>(cnt) + 2, 1u);  // dynamic: keys differ in cost
     __syncthreads();
-    if (ti == RS_TAG_BITSET) { acc = RS_TAG_BITSET; continue; }
-    bool run_rule = acc == RS_TAG_RUN || ti == RS_TAG_RUN;
-    uint32_t card, nruns;
-    block_card_runs(sm.X, card, nruns, sm.red, run_rule);
-    if (run_rule && rs_run_admissible(card, nruns)) acc = RS_TAG_RUN;
-    else acc = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;
-    __syncthreads();
-  }
-  // Once a bitset, always a bitset (bitmap.py:278-287): the rest is an
-  // order-independent OR, so all remaining contributors go in without
-  // barriers between them (their loads overlap).  Bitset contributors
-  // accumulate in registers (a plain read-modify-write of X would race with
-  // other threads' atomics); array/run contributors scatter with atomics and
-  // all-ones stores, which commute.
-  uint64_t racc[4] = {0, 0, 0, 0};
-  for (; i < e; i++) {
-    const uint32_t ci = cont(i);
-    const uint8_t ti = ctype(i, ci);
-    if (ti == RS_TAG_BITSET) {
-      uint64_t w[4];
-      ld_words(S.pool, S.off[ci], t, w);
-#pragma unroll
-      for (int k = 0; k < 4; k++) racc[k] |= w[k];
-    } else {
-      scatter_container(S, ci, ti, sm.X);
+    const uint32_t li = next_li;
+    if (li >= total) break;
+    const uint64_t g = list[li];
+    const uint32_t s = seg_start[g], e = seg_start[g + 1];
+    // metadata of the first DT contributors in one parallel round of loads
+    if (s + t < e) {
+      const uint32_t c = item_c[s + t];
+      mt[t] = S.type[c];
+      mo[t] = S.off[c];
+      mn[t] = S.n[c];
     }
-  }
-  __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 4; k++) sm.X[4 * t + k] |= racc[k];
-  __syncthreads();
-  uint64_t r[4];
-  uint32_t pc = 0;
+    for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
+    __syncthreads();
+    auto meta = [&](uint32_t i, uint8_t &ty, uint64_t &of, uint32_t &n) {
+      if (i - s < DT) { ty = mt[i - s]; of = mo[i - s]; n = mn[i - s]; }
+      else { const uint32_t c = item_c[i]; ty = S.type[c]; of = S.off[c]; n = S.n[c]; }
+    };
+    auto load = [&](uint64_t of, uint32_t nu, uint4 &q0, uint4 &q1) {
+      const uint4 *p = (const uint4 *)(S.pool + of);
+      if ((uint32_t)t < nu) q0 = __ldg(p + t);
+      if ((uint32_t)t + DT < nu) q1 = __ldg(p + t + DT);
+    };
+    uint8_t ty;
+    uint64_t of;
+    uint32_t n;
+    meta(s, ty, of, n);
+    uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
+    load(of, units_of(ty, n), q0, q1);
+    uint8_t acc = ty;  // acc = copy(c0); arrays / runs only in this list
+    for (uint32_t i = s; i < e; i++) {
+      const uint8_t cty = ty;
+      const uint32_t cn = n, cu = units_of(cty, cn);
+      const uint4 c0q = q0, c1q = q1;
+      if (i + 1 < e) {  // the next contributor's payload, in flight during this step
+        meta(i + 1, ty, of, n);
+        load(of, units_of(ty, n), q0, q1);
+      }
+      if ((uint32_t)t < cu) scatter_unit(c0q, t, cn, cty == RS_TAG_ARRAY, X32);
+      if ((uint32_t)t + DT < cu) scatter_unit(c1q, t + DT, cn, cty == RS_TAG_ARRAY, X32);
+      __syncthreads();
+      if (i == s || acc == RS_TAG_BITSET) continue;  // nothing to decide
+      const bool run_rule = acc == RS_TAG_RUN || cty == RS_TAG_RUN;
+      uint32_t card, nruns;
+      block_card_runs(sm.X, card, nruns, sm.red, run_rule);
+      if (run_rule && rs_run_admissible(card, nruns)) acc = RS_TAG_RUN;
+      else acc = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;
+      __syncthreads();
+    }
+    uint64_t r[4];
+    uint32_t pc = 0;
 #pragma unroll
-  for (int k = 0; k < 4; k++) { r[k] = sm.X[4 * t + k]; pc += __popcll(r[k]); }
-  uint32_t card = pc, z = 0;
-  block_sum2(card, z, sm.red);
-  __syncthreads();
-  uint32_t n = encode_result(sm, r, pc, card, acc, opool + g * 8192);
-  if (t == 0) {
-    okey[g] = (uint16_t)(keys[s] >> 40);
-    otype[g] = acc;
-    ocard[g] = card;
-    on[g] = n;
-    ooff[g] = g * 8192;
-  }
+    for (int k = 0; k < 4; k++) { r[k] = sm.X[4 * t + k]; pc += __popcll(r[k]); }
+    uint32_t card = pc, z = 0;
+    block_sum2(card, z, sm.red);
+    __syncthreads();
+    const uint32_t nout = encode_result(sm, r, pc, card, acc, opool + g * 8192);
+    if (t == 0) {
+      okey[g] = (uint16_t)(keys[s] >> 40);
+      otype[g] = acc;
+      ocard[g] = card;
+      on[g] = nout;
+      ooff[g] = g * 8192;
+    }
   }
 }
 
