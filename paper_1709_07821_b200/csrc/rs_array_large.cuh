@@ -60,12 +60,21 @@ struct LargeSmem {
   __device__ __forceinline__ uint8_t *R() const { return X + 16384; }
 };
 
-// 56 KB: four CTAs per SM (4 x (56 + 1 reserved) KB <= 228 KB).  The dynamic
-// window starts 1 KB into the CTA's shared window, so the header and the pad
-// to the first 8 KB boundary take 7 KB and the ring gets 33 KB; large_loop
-// traps if a toolchain ever places the window so that the ring is under
-// 32 KB (a 16 KB item wrapping around the end may hold up to 32 KB).
-constexpr size_t LARGE_SMEM_BYTES = 57344;
+// 44 KB: five CTAs per SM (5 x (44 + 1 reserved) KB <= 228 KB; the kernels
+// are capped at 5 x 288 threads' worth of registers).  The header and the pad
+// to the first 8 KB boundary take at most ~8.5 KB, XA / XB 16 KB, and the
+// ring the rest (>= 19 KB); large_loop traps if it is ever under 16 KB, the
+// largest item (an item that does not fit before the end of the ring waits
+// for the ring to drain and starts at 0).  Four CTAs of 56 KB with a 33 KB
+// ring measured slower: the kernel is issue / barrier bound, so a fifth CTA's
+// warps hide more of the per-pair barriers than the deeper ring hid latency.
+#ifndef RS_AAL_SMEM_KB
+#define RS_AAL_SMEM_KB 56
+#endif
+#ifndef RS_AAL_MINB
+#define RS_AAL_MINB 4
+#endif
+constexpr size_t LARGE_SMEM_BYTES = RS_AAL_SMEM_KB * 1024;
 
 __device__ __forceinline__ LargeSmem large_layout(uint8_t *raw) {
   LargeSmem sm;
@@ -412,7 +421,7 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
   const int t = threadIdx.x;
   const LargeSmem sm = large_layout(raw);
-  if (sm.ring < 4u * 8192u) __trap();  // a wrapped 16 KB item may span up to 32 KB
+  if (sm.ring < 2u * 8192u) __trap();  // the largest item (2 x 4096 values) must fit
   if (t == 0) {
     for (int s = 0; s < NSLOT; s++) {
       rsb::mbar_init(&sm.h->full[s], 1);
@@ -443,7 +452,18 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
           skip = sm.ring - phys;
           pos = 0;
         }
-        const uint32_t span = need + skip;
+        uint32_t span = need + skip;
+        if (span > sm.ring) {
+          // a large item right after the middle of the ring: wait for the
+          // ring to drain, then it starts at 0 with nothing to skip
+          while (oldest < j) {
+            mbar_wait_backoff(&sm.h->empty[oldest % NSLOT], (oldest / NSLOT) & 1);
+            occ -= sm.h->span[oldest % NSLOT];
+            oldest++;
+          }
+          span = need;
+          occ = 0;
+        }
         while (j - oldest >= (uint32_t)NSLOT || occ + span > sm.ring) {
           mbar_wait_backoff(&sm.h->empty[oldest % NSLOT], (oldest / NSLOT) & 1);
           occ -= sm.h->span[oldest % NSLOT];

@@ -297,6 +297,58 @@ __global__ void __launch_bounds__(256) k_merge_pair(uint64_t M, uint64_t npairs,
   }
 }
 
+// The single-pair op (the RoaringBitmap API's a & b, config 1): join and
+// emit in ONE CTA -- with one pair its entry and slot bases are 0, so the
+// scans over pairs vanish and the join's outputs feed the emit in place.
+// pke[0..1] / pue[0..1] get the pair's entry / slot totals for the
+// compaction.  (Two launches and a memset fewer per call: host-bound calls
+// pay ~3 us per launch.)
+__device__ __forceinline__ void emit_entry(bool active, uint32_t e, uint64_t off, uint64_t t,
+                                           const uint16_t *__restrict__ mkey, const uint32_t *__restrict__ mca,
+                                           const uint32_t *__restrict__ mcb, const uint32_t *__restrict__ mpair,
+                                           const DevBatch &A, const DevBatch &B, Entries E, Lists L, int op);
+
+__global__ void __launch_bounds__(256) k_merge_emit1(DevBatch A, DevBatch B, const uint32_t *ia, const uint32_t *ib,
+                                                     int op, uint16_t *__restrict__ mkey, uint32_t *__restrict__ mca,
+                                                     uint32_t *__restrict__ mcb, uint32_t *__restrict__ mpair,
+                                                     uint32_t *__restrict__ keep, uint64_t *__restrict__ ub,
+                                                     uint32_t *__restrict__ pke, uint64_t *__restrict__ pue,
+                                                     Entries E, Lists L) {
+  __shared__ uint16_t kA[2048], kB[2048];
+  using BS = cub::BlockScan<uint64_t, 256>;
+  __shared__ typename BS::TempStorage ts;
+  const uint32_t a = pair_a(ia, 0), b = pair_a(ib, 0);
+  const uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
+  const uint32_t na = (uint32_t)(A.bm_start[a + 1] - a0), nb = (uint32_t)(B.bm_start[b + 1] - b0);
+  for (uint32_t i = threadIdx.x; i < na; i += blockDim.x) kA[i] = A.key[a0 + i];
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) kB[i] = B.key[b0 + i];
+  __syncthreads();
+  for (uint32_t l = threadIdx.x; l < na + nb; l += blockDim.x)
+    merge_position(0, l, 0, a0, b0, na, nb, kA, kB, A, B, op, mkey, mca, mcb, mpair, keep, ub);
+  __syncthreads();  // the join's writes are visible to the whole CTA
+  uint32_t ck = 0;
+  uint64_t cu = 0;
+  for (uint32_t t0 = 0; t0 < na + nb; t0 += blockDim.x) {
+    const uint32_t t = t0 + threadIdx.x;
+    const bool in = t < na + nb;
+    const uint32_t k = in ? keep[t] : 0;
+    const uint64_t v = in ? (((uint64_t)k << 32) | ub[t]) : 0;
+    uint64_t ex, tot;
+    BS(ts).ExclusiveSum(v, ex, tot);
+    emit_entry(in && k, ck + (uint32_t)(ex >> 32), cu + (ex & 0xFFFFFFFFull), t, mkey, mca, mcb, mpair, A, B, E, L,
+               op);
+    ck += (uint32_t)(tot >> 32);
+    cu += tot & 0xFFFFFFFFull;
+    __syncthreads();  // ts reuse
+  }
+  if (threadIdx.x == 0) {
+    pke[0] = 0;
+    pke[1] = ck;
+    pue[0] = 0;
+    pue[1] = cu;
+  }
+}
+
 // One kept merged position becomes entry e with result slot `off`: the
 // entry record and its per-type-pair work list (whole warps must call this:
 // list_append aggregates with ballots).
@@ -694,7 +746,7 @@ int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBat
 // ------------------------------------ large array x array (smem bitset + TMA)
 
 template <int OP>
-__global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(const uint32_t *__restrict__ list,
+__global__ void __launch_bounds__(rsl::LTHREADS, RS_AAL_MINB) k_aa_large_op(const uint32_t *__restrict__ list,
                                                                const uint64_t *__restrict__ laoff,
                                                                const uint64_t *__restrict__ lboff,
                                                                const uint32_t *__restrict__ lnab,
@@ -726,7 +778,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_op(const uint32_t
   rsl::large_loop<OP>(smraw, *cnt, A.pool, B.pool, opool, meta_of, sink);
 }
 
-__global__ void __launch_bounds__(rsl::LTHREADS, 4) k_aa_large_count(const uint64_t *__restrict__ laoff,
+__global__ void __launch_bounds__(rsl::LTHREADS, RS_AAL_MINB) k_aa_large_count(const uint64_t *__restrict__ laoff,
                                                                   const uint64_t *__restrict__ lboff,
                                                                   const uint32_t *__restrict__ lnab,
                                                                   const uint32_t *__restrict__ lpair,
@@ -1149,18 +1201,24 @@ __global__ void __launch_bounds__(256) k_pair_nonempty(uint64_t npairs, const ui
   if (done && last_block_arrives(done, npairs)) block_exclusive_scan<uint32_t>(nz, fb, npairs + 1);
 }
 
+// fbase == nullptr: the single-pair op (one CTA): the pair's kept count is
+// this loop's own total, and the bitmap's cardinality is summed here (the
+// class kernels' atomic sums went to a scratch word, so no memset was needed)
 __global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uint32_t *__restrict__ pbase,
                                                       const uint32_t *__restrict__ fbase, Entries En, OutDesc O,
                                                       uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn,
-                                                      uint64_t *off, uint64_t *bm_start) {
+                                                      uint64_t *off, uint64_t *bm_start, uint64_t *bm_card) {
   using BS = cub::BlockScan<uint32_t, 256>;
   __shared__ typename BS::TempStorage ts;
+  __shared__ unsigned long long csum;
   const uint32_t p = blockIdx.x;
-  uint32_t f = fbase[p];
+  uint32_t f = fbase ? fbase[p] : 0;
   if (threadIdx.x == 0) {
     bm_start[p] = f;
-    if (p == 0) bm_start[npairs] = fbase[npairs];
+    if (p == 0 && fbase) bm_start[npairs] = fbase[npairs];
+    csum = 0;
   }
+  uint64_t my = 0;
   const uint32_t e1 = pbase[p + 1];
   for (uint32_t e0 = pbase[p]; e0 < e1; e0 += blockDim.x) {
     const uint32_t e = e0 + threadIdx.x;
@@ -1174,9 +1232,18 @@ __global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uin
       card[d] = O.card[e];
       nn[d] = O.n[e];
       off[d] = En.off[e];
+      my += O.card[e];
     }
     f += tot;
     __syncthreads();
+  }
+  if (!fbase) {
+    atomicAdd(&csum, (unsigned long long)my);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bm_start[1] = f;
+      bm_card[0] = csum;
+    }
   }
 }
 
@@ -1538,7 +1605,17 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   ub_register(b);
   b->type_mask = result_mask(A->type_mask, B->type_mask);
   host_mark(6);
-  RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
+  // one pair (per-pair entry bases): the compaction sums the bitmap's
+  // cardinality itself, so the class kernels' atomic sums go to scratch and
+  // there is nothing to zero first
+  const bool single = npairs == 1 && !mbase && epos;
+  uint64_t *res_card = b->d_bm_card;
+  if (single) {
+    res_card = (uint64_t *)S.get(16);
+    if (!S.ok()) { set_error("device allocation failed (op scratch)"); return RS_ENOMEM; }
+  } else {
+    RS_CK(cudaMemsetAsync(b->d_bm_card, 0, (npairs + 1) * 8, g_stream));
+  }
   host_mark(7);
   DevBatch dA = A->dev(), dB = B->dev();
   const ClassMask cm = class_mask(A->type_mask, B->type_mask, op);
@@ -1562,18 +1639,18 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     static const int copy_cta = env_int_("RS_COPY_CTAS", 16);  // CTAs per SM (tuning)
     unsigned g = std::min<uint64_t>(grid_for(n, 8), sms * copy_cta);
     RS_LAUNCH_PROF("copy", hcnt ? n : 0, k_copy, g, 256, 0, L.list[CLS_COPY], L.cnt + CLS_COPY, dA, dB, En, O,
-                   b->d_pool, b->d_bm_card);
+                   b->d_pool, res_card);
   }
   if (uint64_t n = n_bb) {
     F.next();
     if (bb_kernel_choice() == 0) {
       RS_LAUNCH_PROF("bitset_pair", hcnt ? n : 0, k_pair_dense<false>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
-                     L.list[CLS_BB], L.cnt + CLS_BB, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                     L.list[CLS_BB], L.cnt + CLS_BB, dA, dB, En, O, b->d_pool, res_card);
     } else {
       switch (bb_stages()) {
-        case 3: RS_TRY(launch_bb_op<3>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
-        case 4: RS_TRY(launch_bb_op<4>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
-        default: RS_TRY(launch_bb_op<2>(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card)); break;
+        case 3: RS_TRY(launch_bb_op<3>(op, L, n, dA, dB, En, O, b->d_pool, res_card)); break;
+        case 4: RS_TRY(launch_bb_op<4>(op, L, n, dA, dB, En, O, b->d_pool, res_card)); break;
+        default: RS_TRY(launch_bb_op<2>(op, L, n, dA, dB, En, O, b->d_pool, res_card)); break;
       }
     }
   }
@@ -1581,10 +1658,10 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     F.next();
     if (env_int_("RS_AA_SMALL_PLAIN", 0))  // the warp-per-pair kernel (A/B only)
       RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
-                     256, 0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                     256, 0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, res_card);
     else
       RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, k_aa_small, std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
-                     0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                     0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, res_card);
   }
   if (uint64_t n = n_aam) {
     F.next();
@@ -1592,33 +1669,41 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     // the 128-thread groups
     if (aa_medium_max(op) <= 512)
       RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<32, 16>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
-                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, res_card);
     else
       RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
-                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, res_card);
   }
   if (uint64_t n = n_aal) {
     F.next();
     if (env_int("RS_AA_LARGE_MERGE", 0))
       RS_LAUNCH_PROF("array_pair_l", hcnt ? n : 0, (k_aa_pair<256, 32>), std::min<uint64_t>(n, sms * 8), 256, 0, op,
-                     L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                     L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, res_card);
     else
-      RS_TRY(launch_aa_large_op(op, L, n, dA, dB, En, O, b->d_pool, b->d_bm_card, hcnt != nullptr));
+      RS_TRY(launch_aa_large_op(op, L, n, dA, dB, En, O, b->d_pool, res_card, hcnt != nullptr));
   }
   if (uint64_t n = n_gen) {
     F.next();
     RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 8), DT, 0, op,
-                   L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                   L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, res_card);
   }
   if (uint64_t n = n_prb) {
     F.next();
     RS_LAUNCH_PROF("probe_pair", hcnt ? n : 0, k_probe, std::min<uint64_t>(grid_for(n, PRB_WARPS), sms * 12),
                    32 * PRB_WARPS, 0, op,
-                   L.list[CLS_PRB], L.cnt + CLS_PRB, dA, dB, En, O, b->d_pool, b->d_bm_card);
+                   L.list[CLS_PRB], L.cnt + CLS_PRB, dA, dB, En, O, b->d_pool, res_card);
   }
   RS_TRY(F.end());
   host_mark(8);
   // compaction: drop empty results (bitmap.py:185-188)
+  if (single) {  // one CTA: kept count and cardinality computed in place
+    RS_LAUNCH(k_compact_pair, 1u, 256, 0, npairs, epos, (const uint32_t *)nullptr, En, O, b->d_key, b->d_type,
+              b->d_card, b->d_n, b->d_off, b->d_bm_start, b->d_bm_card);
+    b->h_valid = false;
+    *out = b;
+    host_mark(9);
+    return RS_OK;
+  }
   if (!mbase && epos && npairs) {  // per-pair entry bases: per-pair compaction
     uint32_t *nz = (uint32_t *)S.get((npairs + 1) * 4), *fb = (uint32_t *)S.get((npairs + 1) * 4);
     if (!S.ok()) { set_error("device allocation failed (compaction)"); return RS_ENOMEM; }
@@ -1627,7 +1712,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
               fb);
     if (!fuse) RS_TRY(scan_exclusive<uint32_t>(nz, fb, npairs + 1));
     RS_LAUNCH(k_compact_pair, (unsigned)npairs, 256, 0, npairs, epos, fb, En, O, b->d_key, b->d_type, b->d_card,
-              b->d_n, b->d_off, b->d_bm_start);
+              b->d_n, b->d_off, b->d_bm_start, b->d_bm_card);
     b->h_valid = false;
     *out = b;
     host_mark(9);
@@ -1761,14 +1846,18 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
     uint64_t *pu = (uint64_t *)S.get((npairs + 1) * 8), *pue = (uint64_t *)S.get((npairs + 1) * 8);
     if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
     const bool fuse = npairs <= FUSED_SCAN_MAX;
-    RS_LAUNCH(k_merge_pair, (unsigned)npairs, 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair,
-              keep, ub, pk, pu, fuse ? L.cnt + NCLS : nullptr, pke, pue);
-    if (!fuse) {
-      RS_TRY(scan_exclusive<uint32_t>(pk, pke, npairs + 1));
-      RS_TRY(scan_exclusive<uint64_t>(pu, pue, npairs + 1));
+    if (npairs == 1 && ub_mode) {  // join + emit in one CTA (no scans over pairs)
+      RS_LAUNCH(k_merge_emit1, 1u, 256, 0, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep, ub, pke, pue, En, L);
+    } else {
+      RS_LAUNCH(k_merge_pair, (unsigned)npairs, 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair,
+                keep, ub, pk, pu, fuse ? L.cnt + NCLS : nullptr, pke, pue);
+      if (!fuse) {
+        RS_TRY(scan_exclusive<uint32_t>(pk, pke, npairs + 1));
+        RS_TRY(scan_exclusive<uint64_t>(pu, pue, npairs + 1));
+      }
+      RS_LAUNCH(k_emit_pair, (unsigned)npairs, 256, 0, mbase, keep, ub, pke, pue, mkey, mca, mcb, mpair, dA, dB, En,
+                L, op);
     }
-    RS_LAUNCH(k_emit_pair, (unsigned)npairs, 256, 0, mbase, keep, ub, pke, pue, mkey, mca, mcb, mpair, dA, dB, En, L,
-              op);
     host_mark(4);
     if (ub_mode)
       return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr,

@@ -31,3 +31,14 @@ for op in ("and", "or"):
         B.pairwise_cardinality(op, B, [0], [1])
     t1 = time.perf_counter()
     print(f"{op} count (host out, sync): {1e6*(t1-t0)/n:.1f} us/call")
+# Python-side fixed costs
+L = _lib.lib()
+t0 = time.perf_counter()
+for _ in range(5000):
+    L.rs_batch_len(B._h)
+print(f"bare ctypes call: {1e6*(time.perf_counter()-t0)/5000:.2f} us")
+from paper_1709_07821_b200.batch import _u32_or_none
+t0 = time.perf_counter()
+for _ in range(5000):
+    _u32_or_none([0]); _u32_or_none([1])
+print(f"two index conversions: {1e6*(time.perf_counter()-t0)/5000:.2f} us")
