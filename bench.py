@@ -34,8 +34,8 @@ sys.path.insert(0, ROOT)
 OPS = ("and", "or", "andnot", "xor")
 NPAIRS = 1024
 NCHUNKS = 256
-E2E_CHUNKS = 16  # e2e pipeline depth: chunks of pairs whose transfer overlaps the previous chunk
-RING = 3         # e2e export: pinned result slots in flight (chunk i reuses chunk i-RING's)
+E2E_CHUNKS = int(os.environ.get("RS_E2E_CHUNKS", 16))  # e2e pipeline: chunks of pairs whose transfer overlaps
+RING = int(os.environ.get("RS_E2E_RING", 3))  # e2e export: pinned result slots in flight (chunk i reuses i-RING's)
 METRIC = "container-pair set ops/sec (AND/OR/ANDNOT/XOR + cardinality counts)"
 UNIT = "container-pairs/s"
 NOMINAL_HBM_GBS = 8000.0
@@ -508,9 +508,27 @@ def run_gpu(args):
                        "per pair) + 4x pairwise_cardinality; all counts read back and payload checks resolved "
                        "at the end of the step"}
         x_ms, xh, xd = e2e_time(True)
+        # the PCIe floor of this box: pinned 1 GiB copies each way (torch, CUDA events)
+        hb = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        db = torch.empty(1 << 30, dtype=torch.uint8, device=f"cuda:{local}")
+        rates = {}
+        for name, fn in (("h2d", lambda: db.copy_(hb, non_blocking=True)), ("d2h", lambda: hb.copy_(db, non_blocking=True))):
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(3):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            rates[name] = 3 * (1 << 30) / (a.elapsed_time(b) * 1e-3) / 1e9
+        del hb, db
+        floor_ms = max(xh / rates["h2d"], xd / rates["d2h"]) / 1e6
+        e2e["pcie_GBps"] = rates
+        e2e["h2d_floor_ms"] = h2d / rates["h2d"] / 1e6
         e2e["with_full_result_export"] = {
             "value": ws * units_per_step / (x_ms * 1e-3), "ms_per_step": x_ms, "h2d_bytes_per_step": int(xh),
-            "d2h_bytes_per_step": int(xd),
+            "d2h_bytes_per_step": int(xd), "transfer_floor_ms": floor_ms,
             "path": "as above, plus every result bitmap copied back as wire images: BitmapBatch.to_wire_async "
                     "(rs_batch_to_wire_async) into a 3-deep ring of pinned slots; each chunk's device->host copy "
                     "runs on the export stream, overlapping the next chunk's host->device copy and ops"}
