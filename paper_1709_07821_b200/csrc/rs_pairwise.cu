@@ -28,7 +28,7 @@ using namespace rs;
 
 namespace {
 
-enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, CLS_PRB = 6, NCLS = 7 };
+enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, CLS_PRB = 6, CLS_AAG = 7, NCLS = 8 };
 
 struct Entries {
   uint16_t *key;
@@ -67,8 +67,21 @@ __constant__ uint32_t c_aa_union_medium = 512;
 // array against a bitset or runs under AND (either side), or an array minus a
 // bitset or runs, keeps a subset of the array: bit / interval probes of its
 // values (CLS_PRB) instead of densifying both sides.
+// Array x array pairs past the small class whose AND (or ANDNOT, small A)
+// keeps a subset of a side at most 1/16 of the other's size go to the
+// galloping class: a warp per pair binary-searches the large side in place
+// (array_intersect_galloping's case, kernels/scalar.py:149-176,
+// _shared.py:14) -- a CTA-per-pair bitset kernel spent ~900 warp
+// instructions per such pair on staging and barriers for <= 256 searches.
+__device__ __forceinline__ bool gallop_pair(uint32_t na, uint32_t nb, int op) {
+  if (na + nb <= 256) return false;
+  if (op == RS_OP_AND) return 16 * min(na, nb) <= max(na, nb);
+  return op == RS_OP_ANDNOT && 16 * na <= nb;
+}
+
 __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb, int op) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
+  if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY && gallop_pair(na, nb, op)) return CLS_AAG;
   if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY)
     return na + nb <= 256 ? CLS_AAS
            : na + nb <= (op == RS_OP_OR || op == RS_OP_XOR ? c_aa_union_medium : c_aa_large_min) ? CLS_AAM
@@ -1084,6 +1097,106 @@ __global__ void __launch_bounds__(256) k_aa_pair(int op, const uint32_t *__restr
 }
 
 // |a ∩ b| of array x array pairs (array_intersect count_only).
+// Galloping pairs (gallop_pair): a warp per pair, persistent over the list.
+// Lane l takes small-side values l, l+32, ... (at most NV per lane) and
+// binary-searches each in the large side, all NV searches of a lane advancing
+// together (NV independent loads per step; the top levels of the large
+// array are shared by every search and stay in L1).  Kept values are
+// compacted in order with warp ballots; the small side is sorted, so the
+// result is.  With `out` (materialized) the result array goes to the entry's
+// slot; the count path adds to acc[pair].
+// 8-ary search (nl <= 4096 = 8^4): four levels of seven independent probes,
+// so a lookup is five dependent global loads instead of thirteen (the search
+// runs in place in HBM / L1, latency-bound).
+__device__ __forceinline__ uint32_t gallop_search(const uint16_t *__restrict__ L, uint32_t nl, uint32_t x) {
+  uint32_t lo = 0;
+#pragma unroll
+  for (uint32_t step = 512; step; step >>= 3) {
+    uint32_t c = 0;
+#pragma unroll
+    for (uint32_t k = 1; k < 8; k++) {
+      const uint32_t i = lo + k * step;
+      c += i < nl && __ldg(L + i) <= x;
+    }
+    lo += c * step;
+  }
+  return nl && __ldg(L + lo) == x;
+}
+
+template <int NV>
+__device__ __forceinline__ uint32_t gallop_warp(const uint16_t *__restrict__ S, uint32_t ns, const uint16_t *__restrict__ L,
+                                                uint32_t nl, bool keep_found, uint16_t *dst, int lane) {
+  uint32_t x[NV], k[NV];
+#pragma unroll
+  for (int j = 0; j < NV; j++) {
+    const uint32_t i = lane + 32 * j;
+    x[j] = i < ns ? __ldg(S + i) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < NV; j++) {
+    const uint32_t i = lane + 32 * j;
+    k[j] = i < ns && gallop_search(L, nl, x[j]) == keep_found;
+  }
+  uint32_t base = 0;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < NV; j++) {
+    const uint32_t m = __ballot_sync(0xffffffffu, k[j]);
+    if (dst && k[j]) dst[base + __popc(m & lt)] = (uint16_t)x[j];
+    base += __popc(m);
+  }
+  if (dst && lane < 8 && ((base + lane) & 7) != 0 && ((base + 7) & ~7u) > base + lane) dst[base + lane] = 0;  // pad
+  return base;
+}
+
+__device__ __forceinline__ uint32_t gallop_dispatch(const uint16_t *S, uint32_t ns, const uint16_t *L, uint32_t nl,
+                                                    bool keep_found, uint16_t *dst, int lane) {
+  if (ns <= 32) return gallop_warp<1>(S, ns, L, nl, keep_found, dst, lane);
+  if (ns <= 64) return gallop_warp<2>(S, ns, L, nl, keep_found, dst, lane);
+  if (ns <= 128) return gallop_warp<4>(S, ns, L, nl, keep_found, dst, lane);
+  return gallop_warp<8>(S, ns, L, nl, keep_found, dst, lane);  // ns <= 4096 / 16
+}
+
+__global__ void __launch_bounds__(256) k_aa_gallop(int op, const uint32_t *__restrict__ list,
+                                                   const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B, Entries E,
+                                                   OutDesc O, uint8_t *__restrict__ opool,
+                                                   uint64_t *__restrict__ res_card) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t total = *cnt, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
+    const uint32_t e = list[it], ca = E.ca[e], cb = E.cb[e];
+    const uint32_t na = A.card[ca], nb = B.card[cb];
+    const uint16_t *pa = (const uint16_t *)(A.pool + A.off[ca]), *pb = (const uint16_t *)(B.pool + B.off[cb]);
+    const bool a_small = op == RS_OP_ANDNOT || na <= nb;  // and: search the smaller side's values
+    const uint32_t card = gallop_dispatch(a_small ? pa : pb, a_small ? na : nb, a_small ? pb : pa,
+                                          a_small ? nb : na, op == RS_OP_AND, (uint16_t *)(opool + E.off[e]), lane);
+    if (lane == 0) {
+      O.type[e] = RS_TAG_ARRAY;
+      O.card[e] = card;
+      O.n[e] = card;
+      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_aa_gallop_count(const uint32_t *__restrict__ lca,
+                                                         const uint32_t *__restrict__ lcb,
+                                                         const uint32_t *__restrict__ lpair,
+                                                         const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
+                                                         uint64_t *__restrict__ acc) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t total = *cnt, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
+    const uint32_t ca = lca[it], cb = lcb[it];
+    const uint32_t na = A.card[ca], nb = B.card[cb];
+    const uint16_t *pa = (const uint16_t *)(A.pool + A.off[ca]), *pb = (const uint16_t *)(B.pool + B.off[cb]);
+    const bool a_small = na <= nb;
+    const uint32_t c = gallop_dispatch(a_small ? pa : pb, a_small ? na : nb, a_small ? pb : pa, a_small ? nb : na,
+                                       true, nullptr, lane);
+    if (lane == 0 && c) atomicAdd((unsigned long long *)&acc[lpair[it]], (unsigned long long)c);
+  }
+}
+
 // |A n B| of small pairs, laid out like k_aa_small: tiny pairs one per lane
 // (scalar intersection count), the rest through the warp merge path.
 __global__ void __launch_bounds__(256) k_aa_count_small(const uint32_t *__restrict__ lca,
@@ -1628,8 +1741,10 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   // more than one of them they run concurrently on side streams
   const uint64_t n_copy = want(CLS_COPY, op != RS_OP_AND), n_bb = want(CLS_BB, cm.bb),
                  n_aas = want(CLS_AAS, cm.aa), n_aam = want(CLS_AAM, cm.aa && aa_medium_possible(op)),
-                 n_aal = want(CLS_AAL, cm.aa), n_gen = want(CLS_GEN, cm.gen), n_prb = want(CLS_PRB, cm.prb);
-  const int nk = (n_copy > 0) + (n_bb > 0) + (n_aas > 0) + (n_aam > 0) + (n_aal > 0) + (n_gen > 0) + (n_prb > 0);
+                 n_aal = want(CLS_AAL, cm.aa), n_gen = want(CLS_GEN, cm.gen), n_prb = want(CLS_PRB, cm.prb),
+                 n_aag = want(CLS_AAG, cm.aa && (op == RS_OP_AND || op == RS_OP_ANDNOT));
+  const int nk = (n_copy > 0) + (n_bb > 0) + (n_aas > 0) + (n_aam > 0) + (n_aal > 0) + (n_gen > 0) + (n_prb > 0) +
+                 (n_aag > 0);
   Fork F;  // (tiny ops are host-bound: the fork's event calls would cost more than they overlap)
   static const int nofork = env_int_("RS_NO_FORK", 0);
   if (nk > 1 && E >= 16384 && !nofork) RS_TRY(F.begin(nk));
@@ -1681,6 +1796,11 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
                      L.list[CLS_AAL], L.cnt + CLS_AAL, dA, dB, En, O, b->d_pool, res_card);
     else
       RS_TRY(launch_aa_large_op(op, L, n, dA, dB, En, O, b->d_pool, res_card, hcnt != nullptr));
+  }
+  if (uint64_t n = n_aag) {
+    F.next();
+    RS_LAUNCH_PROF("array_pair_g", hcnt ? n : 0, k_aa_gallop, std::min<uint64_t>(grid_for(n, 8), sms * 8), 256, 0, op,
+                   L.list[CLS_AAG], L.cnt + CLS_AAG, dA, dB, En, O, b->d_pool, res_card);
   }
   if (uint64_t n = n_gen) {
     F.next();
@@ -1979,6 +2099,8 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
                      lpair + CLS_AAL * L.cap, L.cnt + CLS_AAL, dA, dB, inter);
     else
       RS_TRY(launch_aa_large_count(L, lpair + CLS_AAL * L.cap, dA, dB, inter));
+    RS_LAUNCH_PROF("array_count_g", 0, k_aa_gallop_count, pg, 256, 0, L.list[CLS_AAG], lcb + CLS_AAG * L.cap,
+                   lpair + CLS_AAG * L.cap, L.cnt + CLS_AAG, dA, dB, inter);
   }
   if (cm.gen) {
     F.next();
