@@ -92,6 +92,12 @@ int rs_batch_from_wire(const uint8_t *buf, const uint64_t *offs, uint64_t n, rs_
  * synchronous path; results computed from a batch that then fails are
  * meaningless (but stay in bounds). */
 int rs_batch_from_wire_async(const uint8_t *buf, const uint64_t *offs, uint64_t n, rs_batch **out);
+/* Same result from images already in DEVICE memory (dbuf, doffs[0..n] both
+ * device pointers, offsets relative to dbuf[0] at doffs[0]): the descriptor
+ * walk runs on the device as well (a thread per image), so no host round
+ * trip of the bytes; a malformed image is reported exactly as by
+ * rs_batch_from_wire (the error path copies the images to the host). */
+int rs_batch_from_wire_device(const uint8_t *dbuf, const uint64_t *doffs, uint64_t n, rs_batch **out);
 /* Read back the deferred payload checks: RS_OK or RS_EDECODE (repeatable). */
 int rs_batch_wait(const rs_batch *b);
 

@@ -53,6 +53,7 @@ def _declare(L):
         "rs_kernel_launches": ([], U64),
         "rs_batch_from_wire": ([P, P, U64, pp], I32),
         "rs_batch_from_wire_async": ([P, P, U64, pp], I32),
+        "rs_batch_from_wire_device": ([P, P, U64, pp], I32),
         "rs_batch_wait": ([P], I32),
         "rs_batch_from_u32": ([P, P, U64, I32, pp], I32),
         "rs_batch_free": ([P], I32),

@@ -105,6 +105,16 @@ class BitmapBatch:
             b._keep = buf  # the copy engine reads it after we return
         return b
 
+    @classmethod
+    def from_wire_device(cls, buf_ptr: int, offs_ptr: int, n: int) -> "BitmapBatch":
+        """serde.deserialize of n wire images already in device memory: buf_ptr /
+        offs_ptr are device pointers (uint8 bytes; uint64[n+1] offsets, relative
+        to the byte at buf_ptr for offs[0]) -- e.g. a torch CUDA tensor's
+        data_ptr().  The descriptor walk runs on the device too."""
+        h = C.c_void_p()
+        check(lib().rs_batch_from_wire_device(C.c_void_p(buf_ptr), C.c_void_p(offs_ptr), int(n), C.byref(h)))
+        return cls(h)
+
     def wait(self) -> "BitmapBatch":
         """Raise DecodeError if the deferred payload checks failed."""
         check(lib().rs_batch_wait(self._h))

@@ -994,3 +994,173 @@ extern "C" int rs_batch_key_histogram(const rs_batch *S, uint64_t *hist) {
   dfree(h);
   return RS_OK;
 }
+
+// ------------------------------------------- wire ingest from device memory
+// serde.deserialize (serde.py:87-169) of wire images that are already in HBM
+// (e.g. produced on the device, or copied there by the caller): the
+// descriptor walk runs on the device too -- a thread per image, twice (count,
+// then write), mirroring walk_wire's structural checks in the reference's
+// order -- followed by the same payload gather / check kernel as the host
+// path.  Any error, structural or payload, sends the images to the host path
+// once, which raises the reference's exact first DecodeError: the error path
+// is rare, and its message must match byte for byte.
+namespace {
+
+__device__ __forceinline__ uint16_t dg16(const uint8_t *p) { return (uint16_t)(p[0] | (p[1] << 8)); }
+__device__ __forceinline__ uint32_t dg32(const uint8_t *p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+// Walk image i; emit(k, key, tag, card, n, src_abs) for every container that
+// the reference would have accepted before its first structural error.
+// Returns true if the image is structurally valid.
+template <typename Emit>
+__device__ bool dev_walk_image(const uint8_t *buf, uint64_t o0, uint64_t len, Emit emit, uint32_t &nvalid,
+                               uint64_t &pool) {
+  const uint8_t *d = buf + o0;
+  uint64_t off = 0, start = 0;
+  nvalid = 0;
+  pool = 0;
+  auto need = [&](uint64_t nb) -> bool {
+    if (len - off < nb) return false;
+    start = off;
+    off += nb;
+    return true;
+  };
+  if (!need(4)) return false;
+  if (d[0] != 'R' || d[1] != 'O' || d[2] != 'A' || d[3] != 'R') return false;
+  if (!need(4)) return false;
+  const uint32_t count = dg32(d + start);
+  int32_t prev_key = -1;
+  for (uint32_t k = 0; k < count; k++) {  // descriptor stage: every descriptor before any payload
+    if (!need(8)) return false;
+    const uint16_t kk = dg16(d + start);
+    const uint8_t tag = d[start + 2], pad = d[start + 3];
+    if (pad != 0 || tag < 1 || tag > 3 || (int32_t)kk <= prev_key) return false;
+    prev_key = kk;
+  }
+  for (uint32_t k = 0; k < count; k++) {
+    const uint8_t *dd = d + 8 + 8ull * k;
+    const uint16_t kk = dg16(dd);
+    const uint8_t tag = dd[2];
+    const uint32_t cc = dg32(dd + 4);
+    uint32_t nn;
+    if (tag == RS_TAG_ARRAY) {
+      if (!(cc >= 1 && cc <= RS_ARRAY_MAX) || !need(2ull * cc)) return false;
+      nn = cc;
+    } else if (tag == RS_TAG_BITSET) {
+      if (!need(8192)) return false;
+      nn = RS_WORDS;
+    } else {
+      if (!need(2)) return false;
+      nn = dg16(d + start);
+      if (nn == 0 || nn > RS_RUN_MAX_RUNS || !need(4ull * nn)) return false;  // (> 2047 runs: never admissible)
+    }
+    emit(k, kk, tag, cc, nn, o0 + start);
+    nvalid = k + 1;
+    pool += rs_pad16(rs_payload_bytes(tag, nn));
+  }
+  return off == len;
+}
+
+__global__ void k_devwire_count(uint64_t n, const uint8_t *__restrict__ buf, const uint64_t *__restrict__ offs,
+                                uint64_t *__restrict__ ccount, uint64_t *__restrict__ pbytes, int *__restrict__ bad) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) { ccount[n] = 0; pbytes[n] = 0; return; }
+  uint32_t nv;
+  uint64_t pool;
+  const bool ok = dev_walk_image(buf, offs[i] - offs[0], offs[i + 1] - offs[i],
+                                 [](uint32_t, uint16_t, uint8_t, uint32_t, uint32_t, uint64_t) {}, nv, pool);
+  ccount[i] = nv;
+  pbytes[i] = pool;
+  if (!ok) atomicOr(bad, 1);
+}
+
+__global__ void k_devwire_write(uint64_t n, const uint8_t *__restrict__ buf, const uint64_t *__restrict__ offs,
+                                const uint64_t *__restrict__ cbase, const uint64_t *__restrict__ pbase,
+                                uint64_t *__restrict__ bm_start, uint16_t *key, uint8_t *type, uint32_t *card,
+                                uint32_t *nn, uint64_t *off, uint64_t *__restrict__ src, unsigned *__restrict__ tmask) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  bm_start[i] = cbase[i];
+  if (i == n) return;
+  const uint64_t cb = cbase[i];
+  uint64_t poff = pbase[i];
+  unsigned tm = 0;
+  uint32_t nv;
+  uint64_t pool;
+  dev_walk_image(buf, offs[i] - offs[0], offs[i + 1] - offs[i],
+                 [&](uint32_t k, uint16_t kk, uint8_t tag, uint32_t cc, uint32_t n_, uint64_t s) {
+                   const uint64_t c = cb + k;
+                   key[c] = kk; type[c] = tag; card[c] = cc; nn[c] = n_; off[c] = poff; src[c] = s;
+                   poff += rs_pad16(rs_payload_bytes(tag, n_));
+                   tm |= 1u << tag;
+                 },
+                 nv, pool);
+  if (tm) atomicOr(tmask, tm);
+}
+
+}  // namespace
+
+extern "C" int rs_batch_from_wire_device(const uint8_t *dbuf, const uint64_t *doffs, uint64_t n, rs_batch **out) {
+  RS_TRY(ensure_device());
+  *out = nullptr;
+  uint64_t *ccount = (uint64_t *)dalloc((n + 1) * 8), *pbytes = (uint64_t *)dalloc((n + 1) * 8);
+  uint64_t *cbase = (uint64_t *)dalloc((n + 1) * 8), *pbase = (uint64_t *)dalloc((n + 1) * 8);
+  int *flags = (int *)dalloc(16);
+  if (!ccount || !pbytes || !cbase || !pbase || !flags) { set_error("device allocation failed (device wire)"); return RS_ENOMEM; }
+  auto cleanup = [&]() { dfree(ccount); dfree(pbytes); dfree(cbase); dfree(pbase); dfree(flags); };
+  // host fallback for malformed images: the exact first error, from the host walk
+  auto host_path = [&]() -> int {
+    std::vector<uint64_t> h_offs(n + 1);
+    int rc = d2h(h_offs.data(), doffs, (n + 1) * 8);
+    if (rc) return rc;
+    const uint64_t bytes = h_offs[n] - h_offs[0];
+    std::vector<uint8_t> h_buf(bytes ? bytes : 1);
+    if (bytes) {
+      rc = d2h(h_buf.data(), dbuf, bytes);
+      if (rc) return rc;
+    }
+    const uint64_t base = h_offs[0];
+    for (auto &o : h_offs) o -= base;
+    return rs_batch_from_wire(h_buf.data(), h_offs.data(), n, out);
+  };
+  RS_CK(cudaMemsetAsync(flags, 0, 16, g_stream));
+  const unsigned gn = (unsigned)((n + 1 + 127) / 128);
+  RS_LAUNCH(k_devwire_count, gn, 128, 0, n, dbuf, doffs, ccount, pbytes, flags);
+  RS_TRY(scan_exclusive<uint64_t>(ccount, cbase, n + 1));
+  RS_TRY(scan_exclusive<uint64_t>(pbytes, pbase, n + 1));
+  struct { uint64_t C, P; int bad; } h;
+  RS_CK(cudaMemcpyAsync(&h.C, cbase + n, 8, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaMemcpyAsync(&h.P, pbase + n, 8, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaMemcpyAsync(&h.bad, flags, 4, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaStreamSynchronize(g_stream));
+  if (h.bad) { cleanup(); return host_path(); }
+  rs_batch *b = new rs_batch();
+  int rc = batch_alloc(b, n, h.C, h.P);
+  uint64_t *src = (uint64_t *)dalloc((h.C ? h.C : 1) * 8);
+  uint8_t *vcode = (uint8_t *)dalloc(h.C ? h.C : 1);
+  uint32_t *vval = (uint32_t *)dalloc((h.C ? h.C : 1) * 4);
+  if (rc || !src || !vcode || !vval) {
+    rs_batch_free(b); cleanup(); dfree(src); dfree(vcode); dfree(vval);
+    set_error("device allocation failed (device wire)");
+    return RS_ENOMEM;
+  }
+  RS_LAUNCH(k_devwire_write, gn, 128, 0, n, dbuf, doffs, cbase, pbase, b->d_bm_start, b->d_key, b->d_type, b->d_card,
+            b->d_n, b->d_off, src, (unsigned *)(flags + 2));
+  if (h.C)
+    RS_LAUNCH(k_wire_gather_validate, (unsigned)((h.C * 32 + 255) / 256), 256, 0, h.C, h.C, dbuf, src, b->dev(),
+              b->d_pool, vcode, vval, flags + 1, (uint32_t *)nullptr);
+  int hf[2] = {0, 0};
+  RS_CK(cudaMemcpyAsync(hf, flags + 1, 8, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaStreamSynchronize(g_stream));
+  dfree(src); dfree(vcode); dfree(vval);
+  if (hf[0]) { rs_batch_free(b); cleanup(); return host_path(); }
+  cleanup();
+  b->type_mask = (uint8_t)hf[1];
+  b->h_valid = false;
+  RS_TRY(finalize_batch(b));
+  *out = b;
+  return RS_OK;
+}

@@ -155,3 +155,33 @@ def test_to_wire_async_matches_sync_export(pkg):
     R = A.pairwise("or", B)
     with pytest.raises(ValueError):
         R.to_wire_async(np.zeros(16, np.uint8))
+
+
+def test_from_wire_device_matches_host_ingest(pkg):
+    """rs_batch_from_wire_device: images already in HBM, descriptor walk on the
+    device -- same batch as the host path on the reference's golden images
+    (all container types), and the exact DecodeError on every malformed one."""
+    import torch
+    from tests.golden_io import load
+    g = load()
+    ws = [g.wire(a) for a in g["pair_a"]] + [g.wire(b) for b in g["pair_b"]] + [b"ROAR\x00\x00\x00\x00"]
+    buf = np.frombuffer(b"".join(ws), np.uint8)
+    offs = np.concatenate([[0], np.cumsum([len(w) for w in ws])]).astype(np.uint64)
+    dbuf = torch.from_numpy(buf.copy()).cuda()
+    doffs = torch.from_numpy(offs.astype(np.int64)).cuda()
+    D = pkg.BitmapBatch.from_wire_device(dbuf.data_ptr(), doffs.data_ptr(), len(ws))
+    H = pkg.BitmapBatch.from_wire(ws)
+    assert D.to_wire_list() == ws
+    assert np.array_equal(D.digests(), H.digests())
+    assert np.array_equal(D.cardinalities(), H.cardinalities())
+    assert D.pairwise("xor", H).to_wire_list() == H.pairwise("xor", H).to_wire_list()
+    # malformed images: the host path's exact error (offset and message)
+    for bi in g["bad"]:
+        img = g.wire(bi)
+        with pytest.raises(pkg.DecodeError) as e1:
+            pkg.BitmapBatch.from_wire([ws[0], img])
+        t = torch.from_numpy(np.frombuffer(ws[0] + img, np.uint8).copy()).cuda()
+        o = torch.tensor([0, len(ws[0]), len(ws[0]) + len(img)], dtype=torch.int64).cuda()
+        with pytest.raises(pkg.DecodeError) as e2:
+            pkg.BitmapBatch.from_wire_device(t.data_ptr(), o.data_ptr(), 2)
+        assert str(e1.value) == str(e2.value) and e1.value.offset == e2.value.offset
