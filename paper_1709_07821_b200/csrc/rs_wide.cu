@@ -275,7 +275,10 @@ __global__ void k_union_classify(uint64_t G, const uint32_t *__restrict__ seg_st
 // ORs, which is folded into the registers at the end and re-zeroed by its
 // owners.  A CTA-per-contributor-chain kernel spent most of its time in
 // dependent load chains (metadata -> payload per contributor).
-constexpr int UT = 128;  // k_union_or threads: thread t owns words [4t, 4t+4) and [4(t+UT), 4(t+UT)+4)
+// k_union_or threads: thread t owns words [4(t + UT h), 4(t + UT h) + 4), h < UH.
+// Small CTAs keep more keys in flight per SM (the kernel waits on dependent
+// metadata -> payload chains): 64 threads give ~2x the keys of 128.
+constexpr int UT = 64, UH = RS_WORDS / (4 * UT);
 __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
                                                  const uint32_t *__restrict__ seg_start,
                                                  const uint32_t *__restrict__ item_c, const uint64_t *__restrict__ keys,
@@ -292,7 +295,7 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
   const int t = threadIdx.x, lane = t & 31;
   uint32_t *X32 = (uint32_t *)X;
 #pragma unroll
-  for (int k = 0; k < 8; k++) X[t + UT * k] = 0;
+  for (int k = 0; k < RS_WORDS / UT; k++) X[t + UT * k] = 0;
   if (t == 0) {
     ebase[UT] = 0;
     next_li = atomicAdd(const_cast<uint32_t *>(cnt) + 2, 1u);  // dynamic: keys differ in cost
@@ -304,7 +307,9 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
     if (li >= total) break;
     const uint32_t g = list[li];
     const uint32_t s = seg_start[g], e = seg_start[g + 1];
-    uint64_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t r[4 * UH];
+#pragma unroll
+    for (int k = 0; k < 4 * UH; k++) r[k] = 0;
     for (uint32_t w0 = s; w0 < e; w0 += UT) {
       // window metadata: thread t = contributor w0 + t
       const bool have = w0 + t < e;
@@ -363,28 +368,14 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
       }
       // bitset contributors: words straight into registers, 2 contributors
       // (4 x 16-byte loads per thread) in flight
-      uint32_t k = 0;
-      for (; k + 2 <= nb; k += 2) {
-        uint64_t w[4][4];
-        ld_words(S.pool, moff[k], t, w[0]);
-        ld_words(S.pool, moff[k], t + UT, w[1]);
-        ld_words(S.pool, moff[k + 1], t, w[2]);
-        ld_words(S.pool, moff[k + 1], t + UT, w[3]);
+      for (uint32_t k = 0; k < nb; k++) {  // each contributor: UH independent 32-byte loads per thread
+        uint64_t w[UH][4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          r[q] |= w[0][q] | w[2][q];
-          r[4 + q] |= w[1][q] | w[3][q];
-        }
-      }
-      if (k < nb) {
-        uint64_t w[2][4];
-        ld_words(S.pool, moff[k], t, w[0]);
-        ld_words(S.pool, moff[k], t + UT, w[1]);
+        for (int h = 0; h < UH; h++) ld_words(S.pool, moff[k], t + UT * h, w[h]);
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          r[q] |= w[0][q];
-          r[4 + q] |= w[1][q];
-        }
+        for (int h = 0; h < UH; h++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) r[4 * h + q] |= w[h][q];
       }
       __syncthreads();  // prefix and nelem visible
       // array / run payloads, flattened over the window in 16-byte units
@@ -437,7 +428,7 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
     }
     uint32_t pc = 0;
 #pragma unroll
-    for (int h = 0; h < 2; h++)
+    for (int h = 0; h < UH; h++)
 #pragma unroll
       for (int q = 0; q < 4; q++) {
         const int wd = 4 * (t + UT * h) + q;
@@ -445,8 +436,8 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
         X[wd] = 0;
         pc += __popcll(r[4 * h + q]);
       }
-    st_words(opool, (uint64_t)g * 8192, t, r);
-    st_words(opool, (uint64_t)g * 8192, t + UT, r + 4);
+#pragma unroll
+    for (int h = 0; h < UH; h++) st_words(opool, (uint64_t)g * 8192, t + UT * h, r + 4 * h);
     pc = __reduce_add_sync(0xffffffffu, pc);
     if (lane == 0) red[t >> 5] = pc;
     __syncthreads();  // also orders the X clears before the next key's scatter
