@@ -289,6 +289,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import oracle as orc
+    import workloads
+    workloads.use_library(orc.build())  # the generator linked into the port's library
     buf, offs = workload(seed=2)
     threads = orc.num_threads()
     S = orc.Session(buf, offs, threads)

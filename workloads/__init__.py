@@ -26,10 +26,19 @@ def build() -> str:
     return LIB
 
 
+def use_library(path: str) -> None:
+    """Load the generator from another library that links synth.c (the
+    bench's reference arm uses oracle/liboracle.so, so that arm maps no
+    other library of this repository)."""
+    global _lib, LIB
+    LIB = path
+    _lib = None
+
+
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(build() if not os.path.exists(LIB) else LIB)
+        L = C.CDLL(LIB if os.path.exists(LIB) else build())
         P, I64, U64, D, I = C.c_void_p, C.c_int64, C.c_uint64, C.c_double, C.c_int
         pp = C.POINTER(C.c_void_p)
         L.syn_uniform.argtypes = [U64, I64, U64, U64, pp, pp]
