@@ -518,26 +518,31 @@ __global__ void __launch_bounds__(DT) k_densify(uint64_t T, const uint32_t *__re
 // memory (16-byte zeroing, 16-byte value loads masked to n, native shared
 // ORs) and streamed out with 16-byte stores.  No block barriers.
 constexpr int DW_WARPS = 4;  // 4 x 8 KB rows of shared memory per CTA; 6 CTAs per SM (80 registers)
+// `list` (optional): densify only items list[0..T) (the rows the CUDA-core
+// tiles read when the tensor-core tiles build their own rows).
 __global__ void __launch_bounds__(32 * DW_WARPS) k_densify_warp(uint64_t T, const uint32_t *__restrict__ item_c,
-                                                                DevBatch S, uint64_t *__restrict__ D) {
+                                                                DevBatch S, uint64_t *__restrict__ D,
+                                                                const uint32_t *__restrict__ list) {
   __shared__ __align__(16) uint4 Xs[DW_WARPS][RS_WORDS / 2];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint4 *X = Xs[wib];
   uint32_t *X32 = (uint32_t *)X;
   const uint64_t step = (uint64_t)gridDim.x * DW_WARPS;
-  uint64_t i = (uint64_t)blockIdx.x * DW_WARPS + wib;
-  if (i >= T) return;
+  uint64_t li = (uint64_t)blockIdx.x * DW_WARPS + wib;
+  if (li >= T) return;
+  uint64_t i = list ? list[li] : li;
   uint32_t c = item_c[i];
   uint8_t type = S.type[c];
   uint64_t off = S.off[c];
   uint32_t n = S.n[c];
   for (;;) {
     // next item's metadata first: its dependent loads overlap this row
-    const uint64_t ni = i + step;
+    const uint64_t nli = li + step;
+    const uint64_t ni = nli < T ? (list ? list[nli] : nli) : ~0ull;
     uint32_t nc = 0, nn = 0;
     uint8_t ntype = 0;
     uint64_t noff = 0;
-    if (ni < T) {
+    if (nli < T) {
       nc = item_c[ni];
       ntype = S.type[nc];
       noff = S.off[nc];
@@ -591,7 +596,8 @@ __global__ void __launch_bounds__(32 * DW_WARPS) k_densify_warp(uint64_t T, cons
       for (int q = 0; q < 16; q++) __stcs(dst + lane + 32 * q, X[lane + 32 * q]);
       __syncwarp();  // the row is read out before the next item zeroes it
     }
-    if (ni >= T) break;
+    if (nli >= T) break;
+    li = nli;
     i = ni;
     c = nc;
     type = ntype;
@@ -826,6 +832,348 @@ __global__ void __launch_bounds__(rsu::UTHREADS, 1)
           for (int j = 0; j < 32; j++) {
             const uint32_t vc = c0 + cb + j;
             const uint32_t cnt = (uint32_t)__uint_as_float(v[j]);  // exact: an integer <= 65,536
+            if (cnt && vc < m && u < vc) {
+              const uint32_t bv = item_bm[s0 + vc];
+              const uint32_t lo = min(bu, bv), hi = max(bu, bv);
+              atomicAdd(&Mx[(uint64_t)lo * N + hi], (unsigned long long)cnt);
+            }
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(UTMEM) : "memory");
+}
+
+// ---------------------------------------------------- all pairs, direct rows
+// (experimental, RS_ALLPAIRS_DIRECT=1; measured 7x slower than the TMA-fed
+// tiles, see rs_all_pairs_cardinality.)
+// The same tensor-core tiles without the densified copy of every row: the
+// producer threads build each row's 256-bit K chunk straight from its
+// container -- a bitset's 32 bytes, or the bits of the array values / runs
+// that fall into the chunk -- so the 8 KB rows are never written to HBM and
+// read back (config 5: 1 GB each way, the densify kernel alone was 0.33 ms).
+// K order does not matter to a Gram matrix, so producer group g walks the
+// contiguous quarter [16384 g, 16384 (g+1)) of every row, one chunk per stage
+// visit; the MMA issuer still visits the stages round-robin.  Array / run
+// rows keep a cursor (and a 16-byte value window plus the next one, loaded
+// ahead) in shared memory; their starting index in the quarter comes from a
+// per-item table (k_quarter_index).  Bitset rows load the next chunk's 32
+// bytes one visit ahead.
+namespace rsd2 {
+// Two row slots per producer thread: (A row, B row) for a block tile with a
+// separate A (its B side has <= 128 rows), (row arow, row arow + 128) when A
+// is the first 128 rows of B.  48 bytes each: 2 x 512 x 48 = 48 KB beside
+// the 4 expanded stages (<= 128 KB) in the 192 KB ring.
+struct RowCur {
+  uint4 win, nwin;   // array / run: elements [wpos, wpos+8) and the next 8; bitset: the next chunk's 32 bytes
+  uint64_t base;     // payload address
+  uint16_t idx, wpos, n;
+  uint8_t type;      // 0 = no row
+};
+static_assert(sizeof(RowCur) == 48, "RowCur layout");
+}  // namespace rsd2
+
+// per grouped item: first array value / run index in each quarter of the chunk
+__global__ void k_quarter_index(uint64_t T, const uint32_t *__restrict__ item_c, DevBatch S, ushort4 *__restrict__ Q) {
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i >= T) return;
+  const uint32_t c = item_c[i];
+  const uint8_t t = S.type[c];
+  const uint32_t n = S.n[c];
+  uint16_t q[4] = {0, 0, 0, 0};
+  if (t != RS_TAG_BITSET) {
+    const uint16_t *v = (const uint16_t *)(S.pool + S.off[c]);
+    for (int g = 1; g < 4; g++) {
+      const uint32_t lim = 16384u * g;
+      uint32_t lo = 0, hi = n;  // first element whose (last) value >= lim
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const uint32_t last = t == RS_TAG_ARRAY ? v[mid] : (uint32_t)v[2 * mid] + v[2 * mid + 1];
+        if (last < lim) lo = mid + 1; else hi = mid;
+      }
+      q[g] = (uint16_t)lo;
+    }
+  }
+  Q[i] = make_ushort4(q[0], q[1], q[2], q[3]);
+}
+
+__device__ __forceinline__ uint32_t elem_of(const uint4 w, uint32_t j) {  // u32 element j < 4 of a window
+  return j == 0 ? w.x : j == 1 ? w.y : j == 2 ? w.z : w.w;
+}
+
+// set bit b (< 256) of the 8-word chunk
+__device__ __forceinline__ void set_chunk_bit(uint32_t (&w)[8], uint32_t b) {
+  const uint32_t word = b >> 5, bit = 1u << (b & 31);
+#pragma unroll
+  for (int k = 0; k < 8; k++) w[k] |= word == (uint32_t)k ? bit : 0u;
+}
+
+// bits [a, b] (inclusive, both < 256) of the 8-word chunk
+__device__ __forceinline__ void set_chunk_range(uint32_t (&w)[8], uint32_t a, uint32_t b) {
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const uint32_t lo = 32u * k, hi = lo + 31;
+    if (b < lo || a > hi) continue;
+    const uint32_t s = a > lo ? a - lo : 0, e = b < hi ? b - lo : 31;
+    w[k] |= (~0u << s) & (~0u >> (31 - e));
+  }
+}
+
+__device__ __forceinline__ uint4 ld_nc16(uint64_t addr) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(addr));
+  return v;
+}
+
+// Asynchronous 16-byte global -> shared copies (LDGSTS): the row data a
+// producer needs at its NEXT visit lands in its shared slot while the tile's
+// other chunks are multiplied; a register prefetch would be waited for as
+// soon as the cursor state is written back to shared memory.
+__device__ __forceinline__ void cp_async16(void *smem, uint64_t gaddr) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(rsu::su32(smem)), "l"(gaddr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// every COMMITTED group done (copies issued since the last commit keep flying)
+__device__ __forceinline__ void cp_async_wait_committed() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Build the 256-bit chunk k (bits [256k, 256k+256)) of one row from its
+// source; r is the row's shared-memory slot (this thread's own).
+__device__ __forceinline__ void row_chunk(rsd2::RowCur *r, uint32_t k, uint32_t (&w)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; j++) w[j] = 0;
+  const uint32_t type = r->type;
+  if (type == 0) return;
+  if (type == RS_TAG_BITSET) {
+    const uint4 a = r->win, b = r->nwin;
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    if ((k & 63) != 63) {  // the next chunk of this quarter, for the next visit
+      cp_async16(&r->win, r->base + 32ull * (k + 1));
+      cp_async16(&r->nwin, r->base + 32ull * (k + 1) + 16);
+    }
+    return;
+  }
+  const uint32_t lo = 256u * k, hi = lo + 256u;
+  const bool arr = type == RS_TAG_ARRAY;
+  const uint32_t per = arr ? 8u : 4u, esz = arr ? 2u : 4u;
+  uint32_t idx = r->idx, wpos = r->wpos;
+  const uint32_t n = r->n;
+  uint4 win = r->win;
+  while (idx < n) {
+    if (idx >= wpos + per) {  // next window (prefetched); fetch the one after it
+      cp_async_wait_all();  // (it may have been issued during this visit)
+      win = r->nwin;
+      r->win = win;
+      wpos += per;
+      if (wpos + per < n) cp_async16(&r->nwin, r->base + (uint64_t)esz * (wpos + per));
+    }
+    const uint32_t j = idx - wpos;
+    if (arr) {
+      const uint32_t x = elem_of(win, j >> 1), v = (j & 1) ? x >> 16 : x & 0xFFFFu;
+      if (v >= hi) break;
+      set_chunk_bit(w, v - lo);
+      idx++;
+    } else {
+      const uint32_t x = elem_of(win, j), st = x & 0xFFFFu, en = st + (x >> 16);
+      if (st >= hi) break;
+      set_chunk_range(w, st > lo ? st - lo : 0u, (en < hi - 1 ? en : hi - 1) - lo);
+      if (en >= hi) break;  // the run continues into the next chunk
+      idx++;
+    }
+  }
+  r->idx = (uint16_t)idx;
+  r->wpos = (uint16_t)wpos;
+}
+
+__device__ __forceinline__ void row_init(rsd2::RowCur *r, bool have, uint32_t item, const uint32_t *item_c,
+                                         const DevBatch &S, const ushort4 *Q, int grp) {
+  r->type = 0;
+  if (!have) return;
+  const uint32_t c = item_c[item];
+  const uint8_t type = S.type[c];
+  const uint32_t n = S.n[c];
+  const uint64_t base = (uint64_t)(S.pool + S.off[c]);
+  r->type = type;
+  r->n = (uint16_t)n;
+  r->base = base;
+  const uint32_t k0 = 64u * grp;
+  if (type == RS_TAG_BITSET) {
+    cp_async16(&r->win, base + 32ull * k0);
+    cp_async16(&r->nwin, base + 32ull * k0 + 16);
+    return;
+  }
+  const ushort4 q = Q[item];
+  const uint32_t idx = grp == 0 ? q.x : grp == 1 ? q.y : grp == 2 ? q.z : q.w;
+  const bool arr = type == RS_TAG_ARRAY;
+  const uint32_t per = arr ? 8u : 4u, esz = arr ? 2u : 4u;
+  const uint32_t wpos = idx & ~(per - 1);
+  r->idx = (uint16_t)idx;
+  r->wpos = (uint16_t)wpos;
+  if (wpos < n) cp_async16(&r->win, base + (uint64_t)esz * wpos);
+  if (wpos + per < n) cp_async16(&r->nwin, base + (uint64_t)esz * (wpos + per));
+}
+
+__global__ void __launch_bounds__(rsu::UTHREADS, 1)
+    k_allpairs_umma_direct(const uint32_t *__restrict__ tp_seg, const uint16_t *__restrict__ tp_r0,
+                           const uint16_t *__restrict__ tp_c0, const uint16_t *__restrict__ tp_nb,
+                           const uint32_t *__restrict__ seg_start, const uint32_t *__restrict__ item_c, DevBatch S,
+                           const ushort4 *__restrict__ Q, const uint32_t *__restrict__ item_bm, uint64_t N,
+                           unsigned long long *__restrict__ Mx) {
+  using namespace rsu;
+  extern __shared__ __align__(1024) uint8_t usm_raw[];
+  uint8_t *usm = (uint8_t *)(((uintptr_t)usm_raw + 1023) & ~(uintptr_t)1023);
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const uint32_t seg = tp_seg[blockIdx.x];
+  const uint32_t s0 = seg_start[seg], m = seg_start[seg + 1] - s0;
+  const uint32_t r0 = tp_r0[blockIdx.x], c0 = tp_c0[blockIdx.x], nb = tp_nb[blockIdx.x];
+  const bool shared_a = r0 == c0;
+  const uint32_t rows_b = max(nb, (uint32_t)UM);
+  const uint32_t sbytes = rows_b * UROWB;
+  uint8_t *xst = usm;                                  // UNST expanded B stages
+  rsd2::RowCur *cur = (rsd2::RowCur *)(usm + UNST * sbytes);  // producer row cursors: [slot][thread], 2 slots
+  uint64_t *full = (uint64_t *)(usm + URING), *empty = full + UNST, *done = empty + UNST;
+  uint32_t *tslot = (uint32_t *)(done + 1);
+  for (uint32_t i = t; i < UNST * sbytes / 16; i += UTHREADS) ((uint4 *)xst)[i] = make_uint4(0, 0, 0, 0);
+  if (t == 0) {
+    for (int i = 0; i < UNST; i++) {
+      ubar_init(&full[i], 4);
+      ubar_init(&empty[i], 1);
+    }
+    ubar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "r"(UTMEM)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tslot;
+  if (warp < 4) {  // unit block scales
+    const uint32_t one = 0x7F7F7F7Fu;
+    for (int c = 0; c < 32; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       tmem + ((uint32_t)(32 * warp) << 16) + USCOL + c),
+                   "r"(one)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  constexpr int NCH = RS_WORDS * 64 / UKC;  // 256-bit chunks per row
+  constexpr int PER = NCH / UNST;           // chunks per producer group (a quarter of the row)
+  if (warp == UPROD / 32) {  // ------------------------------ MMA issuer
+    const uint32_t idesc = idesc_mxf4(UM, (int)nb);
+    const uint64_t db0 = sw128_desc(su32(xst));
+    const uint32_t sstep = sbytes >> 4;
+    const uint32_t sfa = tmem + USCOL, sfb = tmem + USCOL + 16u;
+    uint32_t b = 0, ph = 0;
+    for (int c = 0; c < NCH; c++) {
+      ubar_wait(&full[b], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t db = db0 + (uint64_t)(b * sstep);
+      const uint32_t ta = tmem + UACOL + 32u * b;
+      if (elect_one()) {
+        umma_mxf4(tmem, ta, db, idesc, sfa, sfb, c > 0);
+        umma_mxf4(tmem, ta + 8u, db + 2, idesc, sfa, sfb, true);
+        umma_mxf4(tmem, ta + 16u, db + 4, idesc, sfa, sfb, true);
+        umma_mxf4(tmem, ta + 24u, db + 6, idesc, sfa, sfb, true);
+        umma_commit(&empty[b]);
+        if (c == NCH - 1) umma_commit(done);
+      }
+      __syncwarp();
+      if (++b == (uint32_t)UNST) {
+        b = 0;
+        ph ^= 1u;
+      }
+    }
+  } else if (warp < UPROD / 32) {  // ----------------------- producers
+    // group g = warp / 4 builds chunks 64 g .. 64 g + 63 into stage g; warp q
+    // of the group owns rows 32 q + lane (A) and B rows arow, arow + 128
+    const int grp = warp >> 2, q = warp & 3;
+    const uint32_t nrow_b = c0 < m ? min(nb, m - c0) : 0u, nrow_a = shared_a ? nrow_b : min((uint32_t)UM, m - r0);
+    const uint32_t arow = 32 * q + lane;
+    const int pt = t;  // producer thread index (< UPROD)
+    // slot 0: the A row (= B row arow when shared); slot 1: B row arow (separate
+    // A) or B row arow + 128 (shared A)
+    rsd2::RowCur *c0s = &cur[pt], *c1s = &cur[UPROD + pt];
+    if (shared_a) row_init(c0s, arow < nrow_b, s0 + c0 + arow, item_c, S, Q, grp);
+    else row_init(c0s, arow < nrow_a, s0 + r0 + arow, item_c, S, Q, grp);
+    if (shared_a) row_init(c1s, arow + UM < nrow_b, s0 + c0 + arow + UM, item_c, S, Q, grp);
+    else row_init(c1s, arow < nrow_b, s0 + c0 + arow, item_c, S, Q, grp);
+    cp_async_commit();
+    uint8_t *sb = xst + grp * sbytes;
+    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + UACOL + 32u * grp;
+    uint32_t eph = 0;
+    for (int i = 0; i < PER; i++) {
+      const uint32_t k = (uint32_t)(PER * grp + i);  // this visit's chunk
+      if (i) {
+        ubar_wait(&empty[grp], eph);
+        eph ^= 1u;
+      }
+      cp_async_wait_committed();  // this visit's row data (issued and committed one visit ago)
+      uint32_t e[32];
+      {
+        uint32_t w[8];
+        row_chunk(c0s, k, w);
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const uint4 v = nib32(w[u]);
+          e[4 * u] = v.x; e[4 * u + 1] = v.y; e[4 * u + 2] = v.z; e[4 * u + 3] = v.w;
+          if (shared_a && arow < nrow_b) *(uint4 *)(sb + sw_off((int)arow, 16 * u, (int)rows_b)) = v;
+        }
+      }
+      tmem_st32(ta, e);
+      const uint32_t brow = shared_a ? arow + UM : arow;  // slot 1's B row
+      if (brow < nrow_b) {
+        uint32_t w[8];
+        row_chunk(c1s, k, w);
+#pragma unroll
+        for (int u = 0; u < 8; u++) *(uint4 *)(sb + sw_off((int)brow, 16 * u, (int)rows_b)) = nib32(w[u]);
+      }
+      cp_async_commit();  // the next visit's row data
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) ubar_arrive(&full[grp]);
+    }
+    cp_async_wait_all();
+  }
+  ubar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {  // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3, colh = warp >> 2;
+    if (warp < 8) {
+      const uint32_t u = r0 + 32 * quarter + lane;
+      const uint32_t bu = u < m ? item_bm[s0 + u] : 0;
+      for (uint32_t cb = 128 * colh; cb < 128 * colh + 128 && cb < nb; cb += 32) {
+        uint32_t v[32];
+        const uint32_t tadr = tmem + ((uint32_t)(32 * quarter) << 16) + cb;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(tadr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (u < m) {
+#pragma unroll
+          for (int j = 0; j < 32; j++) {
+            const uint32_t vc = c0 + cb + j;
+            const uint32_t cnt = (uint32_t)__uint_as_float(v[j]);
             if (cnt && vc < m && u < vc) {
               const uint32_t bv = item_bm[s0 + vc];
               const uint32_t lo = min(bu, bv), hi = max(bu, bv);
@@ -1138,6 +1486,16 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   const bool use_umma = !(uv && *uv == '0');
   const char *mv = getenv("RS_ALLPAIRS_UMMA_MIN");
   const uint32_t umma_min = mv && *mv ? (uint32_t)atoi(mv) : 48;
+  // RS_ALLPAIRS_DIRECT=1: the tensor-core tiles build their rows from the
+  // containers (k_allpairs_umma_direct, no densified copy).  Measured 3.3 ms
+  // against 0.44 ms for the TMA-fed tiles on config 5: the producers become
+  // instruction-bound (~1,360 warp instructions per visit against a ~1,300-
+  // cycle budget per visit; each lane walks its row's array values one by
+  // one with divergent, select-heavy bit setting), so the densify + TMA path
+  // stays the default.
+  const char *dv = getenv("RS_ALLPAIRS_DIRECT");
+  const bool direct = use_umma && dv && *dv == '1';
+  std::vector<uint32_t> dlist;  // direct: the items the CUDA-core tiles read
   std::vector<uint32_t> hseg(g.G + 1);
   RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
   std::vector<uint32_t> tseg, useg;
@@ -1147,6 +1505,7 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
     const uint32_t nt = (m + tile - 1) / tile;
     for (uint32_t a = first; a < nt; a++)
       for (uint32_t b2 = a; b2 < nt; b2++) { tseg.push_back((uint32_t)s); ti.push_back(a); tj.push_back(b2); }
+    for (uint32_t r = first * tile; direct && r < m; r++) dlist.push_back(hseg[s] + r);
   };
   auto umma_tile = [&](uint64_t s, uint32_t r0, uint32_t c0, uint32_t nb) {
     useg.push_back((uint32_t)s); ur0.push_back(r0); uc0.push_back(c0); unb.push_back((nb + 15) & ~15u);
@@ -1168,6 +1527,11 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
     }
   }
   uint64_t ntp = tseg.size(), nup = useg.size();
+  const uint64_t nd = direct ? dlist.size() : g.T;  // rows to densify
+  uint32_t *d_dlist = direct ? (uint32_t *)dalloc((nd + 1) * 4) : nullptr;
+  ushort4 *d_Q = direct ? (ushort4 *)dalloc((g.T + 1) * 8) : nullptr;
+  if (direct && (!d_dlist || !d_Q)) { set_error("device allocation failed (all pairs)"); return RS_ENOMEM; }
+  if (direct && nd) RS_TRY(h2d(d_dlist, dlist.data(), nd * 4));
   uint64_t *D = (uint64_t *)dalloc((g.T ? g.T : 1) * 8192);
   uint32_t *item_bm = (uint32_t *)dalloc((g.T + 1) * 4), *d_tseg = (uint32_t *)dalloc((ntp + 1) * 4);
   uint16_t *d_ti = (uint16_t *)dalloc((ntp + 1) * 2), *d_tj = (uint16_t *)dalloc((ntp + 1) * 2);
@@ -1191,20 +1555,30 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
   RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
   trace("allpairs: uploads + memset + item_bm");
-  if (env_flag_("RS_DENSIFY_CTA")) {  // the CTA-per-row kernel (A/B only)
+  if (direct) RS_LAUNCH(k_quarter_index, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->dev(), d_Q);
+  if (env_flag_("RS_DENSIFY_CTA") && !direct) {  // the CTA-per-row kernel (A/B only)
     RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
   } else {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t g_need = (g.T + DW_WARPS - 1) / DW_WARPS;
+    const uint64_t g_need = (nd + DW_WARPS - 1) / DW_WARPS;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g_need, (uint64_t)sms * 6));
-    RS_LAUNCH_PROF("densify", g.T, k_densify_warp, grid, 32 * DW_WARPS, 0, g.T, g.item_c, in->dev(), D);
+    RS_LAUNCH_PROF("densify", nd, k_densify_warp, grid, 32 * DW_WARPS, 0, nd, g.item_c, in->dev(), D, d_dlist);
   }
   trace("allpairs: densify");
   // (running the tensor-core and CUDA-core tiles concurrently on side streams
   // measured no faster: 1.078 vs 1.087 ms, the umma tiles slowing 0.44 -> 0.50)
-  if (nup) {
+  if (nup && direct) {
+    static bool attr_d = false;
+    if (!attr_d) {
+      RS_CK(cudaFuncSetAttribute(k_allpairs_umma_direct, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)rsu::USMEM));
+      attr_d = true;
+    }
+    RS_LAUNCH_PROF("allpairs_umma", nup, k_allpairs_umma_direct, (unsigned)nup, rsu::UTHREADS, rsu::USMEM, d_useg,
+                   d_ur0, d_uc0, d_unb, g.seg_start, g.item_c, in->dev(), d_Q, item_bm, N, Mx);
+  } else if (nup) {
     static bool attr = false;
     if (!attr) {
       RS_CK(cudaFuncSetAttribute(k_allpairs_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsu::USMEM));
@@ -1242,6 +1616,7 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   if (uni) RS_CK(cudaMemcpyAsync(uni, d_uni, npairs * 8, cudaMemcpyDeviceToHost, g_stream));
   RS_TRY(d2h(inter, d_inter, npairs * 8));  // one synchronization for both
   trace("allpairs: readback");
+  dfree(d_dlist); dfree(d_Q);
   dfree(D); dfree(item_bm); dfree(d_tseg); dfree(d_ti); dfree(d_tj); dfree(Mx); dfree(d_inter); dfree(d_uni);
   dfree(d_useg); dfree(d_ur0); dfree(d_uc0); dfree(d_unb);
   g.release();

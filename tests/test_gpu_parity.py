@@ -523,3 +523,29 @@ def test_device_content_digests_match_oracle(pkg):
         rbuf = np.frombuffer(b"".join(rw), np.uint8)
         roffs = np.concatenate([[0], np.cumsum([len(w) for w in rw])]).astype(np.uint64)
         assert np.array_equal(R.digests(), orc.digest_images(rbuf, roffs)), op
+
+
+def test_all_pairs_direct_rows_variant(pkg, monkeypatch):
+    """The experimental direct-row tensor-core tiles (RS_ALLPAIRS_DIRECT=1:
+    rows built from the containers -- bitsets, arrays, runs -- inside the
+    tile kernel) give the oracle's counts, incl. a 300-container key (block
+    tiles with a separate A operand)."""
+    rng = np.random.default_rng(78)
+    imgs = []
+    for i in range(300):
+        kind = i % 3
+        if kind == 0:
+            v = rng.choice(65536, int(rng.integers(1, 4000)), replace=False)
+        elif kind == 1:
+            v = np.nonzero(rng.random(65536) < rng.uniform(0.1, 0.9))[0]
+        else:
+            s0 = int(rng.integers(0, 60000))
+            v = np.arange(s0, s0 + int(rng.integers(1, 5000)))
+        w = orc.from_values(np.asarray(v).astype(np.uint64))
+        imgs.append(orc.run_optimize(w)[0] if i % 4 == 0 else w)
+    offs = np.zeros(len(imgs) + 1, dtype=np.uint64)
+    offs[1:] = np.cumsum([len(x) for x in imgs])
+    buf = np.frombuffer(b"".join(imgs), dtype=np.uint8)
+    monkeypatch.setenv("RS_ALLPAIRS_DIRECT", "1")
+    monkeypatch.setenv("RS_ALLPAIRS_UMMA_MIN", "2")
+    _all_pairs_check(pkg, buf, offs)
