@@ -923,12 +923,6 @@ __device__ __forceinline__ void set_chunk_range(uint32_t (&w)[8], uint32_t a, ui
   }
 }
 
-__device__ __forceinline__ uint4 ld_nc16(uint64_t addr) {
-  uint4 v;
-  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(addr));
-  return v;
-}
-
 // Asynchronous 16-byte global -> shared copies (LDGSTS): the row data a
 // producer needs at its NEXT visit lands in its shared slot while the tile's
 // other chunks are multiplied; a register prefetch would be waited for as
