@@ -24,7 +24,7 @@ __device__ __forceinline__ uint64_t bitmap_of(const uint64_t *__restrict__ bm_st
 __global__ void k_wire_psize(uint64_t nc, DevBatch B, uint64_t *__restrict__ psz) {
   uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (c > nc) return;
-  if (c == nc) { psz[c] = 0; return; }
+  if (c == nc || c >= B.bm_start[B.nb]) { psz[c] = 0; return; }  // (nc may be a capacity)
   uint8_t t = B.type[c];
   uint32_t n = B.n[c];
   psz[c] = t == RS_TAG_ARRAY ? 2ull * n : t == RS_TAG_BITSET ? 8192ull : 2ull + 4ull * n;
@@ -71,7 +71,9 @@ __global__ void k_wire_containers(uint64_t nc, uint64_t nb, DevBatch B, const ui
                                   const uint64_t *__restrict__ imgoff, uint8_t *__restrict__ out) {
   uint64_t c = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
-  if (c >= nc) return;
+  // nc may be a result's entry capacity (no host read-back of its container
+  // count): entries past bm_start[nb] are not containers
+  if (c >= nc || c >= B.bm_start[nb]) return;
   uint64_t i = bitmap_of(B.bm_start, nb, c);
   uint64_t first = B.bm_start[i], n_i = B.bm_start[i + 1] - first;
   uint8_t t = B.type[c];
@@ -279,8 +281,10 @@ extern "C" int rs_batch_to_wire_async(const rs_batch *b, uint8_t *buf, uint64_t 
   RS_TRY(ensure_device());
   if (!b || !offs || !done) { set_error("null batch/offs/done"); return RS_EARG; }
   *done = nullptr;
-  RS_TRY(fetch_host_meta_nopack(b));
-  RS_TRY(resolve_pending(b));
+  // no read-back of the container count: the kernels bound themselves by the
+  // device's bm_start, so the image sizes are the call's only synchronization
+  RS_TRY(materialize(b));
+  if (b->pending) RS_TRY(resolve_pending(b));
   int dev = 0;
   RS_CK(cudaGetDevice(&dev));
   if (!g_export || g_export_dev != dev) {

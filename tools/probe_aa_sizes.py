@@ -18,7 +18,10 @@ def images(rng, npairs, n):
 
 
 rng = np.random.default_rng(1)
-for n, npairs in ((300, 200000), (1000, 60000), (4096, 15000)):
+SIZES = ((300, 200000), (1000, 60000), (4096, 15000))
+if len(sys.argv) > 1:
+    SIZES = [SIZES[int(a)] for a in sys.argv[1].split(",")]
+for n, npairs in SIZES:
     A = rb.BitmapBatch.from_wire(images(rng, npairs, n))
     B = rb.BitmapBatch.from_wire(images(rng, npairs, n))
     dev = torch.empty(npairs, dtype=torch.int64, device="cuda")
