@@ -79,3 +79,22 @@ def test_key_range_selecting_nothing(rb):
     assert R.key_range(0, 65536).to_wire_list() == [EMPTY, EMPTY]
     with pytest.raises(ValueError):
         B.key_range(5, 2)
+
+
+def test_union_many_with_many_contributors_per_key(rb):
+    """Keys with more contributors than one metadata window of the union
+    kernels: 300 bitmaps sharing key 0 as arrays / runs only (the fold, past
+    its 256-contributor window) and key 1 with bitsets among them (the
+    order-free OR, several 64-contributor windows)."""
+    rng = np.random.default_rng(21)
+    imgs = []
+    for i in range(300):
+        k0 = np.unique(rng.integers(0, 65536, int(rng.integers(1, 300))))
+        if i % 3 == 0:
+            s = int(rng.integers(0, 60000))
+            k0 = np.arange(s, s + int(rng.integers(50, 3000)))  # run-like
+        k1 = np.nonzero(rng.random(65536) < 0.2)[0] if i % 7 == 0 else np.unique(rng.integers(0, 65536, 500))
+        w = orc.from_values(np.concatenate([k0, 65536 + k1]).astype(np.uint64))
+        imgs.append(orc.run_optimize(w)[0] if i % 2 == 0 else w)
+    B = rb.BitmapBatch.from_wire(imgs)
+    assert B.union_many().to_wire_list()[0] == orc.union_many(imgs)
