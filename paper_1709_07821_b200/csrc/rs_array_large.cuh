@@ -6,32 +6,50 @@
 //   and / andnot  one bitset X built from the smaller side (and) or from B
 //                 (andnot); the other side is filtered through it with warp
 //                 ballots, so the result comes out sorted;
-//   or / xor      both sides scattered into XA (shared OR, resp. XOR); the
-//                 result words with a popcount scan give the cardinality, and the result is the
-//                 words themselves (> 4096 values: a bitset container) or
-//                 their set bits in order (<= 4096: an array container).
-// AND / ANDNOT with one side at most 1/16 of the other skip the bitset and
-// binary-search the larger array (array_intersect_galloping's case,
-// kernels/scalar.py:149-176).
+//   or / xor      both sides scattered into X (shared OR, resp. XOR); the
+//                 result words with a popcount scan give the cardinality, and
+//                 the result is the words themselves (> 4096 values: a bitset
+//                 container) or their set bits in order (<= 4096: an array
+//                 container).
+// AND / ANDNOT pairs with one side at most 1/16 of the other never get here:
+// the classifier sends them to the galloping kernel (gallop_pair).
 //
-// CTA layout (warp-specialized): warps 0-7 are consumers (256 threads, one
-// pair at a time, synchronizing only among themselves with named barrier 1);
-// warp 8 is the producer.  The producer walks the CTA's items, loads each
-// item's metadata (operand offsets, sizes, output slot, pair) and streams both
-// arrays (variable sizes, 16-byte padded) into a byte ring in shared memory
-// with cp.async.bulk completing on the item slot's `full` mbarrier.  Items
-// take only the bytes they need (a ~12 KB average item leaves room for two
-// more in flight behind it), and consumers hand an item's bytes back through
-// the slot's `empty` mbarrier as soon as its last value has been read.
+// CTA layout (warp-specialized): warps 0-7 are consumers, split into NGRP
+// groups of 256 / NGRP threads; each group works on its own pair with its own
+// bitset (XA / XB) and synchronizes only among itself with named barrier
+// 1 + group.  Warp 8 is the producer.  The producer walks the CTA's items,
+// loads each item's metadata (operand offsets, sizes, output slot, pair) and
+// streams both arrays (variable sizes, 16-byte padded) into a byte ring in
+// shared memory with cp.async.bulk completing on the item slot's `full`
+// mbarrier; group g consumes items g, g + NGRP, ...  Items take only the bytes
+// they need, and a group hands an item's bytes back through the slot's
+// `empty` mbarrier as soon as its last value has been read.
+//
+// Two groups of four warps (the default) against one group of eight: a pair's
+// fixed work -- metadata, barriers, loop set-up, scan -- is per warp, and most
+// large pairs hold a few hundred values, so eight warps per pair left most
+// lanes idle; two pairs in flight per CTA halve that overhead per pair.
 #pragma once
 #include "rs_internal.cuh"
 #include "rs_bitset.cuh"
 
 namespace rsl {
 
-constexpr int LT = 256;               // consumer threads
-constexpr int LTHREADS = LT + 32;     // + one producer warp
-constexpr int NSLOT = 8;              // items in flight (metadata + barrier slots)
+#ifndef RS_AAL_GROUPS
+#define RS_AAL_GROUPS 2
+#endif
+constexpr int NGRP = RS_AAL_GROUPS;     // consumer groups (1 or 2)
+constexpr int NCONS = 256;              // consumer threads
+constexpr int LT = NCONS / NGRP;        // threads per group (one pair at a time)
+constexpr int WG = LT / 32;             // warps per group
+constexpr int QW = RS_WORDS / LT;       // 64-bit result words per thread (or / xor)
+constexpr int NROW = QW / 2;            // packed 16-bit scan rows (two words each)
+constexpr int LTHREADS = NCONS + 32;    // + one producer warp
+#ifndef RS_AAL_MAXR
+#define RS_AAL_MAXR 8
+#endif
+constexpr int NSLOT = 8;                // items in flight (metadata + barrier slots)
+static_assert(NGRP == 1 || NGRP == 2, "one or two consumer groups");
 
 struct LargeMeta {
   uint32_t na, nb, e, pair;
@@ -48,7 +66,7 @@ struct LargeHdr {
   uint64_t empty[NSLOT];
   LargeMeta meta[NSLOT];
   uint32_t span[NSLOT];  // producer only: ring bytes each item holds (incl. the wrap skip)
-  uint32_t red[2][2][LT / 32];
+  uint32_t red[NGRP][2][NROW][WG];  // per group, double-buffered scan scratch
 };
 
 struct LargeSmem {
@@ -60,20 +78,27 @@ struct LargeSmem {
   __device__ __forceinline__ uint8_t *R() const { return X + 16384; }
 };
 
-// 44 KB: five CTAs per SM (5 x (44 + 1 reserved) KB <= 228 KB; the kernels
-// are capped at 5 x 288 threads' worth of registers).  The header and the pad
-// to the first 8 KB boundary take at most ~8.5 KB, XA / XB 16 KB, and the
-// ring the rest (>= 19 KB); large_loop traps if it is ever under 16 KB, the
-// largest item (an item that does not fit before the end of the ring waits
-// for the ring to drain and starts at 0).  Four CTAs of 56 KB with a 33 KB
-// ring measured slower: the kernel is issue / barrier bound, so a fifth CTA's
-// warps hide more of the per-pair barriers than the deeper ring hid latency.
+// 56 KB: four CTAs per SM.  The header and the pad to the first 8 KB boundary
+// take at most ~8.5 KB, XA / XB 16 KB, and the ring the rest (>= 31 KB);
+// large_loop traps if it is ever under 16 KB, the largest item (an item that
+// does not fit before the end of the ring waits for the ring to drain and
+// starts at 0).  A fifth CTA (44 KB) measured slower.
 #ifndef RS_AAL_SMEM_KB
 #define RS_AAL_SMEM_KB 56
 #endif
-#ifndef RS_AAL_MINB
-#define RS_AAL_MINB 4
+// Register budget: the AND / ANDNOT op kernels (probe rounds whose kept
+// values are written out) run three CTAs per SM with up to 72 registers --
+// at four CTAs' 56 they spill ~120 bytes per thread, and measured 1.65 /
+// 2.14 ms against 1.39 / 1.97 ms on config 3; OR / XOR and the counts keep
+// four CTAs (1.74 / 1.10 ms against 1.85 / 1.15 ms at three).
+// RS_AAL_MINB overrides both (tuning).
+constexpr int large_min_blocks(int op) {
+#ifdef RS_AAL_MINB
+  return RS_AAL_MINB + 0 * op;
+#else
+  return op == RS_OP_AND || op == RS_OP_ANDNOT ? 3 : 4;
 #endif
+}
 constexpr size_t LARGE_SMEM_BYTES = RS_AAL_SMEM_KB * 1024;
 
 __device__ __forceinline__ LargeSmem large_layout(uint8_t *raw) {
@@ -87,7 +112,12 @@ __device__ __forceinline__ LargeSmem large_layout(uint8_t *raw) {
   return sm;
 }
 
-__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(LT) : "memory"); }
+// group barrier (named barrier 1 + g, the group's threads only)
+// (immediate ids: a register id makes ptxas reserve all 16 barriers)
+__device__ __forceinline__ void gbar(int g) {
+  if (NGRP == 1 || g == 0) asm volatile("bar.sync 1, %0;" ::"n"(LT) : "memory");
+  else asm volatile("bar.sync 2, %0;" ::"n"(LT) : "memory");
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rsb::smem_u32(bar)) : "memory");
@@ -107,48 +137,41 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t phase)
       : "memory");
 }
 
-// consumer-only exclusive scan with total (one named barrier); the scratch is
-// double-buffered by item parity so no trailing barrier is needed
-__device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t (*red2)[LT / 32], uint32_t &total) {
-  uint32_t *red = red2[0];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x = v;
+// Group-wide exclusive scan of N packed vectors (16-bit fields): exclusive
+// prefixes e[] and totals T[] (one group barrier).
+template <int N>
+__device__ __forceinline__ void gscan(const uint32_t (&v)[N], uint32_t (*red)[WG], int g, int t, uint32_t (&e)[N],
+                                      uint32_t (&T)[N]) {
+  const int lane = t & 31, w = t >> 5;
+  uint32_t x[N];
+#pragma unroll
+  for (int j = 0; j < N; j++) x[j] = v[j];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) red[w] = x;
-  cbar();
-  uint32_t pre = 0, tot = 0;
 #pragma unroll
-  for (int k = 0; k < LT / 32; k++) {
-    const uint32_t s = red[k];
-    pre += k < w ? s : 0;
-    tot += s;
+    for (int j = 0; j < N; j++) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x[j], o);
+      if (lane >= o) x[j] += y;
+    }
   }
-  total = tot;
-  return pre + x - v;
-}
-
-// cscan over two packed vectors (16-bit fields): exclusive prefix and totals
-__device__ __forceinline__ void cscan2(uint32_t v0, uint32_t v1, uint32_t (*red)[LT / 32], uint32_t &e0,
-                                       uint32_t &e1, uint32_t &T0, uint32_t &T1) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  uint32_t x0 = v0, x1 = v1;
+  if (lane == 31) {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
-    if (lane >= o) { x0 += y0; x1 += y1; }
+    for (int j = 0; j < N; j++) red[j][w] = x[j];
   }
-  if (lane == 31) { red[0][w] = x0; red[1][w] = x1; }
-  cbar();
-  e0 = x0 - v0; e1 = x1 - v1; T0 = 0; T1 = 0;
+  gbar(g);
 #pragma unroll
-  for (int k = 0; k < LT / 32; k++) {
-    const uint32_t a = red[0][k], b = red[1][k];
-    T0 += a; T1 += b;
-    if (k < w) { e0 += a; e1 += b; }
+  for (int j = 0; j < N; j++) {
+    e[j] = x[j] - v[j];
+    T[j] = 0;
+  }
+#pragma unroll
+  for (int k = 0; k < WG; k++) {
+#pragma unroll
+    for (int j = 0; j < N; j++) {
+      const uint32_t a = red[j][k];
+      T[j] += a;
+      if (k < w) e[j] += a;
+    }
   }
 }
 
@@ -181,11 +204,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 // (a value of both sides toggles twice; two values of one side sharing a word
 // have distinct bits, so their combined mask is the same either way).
 template <bool XOR = false>
-__device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t X) {
+__device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t X, int t) {
   const uint32_t *w = (const uint32_t *)v;
   const uint32_t nw = n >> 1;
 #pragma unroll 4
-  for (uint32_t i = threadIdx.x; i < nw; i += LT) {
+  for (uint32_t i = t; i < nw; i += LT) {
     const uint32_t x = w[i];
     const uint32_t alo = X | ((x >> 3) & 0x1FFCu), ahi = X | ((x >> 19) & 0x1FFCu);
     const uint32_t blo = __funnelshift_l(0u, 1u, x), bhi = __funnelshift_l(0u, 1u, x >> 16);
@@ -193,47 +216,43 @@ __device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t 
     red_set<XOR>(alo, same ? blo | bhi : blo);
     if (!same) red_set<XOR>(ahi, bhi);
   }
-  if ((n & 1) && threadIdx.x == LT - 1) {
+  if ((n & 1) && t == LT - 1) {
     const uint32_t x = v[n - 1];
     red_set<XOR>(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
   }
 }
 
-// Keep the values of P (np, sorted) whose bit in X equals WANT, in order:
-// warp w probes a contiguous run of P (NR rounds of 32 value pairs), the kept
-// flags become ballots, a CTA scan of the warp totals places each run, and
-// the kept values go straight to dst with 16-bit stores (consecutive lanes
-// write consecutive values).  Returns the kept count on every consumer.  NR
-// (<= 8) is a template parameter -- probe_filter dispatches on it once per
-// pair -- so the rounds are straight-line code (guarded rounds cost ~90
-// instructions per warp per pair in branches alone); the reads are clamped
-// into P, so lanes past the end only drop out of the ballots.
+// One chunk of probe_filter: value pairs [c2, c2 + WG * NR * 32) of P, warp w
+// a contiguous run of NR rounds of 32 value pairs.  The kept flags become
+// ballots, a group scan of the warp totals places each run after the `out`
+// values kept by earlier chunks, and the kept values go straight to dst with
+// 16-bit stores (consecutive lanes write consecutive values).  NR is a
+// template parameter so the rounds are straight-line code (guarded rounds
+// cost ~90 instructions per warp per pair in branches alone); the reads are
+// clamped into P, so lanes past the end only drop out of the ballots.
 template <uint32_t WANT, int NR>
-__device__ __forceinline__ uint32_t probe_filter_n(const uint16_t *P, uint32_t np, uint32_t X, uint16_t *dst,
-                                                   uint32_t (*red2)[LT / 32], uint64_t *release) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t *P32 = (const uint32_t *)P;
+__device__ __forceinline__ uint32_t probe_chunk(const uint32_t *P32, uint32_t np, uint32_t c2, uint32_t X,
+                                                uint16_t *dst, uint32_t out, uint32_t *red, int g, int t,
+                                                uint64_t *release) {
+  const int lane = t & 31, w = t >> 5;
   const uint32_t np2 = (np + 1) >> 1;
-  const uint32_t beg = w * NR * 32u + lane, last = np2 - 1;
-  uint32_t BL[NR], BH[NR], XV[NR], tot = 0;
+  const uint32_t beg = c2 + w * NR * 32u + lane, last = np2 ? np2 - 1 : 0;
+  uint32_t BL[NR], BH[NR], tot = 0;
 #pragma unroll
   for (int r = 0; r < NR; r++) {
     const uint32_t i = beg + 32u * r;
     const uint32_t x = P32[min(i, last)];
-    XV[r] = x;
     const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
     const uint32_t bl = __funnelshift_r(wl, 0u, x) & 1u, bh = __funnelshift_r(wh, 0u, x >> 16) & 1u;
     BL[r] = __ballot_sync(0xffffffffu, (bl == WANT) & (i < np2));
     BH[r] = __ballot_sync(0xffffffffu, (bh == WANT) & (2 * i + 1 < np));
     tot += __popc(BL[r]) + __popc(BH[r]);
   }
-  uint32_t *red = red2[0];
   if (lane == 0) red[w] = tot;
-  cbar();
-  if (threadIdx.x == 0) mbar_arrive(release);  // P's values are in registers
-  uint32_t base = 0, total = 0;
+  gbar(g);
+  uint32_t base = out, total = 0;
 #pragma unroll
-  for (int k = 0; k < LT / 32; k++) {
+  for (int k = 0; k < WG; k++) {
     const uint32_t s = red[k];
     base += k < w ? s : 0;
     total += s;
@@ -244,133 +263,134 @@ __device__ __forceinline__ uint32_t probe_filter_n(const uint16_t *P, uint32_t n
     for (int r = 0; r < NR; r++) {
       const uint32_t bl = BL[r], bh = BH[r];
       const uint32_t klo = (bl >> lane) & 1u, khi = (bh >> lane) & 1u;
-      const uint32_t x = XV[r];
+      const uint32_t x = P32[min(beg + 32u * r, last)];  // re-read: fewer live registers
       const uint32_t pos = base + __popc(bl & lt) + __popc(bh & lt);
       if (klo) dst[pos] = (uint16_t)x;
       if (khi) dst[pos + klo] = (uint16_t)(x >> 16);
       base += __popc(bl) + __popc(bh);
     }
-    const uint32_t padded = (total + 7u) & ~7u;
-    if (threadIdx.x < 8 && total + threadIdx.x < padded) dst[total + threadIdx.x] = 0;
   }
+  if (release) mbar_arrive(release);  // this thread's last read of P (the slot counts LT arrivals)
   return total;
 }
 
+// Keep the values of P (np >= 1, sorted) whose bit in X equals WANT, in order,
+// in chunks of at most 8 rounds per warp (one chunk with eight warps per
+// group; two for np > 2048 with four).  Chunks alternate the two scratch rows
+// starting at `parity`, so a chunk never overwrites a total another thread of
+// the group may still be reading.  Each thread arrives on `release` after its
+// last read of P (in the last chunk).  Returns the kept count on every thread of the group.
 template <uint32_t WANT>
 __device__ __forceinline__ uint32_t probe_filter(const uint16_t *P, uint32_t np, uint32_t X, uint16_t *dst,
-                                                 uint32_t (*red2)[LT / 32], uint64_t *release) {
-  switch ((((np + 1) >> 1) + 255) >> 8) {  // rounds of 32 value pairs per warp (np >= 1)
-    case 1: return probe_filter_n<WANT, 1>(P, np, X, dst, red2, release);
-    case 2: return probe_filter_n<WANT, 2>(P, np, X, dst, red2, release);
-    case 3: return probe_filter_n<WANT, 3>(P, np, X, dst, red2, release);
-    case 4: return probe_filter_n<WANT, 4>(P, np, X, dst, red2, release);
-    case 5: return probe_filter_n<WANT, 5>(P, np, X, dst, red2, release);
-    case 6: return probe_filter_n<WANT, 6>(P, np, X, dst, red2, release);
-    case 7: return probe_filter_n<WANT, 7>(P, np, X, dst, red2, release);
-    default: return probe_filter_n<WANT, 8>(P, np, X, dst, red2, release);
+                                                 uint32_t (*red2)[NROW][WG], int parity, int g, int t,
+                                                 uint64_t *release) {
+  const uint32_t *P32 = (const uint32_t *)P;
+  constexpr uint32_t PER_ROUND = WG * 32u;  // value pairs per round over the group
+  constexpr uint32_t MAXR = RS_AAL_MAXR;
+  uint32_t rounds = (((np + 1) >> 1) + PER_ROUND - 1) / PER_ROUND;
+  if (rounds == 0) rounds = 1;
+  uint32_t out = 0, c2 = 0;
+  int buf = parity;
+  for (;;) {
+    const bool lastc = rounds <= MAXR;
+    uint32_t *red = red2[buf][0];
+    uint64_t *rel = lastc ? release : nullptr;
+    uint32_t got;
+    switch (lastc ? rounds : (uint32_t)MAXR) {
+      case 1: got = probe_chunk<WANT, 1>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      case 2: got = probe_chunk<WANT, 2>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      case 3: got = probe_chunk<WANT, 3>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      case 4: got = probe_chunk<WANT, 4>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      case 5: got = probe_chunk<WANT, 5>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      case 6: got = probe_chunk<WANT, 6>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      case 7: got = probe_chunk<WANT, 7>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+      default: got = probe_chunk<WANT, 8>(P32, np, c2, X, dst, out, red, g, t, rel); break;
+    }
+    out += got;
+    if (lastc) break;
+    rounds -= MAXR;
+    c2 += MAXR * PER_ROUND;
+    buf ^= 1;
   }
+  if (dst && out) {
+    const uint32_t padded = (out + 7u) & ~7u;
+    if (t < 8 && out + t < padded) dst[out + t] = 0;
+  }
+  return out;
 }
 
 // Copy `total` staged u16 values to dst with 128-bit stores (16-byte zero pad).
-__device__ __forceinline__ void flush_stage(uint16_t *stage, uint32_t total, uint8_t *dst) {
-  const int t = threadIdx.x;
+__device__ __forceinline__ void flush_stage(uint16_t *stage, uint32_t total, uint8_t *dst, int g, int t) {
   const uint32_t nvec = (2 * total + 15) >> 4;
   if (t < 8 && total + t < nvec * 8) stage[total + t] = 0;
-  cbar();
+  gbar(g);
   for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)stage)[v];
 }
 
-// Sorted-array membership: is x in v[0, n)?  (n <= 4096: 12 probes)
-__device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_t x) {
-  uint32_t lo = 0, len = n;
-  while (len > 1) {
-    const uint32_t half = len >> 1;
-    if (v[lo + half] <= x) lo += half;
-    len -= half;
-  }
-  return n && v[lo] == x;
-}
-
-// One pair (consumers only).  `release` (the item's ring slot) is arrived on
-// exactly once, after the barrier that follows the last read of the staged
-// values.
-//   and / andnot: X (XA / XB alternate by pair parity) is cleared after the
-//     scan barrier; the next pair uses the other one.
-//   or / xor: XA only; each thread reads and clears the words it owns
-//     (t + 256q) before the scan barrier, which every consumer passes before
-//     the next pair's scatter; array results are staged in XA (re-zeroed
-//     behind a barrier).
+// One pair (the group's threads only; t = thread within the group).
+// `release` (the item's ring slot) is arrived on once by every thread of the
+// group, after that thread's last read of the staged values (a slot's items
+// always go to the same group: k % NSLOT fixes k % NGRP).
+//   and / andnot: two groups: the group's own bitset, cleared after the probe
+//     and fenced by a barrier at the start of the group's next pair; one
+//     group: XA / XB alternate by pair parity, so no fence is needed.
+//   or / xor: the group's bitset (XA with one group); each thread reads and
+//     clears the words it owns (t + LT q) before the cardinality barrier,
+//     which every thread of the group passes before its next scatter; array
+//     results are staged in the same bitset (re-zeroed behind a barrier).
 template <int op>
-__device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, const uint16_t *A, uint32_t na, const uint16_t *B,
-                               uint32_t nb, uint8_t *dst, int parity, uint8_t &type, uint32_t &nout,
-                               uint64_t *release) {
-  const int t = threadIdx.x;
+__device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t, const uint16_t *A, uint32_t na,
+                                               const uint16_t *B, uint32_t nb, uint8_t *dst, int parity,
+                                               uint8_t &type, uint32_t &nout, uint64_t *release) {
   uint32_t *XA = sm.XA(), *XB = sm.XB();
+  uint32_t(*red2)[NROW][WG] = sm.h->red[g];
   type = RS_TAG_ARRAY;
   if constexpr (op == RS_OP_AND || op == RS_OP_ANDNOT) {
     constexpr bool is_and = op == RS_OP_AND;
-    const bool a_small = is_and ? na <= nb : true;
-    const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
-    if (16 * ns <= nl) {
-      const uint16_t *S = a_small ? A : B, *L = a_small ? B : A;
-      uint32_t v = 0, keep = 0;
-      if ((uint32_t)t < ns) {
-        v = S[t];
-        keep = bsearch16(L, nl, v) == is_and;
-      }
-      uint32_t total;
-      const uint32_t base = cscan(keep, sm.h->red[parity], total);
-      if (t == 0) mbar_arrive(release);
-      nout = total;
-      if (dst && total) {
-        uint16_t *d = (uint16_t *)dst;
-        if (keep) d[base] = (uint16_t)v;
-        const uint32_t padded = (total + 7u) & ~7u;
-        if (t < 8 && total + t < padded) d[total + t] = 0;
-      }
-      return total;
-    }
     // and: build the smaller side, filter the larger; andnot: build B, filter A
     const bool build_a = is_and && na <= nb;
-    uint32_t *X = parity ? XB : XA;
+    uint32_t *X = (NGRP == 2 ? g : parity) ? XB : XA;
+    if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
     const uint32_t xs = rsb::smem_u32(X);
-    scatter(build_a ? A : B, build_a ? na : nb, xs);
-    cbar();
+    scatter(build_a ? A : B, build_a ? na : nb, xs, t);
+    gbar(g);
     const uint32_t total = probe_filter<is_and ? 1u : 0u>(build_a ? B : A, build_a ? nb : na, xs, (uint16_t *)dst,
-                                                           sm.h->red[parity], release);
-    // every probe of X is done (scan barrier above): clear it for pair + 2
-    ((uint4 *)X)[t] = make_uint4(0, 0, 0, 0);
-    ((uint4 *)X)[t + LT] = make_uint4(0, 0, 0, 0);
+                                                           red2, parity, g, t, release);
+    // every probe of X is done (the last chunk's barrier above): clear it
+#pragma unroll
+    for (int q = 0; q < 512 / LT; q++) ((uint4 *)X)[t + LT * q] = make_uint4(0, 0, 0, 0);
     nout = total;
     return total;
   }
   // or / xor: both arrays into one bitset (shared OR / XOR), so the result
   // words are read (and cleared) once
   constexpr bool is_xor = op == RS_OP_XOR;
-  scatter<is_xor>(A, na, rsb::smem_u32(XA));
-  scatter<is_xor>(B, nb, rsb::smem_u32(XA));
-  cbar();
-  if (t == 0) mbar_arrive(release);
-  // result words t + 256q (conflict-free), positions by a packed row scan
-  uint64_t *XA64 = (uint64_t *)XA;
-  uint64_t r[4];
-  uint32_t pq[4];
+  uint32_t *X = (NGRP == 2 && g) ? XB : XA;
+  const uint32_t xs = rsb::smem_u32(X);
+  scatter<is_xor>(A, na, xs, t);
+  scatter<is_xor>(B, nb, xs, t);
+  gbar(g);
+  mbar_arrive(release);
+  // result words t + LT q (conflict-free), positions by a packed row scan
+  uint64_t *X64 = (uint64_t *)X;
+  uint64_t r[QW];
+  uint32_t psum = 0;
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
-    r[q] = XA64[t + LT * q];
-    XA64[t + LT * q] = 0;
-    pq[q] = __popcll(r[q]);
+  for (int q = 0; q < QW; q++) {
+    r[q] = X64[t + LT * q];
+    X64[t + LT * q] = 0;
+    psum += __popcll(r[q]);
   }
   // cardinality first (one warp reduction); the position scan only for an
   // array result
-  uint32_t *red = sm.h->red[parity][0];
+  uint32_t *red = red2[parity][0];
   const int lane = t & 31, w = t >> 5;
-  const uint32_t wsum = __reduce_add_sync(0xffffffffu, pq[0] + pq[1] + pq[2] + pq[3]);
+  const uint32_t wsum = __reduce_add_sync(0xffffffffu, psum);
   if (lane == 0) red[w] = wsum;
-  cbar();
+  gbar(g);
   uint32_t card = 0;
 #pragma unroll
-  for (int k = 0; k < LT / 32; k++) card += red[k];
+  for (int k = 0; k < WG; k++) card += red[k];
   if (!dst || card == 0) {
     nout = card;
     return card;
@@ -378,22 +398,27 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, const uint16
   if (card > RS_ARRAY_MAX) {
     uint64_t *p = (uint64_t *)dst + t;
 #pragma unroll
-    for (int q = 0; q < 4; q++) asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p + LT * q), "l"(r[q]) : "memory");
+    for (int q = 0; q < QW; q++) asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p + LT * q), "l"(r[q]) : "memory");
     type = RS_TAG_BITSET;
     nout = RS_WORDS;
     return card;
   }
-  const uint32_t pk0 = pq[0] | (pq[1] << 16), pk1 = pq[2] | (pq[3] << 16);
-  uint32_t e0, e1, T0, T1;
-  cscan2(pk0, pk1, sm.h->red[parity ^ 1], e0, e1, T0, T1);
-  const uint32_t r0 = T0 & 0xFFFFu, r1 = T0 >> 16, r2 = T1 & 0xFFFFu;
-  uint16_t *stage = (uint16_t *)XA;
-  const uint32_t end[4] = {(e0 & 0xFFFFu) + pq[0], r0 + (e0 >> 16) + pq[1], r0 + r1 + (e1 & 0xFFFFu) + pq[2],
-                           r0 + r1 + r2 + (e1 >> 16) + pq[3]};
+  // word t + LT q's values end at (values of rows < q) + (row q's prefix
+  // before t) + its own count; rows are scanned two per packed vector
+  uint32_t pk[NROW], e[NROW], T[NROW];
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
+  for (int j = 0; j < NROW; j++) pk[j] = __popcll(r[2 * j]) | (__popcll(r[2 * j + 1]) << 16);
+  gscan<NROW>(pk, red2[parity ^ 1], g, t, e, T);
+  uint16_t *stage = (uint16_t *)X;
+  uint32_t rowbase = 0;
+#pragma unroll
+  for (int q = 0; q < QW; q++) {
+    const int j = q >> 1;
+    const uint32_t ex = (q & 1) ? e[j] >> 16 : e[j] & 0xFFFFu;
+    const uint32_t tot = (q & 1) ? T[j] >> 16 : T[j] & 0xFFFFu;
     const uint32_t pos = (uint32_t)(t + LT * q) * 64;
-    uint32_t b = end[q], hi = (uint32_t)(r[q] >> 32), lo = (uint32_t)r[q];
+    uint32_t b = rowbase + ex + (uint32_t)__popcll(r[q]), hi = (uint32_t)(r[q] >> 32), lo = (uint32_t)r[q];
+    rowbase += tot;
     while (hi) {
       const uint32_t p = 31 - __clz(hi);
       stage[--b] = (uint16_t)(pos + 32 + p);
@@ -405,17 +430,17 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, const uint16
       lo ^= 1u << p;
     }
   }
-  flush_stage(stage, card, dst);
+  flush_stage(stage, card, dst, g, t);
   const uint32_t nvec = (2 * card + 15) >> 4;
   for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)stage)[v] = make_uint4(0, 0, 0, 0);
-  cbar();  // XA is zero again before any consumer's next scatter
+  gbar(g);  // X is zero again before the group's next scatter
   nout = card;
   return card;
 }
 
 // Persistent, warp-specialized byte ring over items i = blockIdx.x + k*gridDim.x.
 // meta_of(i, aoff, boff) -> LargeMeta (runs on the producer lane only);
-// sink(meta, card, type, n) runs on every consumer thread after the pair.
+// sink(meta, card, type, n) runs on thread 0 of the group that did the pair.
 template <int op, typename MetaOf, typename Sink>
 __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, const uint8_t *poolB,
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
@@ -425,14 +450,14 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
   if (t == 0) {
     for (int s = 0; s < NSLOT; s++) {
       rsb::mbar_init(&sm.h->full[s], 1);
-      rsb::mbar_init(&sm.h->empty[s], 1);
+      rsb::mbar_init(&sm.h->empty[s], LT);  // every thread of the consuming group arrives
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int w = t; w < 4 * RS_WORDS; w += LTHREADS) sm.XA()[w] = 0;  // XA and XB
   __syncthreads();
-  if (t >= LT) {  // ---------------- producer warp (one elected lane)
-    if (t == LT) {
+  if (t >= NCONS) {  // ---------------- producer warp (one elected lane)
+    if (t == NCONS) {
       uint64_t ao, bo;
       LargeMeta m;
       if (blockIdx.x < count) m = meta_of(blockIdx.x, ao, bo);
@@ -464,6 +489,8 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
           span = need;
           occ = 0;
         }
+        // Items are released out of order across groups; the producer waits
+        // in item order, which only ever delays a slot's reuse.
         while (j - oldest >= (uint32_t)NSLOT || occ + span > sm.ring) {
           mbar_wait_backoff(&sm.h->empty[oldest % NSLOT], (oldest / NSLOT) & 1);
           occ -= sm.h->span[oldest % NSLOT];
@@ -485,7 +512,8 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
     }
     return;
   }
-  for (uint32_t k = 0;; k++) {  // ---------------- consumers
+  const int g = t / LT, tg = t % LT;
+  for (uint32_t k = g;; k += NGRP) {  // ---------------- consumer group g
     const uint32_t i = blockIdx.x + k * gridDim.x;
     if (i >= count) break;
     const int s = k % NSLOT;
@@ -493,10 +521,10 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
     const LargeMeta m = sm.h->meta[s];
     uint8_t type;
     uint32_t n;
-    const uint32_t card = large_pair<op>(sm, (const uint16_t *)(sm.R() + m.aoff), m.na,
-                                     (const uint16_t *)(sm.R() + m.boff), m.nb, opool ? opool + m.dst : nullptr,
-                                     k & 1, type, n, &sm.h->empty[s]);
-    sink(m, card, type, n);
+    const uint32_t card = large_pair<op>(sm, g, tg, (const uint16_t *)(sm.R() + m.aoff), m.na,
+                                         (const uint16_t *)(sm.R() + m.boff), m.nb, opool ? opool + m.dst : nullptr,
+                                         (k / NGRP) & 1, type, n, &sm.h->empty[s]);
+    if (tg == 0) sink(m, card, type, n);
   }
 }
 

@@ -759,7 +759,7 @@ int launch_bb_count(int op, const Lists &L, uint32_t *lpair, DevBatch dA, DevBat
 // ------------------------------------ large array x array (smem bitset + TMA)
 
 template <int OP>
-__global__ void __launch_bounds__(rsl::LTHREADS, RS_AAL_MINB) k_aa_large_op(const uint32_t *__restrict__ list,
+__global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(OP)) k_aa_large_op(const uint32_t *__restrict__ list,
                                                                const uint64_t *__restrict__ laoff,
                                                                const uint64_t *__restrict__ lboff,
                                                                const uint32_t *__restrict__ lnab,
@@ -780,18 +780,16 @@ __global__ void __launch_bounds__(rsl::LTHREADS, RS_AAL_MINB) k_aa_large_op(cons
     m.pair = E.pair[m.e];
     return m;
   };
-  auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t type, uint32_t n) {
-    if (threadIdx.x == 0) {
-      O.type[m.e] = type;
-      O.card[m.e] = card;
-      O.n[m.e] = n;
-      if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
-    }
+  auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t type, uint32_t n) {  // one thread per pair
+    O.type[m.e] = type;
+    O.card[m.e] = card;
+    O.n[m.e] = n;
+    if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
   };
   rsl::large_loop<OP>(smraw, *cnt, A.pool, B.pool, opool, meta_of, sink);
 }
 
-__global__ void __launch_bounds__(rsl::LTHREADS, RS_AAL_MINB) k_aa_large_count(const uint64_t *__restrict__ laoff,
+__global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(-1)) k_aa_large_count(const uint64_t *__restrict__ laoff,
                                                                   const uint64_t *__restrict__ lboff,
                                                                   const uint32_t *__restrict__ lnab,
                                                                   const uint32_t *__restrict__ lpair,
@@ -811,7 +809,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, RS_AAL_MINB) k_aa_large_count(c
     return m;
   };
   auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t, uint32_t) {
-    if (threadIdx.x == 0 && card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);
+    if (card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);  // one thread per pair
   };
   rsl::large_loop<RS_OP_AND>(smraw, *cnt, A.pool, B.pool, nullptr, meta_of, sink);
 }
