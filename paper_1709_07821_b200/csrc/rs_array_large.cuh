@@ -48,7 +48,10 @@ constexpr int LTHREADS = NCONS + 32;    // + one producer warp
 #ifndef RS_AAL_MAXR
 #define RS_AAL_MAXR 8
 #endif
-constexpr int NSLOT = 8;                // items in flight (metadata + barrier slots)
+#ifndef RS_AAL_NSLOT
+#define RS_AAL_NSLOT 8
+#endif
+constexpr int NSLOT = RS_AAL_NSLOT;     // items in flight (metadata + barrier slots)
 static_assert(NGRP == 1 || NGRP == 2, "one or two consumer groups");
 
 struct LargeMeta {
@@ -222,6 +225,69 @@ __device__ __forceinline__ void scatter(const uint16_t *v, uint32_t n, uint32_t 
   }
 }
 
+// 16-byte forms of scatter / membership: a thread takes whole 8-value
+// vectors (t, t + LT, ...), so one LDS.128 feeds eight values and every value
+// costs its address (SHF + LOP3), its bit and one shared RED -- no pairing
+// test, no divergent second RED, no loop bookkeeping per value pair (the
+// 32-bit forms measured ~8 instructions per value on dense 4096-value pairs).
+// Staged arrays start 16-byte aligned in the ring; the last n % 8 values go
+// one per thread.
+template <bool XOR>
+__device__ __forceinline__ void set_pair(uint32_t x, uint32_t X) {
+  red_set<XOR>(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
+  red_set<XOR>(X | ((x >> 19) & 0x1FFCu), __funnelshift_l(0u, 1u, x >> 16));
+}
+
+template <bool XOR = false>
+__device__ __forceinline__ void scatter16(const uint16_t *v, uint32_t n, uint32_t X, int t) {
+  const uint4 *V = (const uint4 *)v;
+  const uint32_t nfull = n >> 3;
+#pragma unroll 2
+  for (uint32_t i = t; i < nfull; i += LT) {
+    const uint4 q = V[i];
+    set_pair<XOR>(q.x, X);
+    set_pair<XOR>(q.y, X);
+    set_pair<XOR>(q.z, X);
+    set_pair<XOR>(q.w, X);
+  }
+  if ((uint32_t)t < (n & 7u)) {
+    const uint32_t x = v[(nfull << 3) + t];
+    red_set<XOR>(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
+  }
+}
+
+__device__ __forceinline__ uint32_t member_pair(uint32_t x, uint32_t X) {
+  const uint32_t wl = lds32(X | ((x >> 3) & 0x1FFCu)), wh = lds32(X | ((x >> 19) & 0x1FFCu));
+  return (__funnelshift_r(wl, 0u, x) & 1u) + (__funnelshift_r(wh, 0u, x >> 16) & 1u);
+}
+
+// |P intersect X| over the group (counts only: no positions, no ballots).
+// Each thread arrives on `release` after its last read of P.
+__device__ __forceinline__ uint32_t probe_count16(const uint16_t *P, uint32_t np, uint32_t X, uint32_t *red, int g,
+                                                  int t, uint64_t *release) {
+  const uint4 *V = (const uint4 *)P;
+  const uint32_t nfull = np >> 3;
+  uint32_t c = 0;
+#pragma unroll 2
+  for (uint32_t i = t; i < nfull; i += LT) {
+    const uint4 q = V[i];
+    c += member_pair(q.x, X) + member_pair(q.y, X) + member_pair(q.z, X) + member_pair(q.w, X);
+  }
+  if ((uint32_t)t < (np & 7u)) {
+    const uint32_t x = P[(nfull << 3) + t];
+    c += __funnelshift_r(lds32(X | ((x >> 3) & 0x1FFCu)), 0u, x) & 1u;
+  }
+  mbar_arrive(release);
+  const int lane = t & 31, w = t >> 5;
+  const uint32_t ws = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) red[w] = ws;
+  gbar(g);
+  uint32_t total = 0;
+#pragma unroll
+  for (int k = 0; k < WG; k++) total += red[k];
+  return total;
+}
+
 // One chunk of probe_filter: value pairs [c2, c2 + WG * NR * 32) of P, warp w
 // a contiguous run of NR rounds of 32 value pairs.  The kept flags become
 // ballots, a group scan of the warp totals places each run after the `out`
@@ -338,7 +404,7 @@ __device__ __forceinline__ void flush_stage(uint16_t *stage, uint32_t total, uin
 //     clears the words it owns (t + LT q) before the cardinality barrier,
 //     which every thread of the group passes before its next scatter; array
 //     results are staged in the same bitset (re-zeroed behind a barrier).
-template <int op>
+template <int op, bool COUNT>
 __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t, const uint16_t *A, uint32_t na,
                                                const uint16_t *B, uint32_t nb, uint8_t *dst, int parity,
                                                uint8_t &type, uint32_t &nout, uint64_t *release) {
@@ -352,10 +418,14 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
     uint32_t *X = (NGRP == 2 ? g : parity) ? XB : XA;
     if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
     const uint32_t xs = rsb::smem_u32(X);
-    scatter(build_a ? A : B, build_a ? na : nb, xs, t);
+    scatter16(build_a ? A : B, build_a ? na : nb, xs, t);
     gbar(g);
-    const uint32_t total = probe_filter<is_and ? 1u : 0u>(build_a ? B : A, build_a ? nb : na, xs, (uint16_t *)dst,
-                                                           red2, parity, g, t, release);
+    uint32_t total;
+    if constexpr (COUNT && is_and)
+      total = probe_count16(build_a ? B : A, build_a ? nb : na, xs, red2[parity][0], g, t, release);
+    else
+      total = probe_filter<is_and ? 1u : 0u>(build_a ? B : A, build_a ? nb : na, xs, (uint16_t *)dst, red2, parity,
+                                             g, t, release);
     // every probe of X is done (the last chunk's barrier above): clear it
 #pragma unroll
     for (int q = 0; q < 512 / LT; q++) ((uint4 *)X)[t + LT * q] = make_uint4(0, 0, 0, 0);
@@ -367,8 +437,8 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
   constexpr bool is_xor = op == RS_OP_XOR;
   uint32_t *X = (NGRP == 2 && g) ? XB : XA;
   const uint32_t xs = rsb::smem_u32(X);
-  scatter<is_xor>(A, na, xs, t);
-  scatter<is_xor>(B, nb, xs, t);
+  scatter16<is_xor>(A, na, xs, t);
+  scatter16<is_xor>(B, nb, xs, t);
   gbar(g);
   mbar_arrive(release);
   // result words t + LT q (conflict-free), positions by a packed row scan
@@ -441,7 +511,7 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
 // Persistent, warp-specialized byte ring over items i = blockIdx.x + k*gridDim.x.
 // meta_of(i, aoff, boff) -> LargeMeta (runs on the producer lane only);
 // sink(meta, card, type, n) runs on thread 0 of the group that did the pair.
-template <int op, typename MetaOf, typename Sink>
+template <int op, bool COUNT, typename MetaOf, typename Sink>
 __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, const uint8_t *poolB,
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
   const int t = threadIdx.x;
@@ -517,11 +587,17 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
     const uint32_t i = blockIdx.x + k * gridDim.x;
     if (i >= count) break;
     const int s = k % NSLOT;
+#ifdef RS_AAL_SPIN
     rsb::mbar_wait(&sm.h->full[s], (k / NSLOT) & 1);
+#else
+    // suspended in the barrier, not polling: a starved group's spin loop took
+    // 10% of the kernel's issue slots from the group that has data
+    mbar_wait_backoff(&sm.h->full[s], (k / NSLOT) & 1);
+#endif
     const LargeMeta m = sm.h->meta[s];
     uint8_t type;
     uint32_t n;
-    const uint32_t card = large_pair<op>(sm, g, tg, (const uint16_t *)(sm.R() + m.aoff), m.na,
+    const uint32_t card = large_pair<op, COUNT>(sm, g, tg, (const uint16_t *)(sm.R() + m.aoff), m.na,
                                          (const uint16_t *)(sm.R() + m.boff), m.nb, opool ? opool + m.dst : nullptr,
                                          (k / NGRP) & 1, type, n, &sm.h->empty[s]);
     if (tg == 0) sink(m, card, type, n);

@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(OP)) k_aa
     O.n[m.e] = n;
     if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
   };
-  rsl::large_loop<OP>(smraw, *cnt, A.pool, B.pool, opool, meta_of, sink);
+  rsl::large_loop<OP, false>(smraw, *cnt, A.pool, B.pool, opool, meta_of, sink);
 }
 
 __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(-1)) k_aa_large_count(const uint64_t *__restrict__ laoff,
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(-1)) k_aa
   auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t, uint32_t) {
     if (card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);  // one thread per pair
   };
-  rsl::large_loop<RS_OP_AND>(smraw, *cnt, A.pool, B.pool, nullptr, meta_of, sink);
+  rsl::large_loop<RS_OP_AND, true>(smraw, *cnt, A.pool, B.pool, nullptr, meta_of, sink);
 }
 
 template <typename K>
