@@ -61,9 +61,11 @@ struct LargeMeta {
 };
 
 // Shared-memory layout (dynamic; carved at run time by large_layout):
-//   header | pad to 8 KB | XA (8 KB) | XB (8 KB) | byte ring (rest)
+//   header | byte ring | (pad) | XA (8 KB) | XB (8 KB)
 // XA / XB sit on 8 KB boundaries of the shared window so a value's word
-// address is base | offset (see scatter).
+// address is base | offset (see scatter); they take the highest aligned 16 KB
+// of the allocation, so the alignment pad (< 8 KB) comes out of the ring's
+// tail rather than sitting between the header and the bitsets.
 struct LargeHdr {
   uint64_t full[NSLOT];
   uint64_t empty[NSLOT];
@@ -74,21 +76,14 @@ struct LargeHdr {
 
 struct LargeSmem {
   LargeHdr *h;
-  uint8_t *X;     // XA, XB, then the ring
+  uint8_t *X;     // XA, XB
+  uint8_t *ring_base;
   uint32_t ring;  // ring bytes
   __device__ __forceinline__ uint32_t *XA() const { return (uint32_t *)X; }
   __device__ __forceinline__ uint32_t *XB() const { return (uint32_t *)(X + 8192); }
-  __device__ __forceinline__ uint8_t *R() const { return X + 16384; }
+  __device__ __forceinline__ uint8_t *R() const { return ring_base; }
 };
 
-// 56 KB: four CTAs per SM.  The header and the pad to the first 8 KB boundary
-// take at most ~8.5 KB, XA / XB 16 KB, and the ring the rest (>= 31 KB);
-// large_loop traps if it is ever under 16 KB, the largest item (an item that
-// does not fit before the end of the ring waits for the ring to drain and
-// starts at 0).  A fifth CTA (44 KB) measured slower.
-#ifndef RS_AAL_SMEM_KB
-#define RS_AAL_SMEM_KB 56
-#endif
 // Register budget: the AND / ANDNOT op kernels (probe rounds whose kept
 // values are written out) run three CTAs per SM with up to 72 registers --
 // at four CTAs' 56 they spill ~120 bytes per thread, and measured 1.65 /
@@ -102,16 +97,30 @@ constexpr int large_min_blocks(int op) {
   return op == RS_OP_AND || op == RS_OP_ANDNOT ? 3 : 4;
 #endif
 }
-constexpr size_t LARGE_SMEM_BYTES = RS_AAL_SMEM_KB * 1024;
 
-__device__ __forceinline__ LargeSmem large_layout(uint8_t *raw) {
+// Shared memory per CTA: 56 KB, four CTAs per SM (228 KB less 1 KB reserved
+// per CTA); the ring gets ~38 KB.  72 KB for the three-CTA AND / ANDNOT
+// kernels (a 54 KB ring) measured no better on config 3 (AND 1.32 -> 1.44 ms,
+// ANDNOT 1.90 -> 1.79 ms), nor did 16 item slots.  large_loop traps if the ring is ever under 16 KB, the largest item
+// (an item that does not fit before the end of the ring waits for the ring to
+// drain and starts at 0).  RS_AAL_SMEM_KB overrides (tuning).
+constexpr size_t large_smem_bytes(int op, bool count) {
+#ifdef RS_AAL_SMEM_KB
+  return (size_t)RS_AAL_SMEM_KB * 1024 + 0 * op + 0 * count;
+#else
+  return (size_t)56 * 1024 + 0 * op + 0 * count;
+#endif
+}
+
+__device__ __forceinline__ LargeSmem large_layout(uint8_t *raw, uint32_t bytes) {
   LargeSmem sm;
   sm.h = (LargeHdr *)raw;
   const uint32_t b = rsb::smem_u32(raw);
-  const uint32_t x = (b + (uint32_t)sizeof(LargeHdr) + 8191u) & ~8191u;
+  const uint32_t r0 = (b + (uint32_t)sizeof(LargeHdr) + 127u) & ~127u;
+  const uint32_t x = (b + bytes - 16384u) & ~8191u;
   sm.X = raw + (x - b);
-  const uint32_t used = (x - b) + 16384u;
-  sm.ring = used < LARGE_SMEM_BYTES ? ((uint32_t)LARGE_SMEM_BYTES - used) & ~15u : 0u;
+  sm.ring_base = raw + (r0 - b);
+  sm.ring = x > r0 ? (x - r0) & ~15u : 0u;
   return sm;
 }
 
@@ -515,7 +524,8 @@ template <int op, bool COUNT, typename MetaOf, typename Sink>
 __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, const uint8_t *poolB,
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
   const int t = threadIdx.x;
-  const LargeSmem sm = large_layout(raw);
+  constexpr uint32_t SMEM = (uint32_t)large_smem_bytes(op, COUNT);
+  const LargeSmem sm = large_layout(raw, SMEM);
   if (sm.ring < 2u * 8192u) __trap();  // the largest item (2 x 4096 values) must fit
   if (t == 0) {
     for (int s = 0; s < NSLOT; s++) {

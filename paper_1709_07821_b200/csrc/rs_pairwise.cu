@@ -827,7 +827,7 @@ unsigned persistent_grid_t(K kernel, int threads, size_t smem, uint64_t count) {
 template <int OP>
 int launch_aa_large_op_t(const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, Entries En, OutDesc O, uint8_t *pool,
                          uint64_t *res_card, bool exact) {
-  const size_t smem = rsl::LARGE_SMEM_BYTES;
+  const size_t smem = rsl::large_smem_bytes(OP, false);
   static bool attr = false;
   if (!attr) {
     RS_CK(cudaFuncSetAttribute(k_aa_large_op<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -850,7 +850,7 @@ int launch_aa_large_op(int op, const Lists &L, uint64_t n, DevBatch dA, DevBatch
 }
 
 int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch dB, uint64_t *inter) {
-  const size_t smem = rsl::LARGE_SMEM_BYTES;
+  const size_t smem = rsl::large_smem_bytes(RS_OP_AND, true);
   static bool attr = false;
   if (!attr) {
     RS_CK(cudaFuncSetAttribute(k_aa_large_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
