@@ -286,26 +286,56 @@ int h2d_small(void *d, const void *h, size_t bytes) {
 }
 
 // Short scans (the per-op entry/keep/ub arrays of small batches) run in one
-// CTA: one launch instead of CUB's two plus its temp allocation.
-constexpr int SCAN_T = 256, SCAN_V = 8;
-constexpr uint64_t SCAN_SMALL_MAX = 8 * SCAN_T * SCAN_V;
+// CTA: one launch instead of CUB's two plus its temp allocation.  The CTA is
+// 1024 threads wide with 16 (u32) / 8 (u64) values per thread, so up to
+// 16 K / 8 K values take one pass: each pass is a load latency plus a block
+// scan (~2.5 us), and a 256 x 8 CTA spent ~20 us on 15 K values in 8 passes
+// (two such scans per op).
+constexpr int SCAN_T = 1024;
+constexpr uint64_t SCAN_SMALL_MAX = 16384;
+template <typename T>
+constexpr int scan_v() { return sizeof(T) == 4 ? 16 : 8; }
 
 template <typename T, bool INCL>
 __global__ void __launch_bounds__(SCAN_T) k_scan_small(const T *in, T *out, uint32_t n) {
-  using BS = cub::BlockScan<T, SCAN_T>;
-  __shared__ typename BS::TempStorage ts;
+  constexpr int SCAN_V = scan_v<T>();
+  __shared__ T wsum[SCAN_T / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   T carry = 0;
   for (uint32_t base = 0; base < n; base += SCAN_T * SCAN_V) {
-    T v[SCAN_V], r[SCAN_V];
+    // thread-serial sums around one block scan of the per-thread totals
+    T v[SCAN_V], sum = 0;
     const uint32_t i0 = base + threadIdx.x * SCAN_V;
 #pragma unroll
-    for (int k = 0; k < SCAN_V; k++) v[k] = i0 + k < n ? in[i0 + k] : T(0);
-    T tot;
-    if (INCL) BS(ts).InclusiveSum(v, r, tot);
-    else BS(ts).ExclusiveSum(v, r, tot);
+    for (int k = 0; k < SCAN_V; k++) {
+      v[k] = i0 + k < n ? in[i0 + k] : T(0);
+      sum += v[k];
+    }
+    // block exclusive scan of `sum`: warp shuffles, then the 32 warp totals
+    T x = sum;
 #pragma unroll
-    for (int k = 0; k < SCAN_V; k++)
-      if (i0 + k < n) out[i0 + k] = r[k] + carry;
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    T wt = lane < SCAN_T / 32 ? wsum[lane] : T(0), wx = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, wx, o);
+      if (lane >= o) wx += y;
+    }
+    const T wbase = __shfl_sync(0xffffffffu, wx - wt, w);  // warps before w
+    const T tot = __shfl_sync(0xffffffffu, wx, 31);
+    const T excl = wbase + x - sum;
+    T run = excl + carry;
+#pragma unroll
+    for (int k = 0; k < SCAN_V; k++) {
+      if (INCL) run += v[k];
+      if (i0 + k < n) out[i0 + k] = run;
+      if (!INCL) run += v[k];
+    }
     carry += tot;
     __syncthreads();
   }
