@@ -2108,14 +2108,18 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
                   uint64_t *inter) {
   DevBatch dA = A->dev(), dB = B->dev();
   const ClassMask cm = class_mask(A->type_mask, B->type_mask, RS_OP_AND);
-  const unsigned pg = sm_count() * 8;
+  // Persistent grids, but never more CTAs than the list can fill (one item
+  // per warp / per CTA): a one-pair call of a few thousand container pairs
+  // would otherwise launch 1184 mostly idle CTAs per class kernel.
+  const unsigned pg = std::min<uint64_t>(sm_count() * 8, grid_for(L.cap, 8));
+  const unsigned pg_cta = std::min<uint64_t>(sm_count() * 8, std::max<uint64_t>(L.cap, 1));
   const int nk = cm.bb + cm.aa + cm.gen + cm.prb;  // independent: concurrent on side streams
   Fork F;
   if (nk > 1 && L.cap >= 16384) RS_TRY(F.begin(nk));
   if (cm.bb) {
     F.next();
     if (bb_kernel_choice() == 0) {
-      RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg, DT, 0, op_kernel, L.list[CLS_BB],
+      RS_LAUNCH_PROF("bitset_count", 0, k_pair_count<false>, pg_cta, DT, 0, op_kernel, L.list[CLS_BB],
                      lcb + CLS_BB * L.cap, lpair + CLS_BB * L.cap, L.cnt + CLS_BB, dA, dB, inter);
     } else {
       uint32_t *lp = lpair + CLS_BB * L.cap;
@@ -2153,12 +2157,13 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
   }
   if (cm.gen) {
     F.next();
-    RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg, DT, 0, op_kernel, L.list[CLS_GEN],
+    RS_LAUNCH_PROF("generic_count", 0, k_pair_count<true>, pg_cta, DT, 0, op_kernel, L.list[CLS_GEN],
                    lcb + CLS_GEN * L.cap, lpair + CLS_GEN * L.cap, L.cnt + CLS_GEN, dA, dB, inter);
   }
   if (cm.prb) {
     F.next();
-    RS_LAUNCH_PROF("probe_count", 0, k_probe_count, sm_count() * 12, 32 * PRB_WARPS, 0, L.list[CLS_PRB],
+    RS_LAUNCH_PROF("probe_count", 0, k_probe_count, std::min<uint64_t>(sm_count() * 12, grid_for(L.cap, PRB_WARPS)),
+                   32 * PRB_WARPS, 0, L.list[CLS_PRB],
                    lcb + CLS_PRB * L.cap,
                    lpair + CLS_PRB * L.cap, L.cnt + CLS_PRB, dA, dB, inter);
   }
