@@ -2171,6 +2171,72 @@ int launch_counts(int op_kernel, const rs_batch *A, const rs_batch *B, Lists L, 
 }
 }  // namespace
 
+// ---------------------------------------------- small count calls: graphs
+//
+// A few-pair count (config 1: one pair, ~10 launches of tiny grids, then a
+// synchronizing read-back) is host- and launch-latency-bound.  Its launch
+// sequence is captured once into a CUDA graph and replayed: everything the
+// kernels see -- the batches' device arrays, the scratch addresses (the bump
+// arena is deterministic for an identical call), the grid sizes (derived from
+// the container counts and type masks) -- is in the key, and the per-call
+// inputs (pair indices, bases) go through a page-locked upload block that the
+// graph's first node copies to the device; the counts come back through a
+// page-locked block the last node fills.  RS_NO_GRAPH=1 disables it.
+struct CountGraphKey {
+  DevBatch a, b;
+  uint64_t amask, bmask, op, on_dev, npairs, Ma, maxk, up_bytes, top;
+  const void *arena, *counts, *stream;
+};
+struct CountGraph {
+  CountGraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  void *h_up = nullptr, *h_out = nullptr;
+  uint64_t launches = 0, last_use = 0;
+};
+std::vector<CountGraph> g_count_graphs;
+uint64_t g_count_graph_clock = 0;
+constexpr size_t COUNT_GRAPHS_MAX = 16;
+// A key is captured on its third sighting (capture + instantiation cost
+// ~1 ms: a stream of distinct one-off calls must never pay it); keys whose
+// capture failed are not retried.
+struct SeenKey {
+  CountGraphKey key;
+  uint32_t hits;
+};
+std::vector<SeenKey> g_count_seen;  // small ring of recent keys
+size_t g_count_seen_next = 0;
+constexpr size_t COUNT_SEEN_MAX = 64;
+constexpr uint32_t COUNT_CAPTURE_AFTER = 3, COUNT_CAPTURE_FAILED = ~0u;
+
+uint32_t count_key_sighting(const CountGraphKey &k) {
+  for (auto &e : g_count_seen)
+    if (!memcmp(&e.key, &k, sizeof k)) return e.hits == COUNT_CAPTURE_FAILED ? e.hits : ++e.hits;
+  if (g_count_seen.size() < COUNT_SEEN_MAX) g_count_seen.push_back({k, 1});
+  else g_count_seen[g_count_seen_next++ % COUNT_SEEN_MAX] = {k, 1};
+  return 1;
+}
+void count_key_failed(const CountGraphKey &k) {
+  for (auto &e : g_count_seen)
+    if (!memcmp(&e.key, &k, sizeof k)) e.hits = COUNT_CAPTURE_FAILED;
+}
+
+void count_graph_free(CountGraph &g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.h_up) cudaFreeHost(g.h_up);
+  if (g.h_out) cudaFreeHost(g.h_out);
+  g.exec = nullptr;
+  g.h_up = g.h_out = nullptr;
+}
+
+CountGraph *count_graph_find(const CountGraphKey &k) {
+  for (auto &g : g_count_graphs)
+    if (!memcmp(&g.key, &k, sizeof k)) {
+      g.last_use = ++g_count_graph_clock;
+      return &g;
+    }
+  return nullptr;
+}
+
 extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia,
                                        const uint32_t *ib, uint64_t npairs, uint64_t *counts, int counts_on_device) {
   RS_TRY(check_op(op));
@@ -2197,27 +2263,132 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
   const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
+  const size_t top0 = Scratch::top;
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   Lists L = make_lists(S, Ma);
   uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);
   uint64_t *inter = o_inter == Upload::NONE ? (uint64_t *)S.get((npairs + 1) * 8) : nullptr;
   uint64_t *dout = counts_on_device ? counts : (uint64_t *)S.get((npairs + 1) * 8);
-  if (!S.ok()) { set_error("device allocation failed (count)"); return RS_ENOMEM; }
-  RS_TRY(U.commit(S));
+  U.d = U.h.empty() ? nullptr : (uint8_t *)S.get(U.h.size());
+  if (!S.ok() || (!U.h.empty() && !U.d)) { set_error("device allocation failed (count)"); return RS_ENOMEM; }
   const uint32_t *dia = U.at<uint32_t>(o_ia), *dib = U.at<uint32_t>(o_ib);
   L.cnt = U.at<uint32_t>(o_cnt);
-  if (inter) RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
-  else inter = U.at<uint64_t>(o_inter);
   DevBatch dA = A->dev(), dB = B->dev();
   if (hbases) mbase = U.at<uint64_t>(o_mb);
-  else RS_TRY(pair_bases_device(npairs, dA, dB, dia, dib, 1, msz, mbase));
-  if (Ma && maxk <= MERGE_SMEM_KEYS && (npairs >= 2 * sm_count() || Ma <= 512 * npairs))
-    RS_LAUNCH(k_match_pair, (unsigned)npairs, 256, 0, mbase, dA, dB, dia, dib, L, lcb, lpair);
-  else
-    RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
-  RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
-  RS_LAUNCH(k_formula, grid_for(npairs, 256), 256, 0, npairs, op, A->d_bm_card, B->d_bm_card, dia, dib, inter, dout);
+  if (!inter) inter = U.at<uint64_t>(o_inter);
+
+  // the whole device side of the call; `up` is the host block to upload from
+  static const bool gdbg = env_int("RS_GRAPH_DEBUG", 0) != 0;
+  auto stage = [&](const char *what) {
+    if (!gdbg) return;
+    cudaStreamCaptureStatus st;
+    if (cudaStreamIsCapturing(g_stream, &st) == cudaSuccess && st == cudaStreamCaptureStatusInvalidated)  // (g_stream = the capture stream here)
+      fprintf(stderr, "[rs graph] capture invalidated by: %s\n", what);
+  };
+  auto enqueue = [&](const void *up, uint64_t *hout) -> int {
+    RS_TRY(h2d_small(U.d, up, U.h.size()));
+    stage("upload");
+    if (o_inter == Upload::NONE) RS_CK(cudaMemsetAsync(inter, 0, (npairs + 1) * 8, g_stream));
+    if (!hbases) RS_TRY(pair_bases_device(npairs, dA, dB, dia, dib, 1, msz, mbase));
+    if (Ma && maxk <= MERGE_SMEM_KEYS && (npairs >= 2 * sm_count() || Ma <= 512 * npairs))
+      RS_LAUNCH(k_match_pair, (unsigned)npairs, 256, 0, mbase, dA, dB, dia, dib, L, lcb, lpair);
+    else
+      RS_LAUNCH(k_match, grid_for(Ma, 256), 256, 0, Ma, npairs, mbase, dA, dB, dia, dib, L, lcb, lpair);
+    stage("match");
+    RS_TRY(launch_counts(RS_OP_AND, A, B, L, lcb, lpair, inter));
+    stage("counts");
+    RS_LAUNCH(k_formula, grid_for(npairs, 256), 256, 0, npairs, op, A->d_bm_card, B->d_bm_card, dia, dib, inter,
+              dout);
+    if (hout) RS_CK(cudaMemcpyAsync(hout, dout, npairs * 8, cudaMemcpyDeviceToHost, g_stream));
+    return RS_OK;
+  };
+
+  static const bool graphs_on = env_int("RS_NO_GRAPH", 0) == 0;
+  // (host read-back calls only: their synchronization is what makes the
+  // page-locked upload block free for the next call)
+  if (graphs_on && !counts_on_device && npairs <= 64 && hbases && o_inter != Upload::NONE && S.spill.empty() &&
+      !g_prof_on) {
+    CountGraphKey k;
+    memset(&k, 0, sizeof k);
+    k.a = dA;
+    k.b = dB;
+    k.amask = A->type_mask;
+    k.bmask = B->type_mask;
+    k.op = (uint64_t)op;
+    k.on_dev = (uint64_t)counts_on_device;
+    k.npairs = npairs;
+    k.Ma = Ma;
+    k.maxk = maxk;
+    k.up_bytes = U.h.size();
+    k.top = top0;
+    k.arena = Scratch::arena;
+    k.counts = counts_on_device ? counts : nullptr;
+    k.stream = g_stream;
+    CountGraph *g = count_graph_find(k);
+    static const bool dbg = env_int("RS_GRAPH_DEBUG", 0) != 0;
+    const uint32_t seen = g ? 0 : count_key_sighting(k);
+    if (!g && seen >= COUNT_CAPTURE_AFTER && seen != COUNT_CAPTURE_FAILED) {
+      CountGraph ng;
+      ng.key = k;
+      if (cudaMallocHost(&ng.h_up, std::max<size_t>(U.h.size(), 16)) == cudaSuccess &&
+          cudaMallocHost(&ng.h_out, std::max<uint64_t>(npairs * 8, 16)) == cudaSuccess) {
+        const uint64_t l0 = g_launches;
+        cudaGraph_t graph = nullptr;
+        // captured on a private stream (the library stream may be the legacy
+        // default stream, which cannot be captured); the graph is launched
+        // on the library stream
+        static cudaStream_t cap = nullptr;
+        static int cap_dev = -1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cap && cap_dev != dev) cap = nullptr;  // (leaked per device switch; rare)
+        if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) == cudaSuccess) cap_dev = dev;
+        cudaError_t e = cap ? cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) : cudaErrorNotReady;
+        bool ok = e == cudaSuccess;
+        if (ok) {
+          const cudaStream_t saved = g_stream;
+          g_stream = cap;
+          const int rc = enqueue(ng.h_up, counts_on_device ? nullptr : (uint64_t *)ng.h_out);
+          g_stream = saved;
+          e = cudaStreamEndCapture(cap, &graph);
+          ok = e == cudaSuccess && rc == RS_OK && graph;
+          if (dbg && rc != RS_OK) fprintf(stderr, "[rs graph] capture enqueue failed: %s\n", rs_last_error());
+        }
+        if (ok) ok = (e = cudaGraphInstantiate(&ng.exec, graph, 0)) == cudaSuccess;
+        if (dbg) fprintf(stderr, "[rs graph] capture npairs=%llu Ma=%llu: %s\n", (unsigned long long)npairs,
+                         (unsigned long long)Ma, ok ? "ok" : cudaGetErrorString(e));
+        if (!ok) count_key_failed(k);
+        if (graph) cudaGraphDestroy(graph);
+        ng.launches = g_launches - l0;
+        g_launches = l0;
+        cudaGetLastError();  // a failed capture falls back to plain launches
+        if (ok) {
+          if (g_count_graphs.size() >= COUNT_GRAPHS_MAX) {  // evict the least recently used
+            auto lru = std::min_element(g_count_graphs.begin(), g_count_graphs.end(),
+                                        [](const CountGraph &x, const CountGraph &y) { return x.last_use < y.last_use; });
+            count_graph_free(*lru);
+            g_count_graphs.erase(lru);
+          }
+          ng.last_use = ++g_count_graph_clock;
+          g_count_graphs.push_back(ng);
+          g = &g_count_graphs.back();
+        }
+      }
+      if (!g) count_graph_free(ng);
+    }
+    if (g) {
+      memcpy(g->h_up, U.h.data(), U.h.size());
+      RS_CK(cudaGraphLaunch(g->exec, g_stream));
+      g_launches += g->launches;
+      if (!counts_on_device) {
+        RS_CK(cudaStreamSynchronize(g_stream));
+        memcpy(counts, g->h_out, npairs * 8);
+      }
+      return RS_OK;
+    }
+  }
+  RS_TRY(enqueue(U.h.data(), nullptr));
   if (!counts_on_device) RS_TRY(d2h(counts, dout, npairs * 8));
   return RS_OK;
 }
