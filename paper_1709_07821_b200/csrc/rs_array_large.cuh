@@ -247,20 +247,38 @@ __device__ __forceinline__ void set_pair(uint32_t x, uint32_t X) {
   red_set<XOR>(X | ((x >> 19) & 0x1FFCu), __funnelshift_l(0u, 1u, x >> 16));
 }
 
+// Vector width of the scatter / membership loads (bytes per lane: 4, 8 or
+// 16).  Wider loads cost fewer instructions per value; narrower ones keep a
+// warp's lanes closer to consecutive 32-bit words of a dense array: on a
+// 1/16-dense array a lane's 2 / 4 / 8 values span ~1 / 2 / 4 words, so at
+// every step lanes l and l + 32 / 16 / 8 land in one bank -- none, 2-way and
+// 4-way conflicts for the REDs and probes.  C3: 9.66 ms at 16 bytes, 9.19 at
+// 8, 9.21 at 4.  (Rotating each lane's word order by its bank group measured
+// no better.)
+#ifndef RS_AAL_VEC
+#define RS_AAL_VEC 8
+#endif
+template <int VB> struct LaneVec;
+template <> struct LaneVec<4> { using T = uint32_t; };
+template <> struct LaneVec<8> { using T = uint2; };
+template <> struct LaneVec<16> { using T = uint4; };
+__device__ __forceinline__ uint32_t vword(uint32_t v, int) { return v; }
+__device__ __forceinline__ uint32_t vword(uint2 v, int k) { return k ? v.y : v.x; }
+__device__ __forceinline__ uint32_t vword(uint4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
 template <bool XOR = false>
 __device__ __forceinline__ void scatter16(const uint16_t *v, uint32_t n, uint32_t X, int t) {
-  const uint4 *V = (const uint4 *)v;
-  const uint32_t nfull = n >> 3;
+  constexpr int VB = RS_AAL_VEC, NV = VB / 2;  // values per lane vector
+  using V = typename LaneVec<VB>::T;
+  const V *vp = (const V *)v;
+  const uint32_t nfull = n / NV;
 #pragma unroll 2
   for (uint32_t i = t; i < nfull; i += LT) {
-    const uint4 q = V[i];
-    set_pair<XOR>(q.x, X);
-    set_pair<XOR>(q.y, X);
-    set_pair<XOR>(q.z, X);
-    set_pair<XOR>(q.w, X);
+    const V q = vp[i];
+#pragma unroll
+    for (int k = 0; k < VB / 4; k++) set_pair<XOR>(vword(q, k), X);
   }
-  if ((uint32_t)t < (n & 7u)) {
-    const uint32_t x = v[(nfull << 3) + t];
+  if ((uint32_t)t < n - nfull * NV) {
+    const uint32_t x = v[nfull * NV + t];
     red_set<XOR>(X | ((x >> 3) & 0x1FFCu), __funnelshift_l(0u, 1u, x));
   }
 }
@@ -274,16 +292,19 @@ __device__ __forceinline__ uint32_t member_pair(uint32_t x, uint32_t X) {
 // Each thread arrives on `release` after its last read of P.
 __device__ __forceinline__ uint32_t probe_count16(const uint16_t *P, uint32_t np, uint32_t X, uint32_t *red, int g,
                                                   int t, uint64_t *release) {
-  const uint4 *V = (const uint4 *)P;
-  const uint32_t nfull = np >> 3;
+  constexpr int VB = RS_AAL_VEC, NV = VB / 2;
+  using V = typename LaneVec<VB>::T;
+  const V *vp = (const V *)P;
+  const uint32_t nfull = np / NV;
   uint32_t c = 0;
 #pragma unroll 2
   for (uint32_t i = t; i < nfull; i += LT) {
-    const uint4 q = V[i];
-    c += member_pair(q.x, X) + member_pair(q.y, X) + member_pair(q.z, X) + member_pair(q.w, X);
+    const V q = vp[i];
+#pragma unroll
+    for (int k = 0; k < VB / 4; k++) c += member_pair(vword(q, k), X);
   }
-  if ((uint32_t)t < (np & 7u)) {
-    const uint32_t x = P[(nfull << 3) + t];
+  if ((uint32_t)t < np - nfull * NV) {
+    const uint32_t x = P[nfull * NV + t];
     c += __funnelshift_r(lds32(X | ((x >> 3) & 0x1FFCu)), 0u, x) & 1u;
   }
   mbar_arrive(release);
