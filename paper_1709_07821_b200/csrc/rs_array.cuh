@@ -93,6 +93,38 @@ __device__ __forceinline__ void merge_walk(int op, const uint16_t *A, int na, co
   }
 }
 
+// The same walk, fully unrolled, keeping the VT items' values and keep flags
+// in registers (static indices), so a materialized pair walks once: the kept
+// values go to their scanned positions straight from registers.
+template <int VT>
+__device__ __forceinline__ void merge_walk_reg(int op, const uint16_t *A, int na, const uint16_t *B, int nb, int i,
+                                               int j, uint16_t (&kv)[VT], uint32_t &km) {
+  const int total = na + nb;
+  km = 0;
+#pragma unroll
+  for (int k = 0; k < VT; k++) {
+    const bool valid = i + j < total;
+    const bool takeA = j >= nb || (i < na && A[i] <= B[j]);
+    uint16_t v;
+    bool keep;
+    if (takeA) {
+      v = i < na ? A[i] : 0;
+      const bool both = j < nb && B[j] == v;
+      keep = op == RS_OP_AND ? both : op == RS_OP_OR ? true : !both;
+    } else {
+      v = B[j];
+      const bool both = i > 0 && A[i - 1] == v;
+      keep = (op == RS_OP_OR || op == RS_OP_XOR) && !both;
+    }
+    kv[k] = v;
+    km |= (uint32_t)(valid && keep) << k;
+    if (valid) {
+      i += takeA;
+      j += !takeA;
+    }
+  }
+}
+
 template <int GT, int VT>
 struct alignas(16) AASmem {
   static constexpr int CAP = GT * VT;                       // merged items per group
@@ -148,15 +180,37 @@ __device__ __forceinline__ uint32_t aa_pair_thread(int op, const uint16_t *A, ui
   return k;
 }
 
-template <int GT, int VT>
-__device__ uint32_t aa_pair(int op, bool count_only, const uint8_t *pa, int na, const uint8_t *pb, int nb,
+// OPC >= 0: the op as a compile-time constant (the caller's kernel is
+// instantiated per op, so the keep rules fold away).
+template <int GT, int VT, int OPC = -1>
+__device__ uint32_t aa_pair(int op_rt, bool count_only, const uint8_t *pa, int na, const uint8_t *pb, int nb,
                             AASmem<GT, VT> &sm, int gid, uint8_t *dst, uint8_t &type, uint32_t &nout) {
+  const int op = OPC >= 0 ? OPC : op_rt;
   const int lt = threadIdx.x % GT;
   stage<GT>(sm.a, pa, na, lt);
   stage<GT>(sm.b, pb, nb, lt);
   group_sync<GT>(gid);
   const int diag = min(lt * VT, na + nb);
   const int i0 = merge_path(sm.a, na, sm.b, nb, diag), j0 = diag - i0;
+  if constexpr (!AASmem<GT, VT>::BITSET && VT <= 16) {  // one walk, kept items in registers
+    uint16_t kv[VT];
+    uint32_t km;
+    merge_walk_reg<VT>(op, sm.a, na, sm.b, nb, i0, j0, kv, km);
+    uint32_t total;
+    uint32_t pos = group_scan<GT>((uint32_t)__popc(km), total, sm.ws, gid);
+    type = RS_TAG_ARRAY;
+    nout = total;
+    if (count_only || total == 0) return total;
+#pragma unroll
+    for (int k = 0; k < VT; k++)
+      if ((km >> k) & 1u) sm.out[pos++] = kv[k];
+    group_sync<GT>(gid);
+    const int nvec = (2 * (int)total + 15) >> 4;
+    if (lt < 8 && (int)total + lt < nvec * 8) sm.out[total + lt] = 0;
+    group_sync<GT>(gid);
+    for (int k = lt; k < nvec; k += GT) ((uint4 *)dst)[k] = ((const uint4 *)sm.out)[k];
+    return total;
+  }
   uint32_t cnt = 0;
   merge_walk<VT>(op, sm.a, na, sm.b, nb, i0, j0, [&](uint16_t) { cnt++; });
   uint32_t total;

@@ -1062,7 +1062,8 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe_count(const uint32_t *
 // instructions on each of them whatever its size.
 __constant__ uint32_t c_aa_tiny = 64;
 
-__global__ void __launch_bounds__(256) k_aa_small(int op, const uint32_t *__restrict__ list,
+template <int op>
+__global__ void __launch_bounds__(256) k_aa_small(const uint32_t *__restrict__ list,
                                                   const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B, Entries E,
                                                   OutDesc O, uint8_t *__restrict__ opool,
                                                   uint64_t *__restrict__ res_card) {
@@ -1105,7 +1106,7 @@ __global__ void __launch_bounds__(256) k_aa_small(int op, const uint32_t *__rest
                      nb1 = __shfl_sync(0xffffffffu, nb, src);
       uint8_t type;
       uint32_t n;
-      const uint32_t card = rsa::aa_pair<32, 8>(op, false, A.pool + A.off[ca1], (int)na1, B.pool + B.off[cb1],
+      const uint32_t card = rsa::aa_pair<32, 8, op>(op, false, A.pool + A.off[ca1], (int)na1, B.pool + B.off[cb1],
                                                 (int)nb1, sm[gid], gid, opool + E.off[e1], type, n);
       if (lane == 0) {
         O.type[e1] = type;
@@ -1118,7 +1119,7 @@ __global__ void __launch_bounds__(256) k_aa_small(int op, const uint32_t *__rest
   }
 }
 
-template <int GT, int VT>
+template <int GT, int VT, int OPC = -1>
 __global__ void __launch_bounds__(256) k_aa_pair(int op, const uint32_t *__restrict__ list, const uint32_t *__restrict__ cnt,
                                                  DevBatch A, DevBatch B, Entries E, OutDesc O,
                                                  uint8_t *__restrict__ opool, uint64_t *__restrict__ res_card) {
@@ -1130,7 +1131,7 @@ __global__ void __launch_bounds__(256) k_aa_pair(int op, const uint32_t *__restr
     const uint32_t e = list[i], ca = E.ca[e], cb = E.cb[e];
     uint8_t type;
     uint32_t n;
-    uint32_t card = rsa::aa_pair<GT, VT>(op, false, A.pool + A.off[ca], (int)A.card[ca], B.pool + B.off[cb],
+    uint32_t card = rsa::aa_pair<GT, VT, OPC>(op, false, A.pool + A.off[ca], (int)A.card[ca], B.pool + B.off[cb],
                                          (int)B.card[cb], sm[gid], gid, opool + E.off[e], type, n);
     if (lt == 0) {
       O.type[e] = type;
@@ -1824,17 +1825,32 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
       RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, (k_aa_pair<32, 8>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
                      256, 0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, res_card);
     else
-      RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, k_aa_small, std::min<uint64_t>(grid_for(n, 8), sms * 8), 256,
-                     0, op, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, res_card);
+      switch (op) {  // one instantiation per op: the keep rules are constants
+#define RS_AAS(OP) RS_LAUNCH_PROF("array_pair_s", hcnt ? n : 0, k_aa_small<OP>, std::min<uint64_t>(grid_for(n, 8), sms * 8), \
+                                  256, 0, L.list[CLS_AAS], L.cnt + CLS_AAS, dA, dB, En, O, b->d_pool, res_card)
+        case RS_OP_AND: RS_AAS(RS_OP_AND); break;
+        case RS_OP_OR: RS_AAS(RS_OP_OR); break;
+        case RS_OP_ANDNOT: RS_AAS(RS_OP_ANDNOT); break;
+        default: RS_AAS(RS_OP_XOR); break;
+#undef RS_AAS
+      }
   }
   if (uint64_t n = n_aam) {
     F.next();
     // medium pairs: a warp per pair (16 items per lane) up to 512 items, else
     // the 128-thread groups
-    if (aa_medium_max(op) <= 512)
-      RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<32, 16>), std::min<uint64_t>(grid_for(n, 8), sms * 8),
-                     256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, res_card);
-    else
+    if (aa_medium_max(op) <= 512) {
+      switch (op) {  // per-op instantiations (constant keep rules)
+#define RS_AAM(OP) RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<32, 16, OP>), \
+                                  std::min<uint64_t>(grid_for(n, 8), sms * 8), 256, 0, op, L.list[CLS_AAM], \
+                                  L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, res_card)
+        case RS_OP_AND: RS_AAM(RS_OP_AND); break;
+        case RS_OP_OR: RS_AAM(RS_OP_OR); break;
+        case RS_OP_ANDNOT: RS_AAM(RS_OP_ANDNOT); break;
+        default: RS_AAM(RS_OP_XOR); break;
+#undef RS_AAM
+      }
+    } else
       RS_LAUNCH_PROF("array_pair_m", hcnt ? n : 0, (k_aa_pair<128, 16>), std::min<uint64_t>(grid_for(n, 2), sms * 8),
                      256, 0, op, L.list[CLS_AAM], L.cnt + CLS_AAM, dA, dB, En, O, b->d_pool, res_card);
   }
