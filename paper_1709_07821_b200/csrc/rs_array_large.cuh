@@ -423,6 +423,17 @@ __device__ __forceinline__ void flush_stage(uint16_t *stage, uint32_t total, uin
   for (uint32_t v = t; v < nvec; v += LT) ((uint4 *)dst)[v] = ((const uint4 *)stage)[v];
 }
 
+// Sorted-array membership: is x in v[0, n)?  (n <= 4096: 12 probes)
+__device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, len = n;
+  while (len > 1) {
+    const uint32_t half = len >> 1;
+    if (v[lo + half] <= x) lo += half;
+    len -= half;
+  }
+  return n && v[lo] == x;
+}
+
 // One pair (the group's threads only; t = thread within the group).
 // `release` (the item's ring slot) is arrived on once by every thread of the
 // group, after that thread's last read of the staged values (a slot's items
@@ -447,6 +458,34 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
     const bool build_a = is_and && na <= nb;
     uint32_t *X = (NGRP == 2 ? g : parity) ? XB : XA;
     if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
+    {  // galloping pairs (gallop_pair): the small side's values binary-searched in the staged large side
+      const bool a_small = is_and ? na <= nb : true;
+      const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
+      if (16 * ns <= nl) {
+        const uint16_t *Sv = a_small ? A : B, *Lv = a_small ? B : A;
+        uint32_t v[2], k[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint32_t i = t + LT * h;  // ns <= 4096 / 16 = 256 = 2 LT
+          v[h] = i < ns ? Sv[i] : 0u;
+          k[h] = i < ns && bsearch16(Lv, nl, v[h]) == is_and;
+        }
+        mbar_arrive(release);  // this thread's last read of the staged values
+        const uint32_t pk[1] = {k[0] | (k[1] << 16)};
+        uint32_t e[1], T[1];
+        gscan<1>(pk, red2[parity], g, t, e, T);
+        const uint32_t n0 = T[0] & 0xFFFFu, total = n0 + (T[0] >> 16);
+        if (!COUNT && dst && total) {
+          uint16_t *d = (uint16_t *)dst;
+          if (k[0]) d[e[0] & 0xFFFFu] = (uint16_t)v[0];
+          if (k[1]) d[n0 + (e[0] >> 16)] = (uint16_t)v[1];
+          const uint32_t padded = (total + 7u) & ~7u;
+          if (t < 8 && total + t < padded) d[total + t] = 0;
+        }
+        nout = total;
+        return total;
+      }
+    }
     const uint32_t xs = rsb::smem_u32(X);
     scatter16(build_a ? A : B, build_a ? na : nb, xs, t);
     gbar(g);
