@@ -138,5 +138,91 @@ static __device__ uint32_t encode_result(DenseSmem &sm, const uint64_t r[4], uin
   return nruns;
 }
 
+// The two operands' words, thread t's four: bitset sides straight from the
+// pool, array / run sides densified into sm.X (a) / sm.Y (b) first.  GEN =
+// false: both sides are known bitsets (no shared memory, no barrier).
+template <bool GEN>
+static __device__ __forceinline__ void operand_words(const DevBatch &A, uint32_t ca, uint8_t ta, const DevBatch &B,
+                                                     uint32_t cb, uint8_t tb, uint64_t *X, uint64_t *Y,
+                                                     uint64_t ra[4], uint64_t rb[4]) {
+  const int t = threadIdx.x;
+  if (!GEN) {
+    ld_words(A.pool, A.off[ca], t, ra);
+    ld_words(B.pool, B.off[cb], t, rb);
+    return;
+  }
+  const bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    if (da) X[4 * t + k] = 0;
+    if (db) Y[4 * t + k] = 0;
+  }
+  __syncthreads();
+  if (da) scatter_container(A, ca, ta, X);
+  if (db) scatter_container(B, cb, tb, Y);
+  __syncthreads();
+  if (da) { for (int k = 0; k < 4; k++) ra[k] = X[4 * t + k]; } else ld_words(A.pool, A.off[ca], t, ra);
+  if (db) { for (int k = 0; k < 4; k++) rb[k] = Y[4 * t + k]; } else ld_words(B.pool, B.off[cb], t, rb);
+}
+
+// container_pairwise(op, a, b) of one matched pair by the whole CTA
+// (containers.py:450-529): word op, popcount and run count, the exact
+// result-type choice, and the encoded result at dst.
+// Returns the cardinality (0: nothing written); type and n of the result.
+// Ends with the CTA's shared memory free for reuse.
+template <bool GEN>
+static __device__ uint32_t dense_pair(int op, const DevBatch &A, uint32_t ca, uint8_t ta, const DevBatch &B,
+                                      uint32_t cb, uint8_t tb, DenseSmem &sm, uint8_t *dst, uint8_t &type,
+                                      uint32_t &n) {
+  const int t = threadIdx.x;
+  uint64_t ra[4], rb[4], r[4];
+  operand_words<GEN>(A, ca, ta, B, cb, tb, sm.X, sm.Y, ra, rb);
+  uint32_t pc = 0, nr = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    r[k] = rs_word_op(op, ra[k], rb[k]);
+    pc += __popcll(r[k]);
+  }
+  const bool consider = GEN && rs_consider_run(ta, tb, op);
+  if (consider) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) sm.X[4 * t + k] = r[k];
+    __syncthreads();
+    uint64_t prev = t ? sm.X[4 * t - 1] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      uint64_t cin = (k ? r[k - 1] : prev) >> 63;
+      nr += __popcll(r[k] & ~((r[k] << 1) | cin));  // _run_count_of_words, containers.py:173-178
+    }
+  }
+  uint32_t card = pc, nruns = nr;
+  block_sum2(card, nruns, sm.red);
+  if (card == 0) type = RS_TAG_ARRAY;
+  else if (consider && rs_run_admissible(card, nruns)) type = RS_TAG_RUN;  // container_normalize
+  else type = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;       // from_words / from_values
+  n = 0;
+  if (card) {
+    __syncthreads();  // smem Y may still be read by the densify phase
+    n = encode_result(sm, r, pc, card, type, dst);
+  }
+  __syncthreads();  // smem reuse by the caller's next pair
+  return card;
+}
+
+// |a AND b| of one matched pair by the whole CTA (the count path); the
+// block total is returned on every thread.
+template <bool GEN>
+static __device__ uint32_t dense_and_count(const DevBatch &A, uint32_t ca, uint8_t ta, const DevBatch &B,
+                                           uint32_t cb, uint8_t tb, uint64_t *X, uint64_t *Y, uint32_t (*red)[2]) {
+  uint64_t ra[4], rb[4];
+  operand_words<GEN>(A, ca, ta, B, cb, tb, X, Y, ra, rb);
+  uint32_t pc = 0, z = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) pc += __popcll(ra[k] & rb[k]);
+  block_sum2(pc, z, red);
+  __syncthreads();  // smem reuse
+  return pc;
+}
+
 
 }  // namespace rsd

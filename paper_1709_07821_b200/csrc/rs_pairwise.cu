@@ -23,6 +23,7 @@
 #include "rs_array.cuh"
 #include "rs_bitset.cuh"
 #include "rs_array_large.cuh"
+#include "rs_single.h"
 
 using namespace rs;
 
@@ -585,63 +586,16 @@ __global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__res
   for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
   const Item cur = nxt;
   if (item + gridDim.x < total) nxt = fetch(item + gridDim.x);
-  const uint32_t e = cur.e, ca = cur.ca, cb = cur.cb;
-  uint8_t ta = cur.ta, tb = cur.tb;
-  uint64_t ra[4], rb[4];
-  if (!GEN) {
-    ld_words(A.pool, A.off[ca], t, ra);
-    ld_words(B.pool, B.off[cb], t, rb);
-  } else {
-    bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      if (da) sm.X[4 * t + k] = 0;
-      if (db) sm.Y[4 * t + k] = 0;
-    }
-    __syncthreads();
-    if (da) scatter_container(A, ca, ta, sm.X);
-    if (db) scatter_container(B, cb, tb, sm.Y);
-    __syncthreads();
-    if (da) { for (int k = 0; k < 4; k++) ra[k] = sm.X[4 * t + k]; } else ld_words(A.pool, A.off[ca], t, ra);
-    if (db) { for (int k = 0; k < 4; k++) rb[k] = sm.Y[4 * t + k]; } else ld_words(B.pool, B.off[cb], t, rb);
-  }
-  uint64_t r[4];
-  uint32_t pc = 0, nr = 0;
-#pragma unroll
-  for (int k = 0; k < 4; k++) {
-    r[k] = rs_word_op(op, ra[k], rb[k]);
-    pc += __popcll(r[k]);
-  }
-  const bool consider = GEN && rs_consider_run(ta, tb, op);
-  if (consider) {
-#pragma unroll
-    for (int k = 0; k < 4; k++) sm.X[4 * t + k] = r[k];
-    __syncthreads();
-    uint64_t prev = t ? sm.X[4 * t - 1] : 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      uint64_t cin = (k ? r[k - 1] : prev) >> 63;
-      nr += __popcll(r[k] & ~((r[k] << 1) | cin));  // _run_count_of_words, containers.py:173-178
-    }
-  }
-  uint32_t card = pc, nruns = nr;
-  block_sum2(card, nruns, sm.red);
+  const uint32_t e = cur.e;
   uint8_t type;
-  if (card == 0) type = RS_TAG_ARRAY;
-  else if (consider && rs_run_admissible(card, nruns)) type = RS_TAG_RUN;  // container_normalize
-  else type = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;       // from_words / from_values
-  uint32_t n = 0;
-  if (card) {
-    __syncthreads();  // smem Y may still be read by the densify phase
-    n = encode_result(sm, r, pc, card, type, opool + E.off[e]);
-  }
+  uint32_t n;
+  const uint32_t card = dense_pair<GEN>(op, A, cur.ca, cur.ta, B, cur.cb, cur.tb, sm, opool + E.off[e], type, n);
   if (t == 0) {
     O.type[e] = type;
     O.card[e] = card;
     O.n[e] = n;
     if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
   }
-  __syncthreads();  // smem reuse by the next item
   }
 }
 
@@ -658,30 +612,9 @@ __global__ void __launch_bounds__(DT) k_pair_count(int op, const uint32_t *__res
   const uint32_t total = *cnt;
   for (uint32_t i = blockIdx.x; i < total; i += gridDim.x) {
     const uint32_t ca = lca[i], cb = lcb[i];
-    uint64_t ra[4], rb[4];
-    if (!GEN) {
-      ld_words(A.pool, A.off[ca], t, ra);
-      ld_words(B.pool, B.off[cb], t, rb);
-    } else {
-      uint8_t ta = A.type[ca], tb = B.type[cb];
-      bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
-      for (int k = 0; k < 4; k++) {
-        if (da) X[4 * t + k] = 0;
-        if (db) Y[4 * t + k] = 0;
-      }
-      __syncthreads();
-      if (da) scatter_container(A, ca, ta, X);
-      if (db) scatter_container(B, cb, tb, Y);
-      __syncthreads();
-      if (da) { for (int k = 0; k < 4; k++) ra[k] = X[4 * t + k]; } else ld_words(A.pool, A.off[ca], t, ra);
-      if (db) { for (int k = 0; k < 4; k++) rb[k] = Y[4 * t + k]; } else ld_words(B.pool, B.off[cb], t, rb);
-    }
-    uint32_t pc = 0, z = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) pc += __popcll(rs_word_op(op, ra[k], rb[k]));
-    block_sum2(pc, z, red);
+    const uint8_t ta = GEN ? A.type[ca] : (uint8_t)RS_TAG_BITSET, tb = GEN ? B.type[cb] : (uint8_t)RS_TAG_BITSET;
+    const uint32_t pc = dense_and_count<GEN>(A, ca, ta, B, cb, tb, X, Y, red);
     if (t == 0 && pc) atomicAdd((unsigned long long *)&acc[lpair[i]], (unsigned long long)pc);
-    __syncthreads();
   }
 }
 
@@ -1740,6 +1673,14 @@ ClassMask class_mask(uint8_t ma, uint8_t mb, int op) {
 }
 
 // container types an op result may hold (run results need a run input)
+// single-pair calls with at most this many result slots take the one-launch
+// path (its last CTA compacts the slots alone); RS_SINGLE=0 turns it off
+constexpr uint32_t SINGLE_MAX_SLOTS = 4096;
+bool single_path_on() {
+  static const bool on = env_int("RS_SINGLE", 1) != 0;
+  return on;
+}
+
 uint8_t result_mask(uint8_t ma, uint8_t mb) {
   const uint8_t AR = 1 << RS_TAG_ARRAY, BS = 1 << RS_TAG_BITSET, RN = 1 << RS_TAG_RUN;
   return (uint8_t)(AR | BS | ((ma | mb) & RN));
@@ -1993,8 +1934,30 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   }
   // Upper-bound mode (no host sync) when an 8 KB slot per possible output
   // container costs at most ~2x the inputs' pools; else size exactly.
-  const bool ub_mode = env_int("RS_EXACT_ALLOC", 0) == 0 &&
-                       8192.0 * (double)Ecap <= 2.0 * (double)(A->pool_bytes + B->pool_bytes) + 64e6;
+  auto ub_affordable = [&](uint64_t slots) {
+    return 8192.0 * (double)slots <= 2.0 * (double)(A->pool_bytes + B->pool_bytes) + 64e6;
+  };
+  if (npairs == 1 && single_path_on()) {  // one pair of small bitmaps: one launch (rs_single.cu)
+    const uint32_t a = ia ? ia[0] : 0, b = ib ? ib[0] : 0;
+    const uint32_t E = single_pair_slots(op, (uint32_t)(A->h_bm_start[a + 1] - A->h_bm_start[a]),
+                                         (uint32_t)(B->h_bm_start[b + 1] - B->h_bm_start[b]));
+    if (E <= SINGLE_MAX_SLOTS && ub_affordable(E) && env_int("RS_EXACT_ALLOC", 0) == 0) {
+      const uint64_t P = 8192ull * std::max<uint32_t>(E, 1);
+      RS_TRY(ub_reserve(P));
+      rs_batch *r = new rs_batch();
+      int rc = batch_alloc(r, 1, E, P);
+      if (!rc) {
+        ub_register(r);
+        r->type_mask = result_mask(A->type_mask, B->type_mask);
+        rc = single_pair_op(op, A, B, a, b, r);
+      }
+      if (rc) { rs_batch_free(r); return rc; }
+      r->h_valid = false;
+      *out = r;
+      return RS_OK;
+    }
+  }
+  const bool ub_mode = env_int("RS_EXACT_ALLOC", 0) == 0 && ub_affordable(Ecap);
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
   std::vector<uint64_t> hb;
@@ -2274,6 +2237,18 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
     RS_TRY(resolve_pending(B));
   }
   RS_TRY(check_pairs(A, B, ia, ib, npairs));
+  if (npairs == 1 && single_path_on()) {  // one pair of small bitmaps: one launch (rs_single.cu)
+    const uint32_t a = ia ? ia[0] : 0, b = ib ? ib[0] : 0;
+    if (A->h_bm_start[a + 1] - A->h_bm_start[a] <= SINGLE_MAX_SLOTS) {
+      if (counts_on_device) return single_pair_count(op, A, B, a, b, counts);
+      thread_local uint64_t *h = nullptr;  // page-locked: the kernel writes the count there
+      if (!h) RS_CK(cudaMallocHost(&h, 64));
+      RS_TRY(single_pair_count(op, A, B, a, b, h));
+      RS_CK(cudaStreamSynchronize(g_stream));
+      *counts = *(volatile uint64_t *)h;
+      return RS_OK;
+    }
+  }
   Scratch S;
   uint64_t Ma = 0, maxk = 0;
   for (uint64_t p = 0; p < npairs; p++) {
