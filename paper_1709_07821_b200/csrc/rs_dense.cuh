@@ -31,7 +31,26 @@ static __device__ void scatter_container(const DevBatch &S, uint32_t c, uint8_t 
   uint32_t n = S.n[c];
   uint32_t *X32 = (uint32_t *)X;
   if (type == RS_TAG_ARRAY) {
-    for (uint32_t i = threadIdx.x; i < n; i += DT) atomicOr(&X32[v[i] >> 5], 1u << (v[i] & 31));
+    // 16-byte vectors (payloads are 16-byte aligned and padded), a thread's
+    // two loads issued before its ORs: one DRAM round trip for <= 4096
+    // values instead of one per loop iteration
+    const uint4 *v4 = (const uint4 *)v;
+    const uint32_t nv = (n + 7) >> 3;
+    for (uint32_t k0 = threadIdx.x; k0 < nv; k0 += 2 * DT) {
+      const uint4 x[2] = {__ldg(v4 + k0), k0 + DT < nv ? __ldg(v4 + k0 + DT) : make_uint4(0, 0, 0, 0)};
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const uint32_t k = k0 + DT * j;
+        if (k >= nv) break;
+        const uint32_t w[4] = {x[j].x, x[j].y, x[j].z, x[j].w}, left = n - 8 * k;
+#pragma unroll
+        for (int h = 0; h < 8; h++)
+          if ((uint32_t)h < left) {
+            const uint32_t val = (w[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+            atomicOr(&X32[val >> 5], 1u << (val & 31));
+          }
+      }
+    }
     return;
   }
   // one thread per run: the (start, length) loads of all runs are independent

@@ -2030,9 +2030,12 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   if (M)
     RS_LAUNCH(k_merge, grid_for(M, 256), 256, 0, M, npairs, mbase, dA, dB, dia, dib, op, mkey, mca, mcb, mpair, keep,
               ub);
+  host_mark(10);
   RS_TRY(scan_exclusive<uint32_t>(keep, epos, M + 1));
   RS_TRY(scan_exclusive<uint64_t>(ub, uoff, M + 1));
+  host_mark(11);
   RS_LAUNCH(k_emit, grid_for(M, 256), 256, 0, M, keep, epos, uoff, mkey, mca, mcb, mpair, dA, dB, En, L, op);
+  host_mark(12);
   if (ub_mode)
     return run_classes_and_compact(op, A, B, S, En, L, M, 8192 * std::max<uint64_t>(Ecap, 1), nullptr, epos + M,
                                    mbase, epos, npairs, out);
