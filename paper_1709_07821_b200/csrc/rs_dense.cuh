@@ -171,6 +171,10 @@ static __device__ __forceinline__ void operand_words(const DevBatch &A, uint32_t
     return;
   }
   const bool da = ta != RS_TAG_BITSET, db = tb != RS_TAG_BITSET;
+  // a bitset side's words are requested first: they arrive while the other
+  // side is densified
+  if (!da) ld_words(A.pool, A.off[ca], t, ra);
+  if (!db) ld_words(B.pool, B.off[cb], t, rb);
 #pragma unroll
   for (int k = 0; k < 4; k++) {
     if (da) X[4 * t + k] = 0;
@@ -180,8 +184,8 @@ static __device__ __forceinline__ void operand_words(const DevBatch &A, uint32_t
   if (da) scatter_container(A, ca, ta, X);
   if (db) scatter_container(B, cb, tb, Y);
   __syncthreads();
-  if (da) { for (int k = 0; k < 4; k++) ra[k] = X[4 * t + k]; } else ld_words(A.pool, A.off[ca], t, ra);
-  if (db) { for (int k = 0; k < 4; k++) rb[k] = Y[4 * t + k]; } else ld_words(B.pool, B.off[cb], t, rb);
+  if (da) for (int k = 0; k < 4; k++) ra[k] = X[4 * t + k];
+  if (db) for (int k = 0; k < 4; k++) rb[k] = Y[4 * t + k];
 }
 
 // container_pairwise(op, a, b) of one matched pair by the whole CTA

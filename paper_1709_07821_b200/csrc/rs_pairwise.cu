@@ -914,33 +914,40 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe(int op, const uint32_t
     if (xt != RS_TAG_BITSET) warp_load_member_set(W, xt, X.pool + X.off[cx], X.n[cx], lane);
     const uint32_t want = op == RS_OP_AND ? 1u : 0u;
     uint16_t *out = (uint16_t *)(opool + E.off[e]);
-    // lane l takes values [256c + 8l, 256c + 8l + 8) with one 16-byte load
-    // (payloads are 16-byte aligned and zero-padded); a warp scan of the
-    // per-lane kept counts keeps the output in value order
+    // 512 values per round: lane l takes [512c + 8l, +8) and [512c + 256 +
+    // 8l, +8) with two 16-byte loads (payloads are 16-byte aligned and
+    // zero-padded), the next round's loads issued before this round's 16
+    // probes, so a round costs one probe round trip (4096 values: 8, against
+    // 32 dependent round trips at 256 values with in-round value loads).  A
+    // warp scan of the packed per-lane kept counts (first half | second half
+    // << 16) keeps the output in value order.
     uint32_t base = 0;
-    for (uint32_t c0 = 0; c0 < n; c0 += 256) {
-      const uint32_t j = c0 + 8 * lane;
-      uint4 q = make_uint4(0, 0, 0, 0);
-      if (j < n) q = *(const uint4 *)(vals + j);
-      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    auto ld = [&](uint32_t j) { return j < n ? *(const uint4 *)(vals + j) : make_uint4(0, 0, 0, 0); };
+    uint4 n0 = ld(8 * lane), n1 = ld(256 + 8 * lane);
+    for (uint32_t c0 = 0; c0 < n; c0 += 512) {
+      const uint32_t j0 = c0 + 8 * lane, j1 = j0 + 256;
+      const uint32_t w[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+      n0 = ld(j0 + 512);
+      n1 = ld(j1 + 512);
       uint32_t keepm = 0;
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
+      for (int k = 0; k < 16; k++) {
         const uint32_t v = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
-        if (j + k < n && ((M[v >> 6] >> (v & 63)) & 1) == want) keepm |= 1u << k;
+        if ((k < 8 ? j0 + k : j1 + k - 8) < n && ((M[v >> 6] >> (v & 63)) & 1) == want) keepm |= 1u << k;
       }
-      const uint32_t c = __popc(keepm);
+      const uint32_t c = __popc(keepm & 0xFFu) | (__popc(keepm >> 8) << 16);
       uint32_t x = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
-      uint32_t pos = base + x - c;
+      const uint32_t tot = __shfl_sync(0xffffffffu, x, 31), ex = x - c;
+      uint32_t p0 = base + (ex & 0xFFFFu), p1 = base + (tot & 0xFFFFu) + (ex >> 16);
 #pragma unroll
-      for (int k = 0; k < 8; k++)
-        if (keepm >> k & 1) out[pos++] = (uint16_t)((w[k >> 1] >> (16 * (k & 1))) & 0xFFFF);
-      base += __shfl_sync(0xffffffffu, x, 31);
+      for (int k = 0; k < 16; k++)
+        if (keepm >> k & 1) out[k < 8 ? p0++ : p1++] = (uint16_t)((w[k >> 1] >> (16 * (k & 1))) & 0xFFFF);
+      base += (tot & 0xFFFFu) + (tot >> 16);
     }
     const uint32_t padded = (uint32_t)(rs_pad16(2ull * base) >> 1);
     for (uint32_t k = base + lane; k < padded; k += 32) out[k] = 0;
@@ -975,13 +982,17 @@ __global__ void __launch_bounds__(32 * PRB_WARPS) k_probe_count(const uint32_t *
     const uint64_t *M = xt == RS_TAG_BITSET ? (const uint64_t *)(X.pool + X.off[cx]) : W;
     if (xt != RS_TAG_BITSET) warp_load_member_set(W, xt, X.pool + X.off[cx], X.n[cx], lane);
     uint32_t c = 0;
-    for (uint32_t j = 8 * lane; j < n; j += 256) {
-      const uint4 q = *(const uint4 *)(vals + j);
-      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    // (the rounds of k_probe: 512 values, the next round's loads in flight)
+    auto ld = [&](uint32_t j) { return j < n ? *(const uint4 *)(vals + j) : make_uint4(0, 0, 0, 0); };
+    uint4 n0 = ld(8 * lane), n1 = ld(256 + 8 * lane);
+    for (uint32_t j0 = 8 * lane; j0 - 8 * lane < n; j0 += 512) {
+      const uint32_t w[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+      n0 = ld(j0 + 512);
+      n1 = ld(j0 + 768);
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
+      for (int k = 0; k < 16; k++) {
         const uint32_t v = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
-        c += j + k < n ? (uint32_t)((M[v >> 6] >> (v & 63)) & 1) : 0u;
+        c += (k < 8 ? j0 + k : j0 + 248 + k) < n ? (uint32_t)((M[v >> 6] >> (v & 63)) & 1) : 0u;
       }
     }
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
