@@ -12,7 +12,7 @@ A = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, 0, n))
 B = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, n, 2 * n))
 import torch
 dev_out = torch.empty(n, dtype=torch.int64, device="cuda")
-names = ["array_pair_s", "array_pair_m", "array_pair_l", "generic_pair", "copy",
+names = ["array_pair_s", "array_pair_m", "array_pair_l", "array_pair_g", "generic_pair", "copy",
          "array_count_s", "array_count_m", "array_count_l"]
 for op in ("and", "or", "andnot", "xor"):
     for kind in ("op", "count"):
