@@ -81,6 +81,7 @@ struct LargeSmem {
   uint32_t ring;  // ring bytes
   __device__ __forceinline__ uint32_t *XA() const { return (uint32_t *)X; }
   __device__ __forceinline__ uint32_t *XB() const { return (uint32_t *)(X + 8192); }
+  __device__ __forceinline__ uint32_t *Xn(int i) const { return (uint32_t *)(X + 8192 * i); }
   __device__ __forceinline__ uint8_t *R() const { return ring_base; }
 };
 
@@ -104,20 +105,23 @@ constexpr int large_min_blocks(int op) {
 // ANDNOT 1.90 -> 1.79 ms), nor did 16 item slots.  large_loop traps if the ring is ever under 16 KB, the largest item
 // (an item that does not fit before the end of the ring waits for the ring to
 // drain and starts at 0).  RS_AAL_SMEM_KB overrides (tuning).
+// The AND op kernel holds two more bitsets (the dual-bitset pairs below):
+// 72 KB, which its three CTAs per SM (register-bound) fit.
+constexpr int large_nbits(int op, bool count) { return op == RS_OP_AND && !count ? 4 : 2; }
 constexpr size_t large_smem_bytes(int op, bool count) {
 #ifdef RS_AAL_SMEM_KB
-  return (size_t)RS_AAL_SMEM_KB * 1024 + 0 * op + 0 * count;
+  return (size_t)RS_AAL_SMEM_KB * 1024 + 8192 * (large_nbits(op, count) - 2);
 #else
-  return (size_t)56 * 1024 + 0 * op + 0 * count;
+  return (size_t)56 * 1024 + 8192 * (large_nbits(op, count) - 2);
 #endif
 }
 
-__device__ __forceinline__ LargeSmem large_layout(uint8_t *raw, uint32_t bytes) {
+__device__ __forceinline__ LargeSmem large_layout(uint8_t *raw, uint32_t bytes, int nbits) {
   LargeSmem sm;
   sm.h = (LargeHdr *)raw;
   const uint32_t b = rsb::smem_u32(raw);
   const uint32_t r0 = (b + (uint32_t)sizeof(LargeHdr) + 127u) & ~127u;
-  const uint32_t x = (b + bytes - 16384u) & ~8191u;
+  const uint32_t x = (b + bytes - 8192u * nbits) & ~8191u;
   sm.X = raw + (x - b);
   sm.ring_base = raw + (r0 - b);
   sm.ring = x > r0 ? (x - r0) & ~15u : 0u;
@@ -434,90 +438,26 @@ __device__ __forceinline__ bool bsearch16(const uint16_t *v, uint32_t n, uint32_
   return n && v[lo] == x;
 }
 
-// One pair (the group's threads only; t = thread within the group).
-// `release` (the item's ring slot) is arrived on once by every thread of the
-// group, after that thread's last read of the staged values (a slot's items
-// always go to the same group: k % NSLOT fixes k % NGRP).
-//   and / andnot: two groups: the group's own bitset, cleared after the probe
-//     and fenced by a barrier at the start of the group's next pair; one
-//     group: XA / XB alternate by pair parity, so no fence is needed.
-//   or / xor: the group's bitset (XA with one group); each thread reads and
-//     clears the words it owns (t + LT q) before the cardinality barrier,
-//     which every thread of the group passes before its next scatter; array
-//     results are staged in the same bitset (re-zeroed behind a barrier).
-template <int op, bool COUNT>
-__device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t, const uint16_t *A, uint32_t na,
-                                               const uint16_t *B, uint32_t nb, uint8_t *dst, int parity,
-                                               uint8_t &type, uint32_t &nout, uint64_t *release) {
-  uint32_t *XA = sm.XA(), *XB = sm.XB();
-  uint32_t(*red2)[NROW][WG] = sm.h->red[g];
-  type = RS_TAG_ARRAY;
-  if constexpr (op == RS_OP_AND || op == RS_OP_ANDNOT) {
-    constexpr bool is_and = op == RS_OP_AND;
-    // and: build the smaller side, filter the larger; andnot: build B, filter A
-    const bool build_a = is_and && na <= nb;
-    uint32_t *X = (NGRP == 2 ? g : parity) ? XB : XA;
-    if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
-    {  // galloping pairs (gallop_pair): the small side's values binary-searched in the staged large side
-      const bool a_small = is_and ? na <= nb : true;
-      const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
-      if (16 * ns <= nl) {
-        const uint16_t *Sv = a_small ? A : B, *Lv = a_small ? B : A;
-        uint32_t v[2], k[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const uint32_t i = t + LT * h;  // ns <= 4096 / 16 = 256 = 2 LT
-          v[h] = i < ns ? Sv[i] : 0u;
-          k[h] = i < ns && bsearch16(Lv, nl, v[h]) == is_and;
-        }
-        mbar_arrive(release);  // this thread's last read of the staged values
-        const uint32_t pk[1] = {k[0] | (k[1] << 16)};
-        uint32_t e[1], T[1];
-        gscan<1>(pk, red2[parity], g, t, e, T);
-        const uint32_t n0 = T[0] & 0xFFFFu, total = n0 + (T[0] >> 16);
-        if (!COUNT && dst && total) {
-          uint16_t *d = (uint16_t *)dst;
-          if (k[0]) d[e[0] & 0xFFFFu] = (uint16_t)v[0];
-          if (k[1]) d[n0 + (e[0] >> 16)] = (uint16_t)v[1];
-          const uint32_t padded = (total + 7u) & ~7u;
-          if (t < 8 && total + t < padded) d[total + t] = 0;
-        }
-        nout = total;
-        return total;
-      }
-    }
-    const uint32_t xs = rsb::smem_u32(X);
-    scatter16(build_a ? A : B, build_a ? na : nb, xs, t);
-    gbar(g);
-    uint32_t total;
-    if constexpr (COUNT && is_and)
-      total = probe_count16(build_a ? B : A, build_a ? nb : na, xs, red2[parity][0], g, t, release);
-    else
-      total = probe_filter<is_and ? 1u : 0u>(build_a ? B : A, build_a ? nb : na, xs, (uint16_t *)dst, red2, parity,
-                                             g, t, release);
-    // every probe of X is done (the last chunk's barrier above): clear it
-#pragma unroll
-    for (int q = 0; q < 512 / LT; q++) ((uint4 *)X)[t + LT * q] = make_uint4(0, 0, 0, 0);
-    nout = total;
-    return total;
-  }
-  // or / xor: both arrays into one bitset (shared OR / XOR), so the result
-  // words are read (and cleared) once
-  constexpr bool is_xor = op == RS_OP_XOR;
-  uint32_t *X = (NGRP == 2 && g) ? XB : XA;
-  const uint32_t xs = rsb::smem_u32(X);
-  scatter16<is_xor>(A, na, xs, t);
-  scatter16<is_xor>(B, nb, xs, t);
-  gbar(g);
-  mbar_arrive(release);
+// The result words of a group's bitset X -- or of X AND X2 (DUAL) -- read
+// and cleared (each thread its words t + LT q), the cardinality, and the
+// result at dst: the words (> 4096 values) or their values in order, staged
+// in X.  Ends with X (and X2) zero behind a group barrier.
+template <bool DUAL>
+__device__ __forceinline__ uint32_t sweep_encode(uint32_t *X, uint32_t *X2, uint8_t *dst,
+                                                 uint32_t (*red2)[NROW][WG], int parity, int g, int t, uint8_t &type,
+                                                 uint32_t &nout) {
   // result words t + LT q (conflict-free), positions by a packed row scan
-  uint64_t *X64 = (uint64_t *)X;
+  uint64_t *X64 = (uint64_t *)X, *Y64 = (uint64_t *)X2;
   uint64_t r[QW];
   uint32_t psum = 0;
 #pragma unroll
   for (int q = 0; q < QW; q++) {
     r[q] = X64[t + LT * q];
     X64[t + LT * q] = 0;
+    if constexpr (DUAL) {
+      r[q] &= Y64[t + LT * q];
+      Y64[t + LT * q] = 0;
+    }
     psum += __popcll(r[q]);
   }
   // cardinality first (one warp reduction); the position scan only for an
@@ -577,15 +517,122 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
   return card;
 }
 
-// Persistent, warp-specialized byte ring over items i = blockIdx.x + k*gridDim.x.
+// One pair (the group's threads only; t = thread within the group).
+// `release` (the item's ring slot) is arrived on once by every thread of the
+// group, after that thread's last read of the staged values (a slot's items
+// always go to the same group: k % NSLOT fixes k % NGRP).
+//   and / andnot: two groups: the group's own bitset, cleared after the probe
+//     and fenced by a barrier at the start of the group's next pair; one
+//     group: XA / XB alternate by pair parity, so no fence is needed.
+//   or / xor: the group's bitset (XA with one group); each thread reads and
+//     clears the words it owns (t + LT q) before the cardinality barrier,
+//     which every thread of the group passes before its next scatter; array
+//     results are staged in the same bitset (re-zeroed behind a barrier).
+template <int op, bool COUNT>
+__device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t, const uint16_t *A, uint32_t na,
+                                               const uint16_t *B, uint32_t nb, uint8_t *dst, int parity,
+                                               uint8_t &type, uint32_t &nout, uint64_t *release) {
+  uint32_t *XA = sm.XA(), *XB = sm.XB();
+  uint32_t(*red2)[NROW][WG] = sm.h->red[g];
+  type = RS_TAG_ARRAY;
+  if constexpr (op == RS_OP_AND || op == RS_OP_ANDNOT) {
+    constexpr bool is_and = op == RS_OP_AND;
+    // and: build the smaller side, filter the larger; andnot: build B, filter A
+    const bool build_a = is_and && na <= nb;
+    uint32_t *X = (NGRP == 2 ? g : parity) ? XB : XA;
+    if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
+    {  // galloping pairs (gallop_pair): the small side's values binary-searched in the staged large side
+      const bool a_small = is_and ? na <= nb : true;
+      const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
+      if (16 * ns <= nl) {
+        const uint16_t *Sv = a_small ? A : B, *Lv = a_small ? B : A;
+        uint32_t v[2], k[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint32_t i = t + LT * h;  // ns <= 4096 / 16 = 256 = 2 LT
+          v[h] = i < ns ? Sv[i] : 0u;
+          k[h] = i < ns && bsearch16(Lv, nl, v[h]) == is_and;
+        }
+        mbar_arrive(release);  // this thread's last read of the staged values
+        const uint32_t pk[1] = {k[0] | (k[1] << 16)};
+        uint32_t e[1], T[1];
+        gscan<1>(pk, red2[parity], g, t, e, T);
+        const uint32_t n0 = T[0] & 0xFFFFu, total = n0 + (T[0] >> 16);
+        if (!COUNT && dst && total) {
+          uint16_t *d = (uint16_t *)dst;
+          if (k[0]) d[e[0] & 0xFFFFu] = (uint16_t)v[0];
+          if (k[1]) d[n0 + (e[0] >> 16)] = (uint16_t)v[1];
+          const uint32_t padded = (total + 7u) & ~7u;
+          if (t < 8 && total + t < padded) d[total + t] = 0;
+        }
+        nout = total;
+        return total;
+      }
+    }
+#ifndef RS_AAL_DUAL_MIN
+#define RS_AAL_DUAL_MIN 2048
+#endif
+    if constexpr (is_and && !COUNT && NGRP == 2) {
+      // large AND pairs: both sides scattered (a shared OR per value) into
+      // the group's two bitsets, then one sweep of their AND -- for ~4096 +
+      // 4096 values cheaper than probing one side value by value (address,
+      // load, bit test, ballot, kept-value stores: ~3x a scatter's
+      // instructions per value); the result is at most min(na, nb) values
+      if (na + nb >= RS_AAL_DUAL_MIN) {
+        uint32_t *X2 = sm.Xn(g + 2);
+        scatter16(A, na, rsb::smem_u32(X), t);
+        scatter16(B, nb, rsb::smem_u32(X2), t);
+        gbar(g);
+        mbar_arrive(release);  // this thread's last read of the staged values
+        return sweep_encode<true>(X, X2, dst, red2, parity, g, t, type, nout);
+      }
+    }
+    const uint32_t xs = rsb::smem_u32(X);
+    scatter16(build_a ? A : B, build_a ? na : nb, xs, t);
+    gbar(g);
+    uint32_t total;
+    if constexpr (COUNT && is_and)
+      total = probe_count16(build_a ? B : A, build_a ? nb : na, xs, red2[parity][0], g, t, release);
+    else
+      total = probe_filter<is_and ? 1u : 0u>(build_a ? B : A, build_a ? nb : na, xs, (uint16_t *)dst, red2, parity,
+                                             g, t, release);
+    // every probe of X is done (the last chunk's barrier above): clear it
+#pragma unroll
+    for (int q = 0; q < 512 / LT; q++) ((uint4 *)X)[t + LT * q] = make_uint4(0, 0, 0, 0);
+    nout = total;
+    return total;
+  }
+  // or / xor: both arrays into one bitset (shared OR / XOR), so the result
+  // words are read (and cleared) once
+  constexpr bool is_xor = op == RS_OP_XOR;
+  uint32_t *X = (NGRP == 2 && g) ? XB : XA;
+  const uint32_t xs = rsb::smem_u32(X);
+  scatter16<is_xor>(A, na, xs, t);
+  scatter16<is_xor>(B, nb, xs, t);
+  gbar(g);
+  mbar_arrive(release);
+  return sweep_encode<false>(X, nullptr, dst, red2, parity, g, t, type, nout);
+}
+
+// Persistent, warp-specialized byte ring over items [0, count), taken
+// dynamically: the producer draws the next item index from *ctr (zero at
+// launch).  A static split (item blockIdx.x + k gridDim.x) left the kernel
+// as slow as its latest-starting CTA: run beside the other classes' kernels
+// on side streams, some CTAs found no free SM slot until those finished and
+// then did a full share -- C3 AND measured 1.15 or 1.55 ms from call to
+// call.  The producer ends each consumer group's sequence with a sentinel
+// item (na = LARGE_END).
 // meta_of(i, aoff, boff) -> LargeMeta (runs on the producer lane only);
 // sink(meta, card, type, n) runs on thread 0 of the group that did the pair.
+constexpr uint32_t LARGE_END = 0xFFFFFFFFu;
+constexpr uint32_t LARGE_CHUNK = 4;
 template <int op, bool COUNT, typename MetaOf, typename Sink>
-__device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, const uint8_t *poolB,
+__device__ void large_loop(uint8_t *raw, uint32_t count, uint32_t *ctr, const uint8_t *poolA, const uint8_t *poolB,
                            uint8_t *opool, MetaOf meta_of, Sink sink) {
   const int t = threadIdx.x;
   constexpr uint32_t SMEM = (uint32_t)large_smem_bytes(op, COUNT);
-  const LargeSmem sm = large_layout(raw, SMEM);
+  constexpr int NB = large_nbits(op, COUNT);
+  const LargeSmem sm = large_layout(raw, SMEM, NB);
   if (sm.ring < 2u * 8192u) __trap();  // the largest item (2 x 4096 values) must fit
   if (t == 0) {
     for (int s = 0; s < NSLOT; s++) {
@@ -594,22 +641,44 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int w = t; w < 4 * RS_WORDS; w += LTHREADS) sm.XA()[w] = 0;  // XA and XB
+  for (int w = t; w < 2 * NB * RS_WORDS; w += LTHREADS) sm.XA()[w] = 0;  // every bitset
   __syncthreads();
   if (t >= NCONS) {  // ---------------- producer warp (one elected lane)
     if (t == NCONS) {
-      uint64_t ao, bo;
+      uint64_t ao = 0, bo = 0;
       LargeMeta m;
-      if (blockIdx.x < count) m = meta_of(blockIdx.x, ao, bo);
+      // items are drawn LARGE_CHUNK at a time (one atomic per item on one
+      // counter cost C3's counts 4 %)
+      uint32_t taken = 0, chunk_end = 0;
+      auto take = [&]() -> uint32_t {
+        if (taken == chunk_end) {
+          taken = atomicAdd(ctr, (uint32_t)LARGE_CHUNK);
+          chunk_end = taken + LARGE_CHUNK;
+        }
+        return taken++;
+      };
+      uint32_t i = take();
+      if (i < count) m = meta_of(i, ao, bo);
       uint32_t phys = 0, occ = 0, oldest = 0;  // next free ring byte, bytes held, oldest unreleased item
       for (uint32_t j = 0;; j++) {
-        const uint32_t i = blockIdx.x + j * gridDim.x;
-        if (i >= count) break;
+        if (i >= count) {  // no work left: a sentinel for each consumer group
+          for (int q = 0; q < NGRP; q++, j++) {
+            while (j - oldest >= (uint32_t)NSLOT) {
+              mbar_wait_backoff(&sm.h->empty[oldest % NSLOT], (oldest / NSLOT) & 1);
+              oldest++;
+            }
+            sm.h->meta[j % NSLOT].na = LARGE_END;
+            rsb::mbar_expect_tx(&sm.h->full[j % NSLOT], 0);
+          }
+          break;
+        }
         const int s = j % NSLOT;
-        // metadata of the next item is fetched before waiting for ring space
+        // the next item's index and metadata are fetched before waiting for
+        // ring space
+        const uint32_t ni = take();
         uint64_t nao = 0, nbo = 0;
         LargeMeta nm = m;
-        if (i + gridDim.x < count) nm = meta_of(i + gridDim.x, nao, nbo);
+        if (ni < count) nm = meta_of(ni, nao, nbo);
         const uint32_t ba = (uint32_t)rs_pad16(2ull * m.na), bb = (uint32_t)rs_pad16(2ull * m.nb);
         const uint32_t need = ba + bb;
         uint32_t pos = phys, skip = 0;
@@ -648,14 +717,13 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
         m = nm;
         ao = nao;
         bo = nbo;
+        i = ni;
       }
     }
     return;
   }
   const int g = t / LT, tg = t % LT;
   for (uint32_t k = g;; k += NGRP) {  // ---------------- consumer group g
-    const uint32_t i = blockIdx.x + k * gridDim.x;
-    if (i >= count) break;
     const int s = k % NSLOT;
 #ifdef RS_AAL_SPIN
     rsb::mbar_wait(&sm.h->full[s], (k / NSLOT) & 1);
@@ -665,6 +733,7 @@ __device__ void large_loop(uint8_t *raw, uint32_t count, const uint8_t *poolA, c
     mbar_wait_backoff(&sm.h->full[s], (k / NSLOT) & 1);
 #endif
     const LargeMeta m = sm.h->meta[s];
+    if (m.na == LARGE_END) break;
     uint8_t type;
     uint32_t n;
     const uint32_t card = large_pair<op, COUNT>(sm, g, tg, (const uint16_t *)(sm.R() + m.aoff), m.na,

@@ -30,6 +30,9 @@ using namespace rs;
 namespace {
 
 enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, CLS_PRB = 6, CLS_AAG = 7, NCLS = 8 };
+// counters after the class sizes: [NCLS, NCLS + 1] fused-scan arrivals,
+// [CNT_LARGE] the large-pair kernel's dynamic item counter (all zeroed per op)
+constexpr int CNT_LARGE = NCLS + 2;
 
 struct Entries {
   uint16_t *key;
@@ -752,8 +755,8 @@ __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(OP)) k_aa
                                                                const uint64_t *__restrict__ laoff,
                                                                const uint64_t *__restrict__ lboff,
                                                                const uint32_t *__restrict__ lnab,
-                                                               const uint32_t *__restrict__ cnt, DevBatch A,
-                                                               DevBatch B, Entries E, OutDesc O,
+                                                               const uint32_t *__restrict__ cnt, uint32_t *ctr,
+                                                               DevBatch A, DevBatch B, Entries E, OutDesc O,
                                                                uint8_t *__restrict__ opool,
                                                                uint64_t *__restrict__ res_card) {
   extern __shared__ __align__(128) uint8_t smraw[];
@@ -775,15 +778,15 @@ __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(OP)) k_aa
     O.n[m.e] = n;
     if (card) atomicAdd((unsigned long long *)&res_card[m.pair], (unsigned long long)card);
   };
-  rsl::large_loop<OP, false>(smraw, *cnt, A.pool, B.pool, opool, meta_of, sink);
+  rsl::large_loop<OP, false>(smraw, *cnt, ctr, A.pool, B.pool, opool, meta_of, sink);
 }
 
 __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(-1)) k_aa_large_count(const uint64_t *__restrict__ laoff,
                                                                   const uint64_t *__restrict__ lboff,
                                                                   const uint32_t *__restrict__ lnab,
                                                                   const uint32_t *__restrict__ lpair,
-                                                                  const uint32_t *__restrict__ cnt, DevBatch A,
-                                                                  DevBatch B, uint64_t *__restrict__ acc) {
+                                                                  const uint32_t *__restrict__ cnt, uint32_t *ctr,
+                                                                  DevBatch A, DevBatch B, uint64_t *__restrict__ acc) {
   extern __shared__ __align__(128) uint8_t smraw[];
   auto meta_of = [&](uint32_t i, uint64_t &ao, uint64_t &bo) {
     rsl::LargeMeta m;
@@ -800,7 +803,7 @@ __global__ void __launch_bounds__(rsl::LTHREADS, rsl::large_min_blocks(-1)) k_aa
   auto sink = [&](const rsl::LargeMeta &m, uint32_t card, uint8_t, uint32_t) {
     if (card) atomicAdd((unsigned long long *)&acc[m.pair], (unsigned long long)card);  // one thread per pair
   };
-  rsl::large_loop<RS_OP_AND, true>(smraw, *cnt, A.pool, B.pool, nullptr, meta_of, sink);
+  rsl::large_loop<RS_OP_AND, true>(smraw, *cnt, ctr, A.pool, B.pool, nullptr, meta_of, sink);
 }
 
 template <typename K>
@@ -824,7 +827,8 @@ int launch_aa_large_op_t(const Lists &L, uint64_t n, DevBatch dA, DevBatch dB, E
   }
   RS_LAUNCH_PROF("array_pair_l", exact ? n : 0, k_aa_large_op<OP>,
                  persistent_grid_t(k_aa_large_op<OP>, rsl::LTHREADS, smem, n), rsl::LTHREADS, smem, L.list[CLS_AAL],
-                 L.aoff + L.cap, L.boff + L.cap, L.nab, L.cnt + CLS_AAL, dA, dB, En, O, pool, res_card);
+                 L.aoff + L.cap, L.boff + L.cap, L.nab, L.cnt + CLS_AAL, L.cnt + CNT_LARGE, dA, dB, En, O, pool,
+                 res_card);
   return RS_OK;
 }
 
@@ -847,7 +851,7 @@ int launch_aa_large_count(const Lists &L, uint32_t *lpair, DevBatch dA, DevBatch
   }
   RS_LAUNCH_PROF("array_count_l", 0, k_aa_large_count,
                  persistent_grid_t(k_aa_large_count, rsl::LTHREADS, smem, L.cap), rsl::LTHREADS, smem,
-                 L.aoff + L.cap, L.boff + L.cap, L.nab, lpair, L.cnt + CLS_AAL, dA, dB, inter);
+                 L.aoff + L.cap, L.boff + L.cap, L.nab, lpair, L.cnt + CLS_AAL, L.cnt + CNT_LARGE, dA, dB, inter);
   return RS_OK;
 }
 
@@ -2007,7 +2011,7 @@ Lists make_lists(Scratch &S, uint64_t cap) {
   Lists L;
   L.cap = cap ? cap : 1;
   for (int c = 0; c < NCLS; c++) L.list[c] = (uint32_t *)S.get(L.cap * 4);
-  L.cnt = (uint32_t *)S.get((NCLS + 2) * 4);  // + the fused-scan arrival counters
+  L.cnt = (uint32_t *)S.get((NCLS + 3) * 4);  // + the fused-scan arrival counters, the large-pair item counter
   L.aoff = (uint64_t *)S.get(2 * L.cap * 8);  // [0,cap): bitset class, [cap,2cap): large-array class
   L.boff = (uint64_t *)S.get(2 * L.cap * 8);
   L.nab = (uint32_t *)S.get(L.cap * 4);
@@ -2066,7 +2070,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   std::vector<uint64_t> hb;
   const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 0, hb);
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint16_t *mkey = (uint16_t *)S.get((M + 1) * 2);
@@ -2163,7 +2167,7 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   Scratch S;
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
   Entries En;
   En.key = (uint16_t *)S.get((npairs + 1) * 2);
   En.ca = (uint32_t *)S.get((npairs + 1) * 4);
@@ -2368,7 +2372,7 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   std::vector<uint64_t> hb;
   const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 1, hb);
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   const size_t top0 = Scratch::top;
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
@@ -2516,7 +2520,7 @@ extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, cons
   Scratch S;
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 2) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   Lists L = make_lists(S, npairs);
   uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);

@@ -8,6 +8,8 @@ from paper_1709_07821_b200 import _lib
 import workloads as synth
 import torch
 n = 1_000_000
+REPS = int(os.environ.get("REPS", "7"))
+SPREAD = os.environ.get("SPREAD") == "1"
 buf, offs = synth.config3(npairs=n)
 A = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, 0, n))
 B = rb.BitmapBatch.from_wire(synth.slice_images(buf, offs, n, 2 * n))
@@ -21,8 +23,10 @@ for op in ("and", "or", "andnot", "xor"):
             f()
         _lib.synchronize()
         ts = []
-        for _ in range(7):
+        for _ in range(REPS):
             e0 = _lib.Event(); f(); e1 = _lib.Event()
             ts.append(e0.elapsed_ms(e1))
         out[op + ("" if kind == "op" else "_c")] = round(statistics.median(ts), 3)
+        if SPREAD:
+            print(op, kind, " ".join(f"{x:.3f}" for x in ts))
 print(out, "sum", round(sum(out.values()), 3))
