@@ -31,8 +31,9 @@ namespace {
 
 enum { CLS_COPY = 0, CLS_BB = 1, CLS_AAS = 2, CLS_AAM = 3, CLS_AAL = 4, CLS_GEN = 5, CLS_PRB = 6, CLS_AAG = 7, NCLS = 8 };
 // counters after the class sizes: [NCLS, NCLS + 1] fused-scan arrivals,
-// [CNT_LARGE] the large-pair kernel's dynamic item counter (all zeroed per op)
-constexpr int CNT_LARGE = NCLS + 2;
+// [CNT_LARGE], [CNT_GEN] the large-pair and generic-pair kernels' dynamic
+// item counters (all zeroed per op)
+constexpr int CNT_LARGE = NCLS + 2, CNT_GEN = NCLS + 3;
 
 struct Entries {
   uint16_t *key;
@@ -561,12 +562,16 @@ using namespace rsd;
 // Materialized pair op over a work list.  GEN=false: bitset x bitset only
 // (bitset_op_with_count + _container_from_words, containers.py:463-465).
 // GEN=true: any matched pair; array/run sides are densified in smem first.
+// ctr (zero at launch; nullptr: static stride) hands out items dynamically:
+// this kernel runs beside the other classes' kernels, and a CTA that found
+// no free SM slot until they finished took a full static share late.
 template <bool GEN>
 __global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__restrict__ list,
-                                                   const uint32_t *__restrict__ cnt, DevBatch A, DevBatch B,
-                                                   Entries E, OutDesc O, uint8_t *__restrict__ opool,
+                                                   const uint32_t *__restrict__ cnt, uint32_t *ctr, DevBatch A,
+                                                   DevBatch B, Entries E, OutDesc O, uint8_t *__restrict__ opool,
                                                    uint64_t *__restrict__ res_card) {
   __shared__ __align__(16) DenseSmem sm;
+  __shared__ uint32_t s_init[2], s_take[2];
   const int t = threadIdx.x;
   const uint32_t total = *cnt;
   // the next item's metadata chain (list -> entry -> containers) is loaded
@@ -584,21 +589,34 @@ __global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__res
     m.tb = GEN ? B.type[m.cb] : (uint8_t)RS_TAG_BITSET;
     return m;
   };
-  Item nxt;
-  if (blockIdx.x < total) nxt = fetch(blockIdx.x);
-  for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-  const Item cur = nxt;
-  if (item + gridDim.x < total) nxt = fetch(item + gridDim.x);
-  const uint32_t e = cur.e;
-  uint8_t type;
-  uint32_t n;
-  const uint32_t card = dense_pair<GEN>(op, A, cur.ca, cur.ta, B, cur.cb, cur.tb, sm, opool + E.off[e], type, n);
-  if (t == 0) {
-    O.type[e] = type;
-    O.card[e] = card;
-    O.n[e] = n;
-    if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+  uint32_t item = blockIdx.x, next = blockIdx.x + gridDim.x;
+  if (ctr) {
+    if (t == 0) {
+      s_init[0] = atomicAdd(ctr, 1u);
+      s_init[1] = atomicAdd(ctr, 1u);
+    }
+    __syncthreads();
+    item = s_init[0];
+    next = s_init[1];
   }
+  Item nxt;
+  if (item < total) nxt = fetch(item);
+  for (int par = 0; item < total; par ^= 1) {
+    const Item cur = nxt;
+    if (next < total) nxt = fetch(next);
+    if (ctr && t == 0) s_take[par] = atomicAdd(ctr, 1u);  // the item after next (read behind dense_pair's barriers)
+    const uint32_t e = cur.e;
+    uint8_t type;
+    uint32_t n;
+    const uint32_t card = dense_pair<GEN>(op, A, cur.ca, cur.ta, B, cur.cb, cur.tb, sm, opool + E.off[e], type, n);
+    if (t == 0) {
+      O.type[e] = type;
+      O.card[e] = card;
+      O.n[e] = n;
+      if (card) atomicAdd((unsigned long long *)&res_card[E.pair[e]], (unsigned long long)card);
+    }
+    item = next;
+    next = ctr ? s_take[par] : next + gridDim.x;
   }
 }
 
@@ -1862,7 +1880,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     F.next();
     if (bb_kernel_choice() == 0) {
       RS_LAUNCH_PROF("bitset_pair", hcnt ? n : 0, k_pair_dense<false>, std::min<uint64_t>(n, sms * 6), DT, 0, op,
-                     L.list[CLS_BB], L.cnt + CLS_BB, dA, dB, En, O, b->d_pool, res_card);
+                     L.list[CLS_BB], L.cnt + CLS_BB, (uint32_t *)nullptr, dA, dB, En, O, b->d_pool, res_card);
     } else {
       switch (bb_stages()) {
         case 3: RS_TRY(launch_bb_op<3>(op, L, n, dA, dB, En, O, b->d_pool, res_card)); break;
@@ -1928,7 +1946,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   if (uint64_t n = n_gen) {
     F.next();
     RS_LAUNCH_PROF("generic_pair", hcnt ? n : 0, k_pair_dense<true>, std::min<uint64_t>(n, sms * 8), DT, 0, op,
-                   L.list[CLS_GEN], L.cnt + CLS_GEN, dA, dB, En, O, b->d_pool, res_card);
+                   L.list[CLS_GEN], L.cnt + CLS_GEN, L.cnt + CNT_GEN, dA, dB, En, O, b->d_pool, res_card);
   }
   if (uint64_t n = n_prb) {
     F.next();
@@ -2011,7 +2029,7 @@ Lists make_lists(Scratch &S, uint64_t cap) {
   Lists L;
   L.cap = cap ? cap : 1;
   for (int c = 0; c < NCLS; c++) L.list[c] = (uint32_t *)S.get(L.cap * 4);
-  L.cnt = (uint32_t *)S.get((NCLS + 3) * 4);  // + the fused-scan arrival counters, the large-pair item counter
+  L.cnt = (uint32_t *)S.get((NCLS + 4) * 4);  // + the fused-scan arrival counters, the large-pair item counter
   L.aoff = (uint64_t *)S.get(2 * L.cap * 8);  // [0,cap): bitset class, [cap,2cap): large-array class
   L.boff = (uint64_t *)S.get(2 * L.cap * 8);
   L.nab = (uint32_t *)S.get(L.cap * 4);
@@ -2070,7 +2088,7 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   std::vector<uint64_t> hb;
   const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 0, hb);
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 4) * 4);
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint64_t *mbase = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
   uint16_t *mkey = (uint16_t *)S.get((M + 1) * 2);
@@ -2167,7 +2185,7 @@ extern "C" int rs_container_pairwise(int op, const rs_batch *A, const rs_batch *
   Scratch S;
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 4) * 4);
   Entries En;
   En.key = (uint16_t *)S.get((npairs + 1) * 2);
   En.ca = (uint32_t *)S.get((npairs + 1) * 4);
@@ -2372,7 +2390,7 @@ extern "C" int rs_pairwise_cardinality(int op, const rs_batch *A, const rs_batch
   std::vector<uint64_t> hb;
   const bool hbases = pair_bases_host(A, B, ia, ib, npairs, 1, hb);
   const size_t o_mb = hbases ? U.add(hb.data(), (npairs + 1) * 8) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 4) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   const size_t top0 = Scratch::top;
   uint64_t *msz = hbases ? nullptr : (uint64_t *)S.get((npairs + 1) * 8);
@@ -2520,7 +2538,7 @@ extern "C" int rs_container_pairwise_cardinality(int op, const rs_batch *A, cons
   Scratch S;
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
-  const size_t o_cnt = U.add(nullptr, (NCLS + 3) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 4) * 4);
   const size_t o_inter = npairs <= 16384 ? U.add(nullptr, (npairs + 1) * 8) : Upload::NONE;
   Lists L = make_lists(S, npairs);
   uint32_t *lcb = (uint32_t *)S.get(NCLS * L.cap * 4), *lpair = (uint32_t *)S.get(NCLS * L.cap * 4);
