@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(DT) k_union_fold(const uint32_t *__restrict__ 
   __shared__ uint64_t mo[DT];   // contributor payload offset
   __shared__ uint32_t mn[DT];   // contributor n
   __shared__ uint8_t mt[DT];    // contributor type
+  __shared__ uint32_t mc[DT];   // contributor cardinality
   __shared__ uint32_t next_li;
   const int t = threadIdx.x;
   uint32_t *X32 = (uint32_t *)sm.X;
@@ -180,13 +181,14 @@ __global__ void __launch_bounds__(DT) k_union_fold(const uint32_t *__restrict__ 
       mt[t] = S.type[c];
       mo[t] = S.off[c];
       mn[t] = S.n[c];
+      mc[t] = S.card[c];
     }
 #pragma unroll
     for (int k = 0; k < 4; k++) sm.X[4 * t + k] = 0;
     __syncthreads();
-    auto meta = [&](uint32_t i, uint8_t &ty, uint64_t &of, uint32_t &n) {
-      if (i - s < DT) { ty = mt[i - s]; of = mo[i - s]; n = mn[i - s]; }
-      else { const uint32_t c = item_c[i]; ty = S.type[c]; of = S.off[c]; n = S.n[c]; }
+    auto meta = [&](uint32_t i, uint8_t &ty, uint64_t &of, uint32_t &n, uint32_t &cd) {
+      if (i - s < DT) { ty = mt[i - s]; of = mo[i - s]; n = mn[i - s]; cd = mc[i - s]; }
+      else { const uint32_t c = item_c[i]; ty = S.type[c]; of = S.off[c]; n = S.n[c]; cd = S.card[c]; }
     };
     auto load = [&](uint64_t of, uint32_t nu, uint4 &q0, uint4 &q1) {
       const uint4 *p = (const uint4 *)(S.pool + of);
@@ -195,30 +197,52 @@ __global__ void __launch_bounds__(DT) k_union_fold(const uint32_t *__restrict__ 
     };
     uint8_t ty;
     uint64_t of;
-    uint32_t n;
-    meta(s, ty, of, n);
+    uint32_t n, cd;
+    meta(s, ty, of, n, cd);
     uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
     load(of, units_of(ty, n), q0, q1);
+    // The type decisions of the sequence need the running union's card and
+    // run count only where bounds cannot settle them: card lies in
+    // [max of the contributors' cards, sum of them], the run count is at most
+    // the contributors' runs (an array value is a run).  A step the bounds
+    // decide takes no barrier -- the shared ORs of consecutive steps commute
+    // -- and only an undecided one synchronizes and sweeps the words.
     uint8_t acc = ty;  // acc = copy(c0); arrays / runs only in this list
+    uint32_t card_lo = cd, card_hi = cd, runs_hi = ty == RS_TAG_RUN ? n : cd;
     for (uint32_t i = s; i < e; i++) {
       const uint8_t cty = ty;
-      const uint32_t cn = n, cu = units_of(cty, cn);
+      const uint32_t cn = n, cu = units_of(cty, cn), ccd = cd;
       const uint4 c0q = q0, c1q = q1;
       if (i + 1 < e) {  // the next contributor's payload, in flight during this step
-        meta(i + 1, ty, of, n);
+        meta(i + 1, ty, of, n, cd);
         load(of, units_of(ty, n), q0, q1);
       }
       if ((uint32_t)t < cu) scatter_unit(c0q, t, cn, cty == RS_TAG_ARRAY, X32);
       if ((uint32_t)t + DT < cu) scatter_unit(c1q, t + DT, cn, cty == RS_TAG_ARRAY, X32);
-      __syncthreads();
       if (i == s || acc == RS_TAG_BITSET) continue;  // nothing to decide
       const bool run_rule = acc == RS_TAG_RUN || cty == RS_TAG_RUN;
-      uint32_t card, nruns;
-      block_card_runs(sm.X, card, nruns, sm.red, run_rule);
-      if (run_rule && rs_run_admissible(card, nruns)) acc = RS_TAG_RUN;
-      else acc = card <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;
+      card_lo = max(card_lo, ccd);
+      card_hi = min(card_hi + ccd, 65536u);
+      runs_hi = min(runs_hi + (cty == RS_TAG_RUN ? cn : ccd), 65536u);
+      if (run_rule) {  // a run iff admissible (containers.py:202-205) for every card in the bounds
+        const bool sure = card_lo > RS_ARRAY_MAX
+                              ? runs_hi <= RS_RUN_MAX_RUNS
+                              : 2 * runs_hi < card_lo && (card_hi <= RS_ARRAY_MAX || runs_hi <= RS_RUN_MAX_RUNS);
+        if (sure) { acc = RS_TAG_RUN; continue; }
+      } else {  // array / bitset by card
+        if (card_hi <= RS_ARRAY_MAX) { acc = RS_TAG_ARRAY; continue; }
+        if (card_lo > RS_ARRAY_MAX) { acc = RS_TAG_BITSET; continue; }
+      }
+      __syncthreads();  // every step's ORs are in
+      uint32_t cexact, nruns;
+      block_card_runs(sm.X, cexact, nruns, sm.red, run_rule);
+      if (run_rule && rs_run_admissible(cexact, nruns)) acc = RS_TAG_RUN;
+      else acc = cexact <= RS_ARRAY_MAX ? RS_TAG_ARRAY : RS_TAG_BITSET;
+      card_lo = card_hi = cexact;
+      if (run_rule) runs_hi = nruns;
       __syncthreads();
     }
+    __syncthreads();  // the last steps' ORs are in
     uint64_t r[4];
     uint32_t pc = 0;
 #pragma unroll
