@@ -1467,6 +1467,55 @@ __global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uin
   }
 }
 
+// ---------------------------------------------- A-indexed join (and / andnot)
+
+// AND and ANDNOT keep a subset of A's keys, in A's order (bitmap.py:169-210,
+// _KEEP_A / _KEEP_B), so a result entry can sit at its A container's
+// position: entry e = abase[p] + i for container i of pair p's A bitmap,
+// with an 8 KB slot at 8192 e.  One thread per A container finds the key in
+// B's keys, writes the entry and appends it to its class list (or marks an
+// AND miss empty); the merged-position join's two scans over both sides'
+// keys and its emit pass are not needed, and the per-pair compaction drops
+// the empty entries.
+__global__ void k_join_a(uint64_t Ea, uint64_t npairs, const uint64_t *__restrict__ abase, DevBatch A, DevBatch B,
+                         const uint32_t *ia, const uint32_t *ib, int op, Entries E, OutDesc O, Lists L) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  bool active = false;
+  int cls = CLS_COPY;
+  uint32_t nab = 0;
+  uint64_t ao = 0, bo = 0;
+  if (t < Ea) {
+    const uint64_t p = find_pair(abase, npairs, t);
+    const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+    const uint64_t b0 = B.bm_start[b];
+    const uint32_t nb = (uint32_t)(B.bm_start[b + 1] - b0);
+    const uint32_t ca = (uint32_t)(A.bm_start[a] + (t - abase[p]));
+    const uint16_t key = A.key[ca];
+    const uint32_t j = lower_bound16(B.key + b0, nb, key);
+    const bool matched = j < nb && B.key[b0 + j] == key;
+    active = matched || op == RS_OP_ANDNOT;
+    if (active) {
+      const uint32_t cb = matched ? (uint32_t)(b0 + j) : RS_NONE;
+      E.key[t] = key;
+      E.ca[t] = ca;
+      E.cb[t] = cb;
+      E.pair[t] = (uint32_t)p;
+      E.off[t] = 8192ull * t;
+      if (matched) {
+        cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
+        if (tma_class(cls)) {
+          ao = A.off[ca];
+          bo = B.off[cb];
+          nab = A.card[ca] | (B.card[cb] << 16);
+        }
+      }
+    } else {
+      O.card[t] = 0;  // an AND miss: nothing kept
+    }
+  }
+  list_append_cta(L, cls, active, (uint32_t)t, ao, bo, nab);
+}
+
 // -------------------------------------------------- count-only join + formula
 
 // count-path append: ca into the class list, cb / pair into parallel arrays
@@ -1823,11 +1872,16 @@ unsigned sm_count() {
 // counter -- the op then runs without any host synchronization.
 int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratch &S, Entries En, Lists L,
                             uint64_t E, uint64_t P, const uint32_t *hcnt, const uint32_t *dE,
-                            const uint64_t *mbase, const uint32_t *epos, uint64_t npairs, rs_batch **out) {
+                            const uint64_t *mbase, const uint32_t *epos, uint64_t npairs, rs_batch **out,
+                            const OutDesc *pre = nullptr) {
   OutDesc O;
-  O.type = (uint8_t *)S.get(E + 1);
-  O.card = (uint32_t *)S.get((E + 1) * 4);
-  O.n = (uint32_t *)S.get((E + 1) * 4);
+  if (pre) {
+    O = *pre;
+  } else {
+    O.type = (uint8_t *)S.get(E + 1);
+    O.card = (uint32_t *)S.get((E + 1) * 4);
+    O.n = (uint32_t *)S.get((E + 1) * 4);
+  }
   uint32_t *keep2 = (uint32_t *)S.get((E + 1) * 4), *fpos = (uint32_t *)S.get((E + 1) * 4);
   if (!S.ok()) { set_error("device allocation failed (op scratch)"); return RS_ENOMEM; }
   host_mark(5);
@@ -2038,6 +2092,43 @@ Lists make_lists(Scratch &S, uint64_t cap) {
 
 }  // namespace
 
+namespace {
+// AND / ANDNOT through the A-indexed join (k_join_a): entries at A's
+// container positions, 8 KB slots, per-pair compaction.  Ea = sum of the
+// pairs' A container counts; npairs <= 16384 (host-computed bases).
+int a_join_op(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib, uint64_t npairs,
+              uint64_t Ea, rs_batch **out) {
+  Scratch S;
+  Upload U;
+  const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
+  std::vector<uint64_t> hb;
+  pair_bases_host(A, B, ia, ib, npairs, 1, hb);  // A-side counts only
+  std::vector<uint32_t> hb32(hb.begin(), hb.end());
+  const size_t o_ab = U.add(hb.data(), (npairs + 1) * 8), o_ab32 = U.add(hb32.data(), (npairs + 1) * 4);
+  const size_t o_cnt = U.add(nullptr, (NCLS + 4) * 4);
+  Entries En;
+  En.key = (uint16_t *)S.get((Ea + 1) * 2);
+  En.ca = (uint32_t *)S.get((Ea + 1) * 4);
+  En.cb = (uint32_t *)S.get((Ea + 1) * 4);
+  En.pair = (uint32_t *)S.get((Ea + 1) * 4);
+  En.off = (uint64_t *)S.get((Ea + 1) * 8);
+  OutDesc O;
+  O.type = (uint8_t *)S.get(Ea + 1);
+  O.card = (uint32_t *)S.get((Ea + 1) * 4);
+  O.n = (uint32_t *)S.get((Ea + 1) * 4);
+  Lists L = make_lists(S, Ea);
+  if (!S.ok()) { set_error("device allocation failed (op)"); return RS_ENOMEM; }
+  RS_TRY(U.commit(S));
+  L.cnt = U.at<uint32_t>(o_cnt);
+  const uint64_t *abase = U.at<uint64_t>(o_ab);
+  RS_LAUNCH(k_join_a, grid_for(Ea, 256), 256, 0, Ea, npairs, abase, A->dev(), B->dev(), U.at<uint32_t>(o_ia),
+            U.at<uint32_t>(o_ib), op, En, O, L);
+  host_mark(4);
+  return run_classes_and_compact(op, A, B, S, En, L, Ea, 8192 * std::max<uint64_t>(Ea, 1), nullptr, nullptr,
+                                 nullptr, U.at<uint32_t>(o_ab32), npairs, out, &O);
+}
+}  // namespace
+
 extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia, const uint32_t *ib,
                            uint64_t npairs, rs_batch **out) {
   host_mark(0);
@@ -2049,11 +2140,12 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   RS_TRY(check_pairs(A, B, ia, ib, npairs));
   host_mark(1);
   Scratch S;
-  uint64_t M = 0, Ecap = 0, maxk = 0;
+  uint64_t M = 0, Ecap = 0, maxk = 0, Ea = 0;
   for (uint64_t p = 0; p < npairs; p++) {
     uint32_t a = ia ? ia[p] : (uint32_t)p, b = ib ? ib[p] : (uint32_t)p;
     uint64_t na = A->h_bm_start[a + 1] - A->h_bm_start[a], nb = B->h_bm_start[b + 1] - B->h_bm_start[b];
     M += na + nb;
+    Ea += na;
     Ecap += op == RS_OP_AND ? std::min(na, nb) : op == RS_OP_ANDNOT ? na : na + nb;
     maxk = std::max(maxk, std::max(na, nb));
   }
@@ -2083,6 +2175,19 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
     }
   }
   const bool ub_mode = env_int("RS_EXACT_ALLOC", 0) == 0 && ub_affordable(Ecap);
+  // per-pair path (CTA per pair, keys in smem, scans over pairs): when the
+  // bitmaps are small enough for smem and there are enough pairs to fill the
+  // GPU (or few positions per pair); a handful of pairs with thousands of keys
+  // each (config 4) keep a thread-per-position join
+  static const int force_pp = env_int("RS_PER_PAIR", -1);  // A/B: 1 forces, 0 disables the per-pair join
+  const bool per_pair = M && maxk <= MERGE_SMEM_KEYS &&
+                        (force_pp >= 0 ? force_pp == 1 : (npairs >= 2 * sm_count() || M <= 1024 * npairs));
+  // AND / ANDNOT otherwise join on A's positions (no scans, no emit pass);
+  // RS_AJOIN=0 keeps the merged-position join
+  static const int ajoin = env_int("RS_AJOIN", 1);
+  if (ajoin && (op == RS_OP_AND || op == RS_OP_ANDNOT) && !per_pair && npairs <= 16384 &&
+      env_int("RS_EXACT_ALLOC", 0) == 0 && ub_affordable(Ea))
+    return a_join_op(op, A, B, ia, ib, npairs, Ea, out);
   Upload U;
   const size_t o_ia = ia ? U.add(ia, npairs * 4) : Upload::NONE, o_ib = ib ? U.add(ib, npairs * 4) : Upload::NONE;
   std::vector<uint64_t> hb;
@@ -2116,13 +2221,6 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
     RS_CK(cudaMemsetAsync(keep, 0, 4, g_stream));
     RS_CK(cudaMemsetAsync(ub, 0, 8, g_stream));
   }
-  // per-pair path (CTA per pair, keys in smem, scans over pairs): when the
-  // bitmaps are small enough for smem and there are enough pairs to fill the
-  // GPU (or few positions per pair); a handful of pairs with thousands of keys
-  // each (config 4) keep the thread-per-position join
-  static const int force_pp = env_int("RS_PER_PAIR", -1);  // A/B: 1 forces, 0 disables the per-pair join
-  const bool per_pair = M && maxk <= MERGE_SMEM_KEYS &&
-                        (force_pp >= 0 ? force_pp == 1 : (npairs >= 2 * sm_count() || M <= 1024 * npairs));
   if (per_pair) {
     // the join, then entry / slot bases from scans over pairs
     uint32_t *pk = (uint32_t *)S.get((npairs + 1) * 4), *pke = (uint32_t *)S.get((npairs + 1) * 4);
