@@ -1424,11 +1424,14 @@ __global__ void __launch_bounds__(256) k_pair_nonempty(uint64_t npairs, const ui
 // fbase == nullptr: the single-pair op (one CTA): the pair's kept count is
 // this loop's own total, and the bitmap's cardinality is summed here (the
 // class kernels' atomic sums went to a scratch word, so no memset was needed)
-__global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uint32_t *__restrict__ pbase,
-                                                      const uint32_t *__restrict__ fbase, Entries En, OutDesc O,
-                                                      uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn,
-                                                      uint64_t *off, uint64_t *bm_start, uint64_t *bm_card) {
-  using BS = cub::BlockScan<uint32_t, 256>;
+// (NT threads: 1024 when pairs hold thousands of entries, each CTA's chunks
+// being serial)
+template <int NT>
+__global__ void __launch_bounds__(NT) k_compact_pair(uint64_t npairs, const uint32_t *__restrict__ pbase,
+                                                     const uint32_t *__restrict__ fbase, Entries En, OutDesc O,
+                                                     uint16_t *key, uint8_t *type, uint32_t *card, uint32_t *nn,
+                                                     uint64_t *off, uint64_t *bm_start, uint64_t *bm_card) {
+  using BS = cub::BlockScan<uint32_t, NT>;
   __shared__ typename BS::TempStorage ts;
   __shared__ unsigned long long csum;
   const uint32_t p = blockIdx.x;
@@ -1472,48 +1475,65 @@ __global__ void __launch_bounds__(256) k_compact_pair(uint64_t npairs, const uin
 // AND and ANDNOT keep a subset of A's keys, in A's order (bitmap.py:169-210,
 // _KEEP_A / _KEEP_B), so a result entry can sit at its A container's
 // position: entry e = abase[p] + i for container i of pair p's A bitmap,
-// with an 8 KB slot at 8192 e.  One thread per A container finds the key in
-// B's keys, writes the entry and appends it to its class list (or marks an
-// AND miss empty); the merged-position join's two scans over both sides'
-// keys and its emit pass are not needed, and the per-pair compaction drops
-// the empty entries.
-__global__ void k_join_a(uint64_t Ea, uint64_t npairs, const uint64_t *__restrict__ abase, DevBatch A, DevBatch B,
-                         const uint32_t *ia, const uint32_t *ib, int op, Entries E, OutDesc O, Lists L) {
-  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  bool active = false;
-  int cls = CLS_COPY;
-  uint32_t nab = 0;
-  uint64_t ao = 0, bo = 0;
-  if (t < Ea) {
-    const uint64_t p = find_pair(abase, npairs, t);
-    const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
-    const uint64_t b0 = B.bm_start[b];
-    const uint32_t nb = (uint32_t)(B.bm_start[b + 1] - b0);
-    const uint32_t ca = (uint32_t)(A.bm_start[a] + (t - abase[p]));
-    const uint16_t key = A.key[ca];
-    const uint32_t j = lower_bound16(B.key + b0, nb, key);
-    const bool matched = j < nb && B.key[b0 + j] == key;
-    active = matched || op == RS_OP_ANDNOT;
-    if (active) {
-      const uint32_t cb = matched ? (uint32_t)(b0 + j) : RS_NONE;
-      E.key[t] = key;
-      E.ca[t] = ca;
-      E.cb[t] = cb;
-      E.pair[t] = (uint32_t)p;
-      E.off[t] = 8192ull * t;
-      if (matched) {
-        cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
-        if (tma_class(cls)) {
-          ao = A.off[ca];
-          bo = B.off[cb];
-          nab = A.card[ca] | (B.card[cb] << 16);
-        }
-      }
-    } else {
-      O.card[t] = 0;  // an AND miss: nothing kept
-    }
+// with an 8 KB slot at 8192 e.  A CTA per chunk of a pair's A containers
+// finds each key in B's keys (staged in shared memory), writes the entry and
+// appends it to its class list (or marks an AND miss empty); the
+// merged-position join's two scans over both sides' keys and its emit pass
+// are not needed, and the per-pair compaction drops the empty entries.
+// A CTA takes JA_CHUNK of one pair's A containers (grid: npairs x chunks of
+// the largest A bitmap), with B's keys staged in shared memory when they fit.
+constexpr uint32_t JA_CHUNK = 512, JA_SMEM_KEYS = 4096;
+__global__ void __launch_bounds__(256) k_join_a(uint32_t chunks, const uint64_t *__restrict__ abase, DevBatch A,
+                                                DevBatch B, const uint32_t *ia, const uint32_t *ib, int op, Entries E,
+                                                OutDesc O, Lists L) {
+  __shared__ uint16_t kB[JA_SMEM_KEYS];
+  const uint32_t p = blockIdx.x / chunks, c = blockIdx.x % chunks;
+  const uint32_t a = pair_a(ia, p), b = pair_a(ib, p);
+  const uint64_t a0 = A.bm_start[a], b0 = B.bm_start[b];
+  const uint32_t na = (uint32_t)(A.bm_start[a + 1] - a0), nb = (uint32_t)(B.bm_start[b + 1] - b0);
+  if (c * JA_CHUNK >= na) return;  // (the whole CTA)
+  const bool staged = nb <= JA_SMEM_KEYS;
+  if (staged) {
+    for (uint32_t u = threadIdx.x; u < nb; u += blockDim.x) kB[u] = B.key[b0 + u];
+    __syncthreads();
   }
-  list_append_cta(L, cls, active, (uint32_t)t, ao, bo, nab);
+  const uint16_t *keys = staged ? kB : B.key + b0;
+  const uint64_t ebase = abase[p];
+  for (uint32_t r = 0; r < JA_CHUNK; r += 256) {
+    const uint32_t i = c * JA_CHUNK + r + threadIdx.x;
+    if (c * JA_CHUNK + r >= na) break;  // (uniform over the CTA)
+    bool active = false;
+    int cls = CLS_COPY;
+    uint32_t nab = 0;
+    uint64_t ao = 0, bo = 0;
+    const uint64_t e = ebase + i;
+    if (i < na) {
+      const uint32_t ca = (uint32_t)(a0 + i);
+      const uint16_t key = A.key[ca];
+      const uint32_t j = lower_bound16(keys, nb, key);
+      const bool matched = j < nb && keys[j] == key;
+      active = matched || op == RS_OP_ANDNOT;
+      if (active) {
+        const uint32_t cb = matched ? (uint32_t)(b0 + j) : RS_NONE;
+        E.key[e] = key;
+        E.ca[e] = ca;
+        E.cb[e] = cb;
+        E.pair[e] = p;
+        E.off[e] = 8192ull * e;
+        if (matched) {
+          cls = classify(A.type[ca], A.card[ca], B.type[cb], B.card[cb], op);
+          if (tma_class(cls)) {
+            ao = A.off[ca];
+            bo = B.off[cb];
+            nab = A.card[ca] | (B.card[cb] << 16);
+          }
+        }
+      } else {
+        O.card[e] = 0;  // an AND miss: nothing kept
+      }
+    }
+    list_append_cta(L, cls, active, (uint32_t)e, ao, bo, nab);
+  }
 }
 
 // -------------------------------------------------- count-only join + formula
@@ -2012,7 +2032,7 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
   host_mark(8);
   // compaction: drop empty results (bitmap.py:185-188)
   if (single) {  // one CTA: kept count and cardinality computed in place
-    RS_LAUNCH(k_compact_pair, 1u, 256, 0, npairs, epos, (const uint32_t *)nullptr, En, O, b->d_key, b->d_type,
+    RS_LAUNCH(k_compact_pair<256>, 1u, 256, 0, npairs, epos, (const uint32_t *)nullptr, En, O, b->d_key, b->d_type,
               b->d_card, b->d_n, b->d_off, b->d_bm_start, b->d_bm_card);
     b->h_valid = false;
     *out = b;
@@ -2026,8 +2046,12 @@ int run_classes_and_compact(int op, const rs_batch *A, const rs_batch *B, Scratc
     RS_LAUNCH(k_pair_nonempty, (unsigned)npairs, 256, 0, npairs, epos, O.card, nz, fuse ? L.cnt + NCLS + 1 : nullptr,
               fb);
     if (!fuse) RS_TRY(scan_exclusive<uint32_t>(nz, fb, npairs + 1));
-    RS_LAUNCH(k_compact_pair, (unsigned)npairs, 256, 0, npairs, epos, fb, En, O, b->d_key, b->d_type, b->d_card,
-              b->d_n, b->d_off, b->d_bm_start, b->d_bm_card);
+if (E > 1024 * npairs)
+      RS_LAUNCH(k_compact_pair<1024>, (unsigned)npairs, 1024, 0, npairs, epos, fb, En, O, b->d_key, b->d_type,
+                b->d_card, b->d_n, b->d_off, b->d_bm_start, b->d_bm_card);
+    else
+      RS_LAUNCH(k_compact_pair<256>, (unsigned)npairs, 256, 0, npairs, epos, fb, En, O, b->d_key, b->d_type,
+                b->d_card, b->d_n, b->d_off, b->d_bm_start, b->d_bm_card);
     b->h_valid = false;
     *out = b;
     host_mark(9);
@@ -2121,7 +2145,10 @@ int a_join_op(int op, const rs_batch *A, const rs_batch *B, const uint32_t *ia, 
   RS_TRY(U.commit(S));
   L.cnt = U.at<uint32_t>(o_cnt);
   const uint64_t *abase = U.at<uint64_t>(o_ab);
-  RS_LAUNCH(k_join_a, grid_for(Ea, 256), 256, 0, Ea, npairs, abase, A->dev(), B->dev(), U.at<uint32_t>(o_ia),
+  uint64_t maxa = 0;
+  for (uint64_t p = 0; p < npairs; p++) maxa = std::max(maxa, hb[p + 1] - hb[p]);
+  const uint32_t chunks = (uint32_t)std::max<uint64_t>((maxa + JA_CHUNK - 1) / JA_CHUNK, 1);
+  RS_LAUNCH(k_join_a, (unsigned)(npairs * chunks), 256, 0, chunks, abase, A->dev(), B->dev(), U.at<uint32_t>(o_ia),
             U.at<uint32_t>(o_ib), op, En, O, L);
   host_mark(4);
   return run_classes_and_compact(op, A, B, S, En, L, Ea, 8192 * std::max<uint64_t>(Ea, 1), nullptr, nullptr,
