@@ -23,6 +23,8 @@
 // cardinality formulas (bitmap.py:225-241) in its last CTA, writing the count
 // straight to its destination (device memory, or page-locked host memory).
 #include <cub/cub.cuh>
+#include <atomic>
+#include <mutex>
 #include "rs_internal.cuh"
 #include "rs_dense.cuh"
 #include "rs_single.h"
@@ -220,16 +222,34 @@ __global__ void __launch_bounds__(DT) k_single_count(int op, DevBatch A, DevBatc
   }
 }
 
-uint32_t next_ticket() {
-  static uint32_t k = 0;
-  return k++ % NTICKET;
+uint32_t next_ticket() {  // (calls from several host threads take distinct tickets)
+  static std::atomic<uint32_t> k{0};
+  return k.fetch_add(1, std::memory_order_relaxed) % NTICKET;
 }
 
-template <typename T>
-T *symbol_ptr(const T &sym) {
-  void *p = nullptr;
-  if (cudaGetSymbolAddress(&p, sym) != cudaSuccess) return nullptr;
-  return (T *)p;
+// the device addresses of the ticket / accumulator arrays, per device
+constexpr int MAX_DEV = 64;
+struct Symbols {
+  uint32_t *tickets = nullptr;
+  unsigned long long *accs = nullptr;
+};
+int symbols(Symbols &out) {
+  static Symbols cache[MAX_DEV];
+  static std::mutex mu;
+  int dev = 0;
+  RS_CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= MAX_DEV) { set_error("device index out of range"); return RS_ECUDA; }
+  std::lock_guard<std::mutex> g(mu);
+  Symbols &c = cache[dev];
+  if (!c.tickets) {
+    void *p = nullptr, *q = nullptr;
+    RS_CK(cudaGetSymbolAddress(&p, g_ticket));
+    RS_CK(cudaGetSymbolAddress(&q, g_acc));
+    c.tickets = (uint32_t *)p;
+    c.accs = (unsigned long long *)q;
+  }
+  out = c;
+  return RS_OK;
 }
 
 }  // namespace
@@ -241,12 +261,9 @@ int single_pair_op(int op, const rs_batch *A, const rs_batch *B, uint32_t a, uin
   const uint32_t b0 = (uint32_t)B->h_bm_start[b], nb = (uint32_t)(B->h_bm_start[b + 1] - b0);
   const bool keep_b = op == RS_OP_OR || op == RS_OP_XOR;
   const uint32_t E = keep_b ? na + nb : na;
-  static uint32_t *tickets = nullptr;
-  if (!tickets && !(tickets = (uint32_t *)symbol_ptr(g_ticket))) {
-    set_error("ticket symbol lookup failed");
-    return RS_ECUDA;
-  }
-  uint32_t *tk = tickets + next_ticket();
+  Symbols sy;
+  RS_TRY(symbols(sy));
+  uint32_t *tk = sy.tickets + next_ticket();
   const DevBatch dA = A->dev(), dB = B->dev();
   const unsigned grid = std::max<uint32_t>(E, 1u);
   rs_batch *r = out;
@@ -270,20 +287,11 @@ uint32_t single_pair_slots(int op, uint32_t na, uint32_t nb) {
 int single_pair_count(int op, const rs_batch *A, const rs_batch *B, uint32_t a, uint32_t b, uint64_t *out) {
   const uint32_t a0 = (uint32_t)A->h_bm_start[a], na = (uint32_t)(A->h_bm_start[a + 1] - a0);
   const uint32_t b0 = (uint32_t)B->h_bm_start[b], nb = (uint32_t)(B->h_bm_start[b + 1] - b0);
-  static uint32_t *tickets = nullptr;
-  static unsigned long long *accs = nullptr;
-  if (!tickets && !(tickets = (uint32_t *)symbol_ptr(g_ticket))) {
-    set_error("ticket symbol lookup failed");
-    return RS_ECUDA;
-  }
-  if (!accs && !(accs = (unsigned long long *)symbol_ptr(g_acc))) {
-    set_error("accumulator symbol lookup failed");
-    return RS_ECUDA;
-  }
+  Symbols sy;
+  RS_TRY(symbols(sy));
   const uint32_t k = next_ticket();
   RS_LAUNCH(k_single_count, std::max<uint32_t>(na, 1u), DT, 0, op, A->dev(), B->dev(), a, b, a0, na, b0, nb, out,
-            tickets + k,
-            accs + k);
+            sy.tickets + k, sy.accs + k);
   return RS_OK;
 }
 
