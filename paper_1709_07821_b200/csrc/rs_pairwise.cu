@@ -2178,8 +2178,9 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   }
   // Upper-bound mode (no host sync) when an 8 KB slot per possible output
   // container costs at most ~2x the inputs' pools; else size exactly.
+  static const int ub_force = env_int("RS_UB_FORCE", 0);  // diagnostics: upper-bound slots whatever they cost
   auto ub_affordable = [&](uint64_t slots) {
-    return 8192.0 * (double)slots <= 2.0 * (double)(A->pool_bytes + B->pool_bytes) + 64e6;
+    return ub_force || 8192.0 * (double)slots <= 2.0 * (double)(A->pool_bytes + B->pool_bytes) + 64e6;
   };
   if (npairs == 1 && single_path_on()) {  // one pair of small bitmaps: one launch (rs_single.cu)
     const uint32_t a = ia ? ia[0] : 0, b = ib ? ib[0] : 0;

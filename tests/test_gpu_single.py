@@ -156,3 +156,29 @@ def test_a_indexed_join_batches(rb):
         assert R.pairwise_cardinality("or", R, list(range(len(ia))), list(range(len(ia)))).tolist() == \
             [orc.cardinality(orc.op(op, imgs[a], imgs[b])) for a, b in zip(ia, ib)]
     assert n == 6
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_batches_every_join(rb, seed):
+    """Random batches whose shapes select every join: one pair (one-launch
+    path), few pairs of many keys (A-indexed join for AND / ANDNOT, the
+    merged-position join for OR / XOR), many pairs of few keys (per-pair
+    join); pair lists with repeats and self-pairs; results and counts against
+    the oracle."""
+    rng = np.random.default_rng(300 + seed)
+    for nbm, kmax, npairs in ((2, 80, 1), (5, 1500, 7), (40, 40, 400)):
+        imgs = []
+        for _ in range(nbm):
+            nk = int(rng.integers(0, kmax + 1))
+            imgs.append(bitmap(rng, np.sort(rng.choice(4 * kmax + 8, nk, replace=False)),
+                               optimize=bool(rng.integers(0, 2))))
+        B = rb.BitmapBatch.from_wire(imgs)
+        ia = rng.integers(0, nbm, npairs).tolist()
+        ib = rng.integers(0, nbm, npairs).tolist()
+        for op in OPS:
+            got = B.pairwise(op, B, ia, ib).to_wire_list()
+            cnt = B.pairwise_cardinality(op, B, ia, ib).tolist()
+            for k, (a, b) in enumerate(zip(ia, ib)):
+                want = orc.op(op, imgs[a], imgs[b])
+                assert got[k] == want, (seed, nbm, op, a, b)
+                assert cnt[k] == orc.cardinality(want), (seed, nbm, op, a, b)
