@@ -1529,8 +1529,42 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   const char *dv = getenv("RS_ALLPAIRS_DIRECT");
   const bool direct = use_umma && dv && *dv == '1';
   std::vector<uint32_t> dlist;  // direct: the items the CUDA-core tiles read
-  std::vector<uint32_t> hseg(g.G + 1);
-  RS_TRY(d2h(hseg.data(), g.seg_start, (g.G + 1) * 4));
+  // The densify needs only the grouping: it is queued right behind the
+  // segment starts' copy to the host, and the host builds and uploads the
+  // tile lists while it runs (the copy is waited for by its event, not by
+  // draining the stream).
+  uint64_t *D = (uint64_t *)dalloc((g.T ? g.T : 1) * 8192);
+  uint32_t *item_bm = (uint32_t *)dalloc((g.T + 1) * 4);
+  if (!D || !item_bm) { set_error("device allocation failed (all pairs)"); return RS_ENOMEM; }
+  thread_local uint32_t *hseg_pin = nullptr;
+  thread_local uint64_t hseg_cap = 0;
+  thread_local cudaEvent_t seg_ev = nullptr;
+  if (hseg_cap < g.G + 1) {
+    if (hseg_pin) cudaFreeHost(hseg_pin);
+    hseg_pin = nullptr;
+    RS_CK(cudaMallocHost(&hseg_pin, (g.G + 1) * 4));
+    hseg_cap = g.G + 1;
+  }
+  if (!seg_ev) RS_CK(cudaEventCreateWithFlags(&seg_ev, cudaEventDisableTiming));
+  RS_CK(cudaMemcpyAsync(hseg_pin, g.seg_start, (g.G + 1) * 4, cudaMemcpyDeviceToHost, g_stream));
+  RS_CK(cudaEventRecord(seg_ev, g_stream));
+  RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
+  auto densify = [&](uint64_t nd, const uint32_t *d_dlist) -> int {
+    if (env_flag_("RS_DENSIFY_CTA") && !d_dlist) {  // the CTA-per-row kernel (A/B only)
+      RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
+    } else {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const uint64_t g_need = (nd + DW_WARPS - 1) / DW_WARPS;
+      const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g_need, (uint64_t)sms * 6));
+      RS_LAUNCH_PROF("densify", nd, k_densify_warp, grid, 32 * DW_WARPS, 0, nd, g.item_c, in->dev(), D, d_dlist);
+    }
+    return RS_OK;
+  };
+  if (!direct) RS_TRY(densify(g.T, nullptr));
+  RS_CK(cudaEventSynchronize(seg_ev));
+  std::vector<uint32_t> hseg(hseg_pin, hseg_pin + g.G + 1);
   std::vector<uint32_t> tseg, useg;
   std::vector<uint16_t> ti, tj, ur0, uc0, unb;
   const uint32_t tile = tiles2 ? AP2_TILE : AP_TILE;
@@ -1565,39 +1599,43 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   ushort4 *d_Q = direct ? (ushort4 *)dalloc((g.T + 1) * 8) : nullptr;
   if (direct && (!d_dlist || !d_Q)) { set_error("device allocation failed (all pairs)"); return RS_ENOMEM; }
   if (direct && nd) RS_TRY(h2d(d_dlist, dlist.data(), nd * 4));
-  uint64_t *D = (uint64_t *)dalloc((g.T ? g.T : 1) * 8192);
-  uint32_t *item_bm = (uint32_t *)dalloc((g.T + 1) * 4), *d_tseg = (uint32_t *)dalloc((ntp + 1) * 4);
-  uint16_t *d_ti = (uint16_t *)dalloc((ntp + 1) * 2), *d_tj = (uint16_t *)dalloc((ntp + 1) * 2);
-  uint32_t *d_useg = (uint32_t *)dalloc((nup + 1) * 4);
-  uint16_t *d_ur0 = (uint16_t *)dalloc((nup + 1) * 2), *d_uc0 = (uint16_t *)dalloc((nup + 1) * 2),
-           *d_unb = (uint16_t *)dalloc((nup + 1) * 2);
+  // the seven tile lists in one page-locked block, one copy (16-byte aligned parts)
+  const uint64_t lt_bytes[7] = {ntp * 4, ntp * 2, ntp * 2, nup * 4, nup * 2, nup * 2, nup * 2};
+  const void *lt_src[7] = {tseg.data(), ti.data(), tj.data(), useg.data(), ur0.data(), uc0.data(), unb.data()};
+  uint64_t lt_off[8] = {0};
+  for (int k = 0; k < 7; k++) lt_off[k + 1] = lt_off[k] + rs_pad16(lt_bytes[k] + 16);
+  thread_local uint8_t *lt_pin = nullptr;
+  thread_local uint64_t lt_cap = 0;
+  thread_local cudaEvent_t lt_ev = nullptr;
+  if (!lt_ev) RS_CK(cudaEventCreateWithFlags(&lt_ev, cudaEventDisableTiming));
+  RS_CK(cudaEventSynchronize(lt_ev));  // the previous call's copy out of the block is done
+  if (lt_cap < lt_off[7]) {
+    if (lt_pin) cudaFreeHost(lt_pin);
+    lt_pin = nullptr;
+    RS_CK(cudaMallocHost(&lt_pin, lt_off[7]));
+    lt_cap = lt_off[7];
+  }
+  for (int k = 0; k < 7; k++)
+    if (lt_bytes[k]) memcpy(lt_pin + lt_off[k], lt_src[k], lt_bytes[k]);
+  uint8_t *d_lists = (uint8_t *)dalloc(lt_off[7]);
   unsigned long long *Mx = (unsigned long long *)dalloc(N * N * 8);
   uint64_t *d_inter = (uint64_t *)dalloc(npairs * 8), *d_uni = (uint64_t *)dalloc(npairs * 8);
-  if (!D || !item_bm || !d_tseg || !d_ti || !d_tj || !d_useg || !d_ur0 || !d_uc0 || !d_unb || !Mx || !d_inter || !d_uni) {
+  if (!d_lists || !Mx || !d_inter || !d_uni) {
     set_error("device allocation failed (all pairs)");
     return RS_ENOMEM;
   }
+  uint32_t *d_tseg = (uint32_t *)(d_lists + lt_off[0]), *d_useg = (uint32_t *)(d_lists + lt_off[3]);
+  uint16_t *d_ti = (uint16_t *)(d_lists + lt_off[1]), *d_tj = (uint16_t *)(d_lists + lt_off[2]),
+           *d_ur0 = (uint16_t *)(d_lists + lt_off[4]), *d_uc0 = (uint16_t *)(d_lists + lt_off[5]),
+           *d_unb = (uint16_t *)(d_lists + lt_off[6]);
   trace("allpairs: tile lists + allocs");
-  RS_TRY(h2d(d_tseg, tseg.data(), ntp * 4));
-  RS_TRY(h2d(d_ti, ti.data(), ntp * 2));
-  RS_TRY(h2d(d_tj, tj.data(), ntp * 2));
-  RS_TRY(h2d(d_useg, useg.data(), nup * 4));
-  RS_TRY(h2d(d_ur0, ur0.data(), nup * 2));
-  RS_TRY(h2d(d_uc0, uc0.data(), nup * 2));
-  RS_TRY(h2d(d_unb, unb.data(), nup * 2));
+  RS_CK(cudaMemcpyAsync(d_lists, lt_pin, lt_off[7], cudaMemcpyHostToDevice, g_stream));
+  RS_CK(cudaEventRecord(lt_ev, g_stream));
   RS_CK(cudaMemsetAsync(Mx, 0, N * N * 8, g_stream));
-  RS_LAUNCH(k_item_bitmap, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->d_bm_start, in->nb, item_bm);
-  trace("allpairs: uploads + memset + item_bm");
-  if (direct) RS_LAUNCH(k_quarter_index, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->dev(), d_Q);
-  if (env_flag_("RS_DENSIFY_CTA") && !direct) {  // the CTA-per-row kernel (A/B only)
-    RS_LAUNCH_PROF("densify", g.T, k_densify, (unsigned)g.T, DT, 0, g.T, g.item_c, in->dev(), D);
-  } else {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t g_need = (nd + DW_WARPS - 1) / DW_WARPS;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g_need, (uint64_t)sms * 6));
-    RS_LAUNCH_PROF("densify", nd, k_densify_warp, grid, 32 * DW_WARPS, 0, nd, g.item_c, in->dev(), D, d_dlist);
+  trace("allpairs: uploads + memset");
+  if (direct) {
+    RS_LAUNCH(k_quarter_index, grid_for(g.T, 256), 256, 0, g.T, g.item_c, in->dev(), d_Q);
+    RS_TRY(densify(nd, d_dlist));
   }
   trace("allpairs: densify");
   // (running the tensor-core and CUDA-core tiles concurrently on side streams
@@ -1650,8 +1688,8 @@ extern "C" int rs_all_pairs_cardinality(const rs_batch *in, uint64_t *inter, uin
   RS_TRY(d2h(inter, d_inter, npairs * 8));  // one synchronization for both
   trace("allpairs: readback");
   dfree(d_dlist); dfree(d_Q);
-  dfree(D); dfree(item_bm); dfree(d_tseg); dfree(d_ti); dfree(d_tj); dfree(Mx); dfree(d_inter); dfree(d_uni);
-  dfree(d_useg); dfree(d_ur0); dfree(d_uc0); dfree(d_unb);
+  dfree(D); dfree(item_bm); dfree(Mx); dfree(d_inter); dfree(d_uni);
+  dfree(d_lists);
   g.release();
   return RS_OK;
 }
