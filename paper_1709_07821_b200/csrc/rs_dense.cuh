@@ -93,6 +93,23 @@ static __device__ __forceinline__ void block_sum2(uint32_t &a, uint32_t &b, uint
   for (int w = 0; w < DT / 32; w++) { a += red[w][0]; b += red[w][1]; }
 }
 
+// The set bits of word w (bit positions pos + 0..63) written in ascending
+// order to out[end - popc(w), end), peeled from the top bit down (FLO on each
+// 32-bit half): ~11 instructions per value, half the __ffsll loop's.
+static __device__ __forceinline__ void peel_down(uint64_t w, uint32_t pos, uint32_t end, uint16_t *out) {
+  uint32_t b = end, hi = (uint32_t)(w >> 32), lo = (uint32_t)w;
+  while (hi) {
+    const uint32_t p = 31 - __clz(hi);
+    out[--b] = (uint16_t)(pos + 32 + p);
+    hi ^= 1u << p;
+  }
+  while (lo) {
+    const uint32_t p = 31 - __clz(lo);
+    out[--b] = (uint16_t)(pos + p);
+    lo ^= 1u << p;
+  }
+}
+
 // Encode the result set held in r[4] (thread t's words) into the chosen
 // container type at dst: bitset words, sorted array (extract_set_bits,
 // scalar.py:61-76) or runs (_runs_from_positions, containers.py:138-147).
@@ -111,12 +128,9 @@ static __device__ uint32_t encode_result(DenseSmem &sm, const uint64_t r[4], uin
     uint32_t base;
     cub::BlockScan<uint32_t, DT>(sm.scan).ExclusiveSum(pc, base);
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      uint64_t w = r[k];
-      while (w) {
-        Y16[base++] = (uint16_t)((4 * t + k) * 64 + __ffsll((long long)w) - 1);
-        w &= w - 1;
-      }
+    for (int k = 0; k < 4; k++) {  // each word peeled from its top bit into its slot range
+      base += (uint32_t)__popcll(r[k]);
+      peel_down(r[k], (uint32_t)(4 * t + k) * 64, base, Y16);
     }
     __syncthreads();
     uint32_t nvec = (uint32_t)(rs_pad16(2ull * card) >> 4);
@@ -144,10 +158,10 @@ static __device__ uint32_t encode_result(DenseSmem &sm, const uint64_t r[4], uin
   uint16_t *Ys = Y16, *Ye = Y16 + 2048;
 #pragma unroll
   for (int k = 0; k < 4; k++) {
-    uint64_t w = S[k];
-    while (w) { Ys[bs++] = (uint16_t)((4 * t + k) * 64 + __ffsll((long long)w) - 1); w &= w - 1; }
-    w = E[k];
-    while (w) { Ye[be++] = (uint16_t)((4 * t + k) * 64 + __ffsll((long long)w) - 1); w &= w - 1; }
+    bs += (uint32_t)__popcll(S[k]);
+    be += (uint32_t)__popcll(E[k]);
+    peel_down(S[k], (uint32_t)(4 * t + k) * 64, bs, Ys);
+    peel_down(E[k], (uint32_t)(4 * t + k) * 64, be, Ye);
   }
   __syncthreads();
   uint32_t *d32 = (uint32_t *)dst;

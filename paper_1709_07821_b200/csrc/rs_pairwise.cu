@@ -566,7 +566,7 @@ using namespace rsd;
 // this kernel runs beside the other classes' kernels, and a CTA that found
 // no free SM slot until they finished took a full static share late.
 template <bool GEN>
-__global__ void __launch_bounds__(DT) k_pair_dense(int op, const uint32_t *__restrict__ list,
+__global__ void __launch_bounds__(DT, 4) k_pair_dense(int op, const uint32_t *__restrict__ list,
                                                    const uint32_t *__restrict__ cnt, uint32_t *ctr, DevBatch A,
                                                    DevBatch B, Entries E, OutDesc O, uint8_t *__restrict__ opool,
                                                    uint64_t *__restrict__ res_card) {
