@@ -405,12 +405,16 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
       // array / run payloads, flattened over the window in 16-byte units
       // (8 array values or 4 runs per load; every unit's load is independent)
       const uint32_t tot = nelem;
-      for (uint32_t f = t; f < tot; f += UT) {
-        uint32_t lo = 0, hi = ne;  // contributor j with ebase[j] <= f < ebase[j+1]
+      uint32_t lo = 0;  // contributor lo with ebase[lo] <= f < ebase[lo+1]
+      if ((uint32_t)t < tot) {  // binary search for the thread's first unit ...
+        uint32_t hi = ne;
         while (hi - lo > 1) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (ebase[mid] <= f) lo = mid; else hi = mid;
+          if (ebase[mid] <= (uint32_t)t) lo = mid; else hi = mid;
         }
+      }
+      for (uint32_t f = t; f < tot; f += UT) {
+        while (lo + 1 < ne && ebase[lo + 1] <= f) lo++;  // ... then forward (units ascend by UT)
         const uint32_t u = f - ebase[lo];
         const uint4 q = __ldg((const uint4 *)(S.pool + eoff[lo]) + u);
         const uint32_t x[4] = {q.x, q.y, q.z, q.w};
