@@ -536,16 +536,18 @@ __global__ void k_copy(const uint32_t *__restrict__ list, const uint32_t *__rest
     const uint32_t e = cur.e;
     if (w + nw < total) cur = fetch(w + nw);
     const uint32_t nv = (uint32_t)(rs_pad16(rs_payload_bytes(t, n)) >> 4);
-    uint32_t i = lane;
-    for (; i + 96 < nv; i += 128) {
-      const uint4 x0 = __ldcs(src + i), x1 = __ldcs(src + i + 32), x2 = __ldcs(src + i + 64),
-                  x3 = __ldcs(src + i + 96);
-      __stcs(dst + i, x0);
-      __stcs(dst + i + 32, x1);
-      __stcs(dst + i + 64, x2);
-      __stcs(dst + i + 96, x3);
+    // rounds of 8 predicated 16-byte loads per lane (4 KB per warp), all
+    // issued before any store: a typical container is one round trip (a
+    // remainder loop of one load -> store per step made it two or three)
+    for (uint32_t i0 = 0; i0 < nv; i0 += 256) {
+      uint4 x[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if (i0 + lane + 32 * k < nv) x[k] = __ldcs(src + i0 + lane + 32 * k);
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if (i0 + lane + 32 * k < nv) __stcs(dst + i0 + lane + 32 * k, x[k]);
     }
-    for (; i < nv; i += 32) __stcs(dst + i, __ldcs(src + i));
     if (lane == 0) {
       O.type[e] = t;
       O.card[e] = card;
