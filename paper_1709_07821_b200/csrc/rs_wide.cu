@@ -413,43 +413,23 @@ __global__ void __launch_bounds__(UT) k_union_or(const uint32_t *__restrict__ li
           if (ebase[mid] <= (uint32_t)t) lo = mid; else hi = mid;
         }
       }
-      for (uint32_t f = t; f < tot; f += UT) {
-        while (lo + 1 < ne && ebase[lo + 1] <= f) lo++;  // ... then forward (units ascend by UT)
-        const uint32_t u = f - ebase[lo];
-        const uint4 q = __ldg((const uint4 *)(S.pool + eoff[lo]) + u);
-        const uint32_t x[4] = {q.x, q.y, q.z, q.w};
-        const uint32_t nv = eunits_n[lo];  // values (array) / runs (run) of the contributor
-        if (etype[lo] == RS_TAG_ARRAY) {
-          const uint32_t v0 = 8 * u;
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const uint32_t lo16 = x[j] & 0xFFFF, hi16 = x[j] >> 16;
-            const bool a = v0 + 2 * j < nv, b = v0 + 2 * j + 1 < nv;
-            const uint32_t wl = lo16 >> 5, wh = hi16 >> 5;
-            const uint32_t bl = 1u << (lo16 & 31), bh = 1u << (hi16 & 31);
-            if (a && b && wl == wh) {
-              atomicOr(&X32[wl], bl | bh);
-            } else {
-              if (a) atomicOr(&X32[wl], bl);
-              if (b) atomicOr(&X32[wh], bh);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            if (4 * u + j >= nv) break;
-            const uint32_t st = x[j] & 0xFFFF, en = st + (x[j] >> 16);
-            const uint32_t ws = st >> 5, we = en >> 5;
-            const uint32_t first = ~0u << (st & 31), last = ~0u >> (31 - (en & 31));
-            if (ws == we) {
-              atomicOr(&X32[ws], first & last);
-            } else {
-              atomicOr(&X32[ws], first);
-              atomicOr(&X32[we], last);
-              for (uint32_t w = ws + 1; w < we; w++) X32[w] = ~0u;  // all-ones commutes with the ORs
-            }
-          }
+      // two units per step, both loads issued before either is scattered
+      // (a load per step waited out a round trip between the scatters)
+      for (uint32_t f = t; f < tot; f += 2 * UT) {
+        while (lo + 1 < ne && ebase[lo + 1] <= f) lo++;  // ... then forward (units ascend)
+        const uint32_t l0 = lo, u0 = f - ebase[l0];
+        const uint4 q0 = __ldg((const uint4 *)(S.pool + eoff[l0]) + u0);
+        const bool two = f + UT < tot;
+        uint32_t l1 = l0, u1 = 0;
+        uint4 q1 = make_uint4(0, 0, 0, 0);
+        if (two) {
+          while (lo + 1 < ne && ebase[lo + 1] <= f + UT) lo++;
+          l1 = lo;
+          u1 = f + UT - ebase[l1];
+          q1 = __ldg((const uint4 *)(S.pool + eoff[l1]) + u1);
         }
+        scatter_unit(q0, u0, eunits_n[l0], etype[l0] == RS_TAG_ARRAY, X32);
+        if (two) scatter_unit(q1, u1, eunits_n[l1], etype[l1] == RS_TAG_ARRAY, X32);
       }
       if (t == 0) ebase[UT] = 0;
       __syncthreads();  // window done: its smem may be reused
