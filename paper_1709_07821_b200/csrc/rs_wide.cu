@@ -1369,6 +1369,110 @@ struct Grouped {
   void release() { dfree(keys); dfree(item_c); dfree(seg_start); }
 };
 
+// ---- grouping by a counting sort over the 2^16 chunk keys (selections of at
+// most CS_MAX_SEL bitmaps).  A bitmap holds each key at most once, so key k's
+// contributors are the set bits of a presence row P[k] (one bit per selection
+// position): its count is the row's popcount, a contributor's rank inside the
+// key is the popcount of the bits below it -- a stable order by selection
+// position with no sort.  Three kernels and a scan replace the grouping
+// keys, the two radix passes, the segment flags / scan / starts and the
+// reorder of the radix path.
+constexpr uint64_t CS_MAX_SEL = 1024;  // presence rows <= 32 words (8 MB); rank <= 32 popcounts
+constexpr uint64_t CS_KEYS = 65536;
+constexpr uint64_t CS_M40 = (1ull << 40) - 1;
+
+__device__ __forceinline__ uint64_t sel_of_item(uint64_t t, uint64_t nsel, const uint64_t *__restrict__ qbase) {
+  uint64_t lo = 0, hi = nsel;
+  while (hi - lo > 1) {
+    const uint64_t m = (lo + hi) >> 1;
+    if (qbase[m] <= t) lo = m; else hi = m;
+  }
+  return lo;
+}
+
+__global__ void k_cs_mark(uint64_t T, uint64_t nsel, const uint64_t *__restrict__ qbase,
+                          const uint64_t *__restrict__ qsrc, DevBatch S, uint32_t W, uint32_t *__restrict__ P) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint64_t k = sel_of_item(t, nsel, qbase);
+  const uint32_t key = S.key[qsrc[k] + (t - qbase[k])];
+  atomicOr(&P[(uint64_t)key * W + (k >> 5)], 1u << (k & 31));
+}
+
+// per key: (nonzero << 40) | count; entry CS_KEYS = 0, so the exclusive scan
+// leaves (G << 40) | T there
+__global__ void k_cs_count(uint32_t W, const uint32_t *__restrict__ P, uint64_t *__restrict__ cnt) {
+  const uint64_t key = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (key > CS_KEYS) return;
+  uint32_t s = 0;
+  if (key < CS_KEYS)
+    for (uint32_t w = 0; w < W; w++) s += __popc(P[key * W + w]);
+  cnt[key] = s ? ((1ull << 40) | s) : 0ull;
+}
+
+__global__ void k_cs_scatter(uint64_t T, uint64_t nsel, const uint64_t *__restrict__ qbase,
+                             const uint64_t *__restrict__ qsrc, DevBatch S, uint32_t W,
+                             const uint32_t *__restrict__ P, const uint64_t *__restrict__ base,
+                             uint64_t *__restrict__ keys, uint32_t *__restrict__ item_c,
+                             uint32_t *__restrict__ seg_start) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (t == 0) {
+    const uint64_t tot = base[CS_KEYS];
+    seg_start[tot >> 40] = (uint32_t)(tot & CS_M40);
+  }
+  if (t >= T) return;
+  const uint64_t k = sel_of_item(t, nsel, qbase);
+  const uint32_t c = (uint32_t)(qsrc[k] + (t - qbase[k]));
+  const uint32_t key = S.key[c];
+  const uint32_t *row = P + (uint64_t)key * W;
+  uint32_t r = __popc(row[k >> 5] & ((1u << (k & 31)) - 1u));
+  for (uint32_t w = 0; w < (uint32_t)(k >> 5); w++) r += __popc(row[w]);
+  const uint64_t b = base[key], pos = (b & CS_M40) + r;
+  keys[pos] = ((uint64_t)key << 40) | t;
+  item_c[pos] = c;
+  if (r == 0) seg_start[b >> 40] = (uint32_t)pos;
+}
+
+// The counting-sort grouping: item_c comes out already in key order.
+int group_by_key_counting(const rs_batch *in, const std::vector<uint64_t> &sel, Grouped &g) {
+  const uint64_t n = sel.size();
+  std::vector<uint64_t> qbase(n + 1, 0), qsrc(n + 1, 0);
+  for (uint64_t k = 0; k < n; k++) {
+    qsrc[k] = in->h_bm_start[sel[k]];
+    qbase[k + 1] = qbase[k] + (in->h_bm_start[sel[k] + 1] - in->h_bm_start[sel[k]]);
+  }
+  const uint64_t T = g.T = qbase[n];
+  const uint32_t W = (uint32_t)((n + 31) / 32);
+  uint64_t *d_q = (uint64_t *)dalloc(2 * (n + 1) * 8);
+  uint32_t *P = (uint32_t *)dalloc(CS_KEYS * W * 4);
+  uint64_t *cnt = (uint64_t *)dalloc((CS_KEYS + 1) * 8), *base = (uint64_t *)dalloc((CS_KEYS + 1) * 8);
+  g.keys = (uint64_t *)dalloc((T + 1) * 8);
+  g.item_c = (uint32_t *)dalloc((T + 1) * 4);
+  g.seg_start = (uint32_t *)dalloc((std::min<uint64_t>(T, CS_KEYS) + 2) * 4);
+  if (!d_q || !P || !cnt || !base || !g.keys || !g.item_c || !g.seg_start) {
+    set_error("device allocation failed (group)");
+    return RS_ENOMEM;
+  }
+  qbase.insert(qbase.end(), qsrc.begin(), qsrc.end());  // one upload: qbase then qsrc
+  RS_TRY(h2d(d_q, qbase.data(), 2 * (n + 1) * 8));
+  const uint64_t *d_qb = d_q, *d_qs = d_q + n + 1;
+  RS_CK(cudaMemsetAsync(P, 0, CS_KEYS * W * 4, g_stream));
+  if (T) RS_LAUNCH(k_cs_mark, grid_for(T, 256), 256, 0, T, n, d_qb, d_qs, in->dev(), W, P);
+  RS_LAUNCH(k_cs_count, grid_for(CS_KEYS + 1, 256), 256, 0, W, P, cnt);
+  RS_TRY(scan_exclusive<uint64_t>(cnt, base, CS_KEYS + 1));
+  RS_LAUNCH(k_cs_scatter, grid_for(T ? T : 1, 256), 256, 0, T, n, d_qb, d_qs, in->dev(), W, P, base, g.keys,
+            g.item_c, g.seg_start);
+  uint64_t tot = 0;
+  RS_TRY(d2h(&tot, base + CS_KEYS, 8));
+  g.G = tot >> 40;
+  dfree(d_q); dfree(P); dfree(cnt); dfree(base);
+  if ((tot & CS_M40) != T) {
+    set_error("grouping lost items (a chunk key repeated inside a bitmap)");
+    return RS_EARG;
+  }
+  return RS_OK;
+}
+
 // Group the containers of bitmaps sel[0..n) (in that order) by chunk key.
 int group_by_key(const rs_batch *in, const std::vector<uint64_t> &sel, Grouped &g) {
   uint64_t n = sel.size();
@@ -1412,6 +1516,8 @@ __global__ void k_reorder_items(uint64_t T, const uint64_t *__restrict__ keys, c
 }
 
 int group_and_reorder(const rs_batch *in, const std::vector<uint64_t> &sel, Grouped &g) {
+  // RS_GROUP_RADIX=1: the radix-sort grouping whatever the selection size (A/B)
+  if (sel.size() <= CS_MAX_SEL && !env_flag_("RS_GROUP_RADIX")) return group_by_key_counting(in, sel, g);
   RS_TRY(group_by_key(in, sel, g));
   uint32_t *sorted_c = (uint32_t *)dalloc((g.T + 1) * 4);
   if (!sorted_c) { set_error("device allocation failed (group)"); return RS_ENOMEM; }

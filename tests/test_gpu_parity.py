@@ -549,3 +549,24 @@ def test_all_pairs_direct_rows_variant(pkg, monkeypatch):
     monkeypatch.setenv("RS_ALLPAIRS_DIRECT", "1")
     monkeypatch.setenv("RS_ALLPAIRS_UMMA_MIN", "2")
     _all_pairs_check(pkg, buf, offs)
+
+
+@pytest.mark.parametrize("radix", ["0", "1"])
+def test_union_many_selection_grouping_paths(pkg, monkeypatch, radix):
+    """union_many over explicit selections -- repeated and out-of-order
+    bitmap indices, and more bitmaps than the counting-sort grouping takes
+    (1,100 > 1,024: the radix-sort grouping) -- with both groupings forced,
+    against the oracle's sequential fold in selection order."""
+    import workloads as synth
+    monkeypatch.setenv("RS_GROUP_RADIX", radix)
+    buf, offs = synth.config4(nbitmaps=12)
+    w = _wires(buf, offs)
+    Bt = pkg.BitmapBatch.from_wire((buf, offs))
+    for sel in ([3, 1, 3, 0, 11, 1], [5], list(range(11, -1, -1)) * 3):
+        assert Bt.union_many(sel).to_wire_list()[0] == orc.union_many([w[i] for i in sel])
+    rng = np.random.default_rng(5)
+    many = [pkg.RoaringBitmap.from_values(rng.integers(0, 1 << 22, int(rng.integers(0, 300)))).serialize()
+            for _ in range(1100)]
+    Bm = pkg.BitmapBatch.from_wire(many)
+    sel = list(rng.permutation(1100)) + [7, 7]
+    assert Bm.union_many(sel).to_wire_list()[0] == orc.union_many([many[i] for i in sel])
