@@ -269,6 +269,33 @@ template <> struct LaneVec<16> { using T = uint4; };
 __device__ __forceinline__ uint32_t vword(uint32_t v, int) { return v; }
 __device__ __forceinline__ uint32_t vword(uint2 v, int k) { return k ? v.y : v.x; }
 __device__ __forceinline__ uint32_t vword(uint4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+// A lane's four values (sorted, one 8-byte vector) with the bits of values
+// that share a 32-bit word merged in registers, so each touched word takes
+// one shared RED: the kernel is bound by the shared-memory pipe, not by issue
+// (ncu on C3 AND: 157 M shared wavefronts = 76 % of the pipe's peak against
+// 67 % issue; 73 M of them for 26.5 M RED instructions, ~2.75 per
+// instruction in bank and same-word conflicts).  On C3's dense arrays
+// (4,096 values: 57 % of adjacent values share a word) a lane's four values
+// touch ~2.3 words, so the three predicated REDs run with ~43 % of their
+// lanes; the cost is a compare and a predicated OR per adjacent pair.
+#ifndef RS_AAL_MERGE
+#define RS_AAL_MERGE 0
+#endif
+template <bool XOR>
+__device__ __forceinline__ void set_vec4_merged(uint32_t x, uint32_t y, uint32_t X) {
+  const uint32_t a0 = X | ((x >> 3) & 0x1FFCu), a1 = X | ((x >> 19) & 0x1FFCu);
+  const uint32_t a2 = X | ((y >> 3) & 0x1FFCu), a3 = X | ((y >> 19) & 0x1FFCu);
+  const uint32_t b0 = __funnelshift_l(0u, 1u, x);
+  uint32_t b1 = __funnelshift_l(0u, 1u, x >> 16), b2 = __funnelshift_l(0u, 1u, y), b3 = __funnelshift_l(0u, 1u, y >> 16);
+  if (a1 == a0) b1 |= b0;
+  else red_set<XOR>(a0, b0);
+  if (a2 == a1) b2 |= b1;
+  else red_set<XOR>(a1, b1);
+  if (a3 == a2) b3 |= b2;
+  else red_set<XOR>(a2, b2);
+  red_set<XOR>(a3, b3);
+}
+
 template <bool XOR = false>
 __device__ __forceinline__ void scatter16(const uint16_t *v, uint32_t n, uint32_t X, int t) {
   constexpr int VB = RS_AAL_VEC, NV = VB / 2;  // values per lane vector
@@ -278,8 +305,11 @@ __device__ __forceinline__ void scatter16(const uint16_t *v, uint32_t n, uint32_
 #pragma unroll 2
   for (uint32_t i = t; i < nfull; i += LT) {
     const V q = vp[i];
+    if constexpr (VB == 8 && RS_AAL_MERGE) set_vec4_merged<XOR>(vword(q, 0), vword(q, 1), X);
+    else {
 #pragma unroll
-    for (int k = 0; k < VB / 4; k++) set_pair<XOR>(vword(q, k), X);
+      for (int k = 0; k < VB / 4; k++) set_pair<XOR>(vword(q, k), X);
+    }
   }
   if ((uint32_t)t < n - nfull * NV) {
     const uint32_t x = v[nfull * NV + t];
@@ -540,8 +570,53 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
     // and: build the smaller side, filter the larger; andnot: build B, filter A
     const bool build_a = is_and && na <= nb;
     uint32_t *X = (NGRP == 2 ? g : parity) ? XB : XA;
-    if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
     {  // galloping pairs (gallop_pair): the small side's values binary-searched in the staged large side
+      const bool a_small = is_and ? na <= nb : true;
+      const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
+#ifndef RS_AAL_GALLOP_WARP
+#define RS_AAL_GALLOP_WARP 64
+#endif
+      if (is_and && 16 * ns <= nl && ns <= RS_AAL_GALLOP_WARP) {  // (andnot: 4 bytes of spill with it, and no such pairs routed here)
+        // at most 64 searches: the group's first warp does them alone (two
+        // per lane, advancing together), places the kept values by ballot
+        // and takes no group barrier; the other warps only hand the item's
+        // bytes back.  (The 128-thread form below spent ~950 warp
+        // instructions on such a pair, most of them the idle warps' share
+        // of the scan and barriers.)
+        const uint16_t *Sv = a_small ? A : B, *Lv = a_small ? B : A;
+        uint32_t total = 0;
+        if (t < 32) {
+          const uint32_t v0 = (uint32_t)t < ns ? Sv[t] : 0u, v1 = (uint32_t)t + 32u < ns ? Sv[t + 32] : 0u;
+          uint32_t lo0 = 0, lo1 = 0, len = nl;
+          while (len > 1) {  // nl >= 16 here
+            const uint32_t half = len >> 1;
+            const uint32_t m0 = Lv[lo0 + half], m1 = Lv[lo1 + half];
+            if (m0 <= v0) lo0 += half;
+            if (m1 <= v1) lo1 += half;
+            len -= half;
+          }
+          const bool k0 = (uint32_t)t < ns && (Lv[lo0] == v0) == is_and;
+          const bool k1 = (uint32_t)t + 32u < ns && (Lv[lo1] == v1) == is_and;
+          const uint32_t b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+          const uint32_t n0 = __popc(b0);
+          total = n0 + __popc(b1);
+          if (!COUNT && dst && total) {
+            uint16_t *d = (uint16_t *)dst;
+            const uint32_t lt = (1u << t) - 1u;
+            if (k0) d[__popc(b0 & lt)] = (uint16_t)v0;
+            if (k1) d[n0 + __popc(b1 & lt)] = (uint16_t)v1;
+            const uint32_t padded = (total + 7u) & ~7u;
+            if (t < 8 && total + t < padded) d[total + t] = 0;
+          }
+        }
+        mbar_arrive(release);  // this thread's last read of the staged values
+        if constexpr (NGRP == 1) gbar(g);  // one group: X alternates by parity and relies on a barrier per pair
+        nout = total;
+        return total;  // valid on the group's first warp (the sink runs on its lane 0)
+      }
+    }
+    if constexpr (NGRP == 2) gbar(g);  // the previous pair's clear of X is complete
+    {
       const bool a_small = is_and ? na <= nb : true;
       const uint32_t ns = a_small ? na : nb, nl = a_small ? nb : na;
       if (16 * ns <= nl) {

@@ -70,10 +70,15 @@ __constant__ uint32_t c_aa_union_medium = 512;
 // Galloping pairs of the COUNT path go to the large-pair kernel, which
 // binary-searches the small side's values in the staged large side (shared
 // memory; the bytes stream in with the TMA) instead of the warp-per-pair
-// in-place search over HBM: C3 counts 0.84 -> 0.79 ms.  The op path keeps the
-// warp kernel (AND 1.24 -> 1.31-1.35 ms the other way).  RS_GALLOP_TMA:
-// bit 0 = counts (default on), bit 1 = ops.
-__constant__ uint32_t c_gallop_tma = 1;
+// in-place search over HBM: C3 counts 0.84 -> 0.79 ms.  The op path does the
+// same for AND pairs of at most 64 searches, which one warp of the large-pair
+// kernel's group handles without a group barrier (rs_array_large.cuh): run
+// as its own kernel, the galloping class waited for the persistent
+// large-pair CTAs to leave the SMs, so C3 AND paid its 0.24 ms in full after
+// them.  Longer small sides keep the warp kernel (the 128-thread form costs
+// ~950 warp instructions per pair).  RS_GALLOP_TMA: bit 0 = counts, bit 1 =
+// ops (both on by default).
+__constant__ uint32_t c_gallop_tma = 3;
 
 // `op` is the materialized op, or AND for the intersection counts.  An
 // array against a bitset or runs under AND (either side), or an array minus a
@@ -94,7 +99,7 @@ __device__ __forceinline__ bool gallop_pair(uint32_t na, uint32_t nb, int op) {
 __device__ __forceinline__ int classify(uint8_t ta, uint32_t na, uint8_t tb, uint32_t nb, int op, bool count = false) {
   if (ta == RS_TAG_BITSET && tb == RS_TAG_BITSET) return CLS_BB;
   if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY && gallop_pair(na, nb, op))
-    return (c_gallop_tma >> (count ? 0 : 1)) & 1u ? CLS_AAL : CLS_AAG;
+    return (count ? c_gallop_tma & 1u : (c_gallop_tma & 2u) && op == RS_OP_AND && min(na, nb) <= 64u) ? CLS_AAL : CLS_AAG;
   if (ta == RS_TAG_ARRAY && tb == RS_TAG_ARRAY)
     return na + nb <= 256 ? CLS_AAS
            : na + nb <= (op == RS_OP_OR || op == RS_OP_XOR ? c_aa_union_medium : c_aa_large_min) ? CLS_AAM
@@ -1786,7 +1791,7 @@ int check_op(int op) {
     RS_CK(cudaMemcpyToSymbol(c_aa_union_medium, &um, sizeof um));
     const uint32_t tiny = (uint32_t)env_int("RS_AA_TINY", 64);  // tuning: largest pair merged by one thread
     RS_CK(cudaMemcpyToSymbol(c_aa_tiny, &tiny, sizeof tiny));
-    const uint32_t gt = (uint32_t)env_int("RS_GALLOP_TMA", 1);
+    const uint32_t gt = (uint32_t)env_int("RS_GALLOP_TMA", 3);
     RS_CK(cudaMemcpyToSymbol(c_gallop_tma, &gt, sizeof gt));
     tuned = 1;
   }
