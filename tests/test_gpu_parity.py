@@ -570,3 +570,53 @@ def test_union_many_selection_grouping_paths(pkg, monkeypatch, radix):
     Bm = pkg.BitmapBatch.from_wire(many)
     sel = list(rng.permutation(1100)) + [7, 7]
     assert Bm.union_many(sel).to_wire_list()[0] == orc.union_many([many[i] for i in sel])
+
+
+@pytest.mark.parametrize("routing", ["3", "1"])
+def test_galloping_pair_boundaries(pkg, monkeypatch, routing):
+    """array_intersect_galloping's case (kernels/scalar.py:149-176) at the
+    edges of its GPU paths: small sides of 1, 31..33, 63..65 and 256 values
+    against large sides at exactly 16x, one under, and 4096; the small side on
+    either operand; subsets, disjoint and interleaved values; one-container
+    pairs (container_pairwise) and the same containers inside bitmaps.  Both
+    routings of the short pairs: one warp of the large-pair kernel's group
+    (RS_GALLOP_TMA=3, the default) and the galloping kernel (=1)."""
+    import subprocess, sys, os, textwrap
+    # the routing constant is read once per process: run the body in a child
+    code = textwrap.dedent("""
+        import numpy as np, sys
+        sys.path.insert(0, %r)
+        import paper_1709_07821_b200 as pkg
+        from oracle import oracle as orc
+        rng = np.random.default_rng(64)
+        wa, wb = [], []
+        for ns in (1, 2, 31, 32, 33, 63, 64, 65, 128, 256):
+            for nl in sorted({max(16 * ns - 1, ns + 1), 16 * ns, 16 * ns + 1, 4096}):
+                if nl > 4096 or ns + nl <= 256:
+                    continue
+                for kind in ("subset", "disjoint", "mixed"):
+                    L = np.sort(rng.choice(65536, size=nl, replace=False)).astype(np.uint64)
+                    if kind == "subset":
+                        S = np.sort(rng.choice(L, size=ns, replace=False))
+                    elif kind == "disjoint":
+                        S = np.sort(rng.choice(np.setdiff1d(np.arange(65536, dtype=np.uint64), L), size=ns, replace=False))
+                    else:
+                        S = np.unique(np.concatenate([rng.choice(L, size=(ns + 1) // 2, replace=False),
+                                                      rng.choice(65536, size=ns, replace=False).astype(np.uint64)]))[:ns]
+                    for small_first in (True, False):
+                        a, b = (S, L) if small_first else (L, S)
+                        wa.append(orc.from_values(a)); wb.append(orc.from_values(b))
+        A = pkg.BitmapBatch.from_wire(wa); B = pkg.BitmapBatch.from_wire(wb)
+        for op in ("and", "or", "andnot", "xor"):
+            want = [orc.op(op, x, y) for x, y in zip(wa, wb)]
+            for got in (A.container_pairwise(op, B).to_wire_list(), A.pairwise(op, B).to_wire_list()):
+                bad = [i for i in range(len(wa)) if got[i] != want[i]]
+                assert not bad, (op, bad[:5])
+            wc = [orc.op_cardinality(op, x, y) for x, y in zip(wa, wb)]
+            assert A.container_pairwise_cardinality(op, B).tolist() == wc, op
+            assert A.pairwise_cardinality(op, B).tolist() == wc, op
+        print("pairs", len(wa))
+    """) % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RS_GALLOP_TMA=routing)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
