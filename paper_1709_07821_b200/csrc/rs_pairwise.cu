@@ -2217,10 +2217,19 @@ extern "C" int rs_pairwise(int op, const rs_batch *A, const rs_batch *B, const u
   static const int force_pp = env_int("RS_PER_PAIR", -1);  // A/B: 1 forces, 0 disables the per-pair join
   const bool per_pair = M && maxk <= MERGE_SMEM_KEYS &&
                         (force_pp >= 0 ? force_pp == 1 : (npairs >= 2 * sm_count() || M <= 1024 * npairs));
-  // AND / ANDNOT otherwise join on A's positions (no scans, no emit pass);
-  // RS_AJOIN=0 keeps the merged-position join
+  // AND / ANDNOT otherwise join on A's positions (no scans, no emit pass)
+  // -- and, since one k_join_a launch replaces the per-pair path's merge /
+  // match / emit passes, also for per-pair batches of at least
+  // RS_AJOIN_MIN_SLOTS A containers (default 32,768) averaging 8 or more per
+  // pair (config 2: AND 1.19 -> 1.11 ms, ANDNOT 1.045 -> 1.016; 4,096 pairs
+  // x 16 keys: AND 0.137 -> 0.117 ms, ANDNOT 0.205 -> 0.195; 16,384 pairs x
+  // 4 keys and 256 pairs x 32 keys measured 3 and 10 % slower and keep the
+  // per-pair join; tools/probe_join.py); RS_AJOIN=0 keeps the
+  // merged-position join
   static const int ajoin = env_int("RS_AJOIN", 1);
-  if (ajoin && (op == RS_OP_AND || op == RS_OP_ANDNOT) && !per_pair && npairs <= 16384 &&
+  static const int ajoin_min_slots = env_int("RS_AJOIN_MIN_SLOTS", 32768);
+  const bool ajoin_over_pp = force_pp < 0 && Ea >= (uint64_t)ajoin_min_slots && Ea >= 8 * npairs;
+  if (ajoin && (op == RS_OP_AND || op == RS_OP_ANDNOT) && (!per_pair || ajoin_over_pp) && npairs <= 16384 &&
       env_int("RS_EXACT_ALLOC", 0) == 0 && ub_affordable(Ea))
     return a_join_op(op, A, B, ia, ib, npairs, Ea, out);
   Upload U;
