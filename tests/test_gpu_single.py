@@ -182,3 +182,47 @@ def test_random_batches_every_join(rb, seed):
                 want = orc.op(op, imgs[a], imgs[b])
                 assert got[k] == want, (seed, nbm, op, a, b)
                 assert cnt[k] == orc.cardinality(want), (seed, nbm, op, a, b)
+
+
+def test_a_indexed_join_over_per_pair_batches():
+    """Per-pair-eligible AND / ANDNOT batches take the A-indexed join once
+    they hold enough A containers (RS_AJOIN_MIN_SLOTS, default 32,768; config
+    2's path).  Forced here on small random batches (many pairs of few keys,
+    empty bitmaps, repeats and self-pairs) with RS_AJOIN_MIN_SLOTS=1, in a
+    child process (the threshold is read once): results and counts against
+    the oracle."""
+    import os, subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import sys
+        sys.path.insert(0, %r)
+        import numpy as np
+        import paper_1709_07821_b200 as rb
+        from oracle import oracle as orc
+        from tests.test_gpu_single import bitmap
+        for seed in range(3):
+            rng = np.random.default_rng(700 + seed)
+            for nbm, kmax, npairs in ((40, 40, 400), (12, 300, 90), (200, 16, 1500)):
+                imgs = []
+                for i in range(nbm):
+                    nk = 0 if i == 3 else int(rng.integers(kmax // 2, kmax + 1))
+                    imgs.append(bitmap(rng, np.sort(rng.choice(4 * kmax + 8, nk, replace=False)),
+                                       optimize=bool(rng.integers(0, 2))))
+                B = rb.BitmapBatch.from_wire(imgs)
+                ia = rng.integers(0, nbm, npairs).tolist()
+                ib = rng.integers(0, nbm, npairs).tolist()
+                memo = {}
+                for op in ("and", "andnot"):
+                    got = B.pairwise(op, B, ia, ib).to_wire_list()
+                    cnt = B.pairwise_cardinality(op, B, ia, ib).tolist()
+                    for k, (a, b) in enumerate(zip(ia, ib)):
+                        if (op, a, b) not in memo:
+                            memo[(op, a, b)] = orc.op(op, imgs[a], imgs[b])
+                        want = memo[(op, a, b)]
+                        assert got[k] == want, (seed, nbm, op, a, b)
+                        assert cnt[k] == orc.cardinality(want), (seed, nbm, op, a, b)
+        print("ok")
+    """) % root
+    env = dict(os.environ, RS_AJOIN_MIN_SLOTS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
