@@ -644,8 +644,10 @@ __device__ __forceinline__ uint32_t large_pair(const LargeSmem &sm, int g, int t
         return total;
       }
     }
+// (threshold swept on C3 AND with the one-warp galloping path in: 1024 /
+// 2048 / 4096 / 8192 / off = 1.173 / 1.151 / 1.136 / 1.14-1.18 / 1.167 ms)
 #ifndef RS_AAL_DUAL_MIN
-#define RS_AAL_DUAL_MIN 2048
+#define RS_AAL_DUAL_MIN 4096
 #endif
     if constexpr (is_and && !COUNT && NGRP == 2) {
       // large AND pairs: both sides scattered (a shared OR per value) into
